@@ -1,0 +1,69 @@
+// nezha/collective.hpp — per-rail allreduce surface.
+//
+// The reference names this module but ships no code for it
+// (proj/tests/CMakeLists.txt:13 is commented out); the API below is the
+// SPEC's, with the ambiguities pinned as DESIGN.md P1/P2/P10 so the CUDA
+// rails and the CPU oracle agree bit for bit.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "nezha/core/types.hpp"
+
+namespace nezha {
+
+enum class Algorithm : std::uint8_t { Ring = 0, RingChunked = 1 };
+
+// Element type of the payload. The reference is fp32-only (types.hpp:60-67);
+// bf16 and int32 are the B200 extensions pinned by DESIGN.md P2.
+enum class DType : std::uint8_t { F32 = 0, BF16 = 1, I32 = 2 };
+
+inline Bytes elementSize(DType d) { return d == DType::BF16 ? 2 : 4; }
+
+/// SPEC.md:179-182. One per (rail, op_seq).
+struct OpHandle {
+  std::uint32_t op_seq = 0;
+  Segment segment;
+  int rail_id = 0;
+  Algorithm algorithm = Algorithm::RingChunked;
+  ReduceOp reduce_op = ReduceOp::Sum;
+};
+
+/// Summation-order geometry of one rail segment (P1 + P10).
+///
+/// The segment is cut into chunks of `chunk_bytes` (the last one shorter);
+/// each chunk's elements are cut into N ring blocks of floor(E_c / N)
+/// elements with the last block absorbing the remainder.
+/// Every element of block b is summed x_b + x_{b+1} + ... + x_{b-1}
+/// (cyclic ascending rank order). The geometry is a property of
+/// the segment, not of whoever executes it: a handoff keeps the failed
+/// rail's geometry, so rerouted chunks reduce to the same bits.
+struct ChunkGeometry {
+  Bytes seg_offset = 0;
+  Bytes seg_length = 0;
+  Bytes chunk_bytes = 0;
+
+  Bytes numChunks() const { return chunk_bytes == 0 ? 0 : (seg_length + chunk_bytes - 1) / chunk_bytes; }
+  Segment chunk(Bytes c) const;
+};
+
+// P10: max(64 KiB, round4down(length / (2N))) for RingChunked; the whole
+// segment for Ring. Always >= 4 and a multiple of 4.
+Bytes defaultChunkBytes(Bytes segment_length, int world, Algorithm algo);
+ChunkGeometry makeGeometry(const Segment& seg, int world, Algorithm algo);
+
+// Ring block (start rank of the sum) of element `elem` of a chunk with
+// `chunk_elems` elements over `world` ranks.
+inline int ringBlockOf(std::uint64_t elem, std::uint64_t chunk_elems, int world) {
+  const std::uint64_t q = chunk_elems / static_cast<std::uint64_t>(world);
+  if (q == 0) return world - 1;
+  const std::uint64_t b = elem / q;
+  return b >= static_cast<std::uint64_t>(world) ? world - 1 : static_cast<int>(b);
+}
+
+// payloads above 2^30 bytes become ceil(S / 256 MiB)
+// contiguous pieces of at most 256 MiB; everything else is one piece.
+std::vector<Segment> splitOversized(Bytes payload);
+
+}  // namespace nezha

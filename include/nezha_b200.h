@@ -1,0 +1,220 @@
+/*
+ * nezha_b200.h — C ABI of the B200-native multi-rail allreduce.
+ *
+ * Plain C: opaque handles, plain pointers and sizes, int return codes
+ * (0 = ok, < 0 = error, message in nz_last_error()). Nothing throws across
+ * this boundary and no torch type appears in it. One process drives one GPU.
+ *
+ * Which reference interface each group replaces (file:line under
+ * /root/reference):
+ *   nz_comm_*      rendezvous(TransportOptions) -> ConnectionSet
+ *                  (proj/include/nezha/transport/transport.hpp:219-238) and
+ *                  FileStore (proj/include/nezha/transport/rendezvous.hpp:19-37):
+ *                  the per-rank bootstrap that builds the full rail mesh.
+ *   nz_buffer_*    UnboundBuffer: the shared
+ *                  reduction buffer every rail reads its segment from.
+ *   nz_rail_*      one rail's ring_allreduce / ring_chunked_allreduce over its
+ *                  segment on top of Channel::send/recv
+ *                  (transport.hpp:89-123); failure injection replaces
+ *                  InMemoryFabric::failRailAtFrame (inmem.hpp:22-24).
+ *   nz_engine_*    the engine-level multi-rail allreduce (SPEC.md:226, :353,
+ *                  :416; named by proj/tests/CMakeLists.txt:17): allocate ->
+ *                  per-rail executors -> join -> Timer -> balancer -> handoff.
+ *   nz_planner_*   the balancer + faults decisions alone,
+ *                  trace driven, CPU only; what the parity tests diff.
+ *   nz_core_*      core cost model (proj/include/nezha/core/math.hpp:9-17,
+ *                  types.hpp:26-44) for FFI callers without C++.
+ */
+#ifndef NEZHA_B200_H
+#define NEZHA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NZ_ABI_VERSION 1
+
+enum {
+  NZ_OK = 0,
+  NZ_ERR_INVALID = -1,      /* std::invalid_argument in the C++ API */
+  NZ_ERR_CUDA = -2,         /* a CUDA runtime / driver call failed */
+  NZ_ERR_SYSTEM = -3,       /* socket / fd / OS failure during bootstrap */
+  NZ_ERR_UNSUPPORTED = -4,  /* e.g. NVLS rail without multicast support */
+  NZ_ERR_RAIL_DOWN = -5,    /* ChannelDownError */
+  NZ_ERR_UNRECOVERABLE = -6,/* UnrecoverableError: no surviving rail */
+  NZ_ERR_TIMEOUT = -7,      /* RendezvousTimeoutError / device watchdog */
+  NZ_ERR_BUFFER = -8        /* output buffer too small */
+};
+
+typedef enum { NZ_F32 = 0, NZ_BF16 = 1, NZ_I32 = 2 } nz_dtype_t;
+
+/* B200 rails. Protocol names in rails TOML: sharp|nvls, glex|ce, tcp|sm. */
+typedef enum { NZ_RAIL_NVLS = 0, NZ_RAIL_CE = 1, NZ_RAIL_SM = 2 } nz_rail_kind_t;
+
+typedef enum { NZ_ALGO_RING = 0, NZ_ALGO_RING_CHUNKED = 1 } nz_algorithm_t;
+
+typedef struct nz_comm nz_comm_t;
+typedef struct nz_buf nz_buf_t;
+typedef struct nz_rail nz_rail_t;
+typedef struct nz_engine nz_engine_t;
+
+const char* nz_last_error(void);
+int nz_abi_version(void);
+/* 1 when this build contains the sm_100a kernels (always, for the product). */
+int nz_has_cuda_kernels(void);
+
+/* ---------------------------------------------------------------- comm --- */
+/* Bootstrap of one rank (one GPU). `session` names the rendezvous: every rank
+ * of one job passes the same string (e.g. "<MASTER_PORT>-<job>"). File
+ * descriptors for peer memory and the multicast object travel over abstract
+ * unix sockets, the FileStore analogue. Blocks until all ranks arrive or
+ * `timeout_ms` passes (NZ_ERR_TIMEOUT). */
+int nz_comm_init(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out);
+int nz_comm_destroy(nz_comm_t* comm);
+int nz_comm_rank(const nz_comm_t* comm);
+int nz_comm_world(const nz_comm_t* comm);
+int nz_comm_device(const nz_comm_t* comm);
+int nz_comm_sm_count(const nz_comm_t* comm);
+int nz_comm_multicast_supported(const nz_comm_t* comm);
+/* Host-side barrier and allgather of small host blobs (`all` holds world*bytes). */
+int nz_comm_barrier(nz_comm_t* comm);
+int nz_comm_allgather(nz_comm_t* comm, const void* mine, size_t bytes, void* all);
+
+/* -------------------------------------------------------------- buffers --- */
+/* Symmetric device buffer: the same size on every rank, mapped into every
+ * rank's address space (peer pointers) and bound to a multicast object when
+ * the fabric supports it. Collective: all ranks call with the same size. */
+int nz_buffer_alloc(nz_comm_t* comm, size_t bytes, nz_buf_t** out);
+int nz_buffer_free(nz_buf_t* buf);
+void* nz_buffer_ptr(const nz_buf_t* buf);
+void* nz_buffer_peer_ptr(const nz_buf_t* buf, int rank);
+void* nz_buffer_mc_ptr(const nz_buf_t* buf); /* NULL without multicast */
+size_t nz_buffer_size(const nz_buf_t* buf);
+/* Copy into / out of this rank's part of the buffer. `src` / `dst` may be
+ * host (pinned or pageable) or device memory. With stream == NULL the copy is
+ * synchronous; otherwise it is enqueued on `stream`. */
+int nz_buffer_write(nz_buf_t* buf, uint64_t offset, const void* src, uint64_t bytes, void* stream);
+int nz_buffer_read(const nz_buf_t* buf, uint64_t offset, void* dst, uint64_t bytes, void* stream);
+int nz_buffer_fill_zero(nz_buf_t* buf, void* stream);
+
+/* ---------------------------------------------------------------- rails --- */
+/* A rail owns a CUDA stream on this rank, its barrier pads and (CE) staging.
+ * `sm_budget` caps the CTAs its kernels use (0 = all SMs). */
+int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rail_t** out);
+int nz_rail_destroy(nz_rail_t* rail);
+int nz_rail_kind(const nz_rail_t* rail);
+/* Blocks the host until all work enqueued on the rail's own streams is done. */
+int nz_rail_synchronize(nz_rail_t* rail);
+void* nz_rail_stream(const nz_rail_t* rail);
+
+/* Allreduce chunks [chunk_begin, chunk_end) of the segment geometry
+ * (seg_off, seg_len, chunk_bytes) from `in` into `out` (out-of-place; in ==
+ * out is allowed when no failure injection is armed). Enqueued on `stream`
+ * (NULL = the rail's own stream); returns without waiting. Summation order:
+ * DESIGN.md P1 (CE, SM: exact; NVLS: switch order). If `fail_chunk` lies in
+ * [chunk_begin, chunk_end) the rail stops before that chunk on every rank and
+ * posts a fault record (nz_rail_poll_fault): deterministic injection of the
+ * trace form (op_seq, rail, chunk k), P10. -1 disables it. */
+int nz_rail_allreduce(nz_rail_t* rail, nz_buf_t* in, nz_buf_t* out, uint64_t seg_off, uint64_t seg_len,
+                      uint64_t chunk_bytes, uint64_t chunk_begin, uint64_t chunk_end, int dtype,
+                      uint32_t op_seq, int64_t fail_chunk, void* stream);
+
+typedef struct {
+  uint32_t valid;      /* 1 once the device posted a fault */
+  uint32_t op_seq;
+  uint64_t chunk;      /* first chunk NOT completed */
+  uint64_t t_fail_ns;  /* %globaltimer when the rail stopped */
+} nz_fault_record_t;
+
+/* Non-blocking read of the rail's mapped fault word; clears it when `consume`. */
+int nz_rail_poll_fault(nz_rail_t* rail, nz_fault_record_t* rec, int consume);
+/* Device watchdog status: 0 ok, else a barrier timed out (the kernel bailed
+ * out instead of hanging). Cleared by reading. */
+int nz_rail_watchdog(nz_rail_t* rail);
+
+/* --------------------------------------------------------------- engine --- */
+typedef struct {
+  int num_rails;             /* 1..3 */
+  int kinds[3];              /* nz_rail_kind_t per rail, rail_id = index */
+  int sm_budget[3];          /* CTA cap per rail (0 = all SMs) */
+  int algorithm;             /* nz_algorithm_t, default RingChunked */
+  double tau;                /* Eq. 3 gate, default 5 */
+  double eta;                /* Eq. 7 step, default 0.05 */
+  double convergence_eps;    /* default 0.01 */
+  double sync_overhead_us;   /* < 0: measure at startup */
+  int window;                /* Timer window, default 100 */
+  int max_iters;             /* default 100 */
+  int demote_after;          /* DESIGN.md P12; 0 disables */
+  const char* rails_toml;    /* optional rails config text; NULL: calibrate */
+  int calibrate_iters;       /* ops per size during startup calibration */
+} nz_engine_config_t;
+
+void nz_engine_config_default(nz_engine_config_t* cfg);
+/* Collective. Builds rails, measures profiles (unless rails_toml is given)
+ * and sync overhead, and initialises the allocation table. */
+int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t** out);
+int nz_engine_destroy(nz_engine_t* eng);
+
+/* In-memory multi-rail allreduce of `bytes` bytes at offset 0 of the
+ * symmetric buffers. `stream` (NULL = legacy default) is the caller's: the
+ * rails fork from it and join back into it. Asynchronous. */
+int nz_engine_allreduce(nz_engine_t* eng, nz_buf_t* in, nz_buf_t* out, uint64_t bytes, int dtype, void* stream);
+/* End to end from host memory (pinned or pageable): H2D into the engine's
+ * UnboundBuffer, multi-rail allreduce, D2H into host_out. Synchronous. */
+int nz_engine_allreduce_host(nz_engine_t* eng, const void* host_in, void* host_out, uint64_t bytes, int dtype);
+/* Arms a failure of `rail_id` at `chunk` of op `op_seq` (trace form P10). */
+int nz_engine_inject_failure(nz_engine_t* eng, uint32_t op_seq, int rail_id, uint64_t chunk);
+/* Readmits a previously failed rail. */
+int nz_engine_readmit(nz_engine_t* eng, int rail_id);
+int nz_engine_synchronize(nz_engine_t* eng);
+uint32_t nz_engine_op_seq(const nz_engine_t* eng);
+
+typedef struct {
+  uint32_t op_seq;
+  int failed_rail;
+  int target_rail;
+  uint64_t orphan_offset;
+  uint64_t orphan_length;
+  double detect_us;   /* device fault stamp -> host monitor saw it */
+  double resume_us;   /* device fault stamp -> survivor started the orphan */
+  double done_us;     /* device fault stamp -> orphan complete */
+} nz_failover_report_t;
+/* Last completed failover (returns NZ_ERR_INVALID when none happened). */
+int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep);
+
+/* JSON snapshots: allocation table + profiles + health, and the plan the
+ * engine would use for `bytes` (segments per rail). */
+int nz_engine_state_json(nz_engine_t* eng, char* out, size_t cap);
+int nz_engine_plan_json(nz_engine_t* eng, uint64_t bytes, char* out, size_t cap);
+
+/* -------------------------------------------------------------- planner --- */
+/* Runs the balancer + fault logic over a scenario (rails, config, op stream,
+ * injected latency model, failures; format in DESIGN.md §5) with no GPU, and
+ * writes the decision log (one JSON object per line). Bit-exact contract with
+ * oracle/planner.py. */
+int nz_planner_run_trace(const char* scenario, char* out, size_t cap);
+
+/* ------------------------------------------------------------ emulation --- */
+/* Single-GPU emulation of one rank of the SM rail (ndst == world: fold and
+ * store to every rank's output) or of the CE rail's local reduce (ndst == 1)
+ * over [lo, hi) with the segment's order geometry. All `world` input and
+ * output buffers live on the current device; no barriers are issued, so the
+ * caller runs the virtual ranks one after another. Lets the exact rail
+ * kernels be parity-tested for N = 2..8 on a single B200. grid <= 0: auto. */
+int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
+                    uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
+                    void* stream);
+
+/* ----------------------------------------------------------------- core --- */
+uint64_t nz_core_ring_volume(int node_count, uint64_t payload);
+int nz_core_bucket_of(uint64_t size);
+uint64_t nz_core_default_chunk_bytes(uint64_t seg_len, int world, int algorithm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NEZHA_B200_H */

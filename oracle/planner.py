@@ -1,0 +1,525 @@
+"""Oracle restatement of the balancer and fault decisions — TEST INFRASTRUCTURE ONLY.
+
+Independent Python restatement of SPEC.md's balancer and
+faults modules with the DESIGN.md pins, over the
+reference's core cost model (proj/src/core/types.cpp:54-77,
+proj/src/core/math.cpp:26-35). It consumes the same scenario text as
+nz_planner_run_trace and must print a byte-identical decision log.
+
+Parity pinning: the reference ships no balancer code or tests
+(proj/tests/CMakeLists.txt:14-16 commented out), so this restatement is pinned
+by the SPEC's own known-answer examples (tests/test_planner_oracle.py, which
+checks every example in SPEC.md:264-328 and :395-411 against this file) —
+"parity pinned to SPEC examples", not to reference outputs.
+"""
+from __future__ import annotations
+
+import math
+
+KMIN, KMAX = 0, 40
+NO_THRESHOLD = None
+PROTO = {"tcp": 0, "sharp": 1, "glex": 2, "custom": 3, "nvls": 1, "ce": 2, "sm": 0}
+
+
+def fmt(v: float) -> str:
+    return "%.17g" % v
+
+
+class Rail:
+    """RailProfile (proj/include/nezha/core/types.hpp:26-44)."""
+
+    def __init__(self, rail_id, t_setup_us, bandwidth_bps, points=()):
+        self.rail_id = rail_id
+        self.t = float(t_setup_us)
+        self.bw = float(bandwidth_bps)
+        self.points = [(int(s), float(l)) for s, l in points]
+
+    def latency(self, size: int) -> float:
+        """messageLatency (types.cpp:54-77)."""
+        pts = self.points
+        if not pts:
+            return self.t + float(size) / self.bw * 1e6
+        if len(pts) == 1 or size <= pts[0][0]:
+            return pts[0][1]
+        hi = 1
+        while hi + 1 < len(pts) and pts[hi][0] < size:
+            hi += 1
+        x0, y0 = pts[hi - 1]
+        x1, y1 = pts[hi]
+        frac = (float(size) - float(x0)) / (float(x1) - float(x0))
+        return y0 + frac * (y1 - y0)
+
+    def throughput(self, size: int) -> float:
+        """realTimeThroughput (math.cpp:26-35)."""
+        if size == 0:
+            return 0.0
+        t = self.latency(size)
+        if t <= 0:
+            return 0.0
+        return float(size) / (t * 1e-6)
+
+
+def split(alpha, S):
+    """P8: round4down shares in rail order, remainder to the last participant."""
+    part = [i for i, a in enumerate(alpha) if a > 0]
+    if not part:
+        raise ValueError("no participant")
+    out = [0] * len(alpha)
+    used = 0
+    for i in part[:-1]:
+        n = int(alpha[i] * float(S)) & ~3
+        if n > S - used:
+            n = (S - used) & ~3
+        out[i] = n
+        used += n
+    out[part[-1]] = S - used
+    return out
+
+
+def rho(rails, alpha, S):
+    """Eq. 3 (P3)."""
+    lens = split(alpha, S)
+    thr = sorted((r.throughput(n) for r, n in zip(rails, lens) if n > 0), reverse=True)
+    if len(thr) < 2:
+        return 1.0
+    if not thr[1] > 0:
+        raise ArithmeticError("degenerate profile")
+    return thr[0] / thr[1]
+
+
+def cold(rails, S):
+    """Eq. 4: (latency, index), ties to the lowest index."""
+    best, t = 0, rails[0].latency(S)
+    for i in range(1, len(rails)):
+        ti = rails[i].latency(S)
+        if ti < t:
+            best, t = i, ti
+    return t, best
+
+
+def hot(rails, alpha, S, sync):
+    """Eq. 5 over participating rails."""
+    if any(a < 0 for a in alpha):
+        raise ValueError("off simplex")
+    tot = 0.0
+    for a in alpha:
+        tot += a
+    if abs(tot - 1.0) > 1e-9:
+        raise ValueError("off simplex")
+    worst = 0.0
+    for r, n in zip(rails, split(alpha, S)):
+        if n > 0:
+            worst = max(worst, r.latency(n))
+    return worst + sync
+
+
+def eq8(T):
+    """init_coefficients with N = number of rails."""
+    if any(not t > 0 for t in T):
+        raise ValueError("invalid telemetry")
+    R = len(T)
+    if R == 1:
+        return [1.0]
+    tot = 0.0
+    for t in T:
+        tot += t
+    return [(tot - t) / (tot * float(R - 1)) for t in T]
+
+
+def eq7(alpha, T, eta, eps):
+    """update_coefficients (P4). Returns (alpha', converged)."""
+    part = [i for i, a in enumerate(alpha) if a > 0]
+    if len(part) < 2:
+        return list(alpha), True
+    m = part[0]
+    tmax = tmin = T[m]
+    tsum = 0.0
+    for i in part:
+        if T[i] > tmax:
+            tmax, m = T[i], i
+        tmin = min(tmin, T[i])
+        tsum += T[i]
+    if tmax - tmin <= eps * tmax:
+        return list(alpha), True
+    tbar = tsum / float(len(part))
+    step = 0.5 * eta * ((tmax - tbar) / tmax)
+    slack = 0.0
+    for i in part:
+        if i != m:
+            slack += tmax - T[i]
+    nxt = list(alpha)
+    nxt[m] = alpha[m] - step
+    for i in part:
+        if i != m:
+            nxt[i] = alpha[i] + step * ((tmax - T[i]) / slack)
+    tot = 0.0
+    for i in range(len(nxt)):
+        if nxt[i] < 0:
+            nxt[i] = 0.0
+        tot += nxt[i]
+    return [a / tot for a in nxt], False
+
+
+def threshold(f, lo, hi):
+    """Eq. 6 bisection in log2 space (P5)."""
+    if f(hi) >= 0:
+        return NO_THRESHOLD
+    if f(lo) < 0:
+        return lo - 1
+    a, b = lo, hi
+    while b - a > 1:
+        m = int(math.floor(math.exp2(0.5 * (math.log2(float(a)) + math.log2(float(b)))) + 0.5))
+        m = max(m, a + 1)
+        m = min(m, b - 1)
+        if f(m) >= 0:
+            a = m
+        else:
+            b = m
+    return a
+
+
+def chunk_bytes(seg_len, world, chunked=True):
+    """P10."""
+    if not chunked:
+        return max(seg_len, 4)
+    return max(65536, (seg_len // (2 * world)) & ~3)
+
+
+class Table:
+    """AllocationTable + balancer control worker."""
+
+    def __init__(self, rails, cfg):
+        self.rails = sorted(rails, key=lambda r: r.rail_id)
+        self.cfg = cfg
+        self.ok = [True] * len(self.rails)
+        self.b = {}
+        self.thr = NO_THRESHOLD
+        self.epoch = 0
+        self.saved = {}
+        self.win = {}  # bucket -> {index: [samples]}
+        self._rebuild()
+
+    # -- helpers
+    def idx(self, rail_id):
+        for i, r in enumerate(self.rails):
+            if r.rail_id == rail_id:
+                return i
+        raise ValueError(rail_id)
+
+    def healthy(self):
+        return [i for i in range(len(self.rails)) if self.ok[i]]
+
+    def restrict(self, a):
+        a = list(a) + [0.0] * (len(self.rails) - len(a))
+        tot = 0.0
+        for i in range(len(a)):
+            if not self.ok[i] or a[i] < 0:
+                a[i] = 0.0
+            tot += a[i]
+        if tot > 0:
+            return [x / tot for x in a]
+        h = sum(self.ok)
+        return [1.0 / h if self.ok[i] else 0.0 for i in range(len(a))]
+
+    def model_alpha(self, k):
+        H = self.healthy()
+        share = max((1 << k) // len(H), 1)
+        init = eq8([self.rails[i].latency(share) for i in H])
+        a = [0.0] * len(self.rails)
+        for j, i in enumerate(H):
+            a[i] = init[j]
+        return a
+
+    @staticmethod
+    def clamp(S):
+        return min(max(S.bit_length() - 1, KMIN), KMAX)
+
+    def f(self, S):
+        H = self.healthy()
+        hp = [self.rails[i] for i in H]
+        a = [self.b[self.clamp(S)]["alpha"][i] for i in H]
+        return hot(hp, a, S, self.cfg["sync_us"]) - cold(hp, S)[0]
+
+    def _rebuild(self):
+        H = self.healthy()
+        if not H:
+            self.thr = NO_THRESHOLD
+            for e in self.b.values():
+                e["hot"] = False
+            self.epoch += 1
+            return
+        before = {k: (e["hot"], e["best"], [x > 0 for x in e["alpha"]]) for k, e in self.b.items()}
+        measured = [k for k in sorted(self.b) if self.b[k]["measured"]]
+        for k in range(KMIN, KMAX + 1):
+            e = self.b.setdefault(k, {"hot": False, "best": 0, "alpha": [], "measured": False, "iters": 0,
+                                      "converged": False, "demoted": False})
+            if e["measured"]:
+                e["alpha"] = self.restrict(e["alpha"])
+            elif measured:
+                near = measured[0]
+                for m in measured:
+                    if abs(m - k) < abs(near - k):
+                        near = m
+                e["alpha"] = self.restrict(self.b[near]["alpha"])
+            else:
+                e["alpha"] = self.model_alpha(k)
+        self.thr = threshold(self.f, self.cfg["probe_lo"], self.cfg["probe_hi"]) if len(H) >= 2 else NO_THRESHOLD
+        hp = [self.rails[i] for i in H]
+        for k in range(KMIN, KMAX + 1):
+            e = self.b[k]
+            e["best"] = H[cold(hp, 1 << k)[1]]
+            e["hot"] = len(H) >= 2 and not e["demoted"] and self.thr is not None and (1 << k) > self.thr
+            part = [x > 0 for x in e["alpha"]]
+            old = before.get(k)
+            if old is None or old[0] != e["hot"] or old[1] != e["best"] or (e["hot"] and old[2] != part):
+                self.win.pop(k, None)
+        self.epoch += 1
+
+    # -- SPEC operations
+    def allocate(self, S):
+        k = self.clamp(S)
+        if not self.healthy():
+            return None
+        e = self.b[k]
+        plan = {"bucket": k, "hot": False, "rho": 1.0, "gated": False, "segs": []}
+        if e["hot"]:
+            H = self.healthy()
+            plan["rho"] = rho([self.rails[i] for i in H], [e["alpha"][i] for i in H], S)
+            if plan["rho"] > self.cfg["tau"]:
+                plan["gated"] = True
+            else:
+                plan["hot"] = True
+                off = 0
+                for i, n in enumerate(split(e["alpha"], S)):
+                    if n:
+                        plan["segs"].append((self.rails[i].rail_id, off, n))
+                        off += n
+                return plan
+        plan["segs"].append((self.rails[e["best"]].rail_id, 0, S))
+        return plan
+
+    def record(self, plan, lat):
+        """record_latency for each rail of one op; returns the flush or None."""
+        if plan["gated"]:
+            return None
+        w = self.win.setdefault(plan["bucket"], {i: [] for i in range(len(self.rails))})
+        full = False
+        for rail_id, us in lat:
+            s = w[self.idx(rail_id)]
+            s.append(us)
+            if len(s) >= self.cfg["window"]:
+                full = True
+        if not full:
+            return None
+        means = []
+        for i in range(len(self.rails)):
+            s = w[i]
+            if s:
+                acc = 0.0
+                for x in s:
+                    acc += x
+                means.append((self.rails[i].rail_id, acc / float(len(s))))
+        self.win.pop(plan["bucket"], None)
+        self._flush(plan["bucket"], means)
+        return means
+
+    def _flush(self, k, means):
+        e = self.b[k]
+        worst = 0.0
+        for _, m in means:
+            worst = max(worst, m)
+        if e["hot"]:
+            T = [0.0] * len(self.rails)
+            for rid, m in means:
+                T[self.idx(rid)] = m
+            if e["iters"] < self.cfg["max_iters"]:
+                part = [0.0 if T[i] <= 0 else a for i, a in enumerate(e["alpha"])]
+                a, conv = eq7(self.restrict(part), T, self.cfg["eta"], self.cfg["eps"])
+                e["alpha"] = self.restrict(a)
+                e["converged"] = conv
+                e["iters"] += 1
+            e["measured"] = True
+            if self.cfg["demote_after"] > 0 and e["iters"] >= self.cfg["demote_after"]:
+                hp = [self.rails[i] for i in self.healthy()]
+                if worst >= cold(hp, 1 << k)[0]:
+                    e["demoted"] = True
+        self._rebuild()
+
+    def fail(self, rail_id):
+        i = self.idx(rail_id)
+        if not self.ok[i]:
+            return
+        self.saved = {k: list(e["alpha"]) for k, e in self.b.items()}
+        self.ok[i] = False
+        self.win.clear()
+        self._rebuild()
+
+    def readmit(self, rail_id):
+        i = self.idx(rail_id)
+        if self.ok[i]:
+            raise ValueError("not failed")
+        self.ok[i] = True
+        for k, a in self.saved.items():
+            if k in self.b and self.b[k]["measured"]:
+                self.b[k]["alpha"] = a
+        self.saved = {}
+        self.win.clear()
+        self._rebuild()
+
+    def json(self):
+        parts = []
+        for k in sorted(self.b):
+            e = self.b[k]
+            parts.append('{"bucket":%d,"hot":%s,"best":%d,"alpha":[%s],"measured":%s,"iters":%d,"converged":%s,'
+                         '"demoted":%s}' % (k, _b(e["hot"]), self.rails[e["best"]].rail_id,
+                                            ",".join(fmt(x) for x in e["alpha"]), _b(e["measured"]), e["iters"],
+                                            _b(e["converged"]), _b(e["demoted"])))
+        healthy = ",".join(str(self.rails[i].rail_id) for i in self.healthy())
+        thr = "null" if self.thr is None else str(self.thr)
+        return '{"epoch":%d,"threshold":%s,"healthy":[%s],"buckets":[%s]}' % (self.epoch, thr, healthy,
+                                                                              ",".join(parts))
+
+
+def _b(x):
+    return "true" if x else "false"
+
+
+M64 = (1 << 64) - 1
+
+
+def splitmix(state):
+    state = (state + 0x9E3779B97F4A7C15) & M64
+    z = state
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return state, z ^ (z >> 31)
+
+
+def unit(x):
+    return float(x >> 11) * (1.0 / 9007199254740992.0)
+
+
+def parse(text):
+    sc = {"world": 8, "chunked": True, "rails": [], "truth": {}, "truth_sync": 0.0, "seed": 0, "sizes": [],
+          "faults": [], "readmits": [],
+          "cfg": {"tau": 5.0, "eta": 0.05, "eps": 0.01, "sync_us": 0.0, "window": 100, "max_iters": 100,
+                  "demote_after": 0, "probe_lo": 4096, "probe_hi": 1 << 30}}
+    keys = {"tau": "tau", "eta": "eta", "eps": "eps", "sync_us": "sync_us", "window": "window",
+            "max_iters": "max_iters", "demote_after": "demote_after"}
+    for line in text.splitlines():
+        line = line.split("#", 1)[0].split()
+        if not line:
+            continue
+        k, a = line[0], line[1:]
+        if k == "world":
+            sc["world"] = int(a[0])
+        elif k == "algorithm":
+            sc["chunked"] = a[0] == "ring_chunked"
+        elif k == "config":
+            for name, val in zip(a[::2], a[1::2]):
+                v = float(val)
+                sc["cfg"][keys[name]] = int(v) if name in ("window", "max_iters", "demote_after") else v
+        elif k == "rail":
+            pts = []
+            if len(a) > 4:
+                assert a[4] == "cal"
+                for p in a[5:]:
+                    s, l = p.split(":")
+                    pts.append((int(s), float(l)))
+            sc["rails"].append(Rail(int(a[0]), float(a[2]), float(a[3]), pts))
+        elif k == "truth":
+            sc["truth"][int(a[0])] = (float(a[1]), float(a[2]), float(a[3]))
+        elif k == "truth_sync":
+            sc["truth_sync"] = float(a[0])
+        elif k == "seed":
+            sc["seed"] = int(a[0])
+        elif k == "ops":
+            sc["sizes"] += [int(a[1])] * int(a[0])
+        elif k == "ops_loguniform":
+            n, lo, hi = int(a[0]), int(a[1]), int(a[2])
+            st = sc["seed"]
+            l0, l1 = math.log2(float(lo)), math.log2(float(hi))
+            for _ in range(n):
+                st, z = splitmix(st)
+                s = int(math.floor(math.exp2(l0 + unit(z) * (l1 - l0)))) & ~3
+                sc["sizes"].append(max(s, 4))
+        elif k == "fail":
+            sc["faults"].append((int(a[0]), int(a[1]), int(a[2])))
+        elif k == "readmit":
+            sc["readmits"].append((int(a[0]), int(a[1])))
+        else:
+            raise ValueError(k)
+    return sc
+
+
+def truth(sc, op, rail_id, n, multi):
+    a, b, jit = sc["truth"][rail_id]
+    st = (sc["seed"] ^ ((op * 0x9E3779B97F4A7C15) & M64) ^ (((rail_id + 1) * 0xBF58476D1CE4E5B9) & M64)) & M64
+    _, z = splitmix(st)
+    u = 2.0 * unit(z) - 1.0
+    us = a + float(n) / b * 1e6
+    us = us * (1.0 + jit * u)
+    if multi:
+        us = us + sc["truth_sync"]
+    return us
+
+
+def run(text: str) -> str:
+    """Decision log for a scenario; must equal nz_planner_run_trace byte for byte."""
+    sc = parse(text)
+    t = Table(sc["rails"], sc["cfg"])
+    healthy = sorted(r.rail_id for r in t.rails)
+    out = []
+    for op, S in enumerate(sc["sizes"]):
+        for (rop, rid) in sc["readmits"]:
+            if rop == op:
+                t.readmit(rid)
+                healthy = sorted(healthy + [rid])
+                out.append('{"readmit":%d,"op":%d}' % (rid, op))
+        plan = t.allocate(S)
+        if plan is None:
+            out.append('{"op":%d,"S":%d,"unrecoverable":true}' % (op, S))
+            continue
+        segs = ",".join("[%d,%d,%d]" % s for s in plan["segs"])
+        out.append('{"op":%d,"S":%d,"bucket":%d,"hot":%s,"rho":%s,"gated":%s,"segs":[%s]}' % (
+            op, S, plan["bucket"], _b(plan["hot"]), fmt(plan["rho"]), _b(plan["gated"]), segs))
+        failed = False
+        for (fop, rid, k) in sc["faults"]:
+            if fop != op:
+                continue
+            failed = True
+            seg = [s for s in plan["segs"] if s[0] == rid]
+            ticket, unrec = "null", False
+            if seg:
+                _, off, n = seg[-1]
+                C = chunk_bytes(n, sc["world"], sc["chunked"])
+                if k * C < n:
+                    cands = sorted(r for r in healthy if r != rid)
+                    if cands:
+                        lens = {r: sum(s[2] for s in plan["segs"] if s[0] == r) for r in cands}
+                        tgt = cands[0]
+                        for r in cands:
+                            if lens[r] > lens[tgt]:
+                                tgt = r
+                        ticket = '{"op_seq":%d,"offset":%d,"length":%d,"source":%d,"target":%d}' % (
+                            op, off + k * C, n - k * C, rid, tgt)
+                    else:
+                        unrec = True
+            out.append('{"fail":{"op":%d,"rail":%d,"chunk":%d},"ticket":%s%s}' % (
+                op, rid, k, ticket, ',"unrecoverable":true' if unrec else ""))
+            healthy = [r for r in healthy if r != rid]
+            t.fail(rid)
+        if failed:
+            continue
+        multi = len(plan["segs"]) > 1
+        lat = [(s[0], truth(sc, op, s[0], s[2], multi)) for s in plan["segs"]]
+        means = t.record(plan, lat)
+        if means is not None:
+            e = t.b[plan["bucket"]]
+            out.append('{"flush":%d,"op":%d,"means":[%s],"epoch":%d,"threshold":%s,"alpha":[%s],"hot":%s,'
+                       '"iters":%d,"converged":%s,"demoted":%s}' % (
+                           plan["bucket"], op, ",".join("[%d,%s]" % (r, fmt(m)) for r, m in means), t.epoch,
+                           "null" if t.thr is None else str(t.thr), ",".join(fmt(x) for x in e["alpha"]),
+                           _b(e["hot"]), e["iters"], _b(e["converged"]), _b(e["demoted"])))
+    out.append(t.json())
+    return "\n".join(out) + "\n"

@@ -1,0 +1,290 @@
+// Bootstrap and symmetric memory: the B200 replacement of the reference's
+// rendezvous + ConnectionSet (proj/include/nezha/transport/transport.hpp:219-238,
+// proj/src/transport/rendezvous.cpp:19-99).
+//
+// The reference publishes listen addresses through a shared directory of
+// JSON records and then dials sockets. Here the "channels" are NVLink
+// mappings, so what has to travel between the rank processes is file
+// descriptors of VMM allocations and of the NVSwitch multicast object. They
+// travel over abstract unix sockets (SCM_RIGHTS), one short connection per
+// message, named after the job's session string.
+#include <fcntl.h>
+#include <poll.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <thread>
+
+#include "internal.h"
+
+namespace nz {
+
+namespace {
+thread_local std::string g_last_error;
+
+struct WireHeader {
+  uint64_t seq;
+  int32_t from;
+  uint32_t bytes;
+  uint32_t nfds;
+  uint32_t pad;
+};
+
+constexpr size_t kMaxMsg = 60 * 1024;
+constexpr int kMaxFds = 16;
+
+sockaddr_un socketName(const std::string& session, int rank, socklen_t* len) {
+  sockaddr_un a{};
+  a.sun_family = AF_UNIX;
+  const std::string name = "nezha-b200-" + session + "-" + std::to_string(rank);
+  if (name.size() + 1 >= sizeof(a.sun_path)) fail(NZ_ERR_INVALID, "session name too long");
+  a.sun_path[0] = '\0';  // abstract namespace: nothing on disk to clean up
+  memcpy(a.sun_path + 1, name.data(), name.size());
+  *len = static_cast<socklen_t>(offsetof(sockaddr_un, sun_path) + 1 + name.size());
+  return a;
+}
+
+using Clock = std::chrono::steady_clock;
+
+void sendTo(nz_comm* c, int peer, uint64_t seq, const void* data, size_t bytes, const std::vector<int>& fds) {
+  socklen_t len;
+  sockaddr_un addr = socketName(c->session, peer, &len);
+  const auto deadline = Clock::now() + std::chrono::milliseconds(c->timeout_ms);
+  int s = -1;
+  while (true) {
+    s = socket(AF_UNIX, SOCK_SEQPACKET | SOCK_CLOEXEC, 0);
+    if (s < 0) fail(NZ_ERR_SYSTEM, std::string("socket: ") + strerror(errno));
+    if (connect(s, reinterpret_cast<sockaddr*>(&addr), len) == 0) break;
+    const int err = errno;
+    close(s);
+    if (err != ECONNREFUSED && err != ENOENT && err != EAGAIN) {
+      fail(NZ_ERR_SYSTEM, std::string("connect: ") + strerror(err));
+    }
+    if (Clock::now() > deadline) fail(NZ_ERR_TIMEOUT, "rendezvous timeout connecting to rank " + std::to_string(peer));
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  WireHeader h{seq, c->rank, static_cast<uint32_t>(bytes), static_cast<uint32_t>(fds.size()), 0};
+  std::vector<char> buf(sizeof(h) + bytes);
+  memcpy(buf.data(), &h, sizeof(h));
+  if (bytes) memcpy(buf.data() + sizeof(h), data, bytes);
+  iovec iov{buf.data(), buf.size()};
+  msghdr m{};
+  m.msg_iov = &iov;
+  m.msg_iovlen = 1;
+  alignas(cmsghdr) char cbuf[CMSG_SPACE(sizeof(int) * kMaxFds)];
+  if (!fds.empty()) {
+    m.msg_control = cbuf;
+    m.msg_controllen = CMSG_SPACE(sizeof(int) * fds.size());
+    cmsghdr* cm = CMSG_FIRSTHDR(&m);
+    cm->cmsg_level = SOL_SOCKET;
+    cm->cmsg_type = SCM_RIGHTS;
+    cm->cmsg_len = CMSG_LEN(sizeof(int) * fds.size());
+    memcpy(CMSG_DATA(cm), fds.data(), sizeof(int) * fds.size());
+  }
+  const ssize_t n = sendmsg(s, &m, MSG_NOSIGNAL);
+  close(s);
+  if (n != static_cast<ssize_t>(buf.size())) fail(NZ_ERR_SYSTEM, std::string("sendmsg: ") + strerror(errno));
+}
+
+// Accepts one message into the stash. Returns false on timeout.
+bool receiveOne(nz_comm* c, int wait_ms) {
+  pollfd p{c->listen_fd, POLLIN, 0};
+  const int r = poll(&p, 1, wait_ms);
+  if (r == 0) return false;
+  if (r < 0) fail(NZ_ERR_SYSTEM, std::string("poll: ") + strerror(errno));
+  const int s = accept4(c->listen_fd, nullptr, nullptr, SOCK_CLOEXEC);
+  if (s < 0) fail(NZ_ERR_SYSTEM, std::string("accept: ") + strerror(errno));
+  std::vector<char> buf(sizeof(WireHeader) + kMaxMsg);
+  iovec iov{buf.data(), buf.size()};
+  msghdr m{};
+  m.msg_iov = &iov;
+  m.msg_iovlen = 1;
+  alignas(cmsghdr) char cbuf[CMSG_SPACE(sizeof(int) * kMaxFds)];
+  m.msg_control = cbuf;
+  m.msg_controllen = sizeof(cbuf);
+  const ssize_t n = recvmsg(s, &m, MSG_CMSG_CLOEXEC);
+  close(s);
+  if (n < static_cast<ssize_t>(sizeof(WireHeader))) fail(NZ_ERR_SYSTEM, "short rendezvous message");
+  WireHeader h;
+  memcpy(&h, buf.data(), sizeof(h));
+  if (h.bytes + sizeof(h) != static_cast<size_t>(n)) fail(NZ_ERR_SYSTEM, "truncated rendezvous message");
+  nz_comm::Msg msg;
+  msg.data.assign(buf.data() + sizeof(h), buf.data() + n);
+  for (cmsghdr* cm = CMSG_FIRSTHDR(&m); cm; cm = CMSG_NXTHDR(&m, cm)) {
+    if (cm->cmsg_level == SOL_SOCKET && cm->cmsg_type == SCM_RIGHTS) {
+      const size_t k = (cm->cmsg_len - CMSG_LEN(0)) / sizeof(int);
+      const int* f = reinterpret_cast<const int*>(CMSG_DATA(cm));
+      msg.fds.insert(msg.fds.end(), f, f + k);
+    }
+  }
+  if (msg.fds.size() != h.nfds) fail(NZ_ERR_SYSTEM, "fd count mismatch in rendezvous message");
+  c->stash[{h.seq, h.from}] = std::move(msg);
+  return true;
+}
+}  // namespace
+
+const DriverApi& drv() {
+  static const DriverApi api = [] {
+    DriverApi a;
+    cudaDriverEntryPointQueryResult q;
+#define NZ_DRV_FN(name)                                                                            \
+  if (cudaGetDriverEntryPoint(#name, reinterpret_cast<void**>(&a.name), cudaEnableDefault, &q) != \
+          cudaSuccess ||                                                                           \
+      q != cudaDriverEntryPointSuccess)                                                            \
+    a.name = nullptr;
+#include "driver_fns.inc"
+#undef NZ_DRV_FN
+    return a;
+  }();
+  return api;
+}
+
+void setLastError(const std::string& msg) { g_last_error = msg; }
+const char* lastError() { return g_last_error.c_str(); }
+
+void fail(int code, const std::string& msg) { throw ApiError(code, msg); }
+
+void checkCuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(NZ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void checkCu(CUresult e, const char* what) {
+  if (e != CUDA_SUCCESS) {
+    const char* s = nullptr;
+    if (drv().cuGetErrorString) drv().cuGetErrorString(e, &s);
+    fail(NZ_ERR_CUDA, std::string(what) + ": " + (s ? s : "unknown CUresult"));
+  }
+}
+
+std::vector<nz_comm::Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std::vector<int>& fds) {
+  if (bytes > kMaxMsg) fail(NZ_ERR_INVALID, "exchange payload too large");
+  if (fds.size() > static_cast<size_t>(kMaxFds)) fail(NZ_ERR_INVALID, "too many fds in one exchange");
+  const uint64_t seq = c->xchg_seq++;
+  std::vector<nz_comm::Msg> out(c->world);
+  out[c->rank].data.assign(static_cast<const char*>(data), static_cast<const char*>(data) + bytes);
+  for (int k = 1; k < c->world; ++k) sendTo(c, (c->rank + k) % c->world, seq, data, bytes, fds);
+  const auto deadline = Clock::now() + std::chrono::milliseconds(c->timeout_ms);
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) continue;
+    while (c->stash.find({seq, p}) == c->stash.end()) {
+      const auto left = std::chrono::duration_cast<std::chrono::milliseconds>(deadline - Clock::now()).count();
+      if (left <= 0 || !receiveOne(c, static_cast<int>(std::min<long long>(left, 1000)))) {
+        if (Clock::now() > deadline) fail(NZ_ERR_TIMEOUT, "rendezvous timeout waiting for rank " + std::to_string(p));
+      }
+    }
+    auto it = c->stash.find({seq, p});
+    out[p] = std::move(it->second);
+    c->stash.erase(it);
+  }
+  return out;
+}
+
+}  // namespace nz
+
+using nz::fail;
+using nz::guarded;
+
+extern "C" {
+
+const char* nz_last_error(void) { return nz::lastError(); }
+int nz_abi_version(void) { return NZ_ABI_VERSION; }
+
+int nz_comm_init(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out) {
+  return guarded([&] {
+    if (!out || !session) fail(NZ_ERR_INVALID, "nz_comm_init: null argument");
+    if (world < 1 || world > nz::kMaxRanks) fail(NZ_ERR_INVALID, "world must be in [1, 8]");
+    if (rank < 0 || rank >= world) fail(NZ_ERR_INVALID, "rank out of range");
+    auto* c = new nz_comm();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->session = session;
+    c->timeout_ms = timeout_ms > 0 ? timeout_ms : 60000;
+    try {
+      NZ_CUDA(cudaSetDevice(device));
+      NZ_CUDA(cudaFree(nullptr));  // create the primary context
+      if (!nz::drv().cuMulticastBindMem || !nz::drv().cuMemCreate) fail(NZ_ERR_CUDA, "CUDA driver entry points unavailable");
+      NZ_CU(NZ_DRV(cuInit)(0));
+      CUdevice dev;
+      NZ_CU(NZ_DRV(cuDeviceGet)(&dev, device));
+      int mc = 0;
+      NZ_CU(NZ_DRV(cuDeviceGetAttribute)(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+      NZ_CU(NZ_DRV(cuDeviceGetAttribute)(&c->sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev));
+      if (world > 1) {
+        c->listen_fd = socket(AF_UNIX, SOCK_SEQPACKET | SOCK_CLOEXEC, 0);
+        if (c->listen_fd < 0) fail(NZ_ERR_SYSTEM, std::string("socket: ") + strerror(errno));
+        socklen_t len;
+        sockaddr_un addr = nz::socketName(c->session, rank, &len);
+        if (bind(c->listen_fd, reinterpret_cast<sockaddr*>(&addr), len) != 0) {
+          fail(NZ_ERR_SYSTEM, std::string("bind rendezvous socket: ") + strerror(errno));
+        }
+        if (listen(c->listen_fd, 256) != 0) fail(NZ_ERR_SYSTEM, std::string("listen: ") + strerror(errno));
+        // Every rank must agree on multicast before any buffer is built.
+        const auto all = nz::exchange(c, &mc, sizeof(mc), {});
+        int agreed = 1;
+        for (const auto& m : all) {
+          int v = 0;
+          memcpy(&v, m.data.data(), sizeof(v));
+          agreed &= (v != 0);
+        }
+        c->multicast = agreed && getenv("NEZHA_DISABLE_MULTICAST") == nullptr;
+      }
+      c->ctrl = nz::allocSymmetric(c, nz::kPadBytes * nz::kMaxRails);
+      NZ_CUDA(cudaMemset(c->ctrl->ptrs[rank], 0, c->ctrl->mapped));
+      NZ_CUDA(cudaDeviceSynchronize());
+      nz::exchange(c, nullptr, 0, {});  // pads are zero everywhere before first use
+    } catch (...) {
+      if (c->listen_fd >= 0) close(c->listen_fd);
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int nz_comm_destroy(nz_comm_t* comm) {
+  return guarded([&] {
+    if (!comm) return;
+    cudaSetDevice(comm->device);
+    cudaDeviceSynchronize();
+    if (comm->ctrl) nz::freeSymmetric(comm->ctrl);
+    for (auto& kv : comm->stash)
+      for (int fd : kv.second.fds) close(fd);
+    if (comm->listen_fd >= 0) close(comm->listen_fd);
+    delete comm;
+  });
+}
+
+int nz_comm_rank(const nz_comm_t* c) { return c ? c->rank : NZ_ERR_INVALID; }
+int nz_comm_world(const nz_comm_t* c) { return c ? c->world : NZ_ERR_INVALID; }
+int nz_comm_device(const nz_comm_t* c) { return c ? c->device : NZ_ERR_INVALID; }
+int nz_comm_sm_count(const nz_comm_t* c) { return c ? c->sm_count : NZ_ERR_INVALID; }
+int nz_comm_multicast_supported(const nz_comm_t* c) { return c ? (c->multicast ? 1 : 0) : NZ_ERR_INVALID; }
+
+int nz_comm_barrier(nz_comm_t* comm) {
+  return guarded([&] {
+    if (!comm) fail(NZ_ERR_INVALID, "null comm");
+    if (comm->world > 1) nz::exchange(comm, nullptr, 0, {});
+  });
+}
+
+int nz_comm_allgather(nz_comm_t* comm, const void* mine, size_t bytes, void* all) {
+  return guarded([&] {
+    if (!comm || (!mine && bytes) || (!all && bytes)) fail(NZ_ERR_INVALID, "null argument");
+    if (comm->world == 1) {
+      if (bytes) memcpy(all, mine, bytes);
+      return;
+    }
+    const auto msgs = nz::exchange(comm, mine, bytes, {});
+    for (int r = 0; r < comm->world; ++r) {
+      if (msgs[r].data.size() != bytes) fail(NZ_ERR_INVALID, "allgather size mismatch across ranks");
+      if (bytes) memcpy(static_cast<char*>(all) + size_t(r) * bytes, msgs[r].data.data(), bytes);
+    }
+  });
+}
+
+}  // extern "C"

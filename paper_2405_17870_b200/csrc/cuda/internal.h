@@ -1,0 +1,106 @@
+// Internal definitions shared by the CUDA translation units of libnezha_b200.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "nezha_b200.h"
+
+namespace nz {
+
+constexpr int kMaxRanks = 8;     // one NVSwitch box
+constexpr int kMaxCtas = 1024;   // barrier slots per rail
+constexpr int kThreads = 512;    // CTA size of the data kernels
+constexpr size_t kPadBytes = size_t(kMaxCtas) * kMaxRanks * sizeof(uint32_t);  // per rail
+constexpr int kMaxRails = 16;    // pads carved from the control buffer
+
+// Error plumbing: C++ exceptions inside, codes + thread-local text outside.
+struct ApiError : std::runtime_error {
+  ApiError(int code, const std::string& what) : std::runtime_error(what), code(code) {}
+  int code;
+};
+void setLastError(const std::string& msg);
+[[noreturn]] void fail(int code, const std::string& msg);
+void checkCuda(cudaError_t e, const char* what);
+void checkCu(CUresult e, const char* what);
+
+#define NZ_CUDA(x) ::nz::checkCuda((x), #x)
+#define NZ_CU(x) ::nz::checkCu((x), #x)
+
+// Driver API entry points, resolved through cudaGetDriverEntryPoint so the
+// library itself has no link-time dependency on libcuda (it loads, and its
+// exports can be checked, on a machine without a GPU driver).
+struct DriverApi {
+#define NZ_DRV_FN(name) decltype(&::name) name = nullptr;
+#include "driver_fns.inc"
+#undef NZ_DRV_FN
+};
+const DriverApi& drv();
+#define NZ_DRV(fn) (::nz::drv().fn)
+
+// Runs `fn`, mapping exceptions to ABI codes.
+template <typename F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return NZ_OK;
+  } catch (const ApiError& e) {
+    setLastError(e.what());
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    setLastError(e.what());
+    return NZ_ERR_INVALID;
+  } catch (const std::exception& e) {
+    setLastError(e.what());
+    return NZ_ERR_SYSTEM;
+  }
+}
+
+}  // namespace nz
+
+// Device-visible description of one symmetric buffer.
+struct nz_buf {
+  nz_comm* comm = nullptr;
+  size_t size = 0;        // bytes requested
+  size_t mapped = 0;      // bytes mapped (granularity rounded)
+  CUmemGenericAllocationHandle local = 0;
+  std::vector<CUmemGenericAllocationHandle> imported;  // per rank (0 for self)
+  std::vector<char*> ptrs;                             // per rank VA in this process
+  CUmemGenericAllocationHandle mc = 0;
+  char* mc_ptr = nullptr;
+};
+
+struct nz_comm {
+  int rank = 0;
+  int world = 1;
+  int device = 0;
+  int sm_count = 0;
+  bool multicast = false;
+  int timeout_ms = 60000;
+  std::string session;
+  int listen_fd = -1;
+  uint64_t xchg_seq = 0;
+  // Messages that arrived early, keyed by (exchange sequence, sender).
+  struct Msg {
+    std::vector<char> data;
+    std::vector<int> fds;
+  };
+  std::map<std::pair<uint64_t, int>, Msg> stash;
+  nz_buf* ctrl = nullptr;  // barrier pads, one kPadBytes region per rail
+  int next_pad = 0;
+};
+
+namespace nz {
+// Host-side exchange: every rank contributes (bytes, fds); returns world
+// messages indexed by rank (own message included, fds only from peers).
+std::vector<nz_comm::Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std::vector<int>& fds);
+nz_buf* allocSymmetric(nz_comm* c, size_t bytes);
+void freeSymmetric(nz_buf* b);
+}  // namespace nz

@@ -1,0 +1,426 @@
+// Device side of the three B200 rails (sm_100a).
+//
+//   K1 nvls_kernel   : multimem.ld_reduce over the NVSwitch multicast address
+//                      of `in`, multimem.st of the sum to the multicast address
+//                      of `out` (the "SHARP" rail: reduction inside the switch).
+//   K2 fold_kernel<.., NDST=1> : copy-engine rail's local reduce of staged
+//                      peer shards (the "GLEX/RDMA" rail's SM step).
+//   K3 fold_kernel<.., NDST=N> : SM rail, 128-bit peer loads from every rank,
+//                      in-register fold in ring order, 128-bit peer stores of
+//                      the sum to every rank (the "TCP" rail).
+//
+// Summation order (P1): an element of ring block b of its chunk is
+// folded x_b + x_{b+1} + ... + x_{b-1}. A CTA walks its contiguous share of
+// the shard run by run (a run = one ring block of one chunk), so the
+// rotation is resolved once per run, not per vector; the rare 16-byte vector
+// that straddles a run boundary is folded element by element.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "nezha_b200.h"
+
+namespace nz {
+
+constexpr int kDevMaxRanks = 8;
+
+struct Geometry {
+  uint64_t seg_off;
+  uint64_t seg_len;
+  uint64_t chunk;
+};
+
+// Cross-rank per-CTA barrier pads of one rail: slot [cta][rank] of rank p's
+// pad is written only by `rank`, with monotonically increasing epochs.
+struct BarrierArgs {
+  uint32_t* local;
+  uint32_t* peer[kDevMaxRanks];
+  uint32_t epoch;
+  int* watchdog;  // host-mapped; set when a wait times out
+};
+
+struct FaultPost {
+  nz_fault_record_t* rec;  // host-mapped, nullptr = nothing to post
+  uint32_t op_seq;
+  uint64_t chunk;
+};
+
+struct FoldArgs {
+  const char* src[kDevMaxRanks];  // rank r's element at byte offset x is src[r] + x
+  char* dst[kDevMaxRanks];        // outputs written at byte offset x
+  uint64_t s, e;                  // this rank's shard [s, e)
+  uint64_t range_bytes;           // whole reduced range, sizes the grid identically on every rank
+  Geometry g;
+  BarrierArgs bar;
+  int use_barrier;
+  int rank;
+  FaultPost post;
+};
+
+struct NvlsArgs {
+  char* mc_in;
+  char* mc_out;
+  FoldArgs f;  // unicast view for the unaligned head / tail and the barrier
+};
+
+// ------------------------------------------------------------ primitives --
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+
+// Per-CTA barrier across ranks. Returns false (and flags the watchdog) if a
+// peer never arrived, so the kernel can exit instead of hanging the GPU.
+// `publish` = this CTA wrote peer-visible data that must land before peers
+// pass the barrier (each thread fences its own stores at system scope).
+template <int N, bool kPublish>
+__device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch, int rank) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  if (kPublish) fence_acq_rel_sys();
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < N) {
+    st_release_sys(b.peer[t] + blockIdx.x * kDevMaxRanks + rank, epoch);
+    const uint32_t* slot = b.local + blockIdx.x * kDevMaxRanks + t;
+    uint64_t t0 = 0;
+    int spins = 0;
+    while (static_cast<int32_t>(ld_acquire_sys(slot) - epoch) < 0) {
+      if (++spins == 64) {
+        spins = 0;
+        const uint64_t now = globaltimer();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > kWatchdogNs) {
+          atomicExch_system(b.watchdog, 1);
+          s_ok = 0;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+__device__ __forceinline__ void post_fault(const FaultPost& p) {
+  if (p.rec && blockIdx.x == 0 && threadIdx.x == 0) {
+    volatile nz_fault_record_t* r = p.rec;
+    r->op_seq = p.op_seq;
+    r->chunk = p.chunk;
+    r->t_fail_ns = globaltimer();
+    __threadfence_system();
+    r->valid = 1;
+  }
+}
+
+// ------------------------------------------------------------ dtype folds --
+struct F32 {
+  static constexpr int kElem = 4;
+  using Acc = float4;
+  __device__ static Acc load(uint4 v) { return make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)); }
+  __device__ static void add(Acc& a, uint4 v) {
+    a.x = a.x + __uint_as_float(v.x);
+    a.y = a.y + __uint_as_float(v.y);
+    a.z = a.z + __uint_as_float(v.z);
+    a.w = a.w + __uint_as_float(v.w);
+  }
+  __device__ static uint4 store(const Acc& a) {
+    return make_uint4(__float_as_uint(a.x), __float_as_uint(a.y), __float_as_uint(a.z), __float_as_uint(a.w));
+  }
+  using Scalar = float;
+  __device__ static float sload(const char* p) { return *reinterpret_cast<const float*>(p); }
+  __device__ static void sstore(char* p, float v) { *reinterpret_cast<float*>(p) = v; }
+  __device__ static float sadd(float a, float b) { return a + b; }
+  __device__ static float sfinal(float a) { return a; }
+};
+
+struct BF16 {
+  static constexpr int kElem = 2;
+  struct Acc {
+    float v[8];
+  };
+  __device__ static void unpack(uint32_t w, float& lo, float& hi) {
+    lo = __uint_as_float(w << 16);
+    hi = __uint_as_float(w & 0xffff0000u);
+  }
+  __device__ static Acc load(uint4 v) {
+    Acc a;
+    unpack(v.x, a.v[0], a.v[1]);
+    unpack(v.y, a.v[2], a.v[3]);
+    unpack(v.z, a.v[4], a.v[5]);
+    unpack(v.w, a.v[6], a.v[7]);
+    return a;
+  }
+  __device__ static void add(Acc& a, uint4 v) {
+    Acc b = load(v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a.v[i] = a.v[i] + b.v[i];
+  }
+  __device__ static uint32_t pack(float lo, float hi) {
+    const uint32_t l = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+    const uint32_t h = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+    return l | (h << 16);
+  }
+  __device__ static uint4 store(const Acc& a) {
+    return make_uint4(pack(a.v[0], a.v[1]), pack(a.v[2], a.v[3]), pack(a.v[4], a.v[5]), pack(a.v[6], a.v[7]));
+  }
+  using Scalar = float;
+  __device__ static float sload(const char* p) {
+    return __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const unsigned short*>(p)) << 16);
+  }
+  __device__ static void sstore(char* p, float v) {
+    *reinterpret_cast<unsigned short*>(p) = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  }
+  __device__ static float sadd(float a, float b) { return a + b; }
+};
+
+struct I32 {
+  static constexpr int kElem = 4;
+  using Acc = uint4;
+  __device__ static Acc load(uint4 v) { return v; }
+  __device__ static void add(Acc& a, uint4 v) {
+    a.x += v.x;
+    a.y += v.y;
+    a.z += v.z;
+    a.w += v.w;
+  }
+  __device__ static uint4 store(const Acc& a) { return a; }
+  using Scalar = uint32_t;
+  __device__ static uint32_t sload(const char* p) { return *reinterpret_cast<const uint32_t*>(p); }
+  __device__ static void sstore(char* p, uint32_t v) { *reinterpret_cast<uint32_t*>(p) = v; }
+  __device__ static uint32_t sadd(uint32_t a, uint32_t b) { return a + b; }
+};
+
+// Ring block (fold start rank) of the element at absolute byte offset x,
+// plus the absolute end of that run. Mirrors nezha::ringBlockOf.
+template <int N, int ES>
+__device__ __forceinline__ int block_at(const Geometry& g, uint64_t x, uint64_t* run_end) {
+  const uint64_t rel = x - g.seg_off;
+  const uint64_t c = rel / g.chunk;
+  const uint64_t cbeg = c * g.chunk;
+  const uint64_t rem = g.seg_len - cbeg;
+  const uint64_t clen = rem < g.chunk ? rem : g.chunk;
+  const uint64_t q = (clen / ES) / N;
+  int b;
+  if (q == 0) {
+    b = N - 1;
+  } else {
+    const uint64_t bb = ((rel - cbeg) / ES) / q;
+    b = bb >= static_cast<uint64_t>(N) ? N - 1 : static_cast<int>(bb);
+  }
+  *run_end = g.seg_off + cbeg + (b == N - 1 ? clen : static_cast<uint64_t>(b + 1) * q * ES);
+  return b;
+}
+
+template <typename DT, int N>
+__device__ __forceinline__ void fold_scalar(const FoldArgs& a, int ndst, uint64_t x) {
+  uint64_t run_end;
+  const int b = block_at<N, DT::kElem>(a.g, x, &run_end);
+  typename DT::Scalar acc = DT::sload(a.src[b] + x);
+#pragma unroll
+  for (int j = 1; j < N; ++j) acc = DT::sadd(acc, DT::sload(a.src[(b + j) % N] + x));
+  for (int d = 0; d < ndst; ++d) DT::sstore(a.dst[d] + x, acc);
+}
+
+// Elements of [lo, hi) one per thread of the whole grid.
+template <typename DT, int N>
+__device__ __forceinline__ void fold_scalar_range(const FoldArgs& a, int ndst, uint64_t lo, uint64_t hi) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * DT::kElem;
+  for (uint64_t x = lo + (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * DT::kElem; x < hi; x += stride) {
+    fold_scalar<DT, N>(a, ndst, x);
+  }
+}
+
+template <int N>
+constexpr int unroll_for() {
+  return N <= 2 ? 4 : (N <= 4 ? 2 : 1);
+}
+
+// Vectors of [x0, x1) (16-byte aligned, one run: fold start rank b).
+template <typename DT, int N, int NDST>
+__device__ __forceinline__ void fold_run(const FoldArgs& a, int ndst, int b, uint64_t x0, uint64_t x1) {
+  constexpr int U = unroll_for<N>();
+  const char* src[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) src[j] = a.src[(b + j) % N];
+  const uint64_t step = static_cast<uint64_t>(blockDim.x) * 16;
+  for (uint64_t base = x0 + threadIdx.x * 16ull; base < x1; base += step * U) {
+    uint4 v[U][N];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t x = base + u * step;
+      if (x < x1) {
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[u][j] = ld_v4(src[j] + x);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t x = base + u * step;
+      if (x < x1) {
+        typename DT::Acc acc = DT::load(v[u][0]);
+#pragma unroll
+        for (int j = 1; j < N; ++j) DT::add(acc, v[u][j]);
+        const uint4 out = DT::store(acc);
+        if (NDST == 1) {
+          st_v4(a.dst[0] + x, out);
+        } else {
+#pragma unroll
+          for (int d = 0; d < N; ++d) st_v4(a.dst[d] + x, out);
+        }
+      }
+    }
+  }
+}
+
+// One rank's shard: scalar head/tail + run-walked vector interior.
+template <typename DT, int N, int NDST>
+__device__ __forceinline__ void fold_shard(const FoldArgs& a) {
+  const int ndst = NDST == 1 ? 1 : N;
+  const uint64_t vs = (a.s + 15) & ~15ull;
+  const uint64_t ve = a.e & ~15ull;
+  if (vs >= ve) {
+    fold_scalar_range<DT, N>(a, ndst, a.s, a.e);
+    return;
+  }
+  fold_scalar_range<DT, N>(a, ndst, a.s, vs);
+  fold_scalar_range<DT, N>(a, ndst, ve, a.e);
+  const uint64_t nvec = (ve - vs) / 16;
+  const uint64_t cb = vs + 16 * (nvec * blockIdx.x / gridDim.x);
+  const uint64_t ce = vs + 16 * (nvec * (blockIdx.x + 1) / gridDim.x);
+  uint64_t x = cb;
+  while (x < ce) {
+    uint64_t run_end;
+    const int b = block_at<N, DT::kElem>(a.g, x, &run_end);
+    uint64_t vend = run_end & ~15ull;
+    if (vend > ce) vend = ce;
+    if (vend > x) {
+      fold_run<DT, N, NDST>(a, ndst, b, x, vend);
+      x = vend;
+    } else {
+      // The vector at x crosses a run boundary: fold its elements one by one.
+      if (threadIdx.x < 16 / DT::kElem) fold_scalar<DT, N>(a, ndst, x + threadIdx.x * DT::kElem);
+      x += 16;
+    }
+  }
+}
+
+template <typename DT, int N, int NDST>
+__global__ void __launch_bounds__(512, 2) fold_kernel(const __grid_constant__ FoldArgs a) {
+  if (a.use_barrier && !cta_barrier<N, false>(a.bar, a.bar.epoch, a.rank)) return;
+  fold_shard<DT, N, NDST>(a);
+  if (a.use_barrier && !cta_barrier<N, true>(a.bar, a.bar.epoch + 1, a.rank)) return;
+  post_fault(a.post);
+}
+
+// ------------------------------------------------------------------ NVLS --
+template <typename DT>
+__device__ __forceinline__ uint4 mm_ld_reduce(const char* p);
+
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<F32>(const char* p) {
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<BF16>(const char* p) {
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<I32>(const char* p) {
+  // ptxas rejects .v4 for integer ld_reduce; four scalar accesses instead.
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 4) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 8) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 12) : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void mm_st(char* p, uint4 v) {
+  // The store moves bits; .f32 is the only accepted 16-byte form.
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
+template <typename DT, int N>
+__global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ NvlsArgs a) {
+  if (!cta_barrier<N, false>(a.f.bar, a.f.bar.epoch, a.f.rank)) return;
+  const uint64_t vs = (a.f.s + 15) & ~15ull;
+  const uint64_t ve = a.f.e & ~15ull;
+  if (vs >= ve) {
+    fold_scalar_range<DT, N>(a.f, N, a.f.s, a.f.e);
+  } else {
+    fold_scalar_range<DT, N>(a.f, N, a.f.s, vs);
+    fold_scalar_range<DT, N>(a.f, N, ve, a.f.e);
+    constexpr int U = 4;
+    const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x * 16;
+    for (uint64_t base = vs + (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; base < ve;
+         base += step * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t x = base + u * step;
+        if (x < ve) v[u] = mm_ld_reduce<DT>(a.mc_in + x);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t x = base + u * step;
+        if (x < ve) mm_st(a.mc_out + x, v[u]);
+      }
+    }
+  }
+  if (!cta_barrier<N, true>(a.f.bar, a.f.bar.epoch + 1, a.f.rank)) return;
+  post_fault(a.f.post);
+}
+
+// CE rail: start / end barriers around the DMA phases, and the fault post.
+template <int N>
+__global__ void barrier_kernel(const __grid_constant__ BarrierArgs b, int rank, FaultPost post) {
+  if (!cta_barrier<N, true>(b, b.epoch, rank)) return;
+  post_fault(post);
+}
+
+}  // namespace nz

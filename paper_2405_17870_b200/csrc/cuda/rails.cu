@@ -1,0 +1,412 @@
+// Host side of the three rails: launch configuration, DMA phases of the
+// copy-engine rail, fault records. One nz_rail per (rank, rail); each owns a
+// CUDA stream, which is the B200 form of the reference's "one collective
+// executor per rail".
+#include <algorithm>
+#include <cstring>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+struct nz_rail {
+  nz_comm* comm = nullptr;
+  int kind = 0;
+  int rail_id = 0;
+  int sm_budget = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaStream_t> side;  // CE: one per peer so several copy engines run at once
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> join;
+  uint32_t* pad_local = nullptr;
+  uint32_t* pad_peer[nz::kMaxRanks] = {};
+  uint32_t epoch = 0;
+  nz_fault_record_t* fault_host = nullptr;
+  nz_fault_record_t* fault_dev = nullptr;
+  int* wd_host = nullptr;
+  int* wd_dev = nullptr;
+  char* staging = nullptr;  // CE: (world-1) slots of staging_slot bytes
+  size_t staging_slot = 0;
+};
+
+namespace nz {
+
+namespace {
+
+int elemSize(int dtype) {
+  switch (dtype) {
+    case NZ_F32:
+    case NZ_I32:
+      return 4;
+    case NZ_BF16:
+      return 2;
+  }
+  fail(NZ_ERR_INVALID, "unknown dtype " + std::to_string(dtype));
+}
+
+// Contiguous shard of [lo, hi) owned by `rank`: interior split at 16-byte
+// boundaries, unaligned head to rank 0, tail to rank world-1.
+void shardOf(uint64_t lo, uint64_t hi, int rank, int world, uint64_t* s, uint64_t* e) {
+  const uint64_t A = (lo + 15) & ~15ull, B = hi & ~15ull;
+  if (A >= B) {
+    *s = rank == 0 ? lo : hi;
+    *e = hi;
+    return;
+  }
+  const uint64_t V = (B - A) / 16;
+  *s = rank == 0 ? lo : A + 16 * (V * rank / world);
+  *e = rank == world - 1 ? hi : A + 16 * (V * (rank + 1) / world);
+}
+
+BarrierArgs barrierArgs(nz_rail* r, uint32_t epoch) {
+  BarrierArgs b{};
+  b.local = r->pad_local;
+  for (int p = 0; p < r->comm->world; ++p) b.peer[p] = r->pad_peer[p];
+  b.epoch = epoch;
+  b.watchdog = r->wd_dev;
+  return b;
+}
+
+int gridFor(nz_rail* r, uint64_t range_bytes, int world, int unroll) {
+  const int budget = r->sm_budget > 0 ? std::min(r->sm_budget, r->comm->sm_count) : r->comm->sm_count;
+  const uint64_t per_rank_vec = range_bytes / 16 / static_cast<uint64_t>(world) + 1;
+  const uint64_t per_cta = static_cast<uint64_t>(kThreads) * unroll;
+  const uint64_t g = (per_rank_vec + per_cta - 1) / per_cta;
+  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, std::min(budget, kMaxCtas))));
+}
+
+template <typename DT, int N, int NDST>
+void launchFold(const FoldArgs& a, int grid, cudaStream_t st) {
+  fold_kernel<DT, N, NDST><<<grid, kThreads, 0, st>>>(a);
+}
+
+template <int N, int NDST>
+void dispatchFoldDT(int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
+  switch (dtype) {
+    case NZ_F32: return launchFold<F32, N, NDST>(a, grid, st);
+    case NZ_BF16: return launchFold<BF16, N, NDST>(a, grid, st);
+    case NZ_I32: return launchFold<I32, N, NDST>(a, grid, st);
+  }
+}
+
+template <int NDST_IS_N>
+void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
+  switch (world) {
+#define NZ_CASE(n) \
+  case n: return dispatchFoldDT<n, NDST_IS_N ? n : 1>(dtype, a, grid, st);
+    NZ_CASE(1) NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
+#undef NZ_CASE
+  }
+}
+
+void dispatchNvls(int world, int dtype, const NvlsArgs& a, int grid, cudaStream_t st) {
+  switch (world) {
+#define NZ_CASE(n)                                                                          \
+  case n:                                                                                   \
+    if (dtype == NZ_F32) return (void)(nvls_kernel<F32, n><<<grid, kThreads, 0, st>>>(a));  \
+    if (dtype == NZ_BF16) return (void)(nvls_kernel<BF16, n><<<grid, kThreads, 0, st>>>(a)); \
+    return (void)(nvls_kernel<I32, n><<<grid, kThreads, 0, st>>>(a));
+    NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
+#undef NZ_CASE
+  }
+}
+
+void launchBarrier(nz_rail* r, uint32_t epoch, FaultPost post, cudaStream_t st) {
+  const BarrierArgs b = barrierArgs(r, epoch);
+  switch (r->comm->world) {
+#define NZ_CASE(n) \
+  case n: barrier_kernel<n><<<1, 32, 0, st>>>(b, r->comm->rank, post); break;
+    NZ_CASE(1) NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
+#undef NZ_CASE
+  }
+}
+
+void ensureStaging(nz_rail* r, size_t slot) {
+  if (slot <= r->staging_slot) return;
+  if (r->staging) NZ_CUDA(cudaFree(r->staging));
+  r->staging = nullptr;
+  const size_t want = (slot + (1u << 20)) & ~((size_t(1) << 20) - 1);
+  NZ_CUDA(cudaMalloc(&r->staging, want * std::max(1, r->comm->world - 1)));
+  r->staging_slot = want;
+}
+
+// One rail op over [lo, hi) with order geometry g. `post` is posted after.
+void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const Geometry& g, int dtype, FaultPost post,
+            cudaStream_t st) {
+  nz_comm* c = r->comm;
+  const int N = c->world;
+  const int me = c->rank;
+  uint64_t s, e;
+  shardOf(lo, hi, me, N, &s, &e);
+  const uint32_t epoch = r->epoch + 1;
+  r->epoch += 2;  // start + end barrier; identical on every rank
+
+  if (N == 1 || r->kind == NZ_RAIL_SM) {
+    FoldArgs a{};
+    for (int p = 0; p < N; ++p) {
+      a.src[p] = in->ptrs[p];
+      a.dst[p] = out->ptrs[p];
+    }
+    a.s = N == 1 ? lo : s;
+    a.e = N == 1 ? hi : e;
+    a.range_bytes = hi - lo;
+    a.g = g;
+    a.bar = barrierArgs(r, epoch);
+    a.use_barrier = N > 1;
+    a.rank = me;
+    a.post = post;
+    const int grid = gridFor(r, hi - lo, N, 2);
+    dispatchFold<1>(N, dtype, a, grid, st);
+    NZ_CUDA(cudaGetLastError());
+    return;
+  }
+
+  if (r->kind == NZ_RAIL_NVLS) {
+    if (!in->mc_ptr || !out->mc_ptr) fail(NZ_ERR_UNSUPPORTED, "NVLS rail needs multicast-bound buffers");
+    NvlsArgs a{};
+    a.mc_in = in->mc_ptr;
+    a.mc_out = out->mc_ptr;
+    for (int p = 0; p < N; ++p) {
+      a.f.src[p] = in->ptrs[p];
+      a.f.dst[p] = out->ptrs[p];
+    }
+    a.f.s = s;
+    a.f.e = e;
+    a.f.range_bytes = hi - lo;
+    a.f.g = g;
+    a.f.bar = barrierArgs(r, epoch);
+    a.f.use_barrier = 1;
+    a.f.rank = me;
+    a.f.post = post;
+    const int grid = gridFor(r, hi - lo, N, 4);
+    dispatchNvls(N, dtype, a, grid, st);
+    NZ_CUDA(cudaGetLastError());
+    return;
+  }
+
+  // Copy-engine rail: barrier, DMA gather of my shard from every peer,
+  // local ring-order reduce, DMA scatter of the sum, barrier.
+  const uint64_t len = e - s;
+  // Staged copies keep the 16-byte phase of the source so the reduce kernel's
+  // vector loads stay aligned: copy from s16 = align_down(s, 16).
+  const uint64_t s16 = s & ~15ull;
+  const uint64_t slen = e - s16;
+  ensureStaging(r, slen);
+  launchBarrier(r, epoch, FaultPost{}, st);
+  if (len > 0) {
+    NZ_CUDA(cudaEventRecord(r->fork, st));
+    for (int j = 1; j < N; ++j) {
+      const int p = (me + j) % N;
+      cudaStream_t ss = r->side[j - 1];
+      NZ_CUDA(cudaStreamWaitEvent(ss, r->fork, 0));
+      NZ_CUDA(cudaMemcpyAsync(r->staging + (j - 1) * r->staging_slot, in->ptrs[p] + s16, slen, cudaMemcpyDeviceToDevice, ss));
+      NZ_CUDA(cudaEventRecord(r->join[j - 1], ss));
+      NZ_CUDA(cudaStreamWaitEvent(st, r->join[j - 1], 0));
+    }
+    FoldArgs a{};
+    for (int p = 0; p < N; ++p) {
+      const int j = (p - me + N) % N;
+      a.src[p] = j == 0 ? in->ptrs[me] : r->staging + (j - 1) * r->staging_slot - s16;
+    }
+    a.dst[0] = out->ptrs[me];
+    a.s = s;
+    a.e = e;
+    a.range_bytes = hi - lo;
+    a.g = g;
+    a.use_barrier = 0;
+    a.rank = me;
+    const int grid = gridFor(r, hi - lo, N, 2);
+    dispatchFold<0>(N, dtype, a, grid, st);
+    NZ_CUDA(cudaGetLastError());
+    NZ_CUDA(cudaEventRecord(r->fork, st));
+    for (int j = 1; j < N; ++j) {
+      const int p = (me + j) % N;
+      cudaStream_t ss = r->side[j - 1];
+      NZ_CUDA(cudaStreamWaitEvent(ss, r->fork, 0));
+      NZ_CUDA(cudaMemcpyAsync(out->ptrs[p] + s, out->ptrs[me] + s, len, cudaMemcpyDeviceToDevice, ss));
+      NZ_CUDA(cudaEventRecord(r->join[j - 1], ss));
+      NZ_CUDA(cudaStreamWaitEvent(st, r->join[j - 1], 0));
+    }
+  }
+  launchBarrier(r, epoch + 1, post, st);
+  NZ_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+// Used by the engine (engine.cpp) without going through the C ABI.
+void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes,
+                   uint64_t chunk_begin, uint64_t chunk_end, int dtype, uint32_t op_seq, int64_t fail_chunk,
+                   cudaStream_t st) {
+  const int es = elemSize(dtype);
+  if (chunk_bytes == 0 || chunk_bytes % es || seg_off % es || seg_len % es) {
+    fail(NZ_ERR_INVALID, "segment geometry not element aligned");
+  }
+  if (in->comm != r->comm || out->comm != r->comm) fail(NZ_ERR_INVALID, "buffer from another comm");
+  if (seg_off + seg_len > in->size || seg_off + seg_len > out->size) fail(NZ_ERR_INVALID, "segment exceeds buffer");
+  const uint64_t nch = (seg_len + chunk_bytes - 1) / chunk_bytes;
+  chunk_end = std::min(chunk_end, nch);
+  if (chunk_begin > chunk_end) fail(NZ_ERR_INVALID, "chunk_begin > chunk_end");
+  uint64_t stop = chunk_end;
+  FaultPost post{};
+  if (fail_chunk >= 0 && static_cast<uint64_t>(fail_chunk) >= chunk_begin && static_cast<uint64_t>(fail_chunk) < chunk_end) {
+    stop = static_cast<uint64_t>(fail_chunk);
+    post.rec = r->fault_dev;
+    post.op_seq = op_seq;
+    post.chunk = stop;
+  }
+  const uint64_t lo = seg_off + std::min(seg_len, chunk_begin * chunk_bytes);
+  const uint64_t hi = seg_off + std::min(seg_len, stop * chunk_bytes);
+  if (!st) st = r->stream;
+  NZ_CUDA(cudaSetDevice(r->comm->device));
+  if (hi > lo) {
+    railOp(r, in, out, lo, hi, Geometry{seg_off, seg_len, chunk_bytes}, dtype, post, st);
+  } else if (post.rec) {
+    launchBarrier(r, r->epoch + 1, post, st);
+    r->epoch += 2;
+  }
+}
+
+}  // namespace nz
+
+using nz::fail;
+using nz::guarded;
+
+extern "C" {
+
+int nz_has_cuda_kernels(void) { return 1; }
+
+int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rail_t** out) {
+  return guarded([&] {
+    if (!comm || !out) fail(NZ_ERR_INVALID, "null argument");
+    if (kind < NZ_RAIL_NVLS || kind > NZ_RAIL_SM) fail(NZ_ERR_INVALID, "unknown rail kind");
+    if (kind == NZ_RAIL_NVLS && comm->world > 1 && !comm->multicast) {
+      fail(NZ_ERR_UNSUPPORTED, "NVLS rail requires NVSwitch multicast support");
+    }
+    if (comm->next_pad >= nz::kMaxRails) fail(NZ_ERR_INVALID, "too many rails on one comm");
+    NZ_CUDA(cudaSetDevice(comm->device));
+    auto* r = new nz_rail();
+    r->comm = comm;
+    r->kind = kind;
+    r->rail_id = rail_id;
+    r->sm_budget = sm_budget;
+    const size_t pad_off = nz::kPadBytes * comm->next_pad++;
+    r->pad_local = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[comm->rank] + pad_off);
+    for (int p = 0; p < comm->world; ++p) r->pad_peer[p] = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[p] + pad_off);
+    NZ_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+    NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
+    if (kind == NZ_RAIL_CE) {
+      for (int j = 1; j < comm->world; ++j) {
+        cudaStream_t s;
+        cudaEvent_t e;
+        NZ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        NZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        r->side.push_back(s);
+        r->join.push_back(e);
+      }
+    }
+    NZ_CUDA(cudaHostAlloc(&r->fault_host, sizeof(nz_fault_record_t), cudaHostAllocMapped));
+    memset(r->fault_host, 0, sizeof(nz_fault_record_t));
+    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->fault_dev), r->fault_host, 0));
+    NZ_CUDA(cudaHostAlloc(&r->wd_host, sizeof(int), cudaHostAllocMapped));
+    *r->wd_host = 0;
+    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->wd_dev), r->wd_host, 0));
+    *out = r;
+  });
+}
+
+int nz_rail_destroy(nz_rail_t* r) {
+  return guarded([&] {
+    if (!r) return;
+    cudaSetDevice(r->comm->device);
+    cudaStreamSynchronize(r->stream);
+    for (auto s : r->side) cudaStreamDestroy(s);
+    for (auto e : r->join) cudaEventDestroy(e);
+    if (r->fork) cudaEventDestroy(r->fork);
+    if (r->stream) cudaStreamDestroy(r->stream);
+    if (r->staging) cudaFree(r->staging);
+    if (r->fault_host) cudaFreeHost(r->fault_host);
+    if (r->wd_host) cudaFreeHost(r->wd_host);
+    delete r;
+  });
+}
+
+int nz_rail_kind(const nz_rail_t* r) { return r ? r->kind : NZ_ERR_INVALID; }
+
+int nz_rail_synchronize(nz_rail_t* r) {
+  return guarded([&] {
+    if (!r) fail(NZ_ERR_INVALID, "null rail");
+    NZ_CUDA(cudaSetDevice(r->comm->device));
+    for (auto s : r->side) NZ_CUDA(cudaStreamSynchronize(s));
+    NZ_CUDA(cudaStreamSynchronize(r->stream));
+  });
+}
+void* nz_rail_stream(const nz_rail_t* r) { return r ? static_cast<void*>(r->stream) : nullptr; }
+
+int nz_rail_allreduce(nz_rail_t* rail, nz_buf_t* in, nz_buf_t* out, uint64_t seg_off, uint64_t seg_len,
+                      uint64_t chunk_bytes, uint64_t chunk_begin, uint64_t chunk_end, int dtype, uint32_t op_seq,
+                      int64_t fail_chunk, void* stream) {
+  return guarded([&] {
+    if (!rail || !in || !out) fail(NZ_ERR_INVALID, "null argument");
+    nz::railAllreduce(rail, in, out, seg_off, seg_len, chunk_bytes, chunk_begin, chunk_end, dtype, op_seq, fail_chunk,
+                      static_cast<cudaStream_t>(stream));
+  });
+}
+
+int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
+                    uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
+                    void* stream) {
+  return guarded([&] {
+    if (world < 1 || world > nz::kMaxRanks || rank < 0 || rank >= world) fail(NZ_ERR_INVALID, "bad world/rank");
+    if (!src || !dst || (ndst != 1 && ndst != world)) fail(NZ_ERR_INVALID, "bad src/dst");
+    const int es = nz::elemSize(dtype);
+    if (chunk_bytes == 0 || chunk_bytes % es || seg_off % es || seg_len % es || lo % es || hi % es || lo > hi ||
+        lo < seg_off || hi > seg_off + seg_len) {
+      fail(NZ_ERR_INVALID, "bad geometry");
+    }
+    nz::FoldArgs a{};
+    for (int p = 0; p < world; ++p) a.src[p] = static_cast<const char*>(src[p]);
+    for (int d = 0; d < ndst; ++d) a.dst[d] = static_cast<char*>(dst[d]);
+    nz::shardOf(lo, hi, rank, world, &a.s, &a.e);
+    a.range_bytes = hi - lo;
+    a.g = nz::Geometry{seg_off, seg_len, chunk_bytes};
+    a.use_barrier = 0;
+    a.rank = rank;
+    int dev = 0, sms = 0;
+    NZ_CUDA(cudaGetDevice(&dev));
+    NZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (grid <= 0) {
+      const uint64_t per_rank_vec = (hi - lo) / 16 / world + 1;
+      grid = static_cast<int>(std::min<uint64_t>(sms, (per_rank_vec + 2 * nz::kThreads - 1) / (2 * nz::kThreads)));
+      grid = std::max(grid, 1);
+    }
+    if (ndst == 1)
+      nz::dispatchFold<0>(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
+    else
+      nz::dispatchFold<1>(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
+    NZ_CUDA(cudaGetLastError());
+  });
+}
+
+int nz_rail_poll_fault(nz_rail_t* r, nz_fault_record_t* rec, int consume) {
+  return guarded([&] {
+    if (!r || !rec) fail(NZ_ERR_INVALID, "null argument");
+    volatile nz_fault_record_t* f = r->fault_host;
+    rec->valid = f->valid;
+    if (!rec->valid) return;
+    __sync_synchronize();
+    rec->op_seq = f->op_seq;
+    rec->chunk = f->chunk;
+    rec->t_fail_ns = f->t_fail_ns;
+    if (consume) f->valid = 0;
+  });
+}
+
+int nz_rail_watchdog(nz_rail_t* r) {
+  if (!r) return NZ_ERR_INVALID;
+  volatile int* w = r->wd_host;
+  const int v = *w;
+  *w = 0;
+  return v;
+}
+
+}  // extern "C"

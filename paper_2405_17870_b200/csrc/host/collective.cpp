@@ -1,0 +1,40 @@
+// Collective geometry helpers (P1, P10).
+#include "nezha/collective.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace nezha {
+
+Segment ChunkGeometry::chunk(Bytes c) const {
+  const Bytes begin = c * chunk_bytes;
+  if (begin >= seg_length) throw std::invalid_argument("chunk index out of range");
+  const Bytes len = std::min(chunk_bytes, seg_length - begin);
+  return Segment{seg_offset + begin, len};
+}
+
+Bytes defaultChunkBytes(Bytes segment_length, int world, Algorithm algo) {
+  if (world < 1) throw std::invalid_argument("defaultChunkBytes: world must be >= 1");
+  if (algo == Algorithm::Ring) return std::max<Bytes>(segment_length, 4);
+  constexpr Bytes kFloor = 64 * 1024;
+  const Bytes even = (segment_length / (2 * static_cast<Bytes>(world))) & ~Bytes{3};
+  return std::max(kFloor, even);
+}
+
+ChunkGeometry makeGeometry(const Segment& seg, int world, Algorithm algo) {
+  return ChunkGeometry{seg.offset, seg.length, defaultChunkBytes(seg.length, world, algo)};
+}
+
+std::vector<Segment> splitOversized(Bytes payload) {
+  if (payload == 0) throw std::invalid_argument("splitOversized: payload must be positive");
+  constexpr Bytes kLimit = Bytes{1} << 30;
+  constexpr Bytes kPiece = Bytes{256} << 20;
+  if (payload <= kLimit) return {Segment{0, payload}};
+  std::vector<Segment> out;
+  for (Bytes off = 0; off < payload; off += kPiece) {
+    out.push_back(Segment{off, std::min(kPiece, payload - off)});
+  }
+  return out;
+}
+
+}  // namespace nezha

@@ -1,0 +1,251 @@
+"""Python mirror of the C ABI objects: Comm, SymmetricBuffer, Rail, Engine.
+
+Thin wrappers: every operation is a call into libnezha_b200.so. Device memory
+is the library's own symmetric VMM allocation (the UnboundBuffer); torch is
+only used by callers for streams and host tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from ctypes import byref, c_void_p
+
+from . import _lib
+from ._lib import check, lib
+
+
+def _ptr(x) -> int | None:
+    """Accepts an int address, a ctypes pointer, a numpy array or a torch tensor."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):
+        return x.ctypes.data
+    return ctypes.cast(x, c_void_p).value
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream  # torch.cuda.Stream
+
+
+class Comm:
+    """One rank of the job (nz_comm_init). Replaces rendezvous() (transport.hpp:219-238)."""
+
+    def __init__(self, rank: int, world: int, device: int, session: str, timeout_ms: int = 120000):
+        h = c_void_p()
+        check(lib().nz_comm_init(rank, world, device, session.encode(), timeout_ms, byref(h)), "nz_comm_init")
+        self.handle = h
+        self.rank, self.world, self.device = rank, world, device
+
+    @classmethod
+    def from_env(cls, session: str | None = None, timeout_ms: int = 120000) -> "Comm":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        local = int(os.environ.get("LOCAL_RANK", str(rank)))
+        if session is None:
+            session = f"{os.environ.get('MASTER_PORT', '0')}-{os.environ.get('TORCHELASTIC_RUN_ID', 'nz')}"
+        return cls(rank, world, local, session, timeout_ms)
+
+    @property
+    def multicast(self) -> bool:
+        return lib().nz_comm_multicast_supported(self.handle) == 1
+
+    @property
+    def sm_count(self) -> int:
+        return lib().nz_comm_sm_count(self.handle)
+
+    def barrier(self) -> None:
+        check(lib().nz_comm_barrier(self.handle), "nz_comm_barrier")
+
+    def allgather_bytes(self, data: bytes) -> list[bytes]:
+        n = len(data)
+        out = ctypes.create_string_buffer(n * self.world)
+        check(lib().nz_comm_allgather(self.handle, data, n, out), "nz_comm_allgather")
+        raw = out.raw
+        return [raw[i * n:(i + 1) * n] for i in range(self.world)]
+
+    def close(self) -> None:
+        if self.handle:
+            check(lib().nz_comm_destroy(self.handle), "nz_comm_destroy")
+            self.handle = None
+
+
+class SymmetricBuffer:
+    """nz_buffer_alloc: the UnboundBuffer."""
+
+    def __init__(self, comm: Comm, nbytes: int):
+        h = c_void_p()
+        check(lib().nz_buffer_alloc(comm.handle, nbytes, byref(h)), "nz_buffer_alloc")
+        self.handle = h
+        self.comm = comm
+        self.nbytes = nbytes
+
+    @property
+    def ptr(self) -> int:
+        return lib().nz_buffer_ptr(self.handle)
+
+    @property
+    def mc_ptr(self) -> int | None:
+        return lib().nz_buffer_mc_ptr(self.handle)
+
+    def write(self, src, nbytes: int, offset: int = 0, stream=None) -> None:
+        check(lib().nz_buffer_write(self.handle, offset, _ptr(src), nbytes, _stream(stream)), "nz_buffer_write")
+
+    def read(self, dst, nbytes: int, offset: int = 0, stream=None) -> None:
+        check(lib().nz_buffer_read(self.handle, offset, _ptr(dst), nbytes, _stream(stream)), "nz_buffer_read")
+
+    def zero(self, stream=None) -> None:
+        check(lib().nz_buffer_fill_zero(self.handle, _stream(stream)), "nz_buffer_fill_zero")
+
+    def free(self) -> None:
+        if self.handle:
+            check(lib().nz_buffer_free(self.handle), "nz_buffer_free")
+            self.handle = None
+
+
+class Rail:
+    """One rail's executor on this rank (nz_rail_create)."""
+
+    def __init__(self, comm: Comm, kind: int, rail_id: int, sm_budget: int = 0):
+        h = c_void_p()
+        check(lib().nz_rail_create(comm.handle, kind, rail_id, sm_budget, byref(h)), "nz_rail_create")
+        self.handle = h
+        self.kind = kind
+        self.rail_id = rail_id
+
+    @property
+    def stream(self) -> int:
+        return lib().nz_rail_stream(self.handle)
+
+    def allreduce(self, inp: SymmetricBuffer, out: SymmetricBuffer, seg_off: int, seg_len: int, chunk_bytes: int,
+                  dtype: int, op_seq: int = 0, chunk_begin: int = 0, chunk_end: int = 1 << 62,
+                  fail_chunk: int = -1, stream=None) -> None:
+        check(lib().nz_rail_allreduce(self.handle, inp.handle, out.handle, seg_off, seg_len, chunk_bytes, chunk_begin,
+                                      chunk_end, dtype, op_seq, fail_chunk, _stream(stream)), "nz_rail_allreduce")
+
+    def synchronize(self) -> None:
+        check(lib().nz_rail_synchronize(self.handle), "nz_rail_synchronize")
+
+    def poll_fault(self, consume: bool = True) -> _lib.FaultRecord | None:
+        rec = _lib.FaultRecord()
+        check(lib().nz_rail_poll_fault(self.handle, byref(rec), 1 if consume else 0), "nz_rail_poll_fault")
+        return rec if rec.valid else None
+
+    def watchdog(self) -> int:
+        return lib().nz_rail_watchdog(self.handle)
+
+    def close(self) -> None:
+        if self.handle:
+            check(lib().nz_rail_destroy(self.handle), "nz_rail_destroy")
+            self.handle = None
+
+
+def default_engine_config() -> _lib.EngineConfig:
+    cfg = _lib.EngineConfig()
+    lib().nz_engine_config_default(byref(cfg))
+    return cfg
+
+
+class Engine:
+    """Multi-rail allreduce engine (nz_engine_*): planner + rails + monitor."""
+
+    def __init__(self, comm: Comm, cfg: _lib.EngineConfig | None = None, **overrides):
+        cfg = cfg or default_engine_config()
+        for k, v in overrides.items():
+            if k == "kinds":
+                cfg.num_rails = len(v)
+                for i, kind in enumerate(v):
+                    cfg.kinds[i] = _lib.RAIL_KINDS[kind] if isinstance(kind, str) else kind
+            elif k == "sm_budget":
+                for i, b in enumerate(v):
+                    cfg.sm_budget[i] = b
+            elif k == "rails_toml":
+                self._toml = v.encode() if isinstance(v, str) else v
+                cfg.rails_toml = self._toml
+            else:
+                setattr(cfg, k, v)
+        h = c_void_p()
+        check(lib().nz_engine_create(comm.handle, byref(cfg), byref(h)), "nz_engine_create")
+        self.handle = h
+        self.comm = comm
+
+    def allreduce(self, inp: SymmetricBuffer, out: SymmetricBuffer, nbytes: int, dtype: int, stream=None) -> None:
+        check(lib().nz_engine_allreduce(self.handle, inp.handle, out.handle, nbytes, dtype, _stream(stream)),
+              "nz_engine_allreduce")
+
+    def allreduce_host(self, host_in, host_out, nbytes: int, dtype: int) -> None:
+        check(lib().nz_engine_allreduce_host(self.handle, _ptr(host_in), _ptr(host_out), nbytes, dtype),
+              "nz_engine_allreduce_host")
+
+    def inject_failure(self, op_seq: int, rail_id: int, chunk: int) -> None:
+        check(lib().nz_engine_inject_failure(self.handle, op_seq, rail_id, chunk), "nz_engine_inject_failure")
+
+    def readmit(self, rail_id: int) -> None:
+        check(lib().nz_engine_readmit(self.handle, rail_id), "nz_engine_readmit")
+
+    def synchronize(self) -> None:
+        check(lib().nz_engine_synchronize(self.handle), "nz_engine_synchronize")
+
+    @property
+    def op_seq(self) -> int:
+        return lib().nz_engine_op_seq(self.handle)
+
+    def last_failover(self) -> dict | None:
+        rep = _lib.FailoverReport()
+        rc = lib().nz_engine_last_failover(self.handle, byref(rep))
+        if rc == _lib.NZ_ERR_INVALID:
+            return None
+        check(rc, "nz_engine_last_failover")
+        return {f: getattr(rep, f) for f, _ in rep._fields_}
+
+    def _json(self, fn, *args) -> dict:
+        cap = 1 << 16
+        while True:
+            buf = ctypes.create_string_buffer(cap)
+            rc = fn(self.handle, *args, buf, cap)
+            if rc == _lib.NZ_ERR_BUFFER:
+                cap *= 4
+                continue
+            check(rc)
+            return json.loads(buf.value.decode())
+
+    def state(self) -> dict:
+        return self._json(lib().nz_engine_state_json)
+
+    def plan(self, nbytes: int) -> dict:
+        return self._json(lib().nz_engine_plan_json, nbytes)
+
+    def close(self) -> None:
+        if self.handle:
+            check(lib().nz_engine_destroy(self.handle), "nz_engine_destroy")
+            self.handle = None
+
+
+def run_trace(scenario: str) -> str:
+    """Planner decisions for a scenario (nz_planner_run_trace), CPU only."""
+    cap = 1 << 20
+    while True:
+        buf = ctypes.create_string_buffer(cap)
+        rc = lib().nz_planner_run_trace(scenario.encode(), buf, cap)
+        if rc == _lib.NZ_ERR_BUFFER:
+            cap *= 8
+            continue
+        check(rc, "nz_planner_run_trace")
+        return buf.value.decode()
+
+
+def emulate_fold(world: int, rank: int, dtype: int, srcs: list[int], dsts: list[int], seg_off: int, seg_len: int,
+                 chunk_bytes: int, lo: int, hi: int, grid: int = 0, stream=None) -> None:
+    """Single-GPU emulation of one rank of the SM / CE rail kernels (nz_emulate_fold)."""
+    s = (c_void_p * len(srcs))(*srcs)
+    d = (c_void_p * len(dsts))(*dsts)
+    check(lib().nz_emulate_fold(world, rank, dtype, s, d, len(dsts), seg_off, seg_len, chunk_bytes, lo, hi, grid,
+                                _stream(stream)), "nz_emulate_fold")

@@ -1,0 +1,146 @@
+"""GPU parity of the three rails against the CPU oracle (P1/P2).
+
+Single-GPU: the SM-rail and CE-reduce kernels are run for every virtual rank
+of an N-rank job with all ranks' buffers on cuda:0 (nz_emulate_fold), so the
+exact production kernels are checked for N = 2..8 on one B200.
+Multi-GPU (>= 2 GPUs in the box): real ranks, one process per GPU, through
+the C ABI (nz_comm_init / nz_buffer_alloc / nz_rail_allreduce).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.conftest import gpu_count
+from tests.mp_util import spawn
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def shard_of(lo, hi, rank, world):
+    """Mirror of nz::shardOf (rails.cu): 16-byte interior split, head to 0, tail to N-1."""
+    A, B = (lo + 15) & ~15, hi & ~15
+    if A >= B:
+        return (lo if rank == 0 else hi), hi
+    V = (B - A) // 16
+    s = lo if rank == 0 else A + 16 * (V * rank // world)
+    e = hi if rank == world - 1 else A + 16 * (V * (rank + 1) // world)
+    return s, e
+
+
+def _bits(a):
+    return a.view(np.uint16) if a.dtype == np.uint16 else a.view(np.uint32)
+
+
+EMU_CASES = [
+    # (world, dtype, nbytes, seg_off, seg_len, chunked)
+    (2, oracle.F32, 1 << 20, 0, 1 << 20, True),
+    (3, oracle.F32, 300_004, 8, 299_988, True),
+    (4, oracle.F32, 4 << 20, 0, 4 << 20, True),
+    (4, oracle.F32, 4 << 20, 0, 4 << 20, False),
+    (4, oracle.BF16, 2_000_006, 2, 1_999_998, True),
+    (4, oracle.I32, 1_048_592, 16, 1_048_560, True),
+    (5, oracle.F32, 777_780, 20, 777_740, True),
+    (8, oracle.F32, 16 << 20, 0, 16 << 20, True),
+    (8, oracle.BF16, 8 << 20, 0, 8 << 20, True),
+    (8, oracle.I32, 1 << 16, 0, 1 << 16, True),
+    (8, oracle.F32, 12, 0, 12, True),          # fewer elements than ranks
+    (7, oracle.F32, 4100, 4, 4092, True),
+    (6, oracle.BF16, 130, 2, 126, False),
+]
+
+
+@pytest.mark.parametrize("world,dtype,nbytes,seg_off,seg_len,chunked", EMU_CASES)
+@pytest.mark.parametrize("mode", ["sm", "ce"])
+def test_emulated_rail_fold_bit_exact(world, dtype, nbytes, seg_off, seg_len, chunked, mode):
+    torch = pytest.importorskip("torch")
+    if gpu_count() < 1:
+        pytest.skip("no GPU")
+    from paper_2405_17870_b200 import emulate_fold
+
+    torch.cuda.set_device(0)
+    es = 2 if dtype == oracle.BF16 else 4
+    inputs = [oracle.synthetic_input(dtype, r, nbytes, seed_base=oracle.SEED_BASE + world * 1000 + nbytes % 997)
+              for r in range(world)]
+    dins = [torch.from_numpy(x.view(np.uint8).copy()).cuda() for x in inputs]
+    douts = [torch.zeros(nbytes, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    chunk = oracle.default_chunk_bytes(seg_len, world, chunked)
+    lo, hi = seg_off, seg_off + seg_len
+    for r in range(world):
+        dst = [d.data_ptr() for d in douts] if mode == "sm" else [douts[r].data_ptr()]
+        emulate_fold(world, r, dtype, [d.data_ptr() for d in dins], dst, seg_off, seg_len, chunk, lo, hi)
+    torch.cuda.synchronize()
+    want = oracle.reduce_range(inputs, dtype, seg_off, seg_len, chunk, lo, hi)
+    for r in range(world):
+        got = douts[r].cpu().numpy().view(want.dtype)
+        if mode == "sm":
+            np.testing.assert_array_equal(_bits(got), _bits(want), err_msg=f"rank {r}")
+        else:
+            s, e = shard_of(lo, hi, r, world)
+            np.testing.assert_array_equal(_bits(got[s // es:e // es]), _bits(want[s // es:e // es]),
+                                          err_msg=f"rank {r} shard")
+
+
+def test_order_revealing_golden_vector():
+    """P1 golden: ranks hold {1e8, 1, -1e8, 1}; block b's fold starts at rank b."""
+    torch = pytest.importorskip("torch")
+    if gpu_count() < 1:
+        pytest.skip("no GPU")
+    from paper_2405_17870_b200 import emulate_fold
+
+    world, n = 4, 4 * 1024  # one chunk of 16 KiB: 4 blocks of 1024 elements
+    vals = [1e8, 1.0, -1e8, 1.0]
+    inputs = [np.full(n, v, dtype=np.float32) for v in vals]
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "order_vector.json")))
+    dins = [torch.from_numpy(x.view(np.uint8).copy()).cuda() for x in inputs]
+    douts = [torch.zeros(n * 4, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    chunk = 65536
+    for r in range(world):
+        emulate_fold(world, r, oracle.F32, [d.data_ptr() for d in dins], [d.data_ptr() for d in douts], 0, n * 4,
+                     chunk, 0, n * 4)
+    torch.cuda.synchronize()
+    got = douts[0].cpu().numpy().view(np.float32)
+    per_block = [float(got[b * 1024]) for b in range(4)]
+    assert per_block == golden["block_results"]
+
+
+MULTI = [
+    {"kind": "sm", "dtype": "f32", "nbytes": 1 << 20},
+    {"kind": "sm", "dtype": "bf16", "nbytes": 3_000_002, "seg_off": 2, "seg_len": 2_999_998},
+    {"kind": "sm", "dtype": "i32", "nbytes": 65_540},
+    {"kind": "ce", "dtype": "f32", "nbytes": 8 << 20},
+    {"kind": "ce", "dtype": "bf16", "nbytes": 1_000_010, "seg_off": 6, "seg_len": 1_000_000},
+    {"kind": "ce", "dtype": "i32", "nbytes": 4096},
+    {"kind": "nvls", "dtype": "f32", "nbytes": 8 << 20},
+    {"kind": "nvls", "dtype": "bf16", "nbytes": 2_000_002},
+    {"kind": "nvls", "dtype": "i32", "nbytes": 1_048_580, "seg_off": 4, "seg_len": 1_048_576},
+    {"kind": "sm", "dtype": "f32", "nbytes": 8192},
+    {"kind": "nvls", "dtype": "f32", "nbytes": 8192},
+    {"kind": "sm", "dtype": "f32", "nbytes": 64 << 20, "fail_chunk": 2},
+    {"kind": "ce", "dtype": "bf16", "nbytes": 32 << 20, "fail_chunk": 1},
+    {"kind": "sm", "dtype": "bf16", "nbytes": 8 << 20, "chunk_begin": 1, "chunk_end": 3},
+    {"kind": "ce", "dtype": "f32", "nbytes": 16 << 20, "chunk_begin": 3},
+    {"kind": "nvls", "dtype": "i32", "nbytes": 16 << 20, "fail_chunk": 2},
+]
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_rails(world):
+    if gpu_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(MULTI)], timeout=600)
+    for rank_res in res:
+        for r in rank_res["results"]:
+            assert r["watchdog"] == 0, r
+            assert r["outside_nonzero"] == 0, r
+            assert r["mismatch"] == 0, r
+            case = MULTI[r["case"]]
+            if case.get("fail_chunk", -1) >= 0:
+                assert r["fault"] is not None and r["fault"]["chunk"] == case["fail_chunk"], r
+            else:
+                assert r["fault"] is None, r

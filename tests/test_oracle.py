@@ -1,0 +1,108 @@
+"""The oracle pinned against the reference: the closed-form ring-order fold
+(oracle/nezha_oracle.c) must equal the literal SPEC ring executed on the
+reference's own InMemoryFabric (oracle/ring_inmem.cpp + libnezha_ref.a built
+from /root/reference/proj/src), bit for bit; plus the SPEC's own examples.
+CPU only."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+needs_ref = pytest.mark.skipif(not oracle.inmem_available(), reason="oracle/_ref not built (needs /root/reference)")
+
+
+def bits(a):
+    return a.view(np.uint16) if a.dtype == np.uint16 else a.view(np.uint32)
+
+
+def test_spec_examples_ring():
+    # N=2, [1, 2] on both ranks -> [2, 4]
+    x = [np.array([1.0, 2.0], dtype=np.float32)] * 2
+    out = oracle.reduce_range(x, oracle.F32, 0, 8, 8, 0, 8)
+    assert out.tolist() == [2.0, 4.0]
+    # N=4, rank r holds constant r -> 6 everywhere
+    x = [np.full(1000, float(r), dtype=np.float32) for r in range(4)]
+    out = oracle.reduce_range(x, oracle.F32, 0, 4000, 4000, 0, 4000)
+    assert np.all(out == 6.0)
+
+
+def test_golden_order_vector():
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "order_vector.json")))
+    n = 4 * 1024
+    x = [np.full(n, v, dtype=np.float32) for v in g["rank_values"]]
+    out = oracle.reduce_range(x, oracle.F32, 0, n * 4, 65536, 0, n * 4)
+    assert [float(out[b * 1024]) for b in range(4)] == g["block_results"]
+
+
+def test_default_chunk_rule():
+    # P10: max(64 KiB, round4down(len / 2N)); Ring = whole segment.
+    assert oracle.default_chunk_bytes(64 << 20, 8) == 4 << 20
+    assert oracle.default_chunk_bytes(1 << 20, 8) == 65536
+    assert oracle.default_chunk_bytes(1_000_006, 2) == 250_000
+    assert oracle.default_chunk_bytes(123, 8, chunked=False) == 123
+
+
+def test_synthetic_inputs_deterministic():
+    a = oracle.synthetic_input(oracle.F32, 3, 4096)
+    b = oracle.synthetic_input(oracle.F32, 3, 4096)
+    assert np.array_equal(a, b) and a.min() >= -1.0 and a.max() < 1.0
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "synthetic_inputs.json")))
+    for key, vals in g["first8"].items():
+        dt, rank = key.split(":")
+        got = oracle.synthetic_input(oracle.__dict__[dt.upper()], int(rank), 32)[:8]
+        assert bits(got).tolist() == vals
+
+
+CASES = [
+    # world, dtype, nbytes, segments(rail, off, len), nrails, chunked
+    (2, oracle.F32, 4096, [(0, 0, 4096)], 1, True),
+    (4, oracle.F32, 1 << 20, [(0, 0, 1 << 19), (1, 1 << 19, 1 << 19)], 2, True),
+    (4, oracle.F32, 1 << 20, [(0, 0, 1 << 20)], 1, False),
+    (3, oracle.F32, 300_000, [(0, 0, 100_000), (1, 100_000, 200_000)], 2, True),
+    (8, oracle.F32, 4 << 20, [(0, 0, 3 << 20), (1, 3 << 20, 1 << 20)], 2, True),
+    (8, oracle.BF16, 2_000_002, [(0, 0, 1_000_000), (1, 1_000_000, 1_000_002)], 2, True),
+    (5, oracle.I32, 777_780, [(0, 0, 777_780)], 1, True),
+    (8, oracle.F32, 40, [(0, 0, 12), (1, 12, 28)], 2, True),
+    (4, oracle.BF16, 70_002, [(0, 0, 70_002)], 1, False),
+    (3, oracle.F32, 1_500_000, [(0, 0, 500_000), (1, 500_000, 600_000), (2, 1_100_000, 400_000)], 3, True),
+]
+
+
+@needs_ref
+@pytest.mark.parametrize("world,dtype,nbytes,segs,nrails,chunked", CASES)
+def test_closed_form_equals_literal_ring_on_reference_fabric(world, dtype, nbytes, segs, nrails, chunked):
+    inputs = [oracle.synthetic_input(dtype, r, nbytes, seed_base=11 + nbytes) for r in range(world)]
+    outs, _, _ = oracle.inmem_allreduce(inputs, dtype, segs, nrails, chunked=chunked)
+    want = oracle.reduce_segments(inputs, dtype,
+                                  [(o, l, oracle.default_chunk_bytes(l, world, chunked)) for _, o, l in segs])
+    for r in range(world):
+        np.testing.assert_array_equal(bits(outs[r]), bits(want), err_msg=f"rank {r}")
+
+
+@needs_ref
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_eq1_volume_accounting(world):
+    # bytes per rank = 2(N-1)S/N within 1% (fp32 payload).
+    for S in (64 * 1024, 8 << 20):
+        inputs = [oracle.synthetic_input(oracle.F32, r, S) for r in range(world)]
+        _, _, sent = oracle.inmem_allreduce(inputs, oracle.F32, [(0, 0, S)], 1)
+        want = 2 * (world - 1) * S / world
+        assert abs(sent - want) <= 0.01 * want
+
+
+@needs_ref
+@pytest.mark.parametrize("fail_chunk", [0, 1, 3, 7])
+@pytest.mark.parametrize("dtype", [oracle.F32, oracle.BF16, oracle.I32])
+def test_handoff_exactly_once(fail_chunk, dtype):
+    # kill rail 1 mid-op; the survivor finishes; result equals the oracle.
+    world, S = 4, 2 << 20
+    segs = [(0, 0, 1 << 20), (1, 1 << 20, 1 << 20)]
+    inputs = [oracle.synthetic_input(dtype, r, S, seed_base=5 + fail_chunk) for r in range(world)]
+    outs, _, _ = oracle.inmem_allreduce(inputs, dtype, segs, 2, fail_rail=1, fail_chunk=fail_chunk)
+    want = oracle.reduce_segments(inputs, dtype, [(o, l, oracle.default_chunk_bytes(l, world)) for _, o, l in segs])
+    for r in range(world):
+        np.testing.assert_array_equal(bits(outs[r]), bits(want))

@@ -1,0 +1,122 @@
+"""One rank of a multi-GPU rail parity run (spawned by tests/mp_util.spawn).
+
+argv[1] = JSON list of cases. Each case reduces one segment geometry on one
+rail and compares this rank's output buffer with the CPU oracle:
+bit-exact for the CE and SM rails (P1/P2) and for int32 on every
+rail; NVLS fp32 within 1e-6 of sum(|x|) per element, NVLS bf16 within one
+bf16 ulp of the oracle (P2). Prints one JSON line.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402  (checker only)
+from paper_2405_17870_b200 import Comm, Rail, SymmetricBuffer  # noqa: E402
+from paper_2405_17870_b200._lib import DTYPES, RAIL_KINDS  # noqa: E402
+
+
+def compare(kind, dtype, got, want, inputs, lo, hi, es):
+    a, b = lo // es, hi // es
+    g, w = got[a:b], want[a:b]
+    if kind != "nvls" or dtype == oracle.I32:
+        ibits = {np.dtype(np.float32): np.uint32, np.dtype(np.int32): np.uint32, np.dtype(np.uint16): np.uint16}
+        bad = np.nonzero(g.view(ibits[g.dtype]) != w.view(ibits[w.dtype]))[0]
+        return {"exact": True, "mismatch": int(bad.size), "first_bad": int(bad[0] + a) if bad.size else -1}
+    if dtype == oracle.F32:
+        scale = np.sum([np.abs(x[a:b].astype(np.float64)) for x in inputs], axis=0)
+        err = np.abs(g.astype(np.float64) - w.astype(np.float64))
+        rel = float(np.max(err / np.maximum(scale, 1e-30))) if err.size else 0.0
+        return {"exact": False, "max_rel_sum_abs": rel, "mismatch": int(np.sum(err / np.maximum(scale, 1e-30) > 1e-6)),
+                "bitexact_frac": float(np.mean(g == w)) if g.size else 1.0}
+    gi, wi = g.astype(np.int32), w.astype(np.int32)
+    ulp = np.abs(gi - wi)  # same-sign bf16 patterns: integer distance = ulps
+    sign_flip = (gi ^ wi) & 0x8000
+    ulp = np.where(sign_flip != 0, np.abs(oracle.bf16_to_f32(g) - oracle.bf16_to_f32(w)) > 0, ulp)
+    return {"exact": False, "max_ulp": int(ulp.max()) if ulp.size else 0, "mismatch": int(np.sum(ulp > 1)),
+            "bitexact_frac": float(np.mean(g == w)) if g.size else 1.0}
+
+
+def main():
+    cases = json.loads(sys.argv[1])
+    comm = Comm.from_env(session=os.environ["NZ_SESSION"])
+    rank, world = comm.rank, comm.world
+    cap = max(c["nbytes"] for c in cases)
+    bin_, bout = SymmetricBuffer(comm, cap), SymmetricBuffer(comm, cap)
+    rails = {}
+    results = []
+    for ci, c in enumerate(cases):
+        kind = c["kind"]
+        if kind not in rails:
+            rails[kind] = Rail(comm, RAIL_KINDS[kind], len(rails), c.get("sm_budget", 0))
+        rail = rails[kind]
+        dt = DTYPES[c["dtype"]]
+        es = 2 if dt == oracle.BF16 else 4
+        nbytes = c["nbytes"]
+        check = c.get("check", True)
+        if check:
+            inputs = [oracle.synthetic_input(dt, r, nbytes, seed_base=oracle.SEED_BASE + 97 * ci) for r in range(world)]
+        else:  # timing-only case: this rank's synthetic input, no oracle comparison
+            inputs = [oracle.synthetic_input(dt, rank, nbytes, seed_base=oracle.SEED_BASE + 97 * ci)]
+        bin_.zero()
+        bout.zero()
+        bin_.write(inputs[rank if check else 0], nbytes)
+        seg_off, seg_len = c.get("seg_off", 0), c.get("seg_len", nbytes)
+        chunk = c.get("chunk") or oracle.default_chunk_bytes(seg_len, world, c.get("chunked", True))
+        nch = (seg_len + chunk - 1) // chunk
+        cb, ce = c.get("chunk_begin", 0), min(c.get("chunk_end", nch), nch)
+        fail = c.get("fail_chunk", -1)
+        comm.barrier()
+        rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce,
+                       fail_chunk=fail)
+        rail.synchronize()
+        wd = rail.watchdog()
+        stop = fail if 0 <= fail < ce and fail >= cb else ce
+        lo, hi = seg_off + min(seg_len, cb * chunk), seg_off + min(seg_len, stop * chunk)
+        res = {"case": ci, "kind": kind, "dtype": c["dtype"], "nbytes": nbytes, "lo": lo, "hi": hi, "watchdog": wd}
+        if check:
+            got = np.zeros(nbytes // es, dtype=oracle.NP_DTYPE[dt])
+            bout.read(got, nbytes)
+            want = np.zeros_like(got)
+            if hi > lo:
+                oracle.reduce_range(inputs, dt, seg_off, seg_len, chunk, lo, hi, want)
+            res.update(compare(kind, dt, got, want, inputs, lo, hi, es))
+            outside = np.concatenate([got[: lo // es], got[hi // es:]])
+            res["outside_nonzero"] = int(np.count_nonzero(outside))
+        rec = rail.poll_fault()
+        res["fault"] = None if rec is None else {"op_seq": rec.op_seq, "chunk": rec.chunk}
+        iters = c.get("iters", 0)
+        if iters:
+            import torch
+            torch.cuda.set_device(comm.device)
+            st = torch.cuda.ExternalStream(rail.stream)
+            for _ in range(3):
+                rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci)
+            comm.barrier()
+            rail.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(iters):
+                rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci)
+            e1.record(st)
+            rail.synchronize()
+            t = e0.elapsed_time(e1) / iters / 1e3
+            res["us"] = t * 1e6
+            res["busbw_GBs"] = 2 * (world - 1) / world * seg_len / t / 1e9 if world > 1 else 0.0
+            res["algbw_GBs"] = seg_len / t / 1e9
+        results.append(res)
+    for r in rails.values():
+        r.close()
+    bin_.free()
+    bout.free()
+    comm.close()
+    print(json.dumps({"rank": rank, "results": results}))
+
+
+if __name__ == "__main__":
+    main()
