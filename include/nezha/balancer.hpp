@@ -150,6 +150,13 @@ class Balancer {
   void setProfiles(std::vector<RailProfile> rails);
   void setSyncOverhead(Micros us);
 
+  // Multi-rank agreement on a flush: maps this rank's per-rail window means
+  // to the values every rank will apply (the engine: max over ranks). Unset
+  // (single process, traces) = identity.
+  using Agreement = std::function<std::vector<std::pair<int, Micros>>(int bucket,
+                                                                     const std::vector<std::pair<int, Micros>>&)>;
+  void setAgreement(Agreement fn) { agree_ = std::move(fn); }
+
   const AllocationTable& table() const { return table_; }
   const std::vector<RailProfile>& rails() const { return rails_; }
   const BalancerConfig& config() const { return cfg_; }
@@ -171,6 +178,7 @@ class Balancer {
   AllocationTable table_;
   std::map<int, std::vector<double>> saved_alpha_;  // alpha snapshot at the last failure
   std::map<int, std::vector<LatencyWindow>> windows_;  // bucket -> per rail index
+  Agreement agree_;
 };
 
 std::string formatDouble(double v);  // "%.17g", shared by every JSON writer

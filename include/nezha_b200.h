@@ -150,6 +150,8 @@ typedef struct {
   int demote_after;          /* DESIGN.md P12; 0 disables */
   const char* rails_toml;    /* optional rails config text; NULL: calibrate */
   int calibrate_iters;       /* ops per size during startup calibration */
+  uint64_t calibrate_max_bytes; /* largest calibrated size (default 1 GiB) */
+  int timer_lag;             /* op k is sampled when op k + lag is issued (default 2) */
 } nz_engine_config_t;
 
 void nz_engine_config_default(nz_engine_config_t* cfg);
@@ -189,6 +191,9 @@ int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep);
  * engine would use for `bytes` (segments per rail). */
 int nz_engine_state_json(nz_engine_t* eng, char* out, size_t cap);
 int nz_engine_plan_json(nz_engine_t* eng, uint64_t bytes, char* out, size_t cap);
+/* The plans (one per 256 MiB piece above 1 GiB) the last allreduce call ran,
+ * with each segment's chunk size: what a checker needs to recompute it. */
+int nz_engine_last_plan_json(nz_engine_t* eng, char* out, size_t cap);
 
 /* -------------------------------------------------------------- planner --- */
 /* Runs the balancer + fault logic over a scenario (rails, config, op stream,

@@ -92,6 +92,8 @@ class EngineConfig(ctypes.Structure):
         ("demote_after", c_int),
         ("rails_toml", c_char_p),
         ("calibrate_iters", c_int),
+        ("calibrate_max_bytes", c_uint64),
+        ("timer_lag", c_int),
     ]
 
 
@@ -151,6 +153,7 @@ _SIGS = {
     "nz_engine_last_failover": (c_int, [c_void_p, POINTER(FailoverReport)]),
     "nz_engine_state_json": (c_int, [c_void_p, c_char_p, c_size_t]),
     "nz_engine_plan_json": (c_int, [c_void_p, c_uint64, c_char_p, c_size_t]),
+    "nz_engine_last_plan_json": (c_int, [c_void_p, c_char_p, c_size_t]),
     "nz_planner_run_trace": (c_int, [c_char_p, c_char_p, c_size_t]),
     "nz_emulate_fold": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64, c_uint64,
                                 c_uint64, c_uint64, c_uint64, c_int, c_void_p]),

@@ -1,0 +1,608 @@
+// Engine: the multi-rail allreduce of one rank (
+// PAPER.md:379 Fig. 6). Planner (Balancer) + rails (rails.cu) + Timer +
+// fault monitor / handoff. See include/nezha/engine.hpp for the contract.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <sstream>
+#include <thread>
+
+#include "../host/planner_trace.hpp"
+#include "internal.h"
+#include "nezha/balancer.hpp"
+#include "nezha/collective.hpp"
+#include "nezha/core/error.hpp"
+#include "nezha/core/math.hpp"
+#include "nezha/engine.hpp"
+#include "nezha/faults.hpp"
+#include "nezha/util/toml.hpp"
+
+
+using nz::fail;
+using nz::guarded;
+
+struct nz_engine {
+  struct Pending {
+    uint32_t op = 0;
+    nezha::Plan plan;
+    cudaEvent_t start = nullptr;
+    std::vector<std::pair<int, cudaEvent_t>> ends;
+    bool skip = false;  // an op that lost a rail is not a Timer sample
+  };
+
+  nz_comm* comm = nullptr;
+  nz_engine_config_t cfg{};
+  std::vector<nezha::RailSpec> specs;  // sorted by rail_id
+  std::vector<nz_rail*> rails;         // parallel to specs
+  std::unique_ptr<nezha::Balancer> bal;
+  std::unique_ptr<nezha::HealthMonitor> health;
+  nezha::Algorithm algo = nezha::Algorithm::RingChunked;
+  uint32_t op_seq = 0;
+  std::deque<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  std::map<uint32_t, std::pair<int, uint64_t>> inject;
+  nz_failover_report_t fo{};
+  bool have_fo = false;
+  bool fo_pending = false;
+  uint64_t* stamps_host = nullptr;  // [0] detect, [1] resume, [2] done, [3] fault
+  uint64_t* stamps_dev = nullptr;
+  cudaStream_t ctrl = nullptr;
+  cudaStream_t io = nullptr;
+  nz_buf* ub_in = nullptr;
+  nz_buf* ub_out = nullptr;
+  std::vector<std::string> last_plans;  // JSON of each piece of the last call
+
+  int index(int rail_id) const {
+    for (size_t i = 0; i < specs.size(); ++i)
+      if (specs[i].rail_id == rail_id) return static_cast<int>(i);
+    fail(NZ_ERR_INVALID, "unknown rail " + std::to_string(rail_id));
+  }
+
+  cudaEvent_t event() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    NZ_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+
+  // Element-wise max over ranks: what every rank applies at a flush.
+  std::vector<std::pair<int, nezha::Micros>> agree(const std::vector<std::pair<int, nezha::Micros>>& mine) {
+    if (comm->world == 1) return mine;
+    std::vector<double> v(specs.size(), -1.0);
+    for (auto& [id, m] : mine) v[index(id)] = m;
+    std::vector<double> all(v.size() * comm->world);
+    const auto msgs = nz::exchange(comm, v.data(), v.size() * sizeof(double), {});
+    for (int r = 0; r < comm->world; ++r) std::memcpy(all.data() + r * v.size(), msgs[r].data.data(), v.size() * sizeof(double));
+    std::vector<std::pair<int, nezha::Micros>> out;
+    for (size_t i = 0; i < v.size(); ++i) {
+      double m = -1.0;
+      for (int r = 0; r < comm->world; ++r) m = std::max(m, all[r * v.size() + i]);
+      if (m >= 0) out.emplace_back(specs[i].rail_id, m);
+    }
+    return out;
+  }
+
+  void harvest(uint32_t upto) {
+    while (!pending.empty() && pending.front().op + static_cast<uint32_t>(cfg.timer_lag) <= upto) {
+      Pending p = std::move(pending.front());
+      pending.pop_front();
+      std::vector<std::pair<int, nezha::Micros>> lat;
+      for (auto& [id, e] : p.ends) {
+        NZ_CUDA(cudaEventSynchronize(e));
+        float ms = 0;
+        NZ_CUDA(cudaEventElapsedTime(&ms, p.start, e));
+        bool found = false;
+        for (auto& pr : lat)
+          if (pr.first == id) {
+            pr.second = std::max(pr.second, static_cast<double>(ms) * 1000.0);
+            found = true;
+          }
+        if (!found) lat.emplace_back(id, static_cast<double>(ms) * 1000.0);
+        pool.push_back(e);
+      }
+      pool.push_back(p.start);
+      if (!p.skip) bal->recordOp(p.plan, lat);
+    }
+  }
+
+  void drainTimer() { harvest(UINT32_MAX - 8); }
+
+  std::vector<int> healthyIds() const { return health->healthyRails(); }
+
+  void finishFailoverReport() {
+    if (!fo_pending) return;
+    volatile uint64_t* s = stamps_host;
+    if (s[2] == 0) return;
+    const double f = static_cast<double>(s[3]);
+    fo.detect_us = (static_cast<double>(s[0]) - f) / 1000.0;
+    fo.resume_us = (static_cast<double>(s[1]) - f) / 1000.0;
+    fo.done_us = (static_cast<double>(s[2]) - f) / 1000.0;
+    have_fo = true;
+    fo_pending = false;
+  }
+
+  // One op (piece) of at most 1 GiB at byte offset `base`.
+  void op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dtype, cudaStream_t user) {
+    const uint32_t seq = op_seq++;
+    harvest(seq);
+    nezha::Plan plan = bal->allocate(len);
+    Pending p;
+    p.op = seq;
+    p.plan = plan;
+    p.start = event();
+    NZ_CUDA(cudaEventRecord(p.start, user));
+    const int world = comm->world;
+    auto inj = inject.find(seq);
+    const nezha::Segment* failed_seg = nullptr;
+    int failed_rail = -1;
+    uint64_t failed_chunk = 0;
+    for (const auto& rs : plan.segments) {
+      nz_rail* r = rails[index(rs.rail_id)];
+      NZ_CUDA(cudaStreamWaitEvent(r->stream, p.start, 0));
+      const uint64_t C = nezha::defaultChunkBytes(rs.segment.length, world, algo);
+      int64_t fail_chunk = -1;
+      if (inj != inject.end() && inj->second.first == rs.rail_id) {
+        fail_chunk = static_cast<int64_t>(inj->second.second);
+        const uint64_t nch = (rs.segment.length + C - 1) / C;
+        if (inj->second.second < nch) {
+          failed_seg = &rs.segment;
+          failed_rail = rs.rail_id;
+          failed_chunk = inj->second.second;
+        }
+      }
+      nz::railAllreduce(r, in, out, base + rs.segment.offset, rs.segment.length, C, 0, UINT64_MAX, dtype, seq,
+                        fail_chunk, r->stream);
+      cudaEvent_t e = event();
+      NZ_CUDA(cudaEventRecord(e, r->stream));
+      p.ends.emplace_back(rs.rail_id, e);
+    }
+    if (inj != inject.end()) {
+      const int rid = inj->second.first;
+      inject.erase(inj);
+      p.skip = true;
+      if (failed_seg) {
+        handoff(p, plan, *failed_seg, failed_rail, failed_chunk, in, out, base, dtype);
+      } else if (health->state(rid).status != nezha::HealthStatus::Failed) {
+        // Idle failure: the rail carried nothing at / after that chunk.
+        health->channelDown(rid);
+        bal->markFailed(rid);
+      }
+    }
+    for (auto& [id, e] : p.ends) NZ_CUDA(cudaStreamWaitEvent(user, e, 0));
+    std::ostringstream o;
+    o << "{\"op\":" << seq << ",\"offset\":" << base << ",\"length\":" << len << ",\"hot\":" << (plan.hot ? "true" : "false")
+      << ",\"segs\":[";
+    for (size_t i = 0; i < plan.segments.size(); ++i) {
+      const auto& rs = plan.segments[i];
+      o << (i ? "," : "") << "[" << rs.rail_id << "," << base + rs.segment.offset << "," << rs.segment.length << ","
+        << nezha::defaultChunkBytes(rs.segment.length, world, algo) << "]";
+    }
+    o << "]}";
+    last_plans.push_back(o.str());
+    pending.push_back(std::move(p));
+  }
+
+  // Exception handler: wait for the device's fault record,
+  // mark the rail Failed, pick the target (P9) and run the orphan chunks on
+  // it with the failed segment's geometry (P10), after its current task.
+  void handoff(Pending& p, const nezha::Plan& plan, const nezha::Segment& seg, int rid, uint64_t k, nz_buf* in,
+               nz_buf* out, uint64_t base, int dtype) {
+    nz_rail* fr = rails[index(rid)];
+    nz_fault_record_t rec{};
+    const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(60);
+    for (;;) {
+      volatile nz_fault_record_t* f = fr->fault_host;
+      if (f->valid) {
+        __sync_synchronize();
+        rec.op_seq = f->op_seq;
+        rec.chunk = f->chunk;
+        rec.t_fail_ns = f->t_fail_ns;
+        f->valid = 0;
+        break;
+      }
+      if (*reinterpret_cast<volatile int*>(fr->wd_host)) fail(NZ_ERR_TIMEOUT, "rail watchdog fired while waiting for a fault");
+      if (std::chrono::steady_clock::now() > deadline) fail(NZ_ERR_TIMEOUT, "fault record never arrived");
+    }
+    std::memset(stamps_host, 0, 4 * sizeof(uint64_t));
+    stamps_host[3] = rec.t_fail_ns;
+    nz::launchStamp(stamps_dev + 0, ctrl);  // detection acknowledged on the device timeline
+    health->channelDown(rid);
+    bal->markFailed(rid);
+    const auto target = nezha::chooseHandoffTarget(plan, rid, healthyIds());
+    if (!target) fail(NZ_ERR_UNRECOVERABLE, "no surviving rail to take over the orphaned segment");
+    const uint64_t C = nezha::defaultChunkBytes(seg.length, comm->world, algo);
+    const nezha::Segment orphan = nezha::orphanOf(seg, C, k);
+    nz_rail* tr = rails[index(*target)];
+    nz::launchStamp(stamps_dev + 1, tr->stream);
+    nz::railAllreduce(tr, in, out, base + seg.offset, seg.length, C, k, UINT64_MAX, dtype, p.op, -1, tr->stream);
+    nz::launchStamp(stamps_dev + 2, tr->stream);
+    cudaEvent_t e = event();
+    NZ_CUDA(cudaEventRecord(e, tr->stream));
+    p.ends.emplace_back(*target, e);
+    fo = nz_failover_report_t{};
+    fo.op_seq = p.op;
+    fo.failed_rail = rid;
+    fo.target_rail = *target;
+    fo.orphan_offset = base + orphan.offset;
+    fo.orphan_length = orphan.length;
+    fo_pending = true;
+  }
+
+  void synchronize() {
+    for (auto* r : rails) {
+      for (auto s : r->side) NZ_CUDA(cudaStreamSynchronize(s));
+      NZ_CUDA(cudaStreamSynchronize(r->stream));
+    }
+    NZ_CUDA(cudaStreamSynchronize(ctrl));
+    for (auto* r : rails)
+      if (*reinterpret_cast<volatile int*>(r->wd_host)) fail(NZ_ERR_TIMEOUT, "rail watchdog fired (a peer never arrived)");
+    finishFailoverReport();
+  }
+
+  void ensureUnbound(uint64_t bytes) {
+    if (ub_in && ub_in->size >= bytes) return;
+    NZ_CUDA(cudaDeviceSynchronize());
+    if (ub_in) nz::freeSymmetric(ub_in);
+    if (ub_out) nz::freeSymmetric(ub_out);
+    ub_in = ub_out = nullptr;
+    ub_in = nz::allocSymmetric(comm, bytes);
+    ub_out = nz::allocSymmetric(comm, bytes);
+  }
+
+  // Startup calibration: each rail alone over a size sweep, then the
+  // coordination cost of a fork/join over all rails.
+  void calibrate() {
+    const uint64_t maxb = std::max<uint64_t>(cfg.calibrate_max_bytes, 1 << 16);
+    ensureUnbound(maxb);
+    const int world = comm->world;
+    std::vector<uint64_t> sizes;
+    for (uint64_t s = 4096; s <= maxb; s *= 4) sizes.push_back(s);
+    cudaEvent_t e0 = event(), e1 = event();
+    std::vector<nezha::RailProfile> profiles;
+    for (size_t i = 0; i < specs.size(); ++i) {
+      if (specs[i].has_profile) {  // given by the rails config: keep it
+        profiles.push_back(specs[i].profile);
+        continue;
+      }
+      nz_rail* r = rails[i];
+      std::vector<double> lat;
+      for (uint64_t s : sizes) {
+        const uint64_t C = nezha::defaultChunkBytes(s, world, algo);
+        const int iters = s <= (1u << 20) ? std::max(cfg.calibrate_iters, 4) : std::max(cfg.calibrate_iters / 4, 2);
+        for (int w = 0; w < 2; ++w) nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
+        NZ_CUDA(cudaEventRecord(e0, r->stream));
+        for (int it = 0; it < iters; ++it)
+          nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
+        NZ_CUDA(cudaEventRecord(e1, r->stream));
+        NZ_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        NZ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        lat.push_back(static_cast<double>(ms) * 1000.0 / iters);
+      }
+      // Ranks agree (max), then the samples are made strictly increasing so
+      // RailProfile::validate accepts them (types.cpp:44-51).
+      if (world > 1) {
+        const auto msgs = nz::exchange(comm, lat.data(), lat.size() * sizeof(double), {});
+        for (int rk = 0; rk < world; ++rk) {
+          const double* v = reinterpret_cast<const double*>(msgs[rk].data.data());
+          for (size_t j = 0; j < lat.size(); ++j) lat[j] = std::max(lat[j], v[j]);
+        }
+      }
+      for (size_t j = 1; j < lat.size(); ++j) lat[j] = std::max(lat[j], lat[j - 1] + 1e-3);
+      nezha::RailProfile p = specs[i].profile;
+      p.rail_id = specs[i].rail_id;
+      p.efficiency_points.clear();
+      for (size_t j = 0; j < sizes.size(); ++j) p.efficiency_points.emplace_back(sizes[j], lat[j]);
+      p.t_setup_us = lat.front();
+      p.bandwidth_bps = static_cast<double>(sizes.back() - sizes.front()) / ((lat.back() - lat.front()) * 1e-6);
+      profiles.push_back(p);
+      specs[i].profile = p;
+      specs[i].has_profile = true;
+    }
+    bal->setProfiles(profiles);
+    if (cfg.sync_overhead_us < 0 && specs.size() > 1) {
+      // Fork/join of every rail on 4 KiB each vs the slowest rail alone.
+      const uint64_t s = 4096;
+      const int iters = 50;
+      double single = 0;
+      for (auto& sp : specs) single = std::max(single, sp.profile.messageLatency(s));
+      cudaStream_t user = io;
+      NZ_CUDA(cudaEventRecord(e0, user));
+      for (int it = 0; it < iters; ++it) {
+        cudaEvent_t f = event();
+        NZ_CUDA(cudaEventRecord(f, user));
+        std::vector<cudaEvent_t> ends;
+        for (size_t i = 0; i < rails.size(); ++i) {
+          NZ_CUDA(cudaStreamWaitEvent(rails[i]->stream, f, 0));
+          nz::railAllreduce(rails[i], ub_in, ub_out, s * i, s, 65536, 0, UINT64_MAX, NZ_F32, 0, -1, rails[i]->stream);
+          cudaEvent_t e = event();
+          NZ_CUDA(cudaEventRecord(e, rails[i]->stream));
+          NZ_CUDA(cudaStreamWaitEvent(user, e, 0));
+          ends.push_back(e);
+        }
+        NZ_CUDA(cudaStreamSynchronize(user));
+        pool.push_back(f);
+        for (auto e : ends) pool.push_back(e);
+      }
+      NZ_CUDA(cudaEventRecord(e1, user));
+      NZ_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      NZ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      double multi = static_cast<double>(ms) * 1000.0 / iters;
+      if (world > 1) {
+        const auto msgs = nz::exchange(comm, &multi, sizeof(multi), {});
+        for (int rk = 0; rk < world; ++rk) multi = std::max(multi, *reinterpret_cast<const double*>(msgs[rk].data.data()));
+      }
+      bal->setSyncOverhead(std::max(0.0, multi - single));
+    }
+    pool.push_back(e0);
+    pool.push_back(e1);
+  }
+
+  std::string stateJson() {
+    std::ostringstream o;
+    o << "{\"op_seq\":" << op_seq << ",\"world\":" << comm->world << ",\"rank\":" << comm->rank
+      << ",\"sync_overhead_us\":" << nezha::formatDouble(bal->config().sync_overhead_us) << ",\"rails\":[";
+    for (size_t i = 0; i < specs.size(); ++i) {
+      const auto& p = bal->rails()[i];
+      o << (i ? "," : "") << "{\"rail_id\":" << specs[i].rail_id << ",\"kind\":\""
+        << (specs[i].kind == NZ_RAIL_NVLS ? "nvls" : specs[i].kind == NZ_RAIL_CE ? "ce" : "sm")
+        << "\",\"protocol\":\"" << nezha::toString(p.protocol) << "\",\"health\":\""
+        << nezha::toString(health->state(specs[i].rail_id).status) << "\",\"t_setup_us\":"
+        << nezha::formatDouble(p.t_setup_us) << ",\"bandwidth_bps\":" << nezha::formatDouble(p.bandwidth_bps)
+        << ",\"calibration\":[";
+      for (size_t j = 0; j < p.efficiency_points.size(); ++j)
+        o << (j ? "," : "") << "[" << p.efficiency_points[j].first << ","
+          << nezha::formatDouble(p.efficiency_points[j].second) << "]";
+      o << "]}";
+    }
+    o << "],\"table\":" << bal->tableJson() << "}";
+    return o.str();
+  }
+};
+
+namespace {
+int copyOut(const std::string& s, char* out, size_t cap) {
+  if (!out) return NZ_ERR_INVALID;
+  if (s.size() + 1 > cap) return NZ_ERR_BUFFER;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return NZ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+void nz_engine_config_default(nz_engine_config_t* c) {
+  if (!c) return;
+  *c = nz_engine_config_t{};
+  c->num_rails = 3;
+  c->kinds[0] = NZ_RAIL_NVLS;
+  c->kinds[1] = NZ_RAIL_CE;
+  c->kinds[2] = NZ_RAIL_SM;
+  c->sm_budget[0] = 0;
+  c->sm_budget[1] = 0;
+  c->sm_budget[2] = 0;
+  c->algorithm = NZ_ALGO_RING_CHUNKED;
+  c->tau = 5.0;
+  c->eta = 0.05;
+  c->convergence_eps = 0.01;
+  c->sync_overhead_us = -1.0;
+  c->window = 100;
+  c->max_iters = 100;
+  c->demote_after = 3;
+  c->rails_toml = nullptr;
+  c->calibrate_iters = 20;
+  c->calibrate_max_bytes = uint64_t{1} << 30;
+  c->timer_lag = 2;
+}
+
+int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t** out) {
+  return guarded([&] {
+    if (!comm || !out) fail(NZ_ERR_INVALID, "null argument");
+    auto eng = std::make_unique<nz_engine>();
+    eng->comm = comm;
+    if (cfg) {
+      eng->cfg = *cfg;
+    } else {
+      nz_engine_config_default(&eng->cfg);
+    }
+    auto& c = eng->cfg;
+    if (c.timer_lag < 1) c.timer_lag = 1;
+    eng->algo = c.algorithm == NZ_ALGO_RING ? nezha::Algorithm::Ring : nezha::Algorithm::RingChunked;
+    if (c.rails_toml) {
+      eng->specs = nezha::parseRailsToml(c.rails_toml);
+    } else {
+      if (c.num_rails < 1 || c.num_rails > 3) fail(NZ_ERR_INVALID, "num_rails must be 1..3");
+      for (int i = 0; i < c.num_rails; ++i) {
+        nezha::RailSpec s;
+        s.rail_id = i;
+        s.kind = c.kinds[i];
+        s.sm_budget = c.sm_budget[i];
+        s.profile.rail_id = i;
+        s.profile.protocol = s.kind == NZ_RAIL_NVLS ? nezha::ProtocolKind::Sharp
+                             : s.kind == NZ_RAIL_CE ? nezha::ProtocolKind::Glex
+                                                    : nezha::ProtocolKind::Tcp;
+        eng->specs.push_back(s);
+      }
+    }
+    std::sort(eng->specs.begin(), eng->specs.end(), [](auto& a, auto& b) { return a.rail_id < b.rail_id; });
+    NZ_CUDA(cudaSetDevice(comm->device));
+    for (auto& s : eng->specs) {
+      nz_rail_t* r = nullptr;
+      const int rc = nz_rail_create(comm, s.kind, s.rail_id, s.sm_budget, &r);
+      if (rc != NZ_OK) fail(rc, nz_last_error());
+      eng->rails.push_back(r);
+    }
+    std::vector<int> ids;
+    std::vector<nezha::RailProfile> profiles;
+    bool all_profiles = true;
+    for (auto& s : eng->specs) {
+      ids.push_back(s.rail_id);
+      all_profiles &= s.has_profile;
+      nezha::RailProfile p = s.profile;
+      if (!s.has_profile) {  // placeholder until calibration replaces it
+        p.t_setup_us = 10;
+        p.bandwidth_bps = 1e11;
+      }
+      profiles.push_back(p);
+    }
+    nezha::BalancerConfig bc;
+    bc.tau = c.tau;
+    bc.eta = c.eta;
+    bc.convergence_eps = c.convergence_eps;
+    bc.sync_overhead_us = c.sync_overhead_us < 0 ? 0.0 : c.sync_overhead_us;
+    bc.window = c.window;
+    bc.max_iters = c.max_iters;
+    bc.demote_after = c.demote_after;
+    eng->bal = std::make_unique<nezha::Balancer>(profiles, bc);
+    nz_engine* raw = eng.get();
+    eng->bal->setAgreement([raw](int, const std::vector<std::pair<int, nezha::Micros>>& m) { return raw->agree(m); });
+    eng->health = std::make_unique<nezha::HealthMonitor>(ids);
+    NZ_CUDA(cudaStreamCreateWithFlags(&eng->ctrl, cudaStreamNonBlocking));
+    NZ_CUDA(cudaStreamCreateWithFlags(&eng->io, cudaStreamNonBlocking));
+    NZ_CUDA(cudaHostAlloc(&eng->stamps_host, 4 * sizeof(uint64_t), cudaHostAllocMapped));
+    std::memset(eng->stamps_host, 0, 4 * sizeof(uint64_t));
+    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eng->stamps_dev), eng->stamps_host, 0));
+    if (!all_profiles || c.sync_overhead_us < 0) eng->calibrate();
+    NZ_CUDA(cudaDeviceSynchronize());
+    *out = eng.release();
+  });
+}
+
+int nz_engine_destroy(nz_engine_t* eng) {
+  return guarded([&] {
+    if (!eng) return;
+    cudaSetDevice(eng->comm->device);
+    cudaDeviceSynchronize();
+    for (auto e : eng->pool) cudaEventDestroy(e);
+    for (auto& p : eng->pending) {
+      cudaEventDestroy(p.start);
+      for (auto& pr : p.ends) cudaEventDestroy(pr.second);
+    }
+    for (auto* r : eng->rails) nz_rail_destroy(r);
+    if (eng->ub_in) nz::freeSymmetric(eng->ub_in);
+    if (eng->ub_out) nz::freeSymmetric(eng->ub_out);
+    if (eng->ctrl) cudaStreamDestroy(eng->ctrl);
+    if (eng->io) cudaStreamDestroy(eng->io);
+    if (eng->stamps_host) cudaFreeHost(eng->stamps_host);
+    delete eng;
+  });
+}
+
+int nz_engine_allreduce(nz_engine_t* eng, nz_buf_t* in, nz_buf_t* out, uint64_t bytes, int dtype, void* stream) {
+  return guarded([&] {
+    if (!eng || !in || !out) fail(NZ_ERR_INVALID, "null argument");
+    const int es = nz::elemSizeOf(dtype);
+    if (bytes % es) fail(NZ_ERR_INVALID, "bytes is not a whole number of elements");
+    if (bytes > in->size || bytes > out->size) fail(NZ_ERR_INVALID, "payload exceeds the buffers");
+    if (bytes == 0) return;
+    NZ_CUDA(cudaSetDevice(eng->comm->device));
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    eng->last_plans.clear();
+    for (const auto& piece : nezha::splitOversized(bytes)) {
+      eng->op(in, out, piece.offset, piece.length, dtype, user);
+    }
+  });
+}
+
+int nz_engine_allreduce_host(nz_engine_t* eng, const void* host_in, void* host_out, uint64_t bytes, int dtype) {
+  return guarded([&] {
+    if (!eng || !host_in || !host_out) fail(NZ_ERR_INVALID, "null argument");
+    if (bytes == 0) return;
+    NZ_CUDA(cudaSetDevice(eng->comm->device));
+    eng->ensureUnbound(bytes);
+    nz_buf* in = eng->ub_in;
+    nz_buf* out = eng->ub_out;
+    NZ_CUDA(cudaMemcpyAsync(in->ptrs[eng->comm->rank], host_in, bytes, cudaMemcpyHostToDevice, eng->io));
+    eng->last_plans.clear();
+    for (const auto& piece : nezha::splitOversized(bytes)) {
+      eng->op(in, out, piece.offset, piece.length, dtype, eng->io);
+    }
+    NZ_CUDA(cudaMemcpyAsync(host_out, out->ptrs[eng->comm->rank], bytes, cudaMemcpyDeviceToHost, eng->io));
+    NZ_CUDA(cudaStreamSynchronize(eng->io));
+    eng->finishFailoverReport();
+  });
+}
+
+int nz_engine_inject_failure(nz_engine_t* eng, uint32_t op_seq, int rail_id, uint64_t chunk) {
+  return guarded([&] {
+    if (!eng) fail(NZ_ERR_INVALID, "null engine");
+    eng->index(rail_id);
+    if (op_seq < eng->op_seq) fail(NZ_ERR_INVALID, "op already issued");
+    eng->inject[op_seq] = {rail_id, chunk};
+  });
+}
+
+int nz_engine_readmit(nz_engine_t* eng, int rail_id) {
+  return guarded([&] {
+    if (!eng) fail(NZ_ERR_INVALID, "null engine");
+    eng->synchronize();
+    eng->drainTimer();
+    eng->health->heartbeat(rail_id, 0);
+    eng->health->readmit(rail_id, 0, 0);
+    eng->bal->readmit(rail_id);
+  });
+}
+
+int nz_engine_synchronize(nz_engine_t* eng) {
+  return guarded([&] {
+    if (!eng) fail(NZ_ERR_INVALID, "null engine");
+    NZ_CUDA(cudaSetDevice(eng->comm->device));
+    eng->synchronize();
+  });
+}
+
+uint32_t nz_engine_op_seq(const nz_engine_t* eng) { return eng ? eng->op_seq : 0; }
+
+int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep) {
+  if (!eng || !rep) return NZ_ERR_INVALID;
+  eng->finishFailoverReport();
+  if (!eng->have_fo) return NZ_ERR_INVALID;
+  *rep = eng->fo;
+  return NZ_OK;
+}
+
+int nz_engine_state_json(nz_engine_t* eng, char* out, size_t cap) {
+  std::string s;
+  const int rc = guarded([&] {
+    if (!eng) fail(NZ_ERR_INVALID, "null engine");
+    s = eng->stateJson();
+  });
+  return rc != NZ_OK ? rc : copyOut(s, out, cap);
+}
+
+int nz_engine_last_plan_json(nz_engine_t* eng, char* out, size_t cap) {
+  if (!eng) return NZ_ERR_INVALID;
+  std::string s = "[";
+  for (size_t i = 0; i < eng->last_plans.size(); ++i) s += (i ? "," : "") + eng->last_plans[i];
+  s += "]";
+  return copyOut(s, out, cap);
+}
+
+int nz_engine_plan_json(nz_engine_t* eng, uint64_t bytes, char* out, size_t cap) {
+  std::string s;
+  const int rc = guarded([&] {
+    if (!eng || bytes == 0) fail(NZ_ERR_INVALID, "bad argument");
+    std::ostringstream o;
+    o << "{\"pieces\":[";
+    bool first = true;
+    for (const auto& piece : nezha::splitOversized(bytes)) {
+      const auto plan = eng->bal->allocate(piece.length);
+      o << (first ? "" : ",") << "{\"offset\":" << piece.offset << ",\"plan\":"
+        << nezha::planJson(0, piece.length, plan) << "}";
+      first = false;
+    }
+    o << "]}";
+    s = o.str();
+  });
+  return rc != NZ_OK ? rc : copyOut(s, out, cap);
+}
+
+}  // extern "C"

@@ -77,6 +77,8 @@ struct nz_buf {
   char* mc_ptr = nullptr;
 };
 
+constexpr int kMaxRanksHost = 8;
+
 struct nz_comm {
   int rank = 0;
   int world = 1;
@@ -97,10 +99,36 @@ struct nz_comm {
   int next_pad = 0;
 };
 
+struct nz_rail {
+  nz_comm* comm = nullptr;
+  int kind = 0;
+  int rail_id = 0;
+  int sm_budget = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<cudaStream_t> side;  // CE: one per peer so several copy engines run at once
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> join;
+  uint32_t* pad_local = nullptr;
+  uint32_t* pad_peer[kMaxRanksHost] = {};
+  uint32_t epoch = 0;
+  nz_fault_record_t* fault_host = nullptr;
+  nz_fault_record_t* fault_dev = nullptr;
+  int* wd_host = nullptr;
+  int* wd_dev = nullptr;
+  char* staging = nullptr;  // CE: (world-1) slots of staging_slot bytes
+  size_t staging_slot = 0;
+};
+
 namespace nz {
 // Host-side exchange: every rank contributes (bytes, fds); returns world
 // messages indexed by rank (own message included, fds only from peers).
 std::vector<nz_comm::Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std::vector<int>& fds);
 nz_buf* allocSymmetric(nz_comm* c, size_t bytes);
 void freeSymmetric(nz_buf* b);
+int elemSizeOf(int dtype);
+// rails.cu
+void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes,
+                   uint64_t chunk_begin, uint64_t chunk_end, int dtype, uint32_t op_seq, int64_t fail_chunk,
+                   cudaStream_t st);
+void launchStamp(uint64_t* dst, cudaStream_t st);
 }  // namespace nz

@@ -8,26 +8,6 @@
 #include "internal.h"
 #include "kernels.cuh"
 
-struct nz_rail {
-  nz_comm* comm = nullptr;
-  int kind = 0;
-  int rail_id = 0;
-  int sm_budget = 0;
-  cudaStream_t stream = nullptr;
-  std::vector<cudaStream_t> side;  // CE: one per peer so several copy engines run at once
-  cudaEvent_t fork = nullptr;
-  std::vector<cudaEvent_t> join;
-  uint32_t* pad_local = nullptr;
-  uint32_t* pad_peer[nz::kMaxRanks] = {};
-  uint32_t epoch = 0;
-  nz_fault_record_t* fault_host = nullptr;
-  nz_fault_record_t* fault_dev = nullptr;
-  int* wd_host = nullptr;
-  int* wd_dev = nullptr;
-  char* staging = nullptr;  // CE: (world-1) slots of staging_slot bytes
-  size_t staging_slot = 0;
-};
-
 namespace nz {
 
 namespace {
@@ -232,6 +212,18 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
 }
 
 }  // namespace
+
+int elemSizeOf(int dtype) { return elemSize(dtype); }
+
+__global__ void stamp_kernel(uint64_t* dst) {
+  *reinterpret_cast<volatile uint64_t*>(dst) = globaltimer();
+  __threadfence_system();
+}
+
+void launchStamp(uint64_t* dst, cudaStream_t st) {
+  stamp_kernel<<<1, 1, 0, st>>>(dst);
+  NZ_CUDA(cudaGetLastError());
+}
 
 // Used by the engine (engine.cpp) without going through the C ABI.
 void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes,

@@ -368,6 +368,7 @@ std::optional<FlushEvent> Balancer::recordOp(const Plan& plan, const std::vector
   }
   std::sort(means.begin(), means.end(), [](auto& a, auto& b) { return a.first < b.first; });
   windows_.erase(plan.bucket);
+  if (agree_) means = agree_(plan.bucket, means);
   FlushEvent fe;
   fe.bucket = plan.bucket;
   fe.means = means;

@@ -25,7 +25,7 @@ HealthMonitor::HealthMonitor(std::vector<int> rail_ids, double interval_us, int 
   }
   std::sort(rail_ids.begin(), rail_ids.end());
   for (int id : rail_ids) states_.push_back(HealthState{id, HealthStatus::Healthy, 0, 0});
-  healthy_since_.assign(states_.size(), 0);
+  healthy_since_.assign(states_.size(), -1.0);  // -1: no heartbeat streak yet
 }
 
 HealthState& HealthMonitor::find(int rail_id) {
@@ -41,10 +41,7 @@ const HealthState& HealthMonitor::state(int rail_id) const {
 void HealthMonitor::heartbeat(int rail_id, double now_us) {
   HealthState& s = find(rail_id);
   const size_t i = &s - states_.data();
-  if (s.status != HealthStatus::Failed && healthy_since_[i] == 0) healthy_since_[i] = now_us;
-  if (s.status == HealthStatus::Failed && (healthy_since_[i] == 0 || now_us < s.last_heartbeat_us)) {
-    healthy_since_[i] = now_us;  // a failed rail starts a fresh healthy streak
-  }
+  if (healthy_since_[i] < 0) healthy_since_[i] = now_us;  // streak starts at the first beat
   s.last_heartbeat_us = now_us;
   if (s.status == HealthStatus::Suspect) s.status = HealthStatus::Healthy;  // Suspect -> Healthy
 }
@@ -64,7 +61,7 @@ std::vector<int> HealthMonitor::tick(double now_us) {
       s.status = next;
       if (next == HealthStatus::Failed) {
         ++s.failure_epoch;
-        healthy_since_[i] = 0;
+        healthy_since_[i] = -1.0;
       }
       changed.push_back(s.rail_id);
     }
@@ -77,14 +74,14 @@ void HealthMonitor::channelDown(int rail_id) {
   if (s.status == HealthStatus::Failed) return;
   s.status = HealthStatus::Failed;
   ++s.failure_epoch;
-  healthy_since_[&s - states_.data()] = 0;
+  healthy_since_[&s - states_.data()] = -1.0;
 }
 
 void HealthMonitor::readmit(int rail_id, double now_us, double hold_us) {
   HealthState& s = find(rail_id);
   const size_t i = &s - states_.data();
   if (s.status != HealthStatus::Failed) throw std::invalid_argument("readmit: rail is not failed");
-  if (healthy_since_[i] == 0 || now_us - healthy_since_[i] < hold_us) {
+  if (healthy_since_[i] < 0 || now_us - healthy_since_[i] < hold_us) {
     throw std::invalid_argument("readmit: rail has not been healthy long enough");
   }
   s.status = HealthStatus::Healthy;

@@ -223,6 +223,9 @@ class Engine:
     def plan(self, nbytes: int) -> dict:
         return self._json(lib().nz_engine_plan_json, nbytes)
 
+    def last_plans(self) -> list:
+        return self._json(lib().nz_engine_last_plan_json)
+
     def close(self) -> None:
         if self.handle:
             check(lib().nz_engine_destroy(self.handle), "nz_engine_destroy")

@@ -1,0 +1,168 @@
+// Product C++ API known-answer tests, doctest style (shim in oracle/shim).
+// Compiled by tests/test_cpp.py against paper_2405_17870_b200/csrc/host.
+#define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
+#include <doctest.h>
+
+#include "nezha/balancer.hpp"
+#include "nezha/collective.hpp"
+#include "nezha/core/error.hpp"
+#include "nezha/engine.hpp"
+#include "nezha/faults.hpp"
+#include "nezha/util/toml.hpp"
+
+using namespace nezha;
+
+TEST_CASE("split_oversized (SPEC.md:212-214)") {
+  CHECK(splitOversized(512ull << 20).size() == 1);
+  CHECK(splitOversized(1ull << 30).size() == 1);
+  auto p = splitOversized(1536ull << 20);
+  CHECK(p.size() == 6);
+  CHECK(p.back().end() == (1536ull << 20));
+  CHECK(splitOversized(1).front().length == 1);
+  CHECK_THROWS_AS(splitOversized(0), std::invalid_argument);
+}
+
+TEST_CASE("chunk geometry (P10)") {
+  CHECK(defaultChunkBytes(64ull << 20, 8, Algorithm::RingChunked) == (4ull << 20));
+  CHECK(defaultChunkBytes(1 << 20, 8, Algorithm::RingChunked) == 65536);
+  CHECK(defaultChunkBytes(123, 8, Algorithm::Ring) == 123);
+  auto g = makeGeometry(Segment{100, 1000000}, 2, Algorithm::RingChunked);
+  CHECK(g.chunk_bytes == 250000);
+  CHECK(g.numChunks() == 4);
+  CHECK(g.chunk(3) == Segment{100 + 750000, 250000});
+  CHECK(ringBlockOf(0, 10, 4) == 0);
+  CHECK(ringBlockOf(9, 10, 4) == 3);
+  CHECK(ringBlockOf(2, 3, 4) == 3);
+}
+
+TEST_CASE("Eq. 4/5/8 known answers (SPEC.md:273, :284, :291-293)") {
+  RailProfile a{.rail_id = 0, .t_setup_us = 10, .bandwidth_bps = 10e9};
+  RailProfile b{.rail_id = 1, .t_setup_us = 1000, .bandwidth_bps = 12.5e9};
+  auto c = coldLatency({a, b}, 1000000);
+  CHECK(c.first == doctest::Approx(110.0));
+  CHECK(c.second == 0);
+  RailProfile x{.rail_id = 0, .t_setup_us = 100, .bandwidth_bps = 1e9};
+  RailProfile y{.rail_id = 1, .t_setup_us = 300, .bandwidth_bps = 1e9};
+  CHECK(hotLatency({x, y}, {0.75, 0.25}, 1000000, 0) == doctest::Approx(850.0));
+  CHECK_THROWS_AS(hotLatency({x, y}, {0.75, 0.75}, 1000000, 0), std::invalid_argument);
+  auto i8 = initCoefficients({100, 300});
+  CHECK(i8[0] == doctest::Approx(0.75));
+  auto i3 = initCoefficients({1, 1, 2});
+  CHECK(i3[2] == doctest::Approx(0.25));
+  CHECK_THROWS_AS(initCoefficients({1, 0}), std::invalid_argument);
+}
+
+TEST_CASE("Eq. 7 step bound and simplex (P4, SPEC.md:297, :340)") {
+  bool conv = false;
+  auto a = updateCoefficients({0.2, 0.3, 0.5}, {50, 80, 200}, 0.05, 0.01, &conv);
+  double l1 = 0, s = 0;
+  const double before[3] = {0.2, 0.3, 0.5};
+  for (int i = 0; i < 3; ++i) {
+    l1 += std::fabs(a[i] - before[i]);
+    s += a[i];
+    CHECK(a[i] >= 0);
+  }
+  CHECK(l1 <= 0.05 + 1e-12);
+  CHECK(std::fabs(s - 1.0) <= 1e-9);
+  CHECK_FALSE(conv);
+  auto same = updateCoefficients({0.5, 0.5}, {100, 100.5}, 0.05, 0.01, &conv);
+  CHECK(conv);
+  CHECK(same[0] == 0.5);
+}
+
+TEST_CASE("Eq. 6 threshold for identical rails = 2 B T_sync (SPEC.md:309)") {
+  RailProfile a{.rail_id = 0, .t_setup_us = 10, .bandwidth_bps = 1e9};
+  RailProfile b{.rail_id = 1, .t_setup_us = 10, .bandwidth_bps = 1e9};
+  auto f = [&](Bytes S) { return hotLatency({a, b}, {0.5, 0.5}, S, 50.0) - coldLatency({a, b}, S).first; };
+  const Bytes t = findThreshold(f, 4096, 1ull << 30);
+  CHECK(static_cast<double>(t) == doctest::Approx(100000.0).epsilon(1e-3));
+}
+
+TEST_CASE("rho gate (SPEC.md:265, :320)") {
+  RailProfile sharp{.rail_id = 0, .t_setup_us = 0, .bandwidth_bps = 0.73e9};
+  RailProfile tcp{.rail_id = 1, .t_setup_us = 0, .bandwidth_bps = 0.06e9};
+  CHECK(efficiencyRatio({sharp, tcp}, {0.5, 0.5}, 32768) == doctest::Approx(0.73 / 0.06));
+  BalancerConfig cfg;
+  Balancer bal({sharp, tcp}, cfg);
+  auto p = bal.allocate(32768);
+  CHECK(p.segments.size() == 1);
+  CHECK(p.segments[0].rail_id == 0);
+}
+
+TEST_CASE("record_latency flushes at the 100th sample (SPEC.md:326-328)") {
+  LatencyWindow w(0, 13, 100);
+  for (int i = 0; i < 99; ++i) CHECK_FALSE(w.record(1.0 + i).has_value());
+  auto m = w.record(100.0);
+  REQUIRE(m.has_value());
+  CHECK(*m == doctest::Approx(50.5));
+  CHECK(w.size() == 0);
+}
+
+TEST_CASE("allocate covers S disjointly in rail order (P8)") {
+  RailProfile a{.rail_id = 0, .t_setup_us = 5, .bandwidth_bps = 1e11};
+  RailProfile b{.rail_id = 1, .t_setup_us = 5, .bandwidth_bps = 1e11};
+  BalancerConfig cfg;
+  cfg.sync_overhead_us = 1;
+  Balancer bal({a, b}, cfg);
+  auto p = bal.allocate(8ull << 20);
+  REQUIRE(p.segments.size() == 2);
+  CHECK(p.segments[0].segment == Segment{0, 4ull << 20});
+  CHECK(p.segments[1].segment == Segment{4ull << 20, 4ull << 20});
+  std::vector<Segment> segs;
+  for (auto& s : p.segments) segs.push_back(s.segment);
+  CHECK(segmentsCoverExactly(segs, 8ull << 20));
+}
+
+TEST_CASE("handoff target = argmax data_length, ties lowest id (P9, SPEC.md:411)") {
+  Plan p;
+  p.segments = {{0, {0, 100}}, {1, {100, 300}}, {2, {400, 300}}};
+  CHECK(*chooseHandoffTarget(p, 0, {0, 1, 2}) == 1);
+  CHECK(*chooseHandoffTarget(p, 1, {0, 1, 2}) == 2);
+  CHECK(!chooseHandoffTarget(p, 0, {0}).has_value());
+  CHECK(orphanOf(Segment{1000, 500}, 100, 2) == Segment{1200, 300});
+  CHECK(orphanOf(Segment{1000, 500}, 100, 5).length == 0);
+}
+
+TEST_CASE("health monitor (SPEC.md:383-406)") {
+  HealthMonitor m({0, 1}, 50000, 2, 3);
+  m.heartbeat(0, 0);
+  m.heartbeat(1, 0);
+  CHECK(m.tick(60000).empty());  // transient 60 ms stall: below threshold
+  auto ch = m.tick(110000);
+  CHECK(ch.size() == 2);
+  CHECK(m.state(0).status == HealthStatus::Suspect);
+  m.heartbeat(0, 120000);
+  CHECK(m.state(0).status == HealthStatus::Healthy);  // Suspect -> Healthy
+  m.tick(160000);
+  CHECK(m.state(1).status == HealthStatus::Failed);
+  m.heartbeat(1, 200000);
+  CHECK(m.state(1).status == HealthStatus::Failed);  // sticky
+  CHECK_THROWS_AS(m.readmit(1, 300000), std::invalid_argument);  // < 1 s healthy
+  m.readmit(1, 1300000);
+  CHECK(m.state(1).status == HealthStatus::Healthy);
+  CHECK_THROWS_AS(m.readmit(0, 0), std::invalid_argument);  // not failed
+  m.channelDown(0);
+  CHECK(m.state(0).status == HealthStatus::Failed);
+}
+
+TEST_CASE("rails TOML schema (SPEC.md:526)") {
+  auto rails = parseRailsToml(R"(
+[[rail]]
+protocol = "sharp"
+t_setup_us = 9.0
+bandwidth_bps = 12.5e9
+calibration = [[1024, 9.0], [8388608, 22140.0]]
+[[rail]]
+protocol = "ce"
+t_setup_us = 40
+bandwidth_bps = 4.0e11
+sm_budget = 16
+)");
+  REQUIRE(rails.size() == 2);
+  CHECK(rails[0].kind == NZ_RAIL_NVLS);
+  CHECK(rails[0].profile.efficiency_points.size() == 2);
+  CHECK(rails[1].kind == NZ_RAIL_CE);
+  CHECK(rails[1].sm_budget == 16);
+  CHECK(rails[1].rail_id == 1);
+  CHECK_THROWS_AS(toml::parse("a = 1\na = 2\n"), std::runtime_error);
+}

@@ -1,0 +1,101 @@
+"""GPU: the multi-rail engine end to end (planner + rails + handoff) against
+the CPU oracle, one process per GPU, through the C ABI."""
+import json
+import os
+
+import pytest
+
+from tests.conftest import gpu_count
+from tests.mp_util import spawn
+
+pytestmark = [pytest.mark.gpu]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "workers", "engine_worker.py")
+
+# Rails with a fixed profile so the hot split is exercised deterministically.
+TOML3 = """
+[[rail]]
+protocol = "nvls"
+t_setup_us = 12.0
+bandwidth_bps = 6.0e11
+[[rail]]
+protocol = "ce"
+t_setup_us = 40.0
+bandwidth_bps = 5.0e11
+[[rail]]
+protocol = "sm"
+t_setup_us = 14.0
+bandwidth_bps = 5.0e11
+"""
+
+
+def _run(world, spec, timeout=600):
+    res = spawn(world, WORKER, [json.dumps(spec)], timeout=timeout)
+    for rk in res:
+        for r in rk["results"]:
+            assert r["mismatch"] == 0, r
+    return res
+
+
+def test_engine_single_gpu_identity():
+    """N = 1: every plan degenerates to a local copy; result = input."""
+    if gpu_count() < 1:
+        pytest.skip("no GPU")
+    spec = {"rails": ["nvls", "ce", "sm"], "calibrate_max_bytes": 1 << 22,
+            "cases": [{"dtype": "f32", "nbytes": 1 << 20}, {"dtype": "bf16", "nbytes": 3_000_002},
+                      {"dtype": "i32", "nbytes": 4096, "host": True}]}
+    _run(1, spec)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_engine_multirail_parity(world):
+    if gpu_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4,
+            "cases": [
+                {"dtype": "f32", "nbytes": 64 << 20, "reps": 10},
+                {"dtype": "bf16", "nbytes": 48 << 20, "reps": 2},
+                {"dtype": "i32", "nbytes": 32 << 20 + 12, "reps": 2},
+                {"dtype": "f32", "nbytes": 8192, "reps": 3},
+                {"dtype": "f32", "nbytes": 1 << 20, "reps": 2, "host": True},
+            ]}
+    res = _run(world, spec, timeout=900)
+    # Every rank ran the same plans (the table is agreed across ranks).
+    plans = [[r["segs"] for r in rk["results"]] for rk in res]
+    assert all(p == plans[0] for p in plans)
+
+
+@pytest.mark.multigpu
+def test_engine_oversized_split():
+    """Payloads above 1 GiB run as 256 MiB pieces."""
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    n = (1 << 30) + (64 << 20)
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "calibrate_max_bytes": 1 << 20,
+            "cases": [{"dtype": "f32", "nbytes": n}]}
+    res = _run(2, spec, timeout=900)
+    r = res[0]["results"][0]
+    assert max(s[1] + s[2] for s in r["segs"]) == n
+    assert len({(s[1] // (256 << 20)) for s in r["segs"]}) == 5
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("fail_rail", [0, 1, 2])
+def test_engine_failover_reroute(fail_rail):
+    world = 4 if gpu_count() >= 4 else 2
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3,
+            "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 3, "fail": [fail_rail, 3], "fail_rep": 1},
+                      {"dtype": "i32", "nbytes": 64 << 20, "reps": 2}]}
+    res = _run(world, spec, timeout=900)
+    for rk in res:
+        fo = [r for r in rk["results"] if "failover" in r][0]["failover"]
+        assert fo is not None and fo["failed_rail"] == fail_rail
+        assert fo["target_rail"] != fail_rail and fo["orphan_length"] > 0
+        # After the failure the rail carries nothing.
+        later = [r for r in rk["results"] if r["case"] == 0 and r["rep"] == 2] + \
+                [r for r in rk["results"] if r["case"] == 1]
+        for r in later:
+            assert all(s[0] != fail_rail for s in r["segs"]), r

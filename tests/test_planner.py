@@ -1,0 +1,240 @@
+"""Planner parity: the product's balancer + faults decisions (C++, reached
+through nz_planner_run_trace in libnezha_b200.so) must equal the oracle's
+independent restatement (oracle/planner.py) byte for byte on the same
+injected per-rail latency / failure traces; plus the SPEC's known answers.
+CPU only."""
+import math
+
+import pytest
+
+from oracle import planner as P
+
+lib_missing = False
+try:
+    from paper_2405_17870_b200 import run_trace
+    from paper_2405_17870_b200 import lib as _lib
+
+    _lib()
+except Exception:  # pragma: no cover
+    lib_missing = True
+
+needs_lib = pytest.mark.skipif(lib_missing, reason="libnezha_b200.so not built")
+
+
+# ------------------------------------------------------------ SPEC known answers
+def test_cold_latency_example():
+    # (10 us, 10 GB/s) and (1000 us, 12.5 GB/s), S = 1e6 -> 110 us on rail 0
+    rails = [P.Rail(0, 10, 10e9), P.Rail(1, 1000, 12.5e9)]
+    t, best = P.cold(rails, 1_000_000)
+    assert best == 0 and t == pytest.approx(110.0)
+    # identical rails -> rail 0 by tie-break
+    assert P.cold([P.Rail(0, 5, 1e9), P.Rail(1, 5, 1e9)], 4096)[1] == 0
+
+
+def test_hot_latency_examples():
+    # (100 us, 1 GB/s), (300 us, 1 GB/s), alpha (0.75, 0.25), S = 1e6 -> 850 us
+    rails = [P.Rail(0, 100, 1e9), P.Rail(1, 300, 1e9)]
+    assert P.hot(rails, [0.75, 0.25], 1_000_000, 0.0) == pytest.approx(850.0)
+    # unit vector -> that rail + sync
+    assert P.hot(rails, [0.0, 1.0], 1_000_000, 7.0) == pytest.approx(300 + 1000 + 7.0)
+    # symmetric halves
+    sym = [P.Rail(0, 10, 1e9), P.Rail(1, 10, 1e9)]
+    assert P.hot(sym, [0.5, 0.5], 2_000_000, 0.0) == pytest.approx(10 + 1000)
+    with pytest.raises(ValueError):
+        P.hot(rails, [0.7, 0.7], 1000, 0.0)
+
+
+def test_init_coefficients_examples():
+    # SPEC.md:291-293
+    assert P.eq8([100.0, 300.0]) == [0.75, 0.25]
+    a = P.eq8([1.0, 1.0, 2.0])
+    assert a == pytest.approx([3 / 8, 3 / 8, 2 / 8]) and sum(a) == pytest.approx(1.0)
+    assert P.eq8([5.0] * 4) == pytest.approx([0.25] * 4)
+    with pytest.raises(ValueError):
+        P.eq8([1.0, 0.0])
+
+
+def test_update_coefficients_properties():
+    # fixed point, direction, simplex, |a'-a|_1 <= eta
+    a, conv = P.eq7([0.5, 0.5], [100.0, 100.0], 0.05, 0.01)
+    assert conv and a == [0.5, 0.5]
+    a, conv = P.eq7([0.5, 0.5], [120.0, 100.0], 0.05, 0.01)
+    assert not conv and a[0] < 0.5 < a[1] and sum(a) == pytest.approx(1.0)
+    a3, _ = P.eq7([0.2, 0.3, 0.5], [50.0, 80.0, 200.0], 0.05, 0.01)
+    assert sum(abs(x - y) for x, y in zip(a3, [0.2, 0.3, 0.5])) <= 0.05 + 1e-12
+
+
+def test_convergence_to_equal_finish_time():
+    # t_setup 100/300 us, equal B, S = 1 MB -> alpha* = (T2-T1+S/B2)/(S/B1+S/B2)
+    rails = [P.Rail(0, 100, 1e9), P.Rail(1, 300, 1e9)]
+    S = 1_000_000
+    want = (300 - 100 + 1000) / (1000 + 1000)
+    a = [0.5, 0.5]
+    for _ in range(2000):
+        lens = P.split(a, S)
+        T = [rails[i].latency(lens[i]) for i in range(2)]
+        a, conv = P.eq7(a, T, 0.05, 0.0005)
+        if conv:
+            break
+    assert abs(a[0] - want) <= 0.05
+
+
+def test_threshold_identical_rails():
+    # identical rails with sync T_sync -> threshold = 2 B T_sync
+    B, Ts = 1e9, 50.0
+    rails = [P.Rail(0, 10, B), P.Rail(1, 10, B)]
+    f = lambda S: P.hot(rails, [0.5, 0.5], S, Ts) - P.cold(rails, S)[0]
+    thr = P.threshold(f, 4096, 1 << 30)
+    assert thr == pytest.approx(2 * B * Ts * 1e-6, rel=1e-3)
+    # sync = 0 -> hot wins everywhere probed
+    f0 = lambda S: P.hot(rails, [0.5, 0.5], S, 0.0) - P.cold(rails, S)[0]
+    assert P.threshold(f0, 4096, 1 << 30) == 4095
+    # hot never wins -> +inf
+    slow = [P.Rail(0, 1, 1e12), P.Rail(1, 10_000, 1e6)]
+    fs = lambda S: P.hot(slow, [0.5, 0.5], S, 0.0) - P.cold(slow, S)[0]
+    assert P.threshold(fs, 4096, 1 << 30) is None
+
+
+def test_rho_gate_examples():
+    # identical rails, equal split -> 1
+    assert P.rho([P.Rail(0, 5, 1e9), P.Rail(1, 5, 1e9)], [0.5, 0.5], 1 << 20) == 1.0
+    # SHARP 0.73 GB/s vs TCP 0.06 GB/s at 32 KB -> ~12.2 > 5
+    S = 32 * 1024
+    sharp = P.Rail(0, 0.0, 0.73e9)
+    tcp = P.Rail(1, 0.0, 0.06e9)
+    assert P.rho([sharp, tcp], [0.5, 0.5], S) == pytest.approx(0.73 / 0.06, rel=1e-6)
+
+
+def test_split_examples():
+    # S = 8 MB, alpha (0.5, 0.5) -> two 4 MB segments
+    assert P.split([0.5, 0.5], 8 << 20) == [4 << 20, 4 << 20]
+    # round4 down, remainder to the last participant
+    assert P.split([1 / 3, 1 / 3, 1 / 3], 1000) == [332, 332, 336]
+    assert P.split([0.0, 1.0, 0.0], 1000) == [0, 1000, 0]
+
+
+# ------------------------------------------------------- product vs oracle traces
+TWO_HOMOG = """
+world 8
+config sync_us 20 window 10 max_iters 100
+rail 0 tcp 30 1.25e9
+rail 1 tcp 30 1.25e9
+truth 0 30 1.25e9 0.05
+truth 1 30 1.25e9 0.05
+truth_sync 20
+seed 3
+ops 40 8192
+ops 60 262144
+ops 80 8388608
+ops 40 67108864
+"""
+
+THREE_HETERO = """
+world 8
+config sync_us 6 window 20 eta 0.1
+rail 0 nvls 12 7.0e11
+rail 1 ce 45 5.0e11
+rail 2 sm 15 4.5e11
+truth 0 14 6.2e11 0.04
+truth 1 40 3.8e11 0.04
+truth 2 16 3.0e11 0.04
+truth_sync 5
+seed 7
+ops_loguniform 3000 8192 4194304
+ops 300 268435456
+"""
+
+FAILOVER = """
+world 8
+config sync_us 6 window 10
+rail 0 nvls 12 7.0e11
+rail 1 ce 45 5.0e11
+rail 2 sm 15 4.5e11 cal 4096:15 65536:16 1048576:18.5 67108864:170 1073741824:2400
+truth 0 14 6.2e11 0.02
+truth 1 40 3.8e11 0.02
+truth 2 16 3.0e11 0.02
+seed 11
+ops 50 268435456
+fail 20 0 7
+ops 30 268435456
+readmit 70 0
+ops 40 1048576
+fail 90 2 0
+ops 20 4096
+"""
+
+GATED = """
+world 4
+config sync_us 1 window 5
+rail 0 sharp 0 0.73e9
+rail 1 tcp 0 0.06e9
+truth 0 1 0.73e9 0
+truth 1 1 0.06e9 0
+seed 1
+ops 30 32768
+ops 30 67108864
+fail 40 1 0
+fail 45 0 0
+ops 10 65536
+"""
+
+RING_ALGO = """
+world 4
+algorithm ring
+config sync_us 3 window 8 demote_after 2
+rail 0 nvls 10 6e11
+rail 1 ce 30 5.5e11
+truth 0 10 3e11 0.1
+truth 1 30 2.5e11 0.1
+seed 5
+ops 100 134217728
+fail 60 1 0
+"""
+
+
+@needs_lib
+@pytest.mark.parametrize("name,scenario", [("two_homog", TWO_HOMOG), ("three_hetero", THREE_HETERO),
+                                           ("failover", FAILOVER), ("gated", GATED), ("ring", RING_ALGO)])
+def test_trace_parity_byte_exact(name, scenario):
+    got = run_trace(scenario)
+    want = P.run(scenario)
+    g, w = got.splitlines(), want.splitlines()
+    for i, (a, b) in enumerate(zip(g, w)):
+        assert a == b, f"{name}: first difference at line {i}:\nproduct: {a}\noracle:  {b}"
+    assert len(g) == len(w)
+
+
+@needs_lib
+def test_trace_behaviour_three_rails():
+    """Config 3 shape: cold for small payloads, hot (split) for large ones, flushes happen."""
+    import json
+
+    lines = [json.loads(l) for l in run_trace(THREE_HETERO).splitlines()]
+    ops = [l for l in lines if "op" in l and "segs" in l]
+    small = [o for o in ops if o["S"] < 64 * 1024]
+    big = [o for o in ops if o["S"] >= 256 << 20]
+    assert all(len(o["segs"]) == 1 for o in small)
+    assert all(len(o["segs"]) == 3 for o in big)
+    assert any("flush" in l for l in lines)
+
+
+@needs_lib
+def test_trace_failover_tickets():
+    import json
+
+    lines = [json.loads(l) for l in run_trace(FAILOVER).splitlines()]
+    fails = [l for l in lines if "fail" in l]
+    first = fails[0]
+    assert first["ticket"]["source"] == 0
+    # target = surviving rail with the largest data_length in that op (P9)
+    op = [l for l in lines if l.get("op") == 20 and "segs" in l][0]
+    lens = {s[0]: s[2] for s in op["segs"] if s[0] != 0}
+    assert first["ticket"]["target"] == max(sorted(lens), key=lambda r: lens[r])
+    seg0 = [s for s in op["segs"] if s[0] == 0][0]
+    C = P.chunk_bytes(seg0[2], 8)
+    assert first["ticket"]["offset"] == seg0[1] + 7 * C
+    assert first["ticket"]["length"] == seg0[2] - 7 * C
+    # after the failure rail 0 never appears until readmitted at op 70
+    for l in lines:
+        if "segs" in l and 20 < l["op"] < 70:
+            assert all(s[0] != 0 for s in l["segs"])
