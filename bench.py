@@ -1,0 +1,430 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 multi-rail allreduce (Nezha, arxiv 2405.17870).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Metric (BASELINE.json): 8-GPU allreduce busbw GB/s vs size (4KB-1GB); 8KB p50
+latency; failover ms. A "step" is one engine allreduce of the headline payload
+(1 GiB fp32, synthetic) on the configured rails (default configs[1]: NVLS +
+copy-engine rails, load balanced). `value` = busbw = ringVolume(N, S) / t with
+t the max over ranks of the device time per step (N = 1: algbw S / t, no
+NVLink exchange exists). Inputs are 1 GiB, larger than the 126 MB L2, so no
+flush is needed between steps. Rank 0 prints one JSON line.
+
+Reference arm (--impl reference): the CPU baseline — the SPEC ring restated on
+the reference's own InMemoryFabric (oracle/_ref, compiled from
+/root/reference/proj/src), ranks as threads, timed on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "8-GPU allreduce busbw GB/s vs size (4KB–1GB); 8KB p50 latency; failover ms"
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (nominal); BASELINE.md roofline
+GiB = 1 << 30
+
+
+def ring_volume(n: int, s: int) -> int:
+    return (2 * (n - 1) * s + n // 2) // n if n >= 2 else 0
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", os.environ.get("RANK", "0"))))
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            p = [x.strip() for x in l.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline ---
+def cpu_baseline(world_sim: int = 8, nbytes: int = 64 << 20, budget_s: float = 20.0):
+    """Config 1 of BASELINE.json on the host: world_sim simulated ranks (threads)
+    on the reference InMemoryFabric, 2 identical rails, static 50/50 split, Ring,
+    64 KiB frames, fp32. Returns the busbw GB/s and the sample description."""
+    import numpy as np
+
+    import oracle  # CPU baseline leg: the only bench use of oracle/
+
+    if not oracle.inmem_available():
+        return None
+    inputs = [oracle.synthetic_input(oracle.F32, r, nbytes) for r in range(world_sim)]
+    outs = [np.zeros_like(inputs[0]) for _ in range(world_sim)]
+    half = (nbytes // 2) & ~3
+    segs = [(0, 0, half), (1, half, nbytes - half)]
+    oracle.inmem_allreduce(inputs, oracle.F32, segs, 2, chunked=False, outputs=outs)  # warm-up
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 20):
+        _, us, _ = oracle.inmem_allreduce(inputs, oracle.F32, segs, 2, chunked=False, outputs=outs)
+        times.append(us * 1e-6)
+    t = statistics.mean(times)
+    threads = world_sim * 2
+    return {"value": round(ring_volume(world_sim, nbytes) / t / 1e9, 4), "unit": "GB/s", "cores": threads,
+            "host_cpus": len(os.sched_getaffinity(0)), "kind": "port",
+            "sample": f"config 1: {world_sim} simulated ranks x 2 rails (threads), fp32 {nbytes >> 20} MiB, static "
+                      f"50/50, Ring, 64 KiB frames, {len(times)} timed ops (mean {t * 1e3:.1f} ms/op); SPEC ring "
+                      f"restated on the reference InMemoryFabric compiled from /root/reference/proj/src"}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    world_sim = max(2, world)
+    nbytes = 64 << 20
+    res = cpu_baseline(world_sim, nbytes, budget_s=max(5.0, 3.0 * args.steps))
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return 0
+    v = res["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ring_volume(world_sim, nbytes) / (v * 1e9) * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"CPU allreduce, {world_sim} simulated ranks, 2 rails 50/50, 64 MiB fp32 sample",
+                       "global_batch": nbytes, "seq_len": 0, "parallelism": f"dp{world_sim} (threads)"},
+            "cpu_baseline": res,
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------- our arm ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rails", default="nvls,ce", help="comma list of nvls|ce|sm (configs[1] = nvls,ce)")
+    ap.add_argument("--bytes", type=int, default=GiB)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
+    ap.add_argument("--tune-ops", type=int, default=200, help="balancer convergence ops before timing")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-failover", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep-max", type=int, default=GiB)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    from paper_2405_17870_b200 import Comm, Engine, Rail, SymmetricBuffer
+    from paper_2405_17870_b200._lib import DTYPES, RAIL_KINDS
+    from paper_2405_17870_b200.runtime import kernel_launch_count
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    session = f"bench-{os.environ.get('MASTER_PORT', '0')}-{os.environ.get('TORCHELASTIC_RUN_ID', str(os.getppid()))}"
+    comm = Comm(rank, world, local, session)
+    kinds = args.rails.split(",")
+    dt = DTYPES[args.dtype]
+    S = args.bytes
+    eng = Engine(comm, kinds=kinds, window=10, eta=0.2, calibrate_max_bytes=min(GiB, max(S, 1 << 20)))
+
+    def max_over_ranks(x: float) -> float:
+        vals = comm.allgather_bytes(json.dumps(x).encode().ljust(32))
+        return max(json.loads(v.decode().strip()) for v in vals)
+
+    cap = max(S, args.sweep_max if not args.no_sweep else 0, 8192)
+    bin_, bout = SymmetricBuffer(comm, cap), SymmetricBuffer(comm, cap)
+    g = torch.Generator(device="cuda").manual_seed(0x4E5A0000 + rank)
+    tdt = {0: torch.float32, 1: torch.bfloat16, 2: torch.int32}[dt]
+    if dt == 2:
+        x = torch.randint(-(1 << 20), 1 << 20, (cap // 4,), device="cuda", generator=g, dtype=torch.int32)
+    else:
+        x = (torch.rand(cap // x_es(dt), device="cuda", generator=g) * 2 - 1).to(tdt)
+    bin_.write(x.data_ptr(), cap)
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+
+    def timed(nbytes, iters, warm):
+        for _ in range(warm):
+            eng.allreduce(bin_, bout, nbytes, dt, stream)
+        eng.synchronize()
+        comm.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            eng.allreduce(bin_, bout, nbytes, dt, stream)
+        e1.record(stream)
+        e1.synchronize()
+        eng.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / iters
+        return max_over_ranks(t)
+
+    # Balancer convergence on the headline size (one-time, like NCCL tuning).
+    for _ in range(args.tune_ops):
+        eng.allreduce(bin_, bout, S, dt, stream)
+    eng.synchronize()
+
+    # ---- headline: K timed steps of S bytes --------------------------------
+    for _ in range(max(args.warmup, 3)):
+        eng.allreduce(bin_, bout, S, dt, stream)
+    eng.synchronize()
+    eng.stats_reset()
+    comm.barrier()
+    torch.cuda.synchronize()
+    launches0 = kernel_launch_count()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.allreduce(bin_, bout, S, dt, stream)
+        e1.record(stream)
+        e1.synchronize()
+    launches = kernel_launch_count() - launches0
+    eng.synchronize()
+    t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.steps)
+    busbw = ring_volume(world, S) / t_step / 1e9
+    algbw = S / t_step / 1e9
+    value = busbw if world > 1 else algbw
+    plan = eng.last_plans()[0] if eng.last_plans() else {}
+    # Dominant rail (largest share): its per-op time on its own stream.
+    peaks = measured_peaks()
+    stats = {k: eng.rail_stats(i) for i, k in enumerate(kinds)}
+    dom = max(range(len(kinds)), key=lambda i: stats[kinds[i]]["bytes"])
+    st = stats[kinds[dom]]
+    roofline = None
+    if st["ops"]:
+        t_rail = max_over_ranks(st["total_us"] / st["ops"] * 1e-6)
+        seg = st["bytes"] / st["ops"]
+        if world > 1:
+            ach = ring_volume(world, int(seg)) / t_rail / 1e9
+            roofline = {"bound": "nvlink", "kernel": f"{kinds[dom]} rail", "achieved": round(ach, 1),
+                        "peak": NVLINK_GBS, "unit": "GB/s", "frac": round(ach / NVLINK_GBS, 4), "traffic": None,
+                        "per_launch_bytes": ring_volume(world, int(seg)),
+                        "note": "achieved = ringVolume(N, segment) / rail time per op (CUDA events on the rail "
+                                "stream); peak = NVLink 5 900 GB/s per direction (nominal; measured peer copy "
+                                "770, B200_PROFILING.md)"}
+        else:
+            hbm = peaks.get("hbm_gbs", 6650.0)
+            ach = 2 * seg / t_rail / 1e9
+            roofline = {"bound": "hbm", "kernel": f"{kinds[dom]} rail (N=1 copy)", "achieved": round(ach, 1),
+                        "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                        "per_launch_bytes": int(2 * seg),
+                        "note": "N=1: the allreduce is a copy in->out, 2S HBM bytes; peak = MEASURED_PEAKS.json "
+                                "hbm_gbs" + ("" if "hbm_gbs" in peaks else " (fallback)")}
+
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+           "config": {"workload": f"configs[1]: {'+'.join(kinds)} rails, load-balanced {args.dtype} allreduce of "
+                                  f"{S} B per rank (value = busbw at this size; N=1: algbw)",
+                      "global_batch": S, "seq_len": 0, "parallelism": f"dp{world}",
+                      "l2": "inputs (1 GiB) larger than the 126 MB L2; no flush",
+                      "algbw_GBs": round(algbw, 2), "busbw_GBs": round(busbw, 2), "plan": plan},
+           "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary()}
+
+    # ---- NCCL on the same sizes --------------------------------------------
+    nccl = {}
+    pg = None
+    if world > 1 and not args.no_nccl:
+        import torch.distributed as dist
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            pg = dist
+        except Exception as e:  # pragma: no cover
+            out["nccl_error"] = str(e)[:200]
+
+    def nccl_time(nbytes, iters):
+        t = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+        for _ in range(5):
+            pg.all_reduce(t)
+        torch.cuda.synchronize()
+        pg.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            pg.all_reduce(t)
+        b.record()
+        b.synchronize()
+        return max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
+
+    if pg is not None:
+        tn = nccl_time(S, max(5, args.steps // 2))
+        nccl["busbw_headline"] = round(ring_volume(world, S) / tn / 1e9, 2)
+        out["nccl_busbw_GBs"] = nccl["busbw_headline"]
+
+    # ---- sweep 4 KiB .. 1 GiB ----------------------------------------------
+    if not args.no_sweep:
+        sweep = []
+        s = 4096
+        while s <= min(args.sweep_max, cap):
+            it = 200 if s <= (1 << 20) else (40 if s <= (64 << 20) else 8)
+            t = timed(s, it, warm=20 if s <= (64 << 20) else 4)
+            row = {"bytes": s, "us": round(t * 1e6, 2), "algbw_GBs": round(s / t / 1e9, 2),
+                   "busbw_GBs": round(ring_volume(world, s) / t / 1e9, 2),
+                   "hot": bool(eng.last_plans()[0]["hot"]) if eng.last_plans() else None,
+                   "rails": sorted({seg[0] for p in eng.last_plans() for seg in p["segs"]})}
+            if pg is not None:
+                tn = nccl_time(s, it)
+                row["nccl_busbw_GBs"] = round(ring_volume(world, s) / tn / 1e9, 2)
+                row["nccl_us"] = round(tn * 1e6, 2)
+            sweep.append(row)
+            s *= 2
+        out["sweep"] = sweep
+
+    # ---- 8 KiB p50 latency: engine (cold start) vs each rail alone vs NCCL --
+    def p50_host(fn, n=300):
+        lat = []
+        for _ in range(n):
+            comm.barrier()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            lat.append(time.perf_counter() - t0)
+        return max_over_ranks(statistics.median(lat) * 1e6)
+
+    lat = {}
+    lat["engine_us"] = round(p50_host(lambda: eng.allreduce(bin_, bout, 8192, dt, stream)), 2)
+    if world > 1:
+        for k in ("nvls", "ce", "sm"):
+            if k == "nvls" and not comm.multicast:
+                continue
+            r = Rail(comm, RAIL_KINDS[k], 10 + len(lat))
+            lat[f"{k}_alone_us"] = round(p50_host(lambda: (r.allreduce(bin_, bout, 0, 8192, 65536, dt),
+                                                            r.synchronize())), 2)
+            r.close()
+        if pg is not None:
+            t8 = torch.empty(2048, dtype=torch.float32, device="cuda")
+            lat["nccl_us"] = round(p50_host(lambda: pg.all_reduce(t8)), 2)
+    out["latency_8k_p50_us"] = lat
+
+    # ---- e2e through the public host API (H2D + allreduce + D2H) ------------
+    if not args.no_e2e:
+        hin = torch.empty(S, dtype=torch.uint8).pin_memory()
+        hout = torch.empty(S, dtype=torch.uint8).pin_memory()
+        hin.copy_(x.view(torch.uint8)[:S].cpu())
+        for _ in range(2):
+            eng.allreduce_host(hin, hout, S, dt)
+        k = max(3, min(args.steps, 10))
+        comm.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            eng.allreduce_host(hin, hout, S, dt)
+        te = max_over_ranks((time.perf_counter() - t0) / k)
+        eng.synchronize()
+        ev = (ring_volume(world, S) if world > 1 else S) / te / 1e9
+        out["e2e"] = {"value": round(ev, 2), "unit": "GB/s", "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
+                      "ms_per_step": round(te * 1e3, 3),
+                      "note": "nz_engine_allreduce_host from pinned host memory, wall clock, max over ranks"}
+
+    # ---- failover: config 4 shape (bf16 256 MiB, largest-alpha rail fails mid-op)
+    if world > 1 and not args.no_failover and len(kinds) > 1:
+        fs = min(256 << 20, cap)
+        plan_f = eng.plan(fs)["pieces"][0]["plan"]
+        segs = plan_f["segs"]
+        if len(segs) > 1:
+            victim = max(segs, key=lambda sgm: sgm[2])
+            nch =-(-victim[2] // max(65536, (victim[2] // (2 * world)) & ~3))
+            eng.inject_failure(eng.op_seq, victim[0], nch // 2)
+            eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
+            eng.synchronize()
+            fo = eng.last_failover()
+            if fo:
+                out["failover"] = {"failed_rail": kinds[fo["failed_rail"]], "target_rail": kinds[fo["target_rail"]],
+                                   "orphan_bytes": fo["orphan_length"], "detect_us": round(fo["detect_us"], 2),
+                                   "resume_us": round(fo["resume_us"], 2), "done_us": round(fo["done_us"], 2),
+                                   "payload": "bf16 256 MiB"}
+                out["failover_ms"] = round(max_over_ranks(fo["resume_us"]) / 1e3, 4)
+            eng.readmit(victim[0])
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
+    if world == 1 and rank == 0 and not args.no_cpu:
+        cb = cpu_baseline()
+        if cb:
+            out["cpu_baseline"] = cb
+
+    out["engine_state"] = {"sync_overhead_us": eng.state()["sync_overhead_us"]}
+    eng.close()
+    bin_.free()
+    bout.free()
+    comm.close()
+    if pg is not None:
+        pg.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out))
+    return 0
+
+
+def x_es(dt: int) -> int:
+    return 2 if dt == 1 else 4
+
+
+if __name__ == "__main__":
+    sys.exit(main())

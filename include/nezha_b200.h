@@ -187,6 +187,14 @@ typedef struct {
 /* Last completed failover (returns NZ_ERR_INVALID when none happened). */
 int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep);
 
+/* Timer totals per rail since the last reset (harvested ops only; call
+ * nz_engine_synchronize first to harvest everything): ops, summed rail time
+ * (fork -> rail done, us) and summed segment bytes. */
+int nz_engine_rail_stats(nz_engine_t* eng, int rail_id, uint64_t* ops, double* total_us, uint64_t* total_bytes);
+int nz_engine_stats_reset(nz_engine_t* eng);
+/* Number of this library's kernels launched by this process so far. */
+uint64_t nz_kernel_launch_count(void);
+
 /* JSON snapshots: allocation table + profiles + health, and the plan the
  * engine would use for `bytes` (segments per rail). */
 int nz_engine_state_json(nz_engine_t* eng, char* out, size_t cap);

@@ -5,6 +5,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -65,6 +67,12 @@ nz_buf* allocSymmetric(nz_comm* c, size_t bytes) {
       gran = std::max(gran, mg);
     }
     b->mapped = (bytes + gran - 1) / gran * gran;
+    if (getenv("NEZHA_DEBUG")) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      fprintf(stderr, "[nezha] rank %d alloc %zu -> %zu (gran %zu) free %zu / %zu MiB\n", c->rank, bytes, b->mapped,
+              gran, fr >> 20, tot >> 20);
+    }
     NZ_CU(NZ_DRV(cuMemCreate)(&b->local, b->mapped, &prop, 0));
     b->ptrs[c->rank] = mapHandle(b->local, b->mapped, gran, c->device);
 

@@ -54,6 +54,12 @@ struct nz_engine {
   nz_buf* ub_in = nullptr;
   nz_buf* ub_out = nullptr;
   std::vector<std::string> last_plans;  // JSON of each piece of the last call
+  struct RailStat {
+    uint64_t ops = 0;
+    double us = 0;
+    uint64_t bytes = 0;
+  };
+  std::vector<RailStat> stats;  // parallel to specs
 
   int index(int rail_id) const {
     for (size_t i = 0; i < specs.size(); ++i)
@@ -108,6 +114,14 @@ struct nz_engine {
         pool.push_back(e);
       }
       pool.push_back(p.start);
+      if (stats.size() != specs.size()) stats.assign(specs.size(), RailStat{});
+      for (auto& [id, us] : lat) {
+        RailStat& st = stats[index(id)];
+        st.ops += 1;
+        st.us += us;
+        for (const auto& rs : p.plan.segments)
+          if (rs.rail_id == id) st.bytes += rs.segment.length;
+      }
       if (!p.skip) bal->recordOp(p.plan, lat);
     }
   }
@@ -244,6 +258,7 @@ struct nz_engine {
     for (auto* r : rails)
       if (*reinterpret_cast<volatile int*>(r->wd_host)) fail(NZ_ERR_TIMEOUT, "rail watchdog fired (a peer never arrived)");
     finishFailoverReport();
+    drainTimer();  // collective point: every rank harvests the same ops here
   }
 
   void ensureUnbound(uint64_t bytes) {
@@ -576,6 +591,23 @@ int nz_engine_state_json(nz_engine_t* eng, char* out, size_t cap) {
     s = eng->stateJson();
   });
   return rc != NZ_OK ? rc : copyOut(s, out, cap);
+}
+
+int nz_engine_rail_stats(nz_engine_t* eng, int rail_id, uint64_t* ops, double* total_us, uint64_t* total_bytes) {
+  return guarded([&] {
+    if (!eng || !ops || !total_us || !total_bytes) fail(NZ_ERR_INVALID, "null argument");
+    const int i = eng->index(rail_id);
+    if (eng->stats.size() != eng->specs.size()) eng->stats.assign(eng->specs.size(), nz_engine::RailStat{});
+    *ops = eng->stats[i].ops;
+    *total_us = eng->stats[i].us;
+    *total_bytes = eng->stats[i].bytes;
+  });
+}
+
+int nz_engine_stats_reset(nz_engine_t* eng) {
+  if (!eng) return NZ_ERR_INVALID;
+  eng->stats.assign(eng->specs.size(), nz_engine::RailStat{});
+  return NZ_OK;
 }
 
 int nz_engine_last_plan_json(nz_engine_t* eng, char* out, size_t cap) {

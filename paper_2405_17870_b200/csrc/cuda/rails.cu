@@ -3,12 +3,16 @@
 // CUDA stream, which is the B200 form of the reference's "one collective
 // executor per rail".
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include "internal.h"
 #include "kernels.cuh"
 
 namespace nz {
+
+// Every kernel this library launches bumps this (nz_kernel_launch_count).
+std::atomic<uint64_t> g_launches{0};
 
 namespace {
 
@@ -57,6 +61,7 @@ int gridFor(nz_rail* r, uint64_t range_bytes, int world, int unroll) {
 template <typename DT, int N, int NDST>
 void launchFold(const FoldArgs& a, int grid, cudaStream_t st) {
   fold_kernel<DT, N, NDST><<<grid, kThreads, 0, st>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 template <int N, int NDST>
@@ -79,6 +84,7 @@ void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_
 }
 
 void dispatchNvls(int world, int dtype, const NvlsArgs& a, int grid, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (world) {
 #define NZ_CASE(n)                                                                          \
   case n:                                                                                   \
@@ -92,6 +98,7 @@ void dispatchNvls(int world, int dtype, const NvlsArgs& a, int grid, cudaStream_
 
 void launchBarrier(nz_rail* r, uint32_t epoch, FaultPost post, cudaStream_t st) {
   const BarrierArgs b = barrierArgs(r, epoch);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (r->comm->world) {
 #define NZ_CASE(n) \
   case n: barrier_kernel<n><<<1, 32, 0, st>>>(b, r->comm->rank, post); break;
@@ -222,6 +229,7 @@ __global__ void stamp_kernel(uint64_t* dst) {
 
 void launchStamp(uint64_t* dst, cudaStream_t st) {
   stamp_kernel<<<1, 1, 0, st>>>(dst);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   NZ_CUDA(cudaGetLastError());
 }
 
@@ -266,6 +274,8 @@ using nz::guarded;
 extern "C" {
 
 int nz_has_cuda_kernels(void) { return 1; }
+
+uint64_t nz_kernel_launch_count(void) { return nz::g_launches.load(); }
 
 int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rail_t** out) {
   return guarded([&] {

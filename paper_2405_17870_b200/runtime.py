@@ -226,10 +226,24 @@ class Engine:
     def last_plans(self) -> list:
         return self._json(lib().nz_engine_last_plan_json)
 
+    def rail_stats(self, rail_id: int) -> dict:
+        ops, us, nbytes = ctypes.c_uint64(), ctypes.c_double(), ctypes.c_uint64()
+        check(lib().nz_engine_rail_stats(self.handle, rail_id, byref(ops), byref(us), byref(nbytes)),
+              "nz_engine_rail_stats")
+        return {"ops": ops.value, "total_us": us.value, "bytes": nbytes.value}
+
+    def stats_reset(self) -> None:
+        check(lib().nz_engine_stats_reset(self.handle), "nz_engine_stats_reset")
+
     def close(self) -> None:
         if self.handle:
             check(lib().nz_engine_destroy(self.handle), "nz_engine_destroy")
             self.handle = None
+
+
+def kernel_launch_count() -> int:
+    """Kernels libnezha_b200.so has launched in this process (nz_kernel_launch_count)."""
+    return int(lib().nz_kernel_launch_count())
 
 
 def run_trace(scenario: str) -> str:

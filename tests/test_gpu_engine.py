@@ -56,7 +56,7 @@ def test_engine_multirail_parity(world):
             "cases": [
                 {"dtype": "f32", "nbytes": 64 << 20, "reps": 10},
                 {"dtype": "bf16", "nbytes": 48 << 20, "reps": 2},
-                {"dtype": "i32", "nbytes": 32 << 20 + 12, "reps": 2},
+                {"dtype": "i32", "nbytes": (32 << 20) + 12, "reps": 2},
                 {"dtype": "f32", "nbytes": 8192, "reps": 3},
                 {"dtype": "f32", "nbytes": 1 << 20, "reps": 2, "host": True},
             ]}
