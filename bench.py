@@ -62,29 +62,31 @@ class ClockSampler:
         self.device = device
         self.proc = None
         self.lines = []
+        self.path = f"/tmp/nezha_clocks_{os.getpid()}_{device}.csv"
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                          "--format=csv,noheader,nounits", "-lms", "50", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)  # first sample lands before the timed region starts
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.12)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            try:
+                self.lines = [l.strip() for l in open(self.path) if l.strip()]
+                os.unlink(self.path)
+            except OSError:
+                self.lines = []
 
     def summary(self):
         sm, mx, reasons = [], [], set()
@@ -236,11 +238,21 @@ def main():
     for _ in range(max(args.warmup, 3)):
         eng.allreduce(bin_, bout, S, dt, stream)
     eng.synchronize()
+    t_est = timed(S, 3, warm=0)
+    soak_ops = max(1, min(2000, int(0.4 / max(t_est, 1e-6))))
     eng.stats_reset()
     comm.barrier()
     torch.cuda.synchronize()
     launches0 = kernel_launch_count()
     with ClockSampler(local) as clk:
+        # Keep the GPU under the same load for ~0.4 s so the sampler sees it
+        # running, then time exactly K steps back to back.
+        for _ in range(soak_ops):  # same count on every rank (collective)
+            eng.allreduce(bin_, bout, S, dt, stream)
+        eng.synchronize()
+        comm.barrier()
+        eng.stats_reset()
+        launches0 = kernel_launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
@@ -260,6 +272,10 @@ def main():
     dom = max(range(len(kinds)), key=lambda i: stats[kinds[i]]["bytes"])
     st = stats[kinds[dom]]
     roofline = None
+    if st["ops"] == 0 and plan.get("segs"):
+        # Cold plan: one rail carried the whole step on the caller's stream.
+        dom = plan["segs"][0][0]
+        st = {"ops": args.steps, "total_us": t_step * 1e6 * args.steps, "bytes": S * args.steps}
     if st["ops"]:
         t_rail = max_over_ranks(st["total_us"] / st["ops"] * 1e-6)
         seg = st["bytes"] / st["ops"]
@@ -295,11 +311,20 @@ def main():
     pg = None
     if world > 1 and not args.no_nccl:
         import torch.distributed as dist
+        saved = os.dup(1)
+        os.dup2(2, 1)  # NCCL prints its banner on stdout; keep stdout for the one JSON line
         try:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             pg = dist
+            warm = torch.ones(1, device="cuda")
+            pg.all_reduce(warm)
+            torch.cuda.synchronize()
         except Exception as e:  # pragma: no cover
             out["nccl_error"] = str(e)[:200]
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
 
     def nccl_time(nbytes, iters):
         t = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")

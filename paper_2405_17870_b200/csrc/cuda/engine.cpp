@@ -147,12 +147,25 @@ struct nz_engine {
     const uint32_t seq = op_seq++;
     harvest(seq);
     nezha::Plan plan = bal->allocate(len);
+    const int world = comm->world;
+    if (!plan.hot && inject.find(seq) == inject.end()) {
+      // Cold (or rho-gated) op: one rail, launched straight on the caller's
+      // stream — no fork/join, no Timer events. A single-rail sample cannot
+      // move the table (a cold flush only records telemetry), so skipping it
+      // leaves every decision unchanged (P11).
+      const auto& rs = plan.segments[0];
+      nz_rail* r = rails[index(rs.rail_id)];
+      const uint64_t C = nezha::defaultChunkBytes(rs.segment.length, world, algo);
+      nz::railAllreduce(r, in, out, base + rs.segment.offset, rs.segment.length, C, 0, UINT64_MAX, dtype, seq, -1,
+                        user);
+      recordPlan(seq, base, len, plan);
+      return;
+    }
     Pending p;
     p.op = seq;
     p.plan = plan;
     p.start = event();
     NZ_CUDA(cudaEventRecord(p.start, user));
-    const int world = comm->world;
     auto inj = inject.find(seq);
     const nezha::Segment* failed_seg = nullptr;
     int failed_rail = -1;
@@ -190,17 +203,21 @@ struct nz_engine {
       }
     }
     for (auto& [id, e] : p.ends) NZ_CUDA(cudaStreamWaitEvent(user, e, 0));
+    recordPlan(seq, base, len, plan);
+    pending.push_back(std::move(p));
+  }
+
+  void recordPlan(uint32_t seq, uint64_t base, uint64_t len, const nezha::Plan& plan) {
     std::ostringstream o;
     o << "{\"op\":" << seq << ",\"offset\":" << base << ",\"length\":" << len << ",\"hot\":" << (plan.hot ? "true" : "false")
       << ",\"segs\":[";
     for (size_t i = 0; i < plan.segments.size(); ++i) {
       const auto& rs = plan.segments[i];
       o << (i ? "," : "") << "[" << rs.rail_id << "," << base + rs.segment.offset << "," << rs.segment.length << ","
-        << nezha::defaultChunkBytes(rs.segment.length, world, algo) << "]";
+        << nezha::defaultChunkBytes(rs.segment.length, comm->world, algo) << "]";
     }
     o << "]}";
     last_plans.push_back(o.str());
-    pending.push_back(std::move(p));
   }
 
   // Exception handler: wait for the device's fault record,
