@@ -429,6 +429,90 @@ def main():
                 out["failover_ms"] = round(max_over_ranks(fo["resume_us"]) / 1e3, 4)
             eng.readmit(victim[0])
 
+    # ---- config 3: mixed 8 KiB - 4 MiB stream through the state machine ------
+    if not args.no_sweep:
+        import random
+
+        rnd = random.Random(7)
+        n_ops = 2000
+        sizes = [max(4, int(2 ** rnd.uniform(13, 22)) & ~3) for _ in range(n_ops)]
+        for s_ in sizes[:50]:
+            eng.allreduce(bin_, bout, s_, dt, stream)
+        eng.synchronize()
+        comm.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for s_ in sizes:
+            eng.allreduce(bin_, bout, s_, dt, stream)
+        b.record(stream)
+        b.synchronize()
+        eng.synchronize()
+        tm = max_over_ranks(a.elapsed_time(b) / 1e3)
+        table = eng.state()["table"]
+        hot_buckets = [e["bucket"] for e in table["buckets"] if e["hot"] and 13 <= e["bucket"] <= 22]
+        out["config3_mixed_stream"] = {"ops": n_ops, "sizes": "log-uniform 8 KiB-4 MiB, seed 7",
+                                       "mean_us_per_op": round(tm / n_ops * 1e6, 2),
+                                       "algbw_GBs": round(sum(sizes) / tm / 1e9, 2),
+                                       "hot_buckets": hot_buckets, "threshold": table["threshold"]}
+        if pg is not None:
+            tt = {s_: torch.empty(s_ // 4, dtype=torch.float32, device="cuda") for s_ in set(sizes)}
+            torch.cuda.synchronize()
+            a.record()
+            for s_ in sizes:
+                pg.all_reduce(tt[s_])
+            b.record()
+            b.synchronize()
+            tn = max_over_ranks(a.elapsed_time(b) / 1e3)
+            out["config3_mixed_stream"]["nccl_mean_us_per_op"] = round(tn / n_ops * 1e6, 2)
+            del tt
+
+    # ---- config 5: DDP gradient-bucket traces ----------------
+    if not args.no_sweep:
+        traces = {"resnet50": [8196000, 31502336, 26255360, 26550272, 9724160],
+                  "bert_large": [4214792, 37903592] + [33591296, 29396992, 37781504] * 11 +
+                                [33591296, 29396992, 131330048]}
+        c5 = {}
+        for name, buckets in traces.items():
+            offs, o = [], 0
+            for nb in buckets:
+                offs.append(o)
+                o += nb
+            if max(buckets) > cap:
+                continue
+            for _ in range(3):
+                for nb in buckets:
+                    eng.allreduce(bin_, bout, nb, dt, stream)
+            eng.synchronize()
+            comm.barrier()
+            iters = 5
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(iters):
+                for nb in buckets:
+                    eng.allreduce(bin_, bout, nb, dt, stream)
+            b.record(stream)
+            b.synchronize()
+            eng.synchronize()
+            t_it = max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
+            row = {"buckets": len(buckets), "bytes": o, "ms_per_iter": round(t_it * 1e3, 3),
+                   "busbw_GBs": round(ring_volume(world, o) / t_it / 1e9, 2) if world > 1 else None}
+            if pg is not None:
+                tb = [torch.empty(nb // 4, dtype=torch.float32, device="cuda") for nb in buckets]
+                for t_ in tb:
+                    pg.all_reduce(t_)
+                torch.cuda.synchronize()
+                a.record()
+                for _ in range(iters):
+                    for t_ in tb:
+                        pg.all_reduce(t_)
+                b.record()
+                b.synchronize()
+                tn = max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
+                row["nccl_ms_per_iter"] = round(tn * 1e3, 3)
+                del tb
+            c5[name] = row
+        out["config5_ddp_buckets"] = c5
+
     # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
     if world == 1 and rank == 0 and not args.no_cpu:
         cb = cpu_baseline()

@@ -148,6 +148,11 @@ class Balancer {
 
   // Recompute threshold / states after a profile change (e.g. calibration).
   void setProfiles(std::vector<RailProfile> rails);
+  // P13: profiles measured with every rail busy at once; they drive the hot
+  // side (Eqs. 3, 5, 6, 8) while the isolated profiles drive Eq. 4. Rails on
+  // one NVSwitch share links, so isolated numbers overstate the hot gain.
+  void setConcurrentProfiles(std::vector<RailProfile> rails);
+  const std::vector<RailProfile>& concurrentProfiles() const { return concurrent_; }
   void setSyncOverhead(Micros us);
 
   // Multi-rank agreement on a flush: maps this rank's per-rail window means
@@ -168,11 +173,13 @@ class Balancer {
   void rebuild();
   std::vector<double> modelAlpha(int bucket) const;
   std::vector<double> restrictToHealthy(std::vector<double> a) const;
-  std::vector<RailProfile> healthyProfiles(std::vector<int>* idx) const;
+  std::vector<RailProfile> healthyProfiles(std::vector<int>* idx, bool concurrent = false) const;
   double hotMinusCold(Bytes S) const;
   void applyFlush(int bucket, const std::vector<std::pair<int, Micros>>& means);
 
   std::vector<RailProfile> rails_;  // sorted by rail_id
+  // Latency of each rail while all rails run together (P13); empty = rails_.
+  std::vector<RailProfile> concurrent_;
   BalancerConfig cfg_;
   std::vector<bool> healthy_;
   AllocationTable table_;

@@ -197,6 +197,16 @@ class Table:
         self.epoch = 0
         self.saved = {}
         self.win = {}  # bucket -> {index: [samples]}
+        self.conc = []
+        self._rebuild()
+
+    @property
+    def hot_rails(self):
+        """P13: the hot side (Eqs. 3, 5, 6, 8) uses the concurrent profiles when given."""
+        return self.conc if self.conc else self.rails
+
+    def set_concurrent(self, rails):
+        self.conc = sorted(rails, key=lambda r: r.rail_id)
         self._rebuild()
 
     # -- helpers
@@ -224,7 +234,7 @@ class Table:
     def model_alpha(self, k):
         H = self.healthy()
         share = max((1 << k) // len(H), 1)
-        init = eq8([self.rails[i].latency(share) for i in H])
+        init = eq8([self.hot_rails[i].latency(share) for i in H])
         a = [0.0] * len(self.rails)
         for j, i in enumerate(H):
             a[i] = init[j]
@@ -236,9 +246,9 @@ class Table:
 
     def f(self, S):
         H = self.healthy()
-        hp = [self.rails[i] for i in H]
+        hp = [self.hot_rails[i] for i in H]
         a = [self.b[self.clamp(S)]["alpha"][i] for i in H]
-        return hot(hp, a, S, self.cfg["sync_us"]) - cold(hp, S)[0]
+        return hot(hp, a, S, self.cfg["sync_us"]) - cold([self.rails[i] for i in H], S)[0]
 
     def _rebuild(self):
         H = self.healthy()
@@ -284,7 +294,7 @@ class Table:
         plan = {"bucket": k, "hot": False, "rho": 1.0, "gated": False, "segs": []}
         if e["hot"]:
             H = self.healthy()
-            plan["rho"] = rho([self.rails[i] for i in H], [e["alpha"][i] for i in H], S)
+            plan["rho"] = rho([self.hot_rails[i] for i in H], [e["alpha"][i] for i in H], S)
             if plan["rho"] > self.cfg["tau"]:
                 plan["gated"] = True
             else:
@@ -401,7 +411,7 @@ def unit(x):
 
 def parse(text):
     sc = {"world": 8, "chunked": True, "rails": [], "truth": {}, "truth_sync": 0.0, "seed": 0, "sizes": [],
-          "faults": [], "readmits": [],
+          "faults": [], "readmits": [], "concurrent": [],
           "cfg": {"tau": 5.0, "eta": 0.05, "eps": 0.01, "sync_us": 0.0, "window": 100, "max_iters": 100,
                   "demote_after": 0, "probe_lo": 4096, "probe_hi": 1 << 30}}
     keys = {"tau": "tau", "eta": "eta", "eps": "eps", "sync_us": "sync_us", "window": "window",
@@ -419,14 +429,14 @@ def parse(text):
             for name, val in zip(a[::2], a[1::2]):
                 v = float(val)
                 sc["cfg"][keys[name]] = int(v) if name in ("window", "max_iters", "demote_after") else v
-        elif k == "rail":
+        elif k in ("rail", "concurrent"):
             pts = []
             if len(a) > 4:
                 assert a[4] == "cal"
                 for p in a[5:]:
                     s, l = p.split(":")
                     pts.append((int(s), float(l)))
-            sc["rails"].append(Rail(int(a[0]), float(a[2]), float(a[3]), pts))
+            sc["rails" if k == "rail" else "concurrent"].append(Rail(int(a[0]), float(a[2]), float(a[3]), pts))
         elif k == "truth":
             sc["truth"][int(a[0])] = (float(a[1]), float(a[2]), float(a[3]))
         elif k == "truth_sync":
@@ -468,6 +478,8 @@ def run(text: str) -> str:
     """Decision log for a scenario; must equal nz_planner_run_trace byte for byte."""
     sc = parse(text)
     t = Table(sc["rails"], sc["cfg"])
+    if sc["concurrent"]:
+        t.set_concurrent(sc["concurrent"])
     healthy = sorted(r.rail_id for r in t.rails)
     out = []
     for op, S in enumerate(sc["sizes"]):

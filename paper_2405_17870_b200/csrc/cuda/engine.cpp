@@ -298,11 +298,13 @@ struct nz_engine {
     for (uint64_t s = 4096; s <= maxb; s *= 4) sizes.push_back(s);
     cudaEvent_t e0 = event(), e1 = event();
     std::vector<nezha::RailProfile> profiles;
+    bool measured_any = false;
     for (size_t i = 0; i < specs.size(); ++i) {
       if (specs[i].has_profile) {  // given by the rails config: keep it
         profiles.push_back(specs[i].profile);
         continue;
       }
+      measured_any = true;
       nz_rail* r = rails[i];
       std::vector<double> lat;
       for (uint64_t s : sizes) {
@@ -339,6 +341,7 @@ struct nz_engine {
       specs[i].has_profile = true;
     }
     bal->setProfiles(profiles);
+    if (measured_any && specs.size() > 1) calibrateConcurrent(sizes, e0);
     if (cfg.sync_overhead_us < 0 && specs.size() > 1) {
       // Fork/join of every rail on 4 KiB each vs the slowest rail alone.
       const uint64_t s = 4096;
@@ -376,6 +379,66 @@ struct nz_engine {
     }
     pool.push_back(e0);
     pool.push_back(e1);
+  }
+
+  // P13: every rail busy at once on a uniform split of S; rail i's latency
+  // for its S/R share under that contention becomes its concurrent profile.
+  void calibrateConcurrent(const std::vector<uint64_t>& sizes, cudaEvent_t start) {
+    const int world = comm->world;
+    const size_t R = specs.size();
+    std::vector<std::vector<double>> lat(R);
+    std::vector<uint64_t> shares;
+    std::vector<cudaEvent_t> ends(R);
+    for (auto& e : ends) e = event();
+    for (uint64_t S : sizes) {
+      const uint64_t share = std::max<uint64_t>((S / R) & ~uint64_t{15}, 16);
+      shares.push_back(share);
+      const int iters = S <= (1u << 20) ? std::max(cfg.calibrate_iters, 4) : std::max(cfg.calibrate_iters / 4, 2);
+      std::vector<double> acc(R, 0.0);
+      for (int it = 0; it < iters + 1; ++it) {
+        NZ_CUDA(cudaEventRecord(start, io));
+        for (size_t i = 0; i < R; ++i) {
+          NZ_CUDA(cudaStreamWaitEvent(rails[i]->stream, start, 0));
+          const uint64_t C = nezha::defaultChunkBytes(share, world, algo);
+          nz::railAllreduce(rails[i], ub_in, ub_out, share * i, share, C, 0, UINT64_MAX, NZ_F32, 0, -1,
+                            rails[i]->stream);
+          NZ_CUDA(cudaEventRecord(ends[i], rails[i]->stream));
+          NZ_CUDA(cudaStreamWaitEvent(io, ends[i], 0));
+        }
+        NZ_CUDA(cudaStreamSynchronize(io));
+        if (it == 0) continue;  // warm-up
+        for (size_t i = 0; i < R; ++i) {
+          float ms = 0;
+          NZ_CUDA(cudaEventElapsedTime(&ms, start, ends[i]));
+          acc[i] += static_cast<double>(ms) * 1000.0;
+        }
+      }
+      for (size_t i = 0; i < R; ++i) lat[i].push_back(acc[i] / iters);
+    }
+    for (auto e : ends) pool.push_back(e);
+    std::vector<nezha::RailProfile> conc;
+    for (size_t i = 0; i < R; ++i) {
+      auto& l = lat[i];
+      if (world > 1) {
+        const auto msgs = nz::exchange(comm, l.data(), l.size() * sizeof(double), {});
+        for (int rk = 0; rk < world; ++rk) {
+          const double* v = reinterpret_cast<const double*>(msgs[rk].data.data());
+          for (size_t j = 0; j < l.size(); ++j) l[j] = std::max(l[j], v[j]);
+        }
+      }
+      for (size_t j = 1; j < l.size(); ++j) l[j] = std::max(l[j], l[j - 1] + 1e-3);
+      nezha::RailProfile p = specs[i].profile;
+      p.efficiency_points.clear();
+      for (size_t j = 0; j < shares.size(); ++j) {
+        if (j && shares[j] <= shares[j - 1]) continue;
+        p.efficiency_points.emplace_back(shares[j], l[j]);
+      }
+      p.t_setup_us = l.front();
+      p.bandwidth_bps =
+          static_cast<double>(shares.back() - shares.front()) / std::max(1e-9, (l.back() - l.front()) * 1e-6);
+      conc.push_back(p);
+    }
+    bal->setConcurrentProfiles(conc);
   }
 
   std::string stateJson() {

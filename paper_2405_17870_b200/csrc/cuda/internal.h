@@ -117,6 +117,9 @@ struct nz_rail {
   int* wd_dev = nullptr;
   char* staging = nullptr;  // CE: (world-1) slots of staging_slot bytes
   size_t staging_slot = 0;
+  nz_buf* ll = nullptr;     // SM: one-shot LL slots [parity][rank][slot_words] of {data, flag}
+  uint64_t ll_slot_words = 0;
+  uint32_t ll_flag = 0;
 };
 
 namespace nz {

@@ -416,6 +416,114 @@ __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ Nv
   post_fault(a.f.post);
 }
 
+// --------------------------------------------------------- LL (one-shot) --
+// Small segments on the SM rail: every rank pushes its words, each tagged
+// with this op's flag in the same 8-byte store ({data, flag} pairs, the LL
+// idea), into slot [rank] of every peer's LL buffer, then polls its own slots
+// and folds in ring order (P1). No barrier round trips: one NVLink one-way
+// latency. Two parities alternate so a rank at most one op ahead never
+// overwrites a slot a peer still reads (stream order on every rank).
+struct LLArgs {
+  const char* in;  // my input, byte offset x at in + x
+  char* out;       // my output
+  uint64_t* peer[kDevMaxRanks];  // each rank's LL buffer (8-byte {data, flag} words)
+  uint64_t* local;
+  uint64_t lo, hi;
+  uint64_t words;       // ceil((hi - lo) / 4)
+  uint64_t slot_words;  // capacity of one (parity, rank) slot
+  Geometry g;
+  uint32_t flag;
+  int parity;
+  int rank;
+  int* watchdog;
+  FaultPost post;
+};
+
+__device__ __forceinline__ uint32_t ll_load_word(const char* base, uint64_t x, uint64_t hi) {
+  if (x + 4 <= hi) return *reinterpret_cast<const uint32_t*>(base + x);
+  return static_cast<uint32_t>(*reinterpret_cast<const unsigned short*>(base + x));  // bf16 tail
+}
+
+template <typename DT, int N>
+__device__ __forceinline__ void ll_fold_word(const LLArgs& a, const uint32_t (&v)[N], uint64_t x) {
+  constexpr int per = 4 / DT::kElem;
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    const uint64_t xe = x + static_cast<uint64_t>(k) * DT::kElem;
+    if (xe >= a.hi) break;
+    uint64_t run_end;
+    const int b = block_at<N, DT::kElem>(a.g, xe, &run_end);
+    if (DT::kElem == 4) {
+      typename DT::Scalar acc;
+      uint32_t w = v[b];
+      memcpy(&acc, &w, 4);
+#pragma unroll
+      for (int j = 1; j < N; ++j) {
+        typename DT::Scalar t;
+        uint32_t wj = v[(b + j) % N];
+        memcpy(&t, &wj, 4);
+        acc = DT::sadd(acc, t);
+      }
+      DT::sstore(a.out + xe, acc);
+    } else {
+      float acc = __uint_as_float(k == 0 ? (v[b] << 16) : (v[b] & 0xffff0000u));
+#pragma unroll
+      for (int j = 1; j < N; ++j) {
+        const uint32_t wj = v[(b + j) % N];
+        acc = acc + __uint_as_float(k == 0 ? (wj << 16) : (wj & 0xffff0000u));
+      }
+      DT::sstore(a.out + xe, acc);
+    }
+  }
+}
+
+template <typename DT, int N>
+__global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs a) {
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t my_slot = (static_cast<uint64_t>(a.parity) * N + a.rank) * a.slot_words;
+  const uint64_t pairs = (a.words + 1) / 2;
+  for (uint64_t p = tid; p < pairs; p += stride) {
+    const uint64_t x = a.lo + 8 * p;
+    const uint32_t d0 = ll_load_word(a.in, x, a.hi);
+    const uint32_t d1 = x + 4 < a.hi ? ll_load_word(a.in, x + 4, a.hi) : 0u;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      uint64_t* dst = a.peer[r] + my_slot + 2 * p;
+      asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(a.flag), "r"(d1),
+                   "r"(a.flag)
+                   : "memory");
+    }
+  }
+  for (uint64_t w = tid; w < a.words; w += stride) {
+    uint32_t v[N];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      const uint64_t* src = a.local + (static_cast<uint64_t>(a.parity) * N + r) * a.slot_words + w;
+      uint32_t d, f;
+      int spins = 0;
+      uint64_t t0 = 0;
+      for (;;) {
+        asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(d), "=r"(f) : "l"(src) : "memory");
+        if (f == a.flag) break;
+        if (++spins == 256) {
+          spins = 0;
+          const uint64_t now = globaltimer();
+          if (t0 == 0) {
+            t0 = now;
+          } else if (now - t0 > kWatchdogNs) {
+            atomicExch_system(a.watchdog, 1);
+            return;
+          }
+        }
+      }
+      v[r] = d;
+    }
+    ll_fold_word<DT, N>(a, v, a.lo + 4 * w);
+  }
+  post_fault(a.post);
+}
+
 // CE rail: start / end barriers around the DMA phases, and the fault post.
 template <int N>
 __global__ void barrier_kernel(const __grid_constant__ BarrierArgs b, int rank, FaultPost post) {

@@ -83,6 +83,21 @@ void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_
   }
 }
 
+constexpr uint64_t kLLMaxBytes = 256 * 1024;  // SM rail one-shot LL path up to this payload
+
+void dispatchLL(int world, int dtype, const LLArgs& a, int grid, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  switch (world) {
+#define NZ_CASE(n)                                                                      \
+  case n:                                                                               \
+    if (dtype == NZ_F32) return (void)(ll_kernel<F32, n><<<grid, kThreads, 0, st>>>(a));  \
+    if (dtype == NZ_BF16) return (void)(ll_kernel<BF16, n><<<grid, kThreads, 0, st>>>(a)); \
+    return (void)(ll_kernel<I32, n><<<grid, kThreads, 0, st>>>(a));
+    NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
+#undef NZ_CASE
+  }
+}
+
 void dispatchNvls(int world, int dtype, const NvlsArgs& a, int grid, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (world) {
@@ -126,6 +141,31 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
   shardOf(lo, hi, me, N, &s, &e);
   const uint32_t epoch = r->epoch + 1;
   r->epoch += 2;  // start + end barrier; identical on every rank
+
+  if (N > 1 && r->kind == NZ_RAIL_SM && r->ll && hi - lo <= kLLMaxBytes && lo % 4 == 0) {
+    LLArgs a{};
+    a.in = in->ptrs[me];
+    a.out = out->ptrs[me];
+    for (int p = 0; p < N; ++p) a.peer[p] = reinterpret_cast<uint64_t*>(r->ll->ptrs[p]);
+    a.local = reinterpret_cast<uint64_t*>(r->ll->ptrs[me]);
+    a.lo = lo;
+    a.hi = hi;
+    a.words = (hi - lo + 3) / 4;
+    a.slot_words = r->ll_slot_words;
+    a.g = g;
+    if (++r->ll_flag == 0) r->ll_flag = 1;  // flag 0 means "never written"
+    a.flag = r->ll_flag;
+    a.parity = static_cast<int>(r->ll_flag & 1u);
+    a.rank = me;
+    a.watchdog = r->wd_dev;
+    a.post = post;
+    const uint64_t threads = (a.words + 1) / 2 > a.words ? (a.words + 1) / 2 : a.words;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads,
+                                                                              c->sm_count)));
+    dispatchLL(N, dtype, a, grid, st);
+    NZ_CUDA(cudaGetLastError());
+    return;
+  }
 
   if (N == 1 || r->kind == NZ_RAIL_SM) {
     FoldArgs a{};
@@ -296,6 +336,14 @@ int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rai
     for (int p = 0; p < comm->world; ++p) r->pad_peer[p] = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[p] + pad_off);
     NZ_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
     NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
+    if (kind == NZ_RAIL_SM && comm->world > 1) {
+      // LL slots: [parity 2][rank N][kLLMaxBytes / 4 words] x 8 bytes, zeroed on every rank first.
+      r->ll_slot_words = nz::kLLMaxBytes / 4;
+      r->ll = nz::allocSymmetric(comm, 2 * comm->world * r->ll_slot_words * sizeof(uint64_t));
+      NZ_CUDA(cudaMemset(r->ll->ptrs[comm->rank], 0, r->ll->mapped));
+      NZ_CUDA(cudaDeviceSynchronize());
+      nz::exchange(comm, nullptr, 0, {});
+    }
     if (kind == NZ_RAIL_CE) {
       for (int j = 1; j < comm->world; ++j) {
         cudaStream_t s;
@@ -326,6 +374,7 @@ int nz_rail_destroy(nz_rail_t* r) {
     if (r->fork) cudaEventDestroy(r->fork);
     if (r->stream) cudaStreamDestroy(r->stream);
     if (r->staging) cudaFree(r->staging);
+    if (r->ll) nz::freeSymmetric(r->ll);
     if (r->fault_host) cudaFreeHost(r->fault_host);
     if (r->wd_host) cudaFreeHost(r->wd_host);
     delete r;

@@ -209,11 +209,12 @@ int Balancer::clampBucket(Bytes S) {
   return std::min(std::max(k, kMinBucket), kMaxBucket);
 }
 
-std::vector<RailProfile> Balancer::healthyProfiles(std::vector<int>* idx) const {
+std::vector<RailProfile> Balancer::healthyProfiles(std::vector<int>* idx, bool concurrent) const {
+  const auto& src = concurrent && !concurrent_.empty() ? concurrent_ : rails_;
   std::vector<RailProfile> out;
   for (size_t i = 0; i < rails_.size(); ++i) {
     if (!healthy_[i]) continue;
-    out.push_back(rails_[i]);
+    out.push_back(src[i]);
     if (idx) idx->push_back(static_cast<int>(i));
   }
   return out;
@@ -239,7 +240,7 @@ std::vector<double> Balancer::restrictToHealthy(std::vector<double> a) const {
 // P11: Eq. 8 applied to the calibrated model's uniform-split latencies.
 std::vector<double> Balancer::modelAlpha(int bucket) const {
   std::vector<int> idx;
-  const auto hp = healthyProfiles(&idx);
+  const auto hp = healthyProfiles(&idx, /*concurrent=*/true);
   std::vector<double> a(rails_.size(), 0.0);
   const Bytes S = bucketFloor(bucket);
   const Bytes share = std::max<Bytes>(S / hp.size(), 1);
@@ -250,13 +251,16 @@ std::vector<double> Balancer::modelAlpha(int bucket) const {
   return a;
 }
 
+// Eq. 6's f(S): hot from the concurrent profiles (rails share the links),
+// cold from the isolated ones.
 double Balancer::hotMinusCold(Bytes S) const {
   std::vector<int> idx;
-  const auto hp = healthyProfiles(&idx);
+  const auto hp = healthyProfiles(&idx, /*concurrent=*/true);
+  const auto cp = healthyProfiles(nullptr, /*concurrent=*/false);
   const auto& e = table_.buckets.at(clampBucket(S));
   std::vector<double> ah;
   for (int i : idx) ah.push_back(e.alpha[i]);
-  return hotLatency(hp, ah, S, cfg_.sync_overhead_us) - coldLatency(hp, S).first;
+  return hotLatency(hp, ah, S, cfg_.sync_overhead_us) - coldLatency(cp, S).first;
 }
 
 void Balancer::rebuild() {
@@ -325,7 +329,7 @@ Plan Balancer::allocate(Bytes S) const {
   const BucketEntry& e = table_.buckets.at(p.bucket);
   if (e.hot) {
     std::vector<int> idx;
-    const auto hp = healthyProfiles(&idx);
+    const auto hp = healthyProfiles(&idx, /*concurrent=*/true);
     std::vector<double> ah;
     for (int i : idx) ah.push_back(e.alpha[i]);
     p.rho = efficiencyRatio(hp, ah, S);
@@ -437,6 +441,19 @@ void Balancer::setProfiles(std::vector<RailProfile> rails) {
     if (rails[i].rail_id != rails_[i].rail_id) throw std::invalid_argument("setProfiles: rail ids changed");
   }
   rails_ = std::move(rails);
+  rebuild();
+}
+
+void Balancer::setConcurrentProfiles(std::vector<RailProfile> rails) {
+  std::sort(rails.begin(), rails.end(), [](const RailProfile& a, const RailProfile& b) { return a.rail_id < b.rail_id; });
+  if (!rails.empty()) {
+    if (rails.size() != rails_.size()) throw std::invalid_argument("setConcurrentProfiles: rail count mismatch");
+    for (size_t i = 0; i < rails.size(); ++i) {
+      rails[i].validate();
+      if (rails[i].rail_id != rails_[i].rail_id) throw std::invalid_argument("setConcurrentProfiles: rail ids differ");
+    }
+  }
+  concurrent_ = std::move(rails);
   rebuild();
 }
 

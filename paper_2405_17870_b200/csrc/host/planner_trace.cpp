@@ -72,7 +72,7 @@ Scenario parseScenario(const std::string& text) {
         else if (k == "demote_after") sc.cfg.demote_after = static_cast<int>(v);
         else bad("config key " + k);
       }
-    } else if (key == "rail") {
+    } else if (key == "rail" || key == "concurrent") {
       RailProfile p;
       std::string proto;
       if (!(ls >> p.rail_id >> proto >> p.t_setup_us >> p.bandwidth_bps)) bad("rail");
@@ -87,7 +87,7 @@ Scenario parseScenario(const std::string& text) {
           p.efficiency_points.emplace_back(std::stoull(pt.substr(0, colon)), std::stod(pt.substr(colon + 1)));
         }
       }
-      sc.rails.push_back(p);
+      (key == "rail" ? sc.rails : sc.concurrent).push_back(p);
     } else if (key == "truth") {
       TruthLine t;
       if (!(ls >> t.rail_id >> t.a_us >> t.b_bps >> t.jitter)) bad("truth");
@@ -155,6 +155,7 @@ std::string planJson(std::uint32_t op, Bytes S, const Plan& p) {
 std::string runTrace(const std::string& text) {
   Scenario sc = parseScenario(text);
   Balancer bal(sc.rails, sc.cfg);
+  if (!sc.concurrent.empty()) bal.setConcurrentProfiles(sc.concurrent);
   std::ostringstream log;
   std::vector<int> healthy;
   for (const auto& r : bal.rails()) healthy.push_back(r.rail_id);

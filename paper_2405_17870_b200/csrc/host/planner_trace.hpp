@@ -37,6 +37,7 @@ struct Scenario {
   Algorithm algorithm = Algorithm::RingChunked;
   BalancerConfig cfg;
   std::vector<RailProfile> rails;
+  std::vector<RailProfile> concurrent;  // optional P13 profiles ("concurrent" lines)
   std::vector<TruthLine> truth;
   double truth_sync_us = 0;
   std::uint64_t seed = 0;

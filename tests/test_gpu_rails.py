@@ -118,7 +118,10 @@ MULTI = [
     {"kind": "nvls", "dtype": "f32", "nbytes": 8 << 20},
     {"kind": "nvls", "dtype": "bf16", "nbytes": 2_000_002},
     {"kind": "nvls", "dtype": "i32", "nbytes": 1_048_580, "seg_off": 4, "seg_len": 1_048_576},
-    {"kind": "sm", "dtype": "f32", "nbytes": 8192},
+    {"kind": "sm", "dtype": "f32", "nbytes": 8192},               # one-shot LL path
+    {"kind": "sm", "dtype": "bf16", "nbytes": 200_002},           # LL, odd bf16 tail word
+    {"kind": "sm", "dtype": "f32", "nbytes": 262_144, "seg_off": 1024, "seg_len": 200_000},  # LL, offset
+    {"kind": "sm", "dtype": "i32", "nbytes": 262_144, "fail_chunk": 0},  # LL range empty -> fault only
     {"kind": "nvls", "dtype": "f32", "nbytes": 8192},
     {"kind": "sm", "dtype": "f32", "nbytes": 64 << 20, "fail_chunk": 2},
     {"kind": "ce", "dtype": "bf16", "nbytes": 32 << 20, "fail_chunk": 1},

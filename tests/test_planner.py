@@ -192,9 +192,25 @@ fail 60 1 0
 """
 
 
+SHARED_LINKS = """
+world 8
+config sync_us 4 window 6 demote_after 2
+rail 0 nvls 12 8.0e11 cal 4096:12 1048576:14 67108864:95 1073741824:1400
+rail 1 ce 40 6.5e11 cal 4096:40 1048576:42 67108864:140 1073741824:1750
+concurrent 0 nvls 12 5.0e11 cal 4096:13 1048576:16 33554432:80 536870912:1150
+concurrent 1 ce 40 3.0e11 cal 4096:41 1048576:45 33554432:150 536870912:1900
+truth 0 13 4.6e11 0.03
+truth 1 41 2.8e11 0.03
+seed 9
+ops 40 1073741824
+ops 40 8388608
+"""
+
+
 @needs_lib
 @pytest.mark.parametrize("name,scenario", [("two_homog", TWO_HOMOG), ("three_hetero", THREE_HETERO),
-                                           ("failover", FAILOVER), ("gated", GATED), ("ring", RING_ALGO)])
+                                           ("failover", FAILOVER), ("gated", GATED), ("ring", RING_ALGO),
+                                           ("shared_links", SHARED_LINKS)])
 def test_trace_parity_byte_exact(name, scenario):
     got = run_trace(scenario)
     want = P.run(scenario)

@@ -52,9 +52,10 @@ def main():
     results = []
     for ci, c in enumerate(cases):
         kind = c["kind"]
-        if kind not in rails:
-            rails[kind] = Rail(comm, RAIL_KINDS[kind], len(rails), c.get("sm_budget", 0))
-        rail = rails[kind]
+        key = (kind, c.get("sm_budget", 0))
+        if key not in rails:
+            rails[key] = Rail(comm, RAIL_KINDS[kind], len(rails), c.get("sm_budget", 0))
+        rail = rails[key]
         dt = DTYPES[c["dtype"]]
         es = 2 if dt == oracle.BF16 else 4
         nbytes = c["nbytes"]
