@@ -87,7 +87,7 @@ void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_
   }
 }
 
-constexpr uint64_t kLLMaxBytes = 256 * 1024;  // SM rail one-shot LL path up to this payload
+constexpr uint64_t kLLMaxBytes = 1024 * 1024;  // SM rail one-shot LL path up to this payload
 
 void dispatchLL(int world, int dtype, const LLArgs& a, int grid, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
