@@ -344,48 +344,84 @@ __global__ void __launch_bounds__(512, 2) fold_kernel(const __grid_constant__ Fo
 }
 
 // ------------------------------------------------------------------ NVLS --
-template <typename DT>
+// WEAK selects .weak instead of .relaxed.sys memory semantics (the barrier
+// around the loop already orders the data); kept as a tuning variant.
+template <typename DT, bool WEAK>
 __device__ __forceinline__ uint4 mm_ld_reduce(const char* p);
 
-template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<F32>(const char* p) {
-  uint4 r;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p)
-               : "memory");
-  return r;
-}
+#define NZ_MM_LDR(SEM, TY)                                                                                  \
+  asm volatile("multimem.ld_reduce." SEM ".global.add." TY " {%0,%1,%2,%3}, [%4];"                        \
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)                                               \
+               : "l"(p)                                                                                   \
+               : "memory")
 
 template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<BF16>(const char* p) {
+__device__ __forceinline__ uint4 mm_ld_reduce<F32, false>(const char* p) {
   uint4 r;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p)
-               : "memory");
+  NZ_MM_LDR("relaxed.sys", "v4.f32");
   return r;
 }
-
 template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<I32>(const char* p) {
+__device__ __forceinline__ uint4 mm_ld_reduce<F32, true>(const char* p) {
+  uint4 r;
+  NZ_MM_LDR("weak", "v4.f32");
+  return r;
+}
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<BF16, false>(const char* p) {
+  uint4 r;
+  NZ_MM_LDR("relaxed.sys", "acc::f32.v4.bf16x2");
+  return r;
+}
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<BF16, true>(const char* p) {
+  uint4 r;
+  NZ_MM_LDR("weak", "acc::f32.v4.bf16x2");
+  return r;
+}
+#undef NZ_MM_LDR
+
+template <bool WEAK>
+__device__ __forceinline__ uint4 mm_ld_reduce_i32(const char* p) {
   // ptxas rejects .v4 for integer ld_reduce; four scalar accesses instead.
   uint4 r;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 4) : "memory");
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 8) : "memory");
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 12) : "memory");
+  if (WEAK) {
+    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
+    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 4) : "memory");
+    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 8) : "memory");
+    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 12) : "memory");
+  } else {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 4) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 8) : "memory");
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 12) : "memory");
+  }
   return r;
 }
-
-__device__ __forceinline__ void mm_st(char* p, uint4 v) {
-  // The store moves bits; .f32 is the only accepted 16-byte form.
-  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
-               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
-               : "memory");
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<I32, false>(const char* p) {
+  return mm_ld_reduce_i32<false>(p);
+}
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<I32, true>(const char* p) {
+  return mm_ld_reduce_i32<true>(p);
 }
 
-template <typename DT, int N>
+template <bool WEAK>
+__device__ __forceinline__ void mm_st(char* p, uint4 v) {
+  // The store moves bits; .f32 is the only accepted 16-byte form.
+  if (WEAK) {
+    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+                 : "memory");
+  } else {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+                 : "memory");
+  }
+}
+
+template <typename DT, int N, int U, bool WEAK>
 __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ NvlsArgs a) {
   if (!cta_barrier<N, false>(a.f.bar, a.f.bar.epoch, a.f.rank)) return;
   const uint64_t vs = (a.f.s + 15) & ~15ull;
@@ -395,7 +431,6 @@ __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ Nv
   } else {
     fold_scalar_range<DT, N>(a.f, N, a.f.s, vs);
     fold_scalar_range<DT, N>(a.f, N, ve, a.f.e);
-    constexpr int U = 4;
     const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x * 16;
     for (uint64_t base = vs + (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 16; base < ve;
          base += step * U) {
@@ -403,12 +438,12 @@ __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ Nv
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t x = base + u * step;
-        if (x < ve) v[u] = mm_ld_reduce<DT>(a.mc_in + x);
+        if (x < ve) v[u] = mm_ld_reduce<DT, WEAK>(a.mc_in + x);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t x = base + u * step;
-        if (x < ve) mm_st(a.mc_out + x, v[u]);
+        if (x < ve) mm_st<WEAK>(a.mc_out + x, v[u]);
       }
     }
   }

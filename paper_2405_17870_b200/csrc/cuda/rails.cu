@@ -102,14 +102,41 @@ void dispatchLL(int world, int dtype, const LLArgs& a, int grid, cudaStream_t st
   }
 }
 
+// NVLS loop variant: unroll U and memory semantics. NEZHA_NVLS_VARIANT
+// (0: U4 relaxed.sys, 1: U4 weak, 2: U8 relaxed.sys, 3: U8 weak) is a tuning
+// knob for the sweeps recorded in profiles/; the default is variant 0.
+int nvlsVariant() {
+  static const int v = [] {
+    const char* e = getenv("NEZHA_NVLS_VARIANT");
+    const int x = e ? atoi(e) : 0;
+    return (x >= 0 && x <= 3) ? x : 0;
+  }();
+  return v;
+}
+
+template <typename DT, int N>
+void launchNvlsDT(const NvlsArgs& a, int grid, cudaStream_t st) {
+  switch (nvlsVariant()) {
+    case 1: nvls_kernel<DT, N, 4, true><<<grid, kThreads, 0, st>>>(a); return;
+    case 2: nvls_kernel<DT, N, 8, false><<<grid, kThreads, 0, st>>>(a); return;
+    case 3: nvls_kernel<DT, N, 8, true><<<grid, kThreads, 0, st>>>(a); return;
+    default: nvls_kernel<DT, N, 4, false><<<grid, kThreads, 0, st>>>(a); return;
+  }
+}
+
+template <int N>
+void launchNvls(int dtype, const NvlsArgs& a, int grid, cudaStream_t st) {
+  if (dtype == NZ_F32) return launchNvlsDT<F32, N>(a, grid, st);
+  if (dtype == NZ_BF16) return launchNvlsDT<BF16, N>(a, grid, st);
+  return launchNvlsDT<I32, N>(a, grid, st);
+}
+
 void dispatchNvls(int world, int dtype, const NvlsArgs& a, int grid, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (world) {
 #define NZ_CASE(n)                                                                          \
   case n:                                                                                   \
-    if (dtype == NZ_F32) return (void)(nvls_kernel<F32, n><<<grid, kThreads, 0, st>>>(a));  \
-    if (dtype == NZ_BF16) return (void)(nvls_kernel<BF16, n><<<grid, kThreads, 0, st>>>(a)); \
-    return (void)(nvls_kernel<I32, n><<<grid, kThreads, 0, st>>>(a));
+    return launchNvls<n>(dtype, a, grid, st);
     NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
 #undef NZ_CASE
   }
