@@ -520,7 +520,10 @@ def main():
         if cb:
             out["cpu_baseline"] = cb
 
-    out["engine_state"] = {"sync_overhead_us": eng.state()["sync_overhead_us"]}
+    st_ = eng.state()
+    out["engine_state"] = {"sync_overhead_us": st_["sync_overhead_us"], "threshold": st_["table"]["threshold"],
+                           "rails": [{"kind": r["kind"], "calibration": r["calibration"]} for r in st_["rails"]],
+                           "concurrent": st_.get("concurrent", [])}
     eng.close()
     bin_.free()
     bout.free()

@@ -458,6 +458,15 @@ struct nz_engine {
           << nezha::formatDouble(p.efficiency_points[j].second) << "]";
       o << "]}";
     }
+    o << "],\"concurrent\":[";
+    const auto& conc = bal->concurrentProfiles();
+    for (size_t i = 0; i < conc.size(); ++i) {
+      o << (i ? "," : "") << "{\"rail_id\":" << conc[i].rail_id << ",\"calibration\":[";
+      for (size_t j = 0; j < conc[i].efficiency_points.size(); ++j)
+        o << (j ? "," : "") << "[" << conc[i].efficiency_points[j].first << ","
+          << nezha::formatDouble(conc[i].efficiency_points[j].second) << "]";
+      o << "]}";
+    }
     o << "],\"table\":" << bal->tableJson() << "}";
     return o.str();
   }

@@ -54,8 +54,10 @@ int gridFor(nz_rail* r, uint64_t range_bytes, int world, int unroll) {
   // sm_budget 0 = the rail's measured sweet spot on B200 (profiles/README.md):
   // NVLS saturates the switch path with 32 CTAs, the SM rail with 64; the
   // rest of the GPU stays free for a concurrent rail or the caller's kernels.
-  const int def = r->kind == NZ_RAIL_NVLS ? 32 : (r->kind == NZ_RAIL_SM ? 64 : r->comm->sm_count);
-  const int budget = std::min(r->sm_budget > 0 ? r->sm_budget : def, r->comm->sm_count);
+  // With one rank every rail is a local copy (HBM-bound): two CTAs per SM.
+  const int def = world == 1 ? 2 * r->comm->sm_count
+                             : (r->kind == NZ_RAIL_NVLS ? 32 : (r->kind == NZ_RAIL_SM ? 64 : r->comm->sm_count));
+  const int budget = world == 1 ? def : std::min(r->sm_budget > 0 ? r->sm_budget : def, r->comm->sm_count);
   const uint64_t per_rank_vec = range_bytes / 16 / static_cast<uint64_t>(world) + 1;
   const uint64_t per_cta = static_cast<uint64_t>(kThreads) * unroll;
   const uint64_t g = (per_rank_vec + per_cta - 1) / per_cta;
