@@ -463,6 +463,7 @@ struct LLArgs {
   char* out;       // my output
   uint64_t* peer[kDevMaxRanks];  // each rank's LL buffer (8-byte {data, flag} words)
   uint64_t* local;
+  uint64_t* mc;  // multicast view of the LL buffers (NVLS-LL: one store reaches every rank)
   uint64_t lo, hi;
   uint64_t words;       // ceil((hi - lo) / 4)
   uint64_t slot_words;  // capacity of one (parity, rank) slot
@@ -512,7 +513,9 @@ __device__ __forceinline__ void ll_fold_word(const LLArgs& a, const uint32_t (&v
   }
 }
 
-template <typename DT, int N>
+// MC = true is the NVLS-LL variant: the push is one multimem.st to the
+// multicast view, which the switch replicates into every rank's slot.
+template <typename DT, int N, bool MC>
 __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs a) {
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -522,12 +525,16 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
     const uint64_t x = a.lo + 8 * p;
     const uint32_t d0 = ll_load_word(a.in, x, a.hi);
     const uint32_t d1 = x + 4 < a.hi ? ll_load_word(a.in, x + 4, a.hi) : 0u;
+    if (MC) {
+      mm_st<false>(reinterpret_cast<char*>(a.mc + my_slot + 2 * p), make_uint4(d0, a.flag, d1, a.flag));
+    } else {
 #pragma unroll
-    for (int r = 0; r < N; ++r) {
-      uint64_t* dst = a.peer[r] + my_slot + 2 * p;
-      asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(a.flag), "r"(d1),
-                   "r"(a.flag)
-                   : "memory");
+      for (int r = 0; r < N; ++r) {
+        uint64_t* dst = a.peer[r] + my_slot + 2 * p;
+        asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(a.flag), "r"(d1),
+                     "r"(a.flag)
+                     : "memory");
+      }
     }
   }
   for (uint64_t w = tid; w < a.words; w += stride) {

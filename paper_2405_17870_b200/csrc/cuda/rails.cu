@@ -91,14 +91,23 @@ void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_
 
 constexpr uint64_t kLLMaxBytes = 1024 * 1024;  // SM rail one-shot LL path up to this payload
 
-void dispatchLL(int world, int dtype, const LLArgs& a, int grid, cudaStream_t st) {
+// LL pays 2 wire bytes per payload byte times N receivers; beyond ~4 MiB / N
+// the two-shot kernels win (measured crossover, profiles/README.md).
+uint64_t llMaxBytes(int world) { return std::min<uint64_t>(kLLMaxBytes, (uint64_t{4} << 20) / world); }
+
+template <int N, bool MC>
+void launchLL(int dtype, const LLArgs& a, int grid, cudaStream_t st) {
+  if (dtype == NZ_F32) return (void)(ll_kernel<F32, N, MC><<<grid, kThreads, 0, st>>>(a));
+  if (dtype == NZ_BF16) return (void)(ll_kernel<BF16, N, MC><<<grid, kThreads, 0, st>>>(a));
+  return (void)(ll_kernel<I32, N, MC><<<grid, kThreads, 0, st>>>(a));
+}
+
+void dispatchLL(int world, int dtype, bool mc, const LLArgs& a, int grid, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (world) {
-#define NZ_CASE(n)                                                                      \
-  case n:                                                                               \
-    if (dtype == NZ_F32) return (void)(ll_kernel<F32, n><<<grid, kThreads, 0, st>>>(a));  \
-    if (dtype == NZ_BF16) return (void)(ll_kernel<BF16, n><<<grid, kThreads, 0, st>>>(a)); \
-    return (void)(ll_kernel<I32, n><<<grid, kThreads, 0, st>>>(a));
+#define NZ_CASE(n) \
+  case n:          \
+    return mc ? launchLL<n, true>(dtype, a, grid, st) : launchLL<n, false>(dtype, a, grid, st);
     NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
 #undef NZ_CASE
   }
@@ -175,12 +184,15 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
   const uint32_t epoch = r->epoch + 1;
   r->epoch += 2;  // start + end barrier; identical on every rank
 
-  if (N > 1 && r->kind == NZ_RAIL_SM && r->ll && hi - lo <= kLLMaxBytes && lo % 4 == 0) {
+  const bool mc_ll = r->kind == NZ_RAIL_NVLS;
+  if (N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= llMaxBytes(N) && lo % 4 == 0 &&
+      (!mc_ll || r->ll->mc_ptr)) {
     LLArgs a{};
     a.in = in->ptrs[me];
     a.out = out->ptrs[me];
     for (int p = 0; p < N; ++p) a.peer[p] = reinterpret_cast<uint64_t*>(r->ll->ptrs[p]);
     a.local = reinterpret_cast<uint64_t*>(r->ll->ptrs[me]);
+    a.mc = reinterpret_cast<uint64_t*>(r->ll->mc_ptr);
     a.lo = lo;
     a.hi = hi;
     a.words = (hi - lo + 3) / 4;
@@ -195,7 +207,7 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     const uint64_t threads = (a.words + 1) / 2 > a.words ? (a.words + 1) / 2 : a.words;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads,
                                                                               c->sm_count)));
-    dispatchLL(N, dtype, a, grid, st);
+    dispatchLL(N, dtype, mc_ll, a, grid, st);
     NZ_CUDA(cudaGetLastError());
     return;
   }
@@ -369,7 +381,7 @@ int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rai
     for (int p = 0; p < comm->world; ++p) r->pad_peer[p] = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[p] + pad_off);
     NZ_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
     NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
-    if (kind == NZ_RAIL_SM && comm->world > 1) {
+    if ((kind == NZ_RAIL_SM || kind == NZ_RAIL_NVLS) && comm->world > 1) {
       // LL slots: [parity 2][rank N][kLLMaxBytes / 4 words] x 8 bytes, zeroed on every rank first.
       r->ll_slot_words = nz::kLLMaxBytes / 4;
       r->ll = nz::allocSymmetric(comm, 2 * comm->world * r->ll_slot_words * sizeof(uint64_t));

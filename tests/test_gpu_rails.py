@@ -122,7 +122,9 @@ MULTI = [
     {"kind": "sm", "dtype": "bf16", "nbytes": 200_002},           # LL, odd bf16 tail word
     {"kind": "sm", "dtype": "f32", "nbytes": 262_144, "seg_off": 1024, "seg_len": 200_000},  # LL, offset
     {"kind": "sm", "dtype": "i32", "nbytes": 262_144, "fail_chunk": 0},  # LL range empty -> fault only
-    {"kind": "nvls", "dtype": "f32", "nbytes": 8192},
+    {"kind": "nvls", "dtype": "f32", "nbytes": 8192},             # NVLS-LL (multicast push)
+    {"kind": "nvls", "dtype": "bf16", "nbytes": 100_002},         # NVLS-LL, odd bf16 tail
+    {"kind": "nvls", "dtype": "i32", "nbytes": 65_540},
     {"kind": "sm", "dtype": "f32", "nbytes": 64 << 20, "fail_chunk": 2},
     {"kind": "ce", "dtype": "bf16", "nbytes": 32 << 20, "fail_chunk": 1},
     {"kind": "sm", "dtype": "bf16", "nbytes": 8 << 20, "chunk_begin": 1, "chunk_end": 3},
