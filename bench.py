@@ -195,7 +195,7 @@ def main():
     kinds = args.rails.split(",")
     dt = DTYPES[args.dtype]
     S = args.bytes
-    eng = Engine(comm, kinds=kinds, window=10, eta=0.2, calibrate_max_bytes=min(GiB, max(S, 1 << 20)))
+    eng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=min(GiB, max(S, 1 << 20)))
 
     def max_over_ranks(x: float) -> float:
         vals = comm.allgather_bytes(json.dumps(x).encode().ljust(32))
@@ -351,7 +351,7 @@ def main():
         s = 4096
         while s <= min(args.sweep_max, cap):
             it = 200 if s <= (1 << 20) else (40 if s <= (64 << 20) else 8)
-            t = timed(s, it, warm=20 if s <= (64 << 20) else 4)
+            t = timed(s, it, warm=20 if s <= (64 << 20) else 12)
             row = {"bytes": s, "us": round(t * 1e6, 2), "algbw_GBs": round(s / t / 1e9, 2),
                    "busbw_GBs": round(ring_volume(world, s) / t / 1e9, 2),
                    "hot": bool(eng.last_plans()[0]["hot"]) if eng.last_plans() else None,

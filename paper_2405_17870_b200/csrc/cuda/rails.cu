@@ -93,7 +93,12 @@ constexpr uint64_t kLLMaxBytes = 1024 * 1024;  // SM rail one-shot LL path up to
 
 // LL pays 2 wire bytes per payload byte times N receivers; beyond ~4 MiB / N
 // the two-shot kernels win (measured crossover, profiles/README.md).
-uint64_t llMaxBytes(int world) { return std::min<uint64_t>(kLLMaxBytes, (uint64_t{4} << 20) / world); }
+// The multicast push (NVLS-LL) saturates earlier than the unicast one: at
+// N = 4 it is 9.1 us at 256 KiB but 24.8 us at 1 MiB vs 20 us two-shot.
+uint64_t llMaxBytes(int world, bool mc) {
+  const uint64_t cap = mc ? (uint64_t{512} << 10) : kLLMaxBytes;
+  return std::min<uint64_t>(cap, (uint64_t{4} << 20) / world);
+}
 
 template <int N, bool MC>
 void launchLL(int dtype, const LLArgs& a, int grid, cudaStream_t st) {
@@ -185,7 +190,7 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
   r->epoch += 2;  // start + end barrier; identical on every rank
 
   const bool mc_ll = r->kind == NZ_RAIL_NVLS;
-  if (N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= llMaxBytes(N) && lo % 4 == 0 &&
+  if (N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= llMaxBytes(N, mc_ll) && lo % 4 == 0 &&
       (!mc_ll || r->ll->mc_ptr)) {
     LLArgs a{};
     a.in = in->ptrs[me];

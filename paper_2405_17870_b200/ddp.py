@@ -1,0 +1,79 @@
+"""PyTorch DDP communication hook backed by the multi-rail engine.
+
+The paper's end users are data-parallel trainers (Gloo apps, Horovod, vTrain;
+PAPER.md:528-531). This hook lets `torch.nn.parallel.DistributedDataParallel`
+reduce its gradient buckets through libnezha_b200.so instead of NCCL:
+
+    state = NezhaHookState.create(process_group)      # one Engine per rank
+    ddp_model.register_comm_hook(state, nezha_allreduce_hook)
+
+Each bucket is copied (device to device) into the engine's symmetric
+UnboundBuffer, all-reduced by the rails, copied back and averaged — all on the
+current CUDA stream, so DDP's own stream ordering covers it. torch is only the
+caller here; the reduction is the C ABI.
+"""
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import BF16, F32, I32
+from .runtime import Comm, Engine, SymmetricBuffer
+
+_DTYPES = {torch.float32: F32, torch.bfloat16: BF16, torch.int32: I32}
+
+
+@dataclass
+class NezhaHookState:
+    comm: Comm
+    engine: Engine
+    ub_in: SymmetricBuffer
+    ub_out: SymmetricBuffer
+    capacity: int
+    world: int
+
+    @classmethod
+    def create(cls, process_group=None, capacity: int = 256 << 20, rails=("nvls", "ce", "sm"),
+               **engine_overrides) -> "NezhaHookState":
+        import torch.distributed as dist
+
+        rank = dist.get_rank(process_group)
+        world = dist.get_world_size(process_group)
+        # Same session string on every rank: agree on it through the process group.
+        token = [f"ddp-{os.getpid()}-{torch.randint(0, 1 << 30, (1,)).item()}"]
+        dist.broadcast_object_list(token, src=0, group=process_group)
+        device = torch.cuda.current_device()
+        comm = Comm(rank, world, device, token[0])
+        if world > 1 and not comm.multicast:
+            rails = tuple(r for r in rails if r != "nvls") or ("sm",)
+        engine = Engine(comm, kinds=list(rails), **engine_overrides)
+        return cls(comm, engine, SymmetricBuffer(comm, capacity), SymmetricBuffer(comm, capacity), capacity, world)
+
+    def close(self) -> None:
+        self.engine.close()
+        self.ub_in.free()
+        self.ub_out.free()
+        self.comm.close()
+
+
+def nezha_allreduce_hook(state: NezhaHookState, bucket) -> torch.futures.Future:
+    """DDP comm hook: mean all-reduce of `bucket.buffer()` through the engine."""
+    t = bucket.buffer()
+    dtype = _DTYPES.get(t.dtype)
+    if dtype is None:
+        raise TypeError(f"nezha hook: unsupported gradient dtype {t.dtype}")
+    nbytes = t.numel() * t.element_size()
+    stream = torch.cuda.current_stream()
+    done = 0
+    while done < nbytes:  # buckets larger than the UnboundBuffer go in pieces
+        n = min(state.capacity, nbytes - done)
+        state.ub_in.write(t.data_ptr() + done, n, stream=stream)
+        state.engine.allreduce(state.ub_in, state.ub_out, n, dtype, stream)
+        state.ub_out.read(t.data_ptr() + done, n, stream=stream)
+        done += n
+    t.div_(state.world)
+    fut = torch.futures.Future()
+    fut.set_result(t)
+    return fut

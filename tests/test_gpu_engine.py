@@ -99,3 +99,13 @@ def test_engine_failover_reroute(fail_rail):
                 [r for r in rk["results"] if r["case"] == 1]
         for r in later:
             assert all(s[0] != fail_rail for s in r["segs"]), r
+
+
+@pytest.mark.multigpu
+def test_ddp_comm_hook_matches_nccl():
+    """The engine as a PyTorch DDP comm hook (paper_2405_17870_b200/ddp.py)."""
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = spawn(2, os.path.join(ROOT, "tests", "workers", "ddp_worker.py"), timeout=600)
+    for r in res:
+        assert r["ok"], r
