@@ -169,6 +169,12 @@ class Balancer {
   static int clampBucket(Bytes S);
   std::string tableJson() const;
 
+  // Warm restart: profiles, concurrent profiles, sync overhead
+  // and every measured / demoted bucket as JSON; loadState restores them on a
+  // balancer with the same rail ids (health is runtime state, not restored).
+  std::string saveState() const;
+  void loadState(const std::string& json);
+
  private:
   void rebuild();
   std::vector<double> modelAlpha(int bucket) const;

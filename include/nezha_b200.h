@@ -187,6 +187,12 @@ typedef struct {
 /* Last completed failover (returns NZ_ERR_INVALID when none happened). */
 int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep);
 
+/* Warm restart: the allocation table, calibrated profiles and
+ * sync overhead as JSON; load it on every rank (same text) to skip
+ * re-convergence. */
+int nz_engine_save_state(nz_engine_t* eng, char* out, size_t cap);
+int nz_engine_load_state(nz_engine_t* eng, const char* json);
+
 /* Timer totals per rail since the last reset (harvested ops only; call
  * nz_engine_synchronize first to harvest everything): ops, summed rail time
  * (fork -> rail done, us) and summed segment bytes. */

@@ -156,6 +156,8 @@ _SIGS = {
     "nz_engine_last_plan_json": (c_int, [c_void_p, c_char_p, c_size_t]),
     "nz_engine_rail_stats": (c_int, [c_void_p, c_int, POINTER(c_uint64), POINTER(c_double), POINTER(c_uint64)]),
     "nz_engine_stats_reset": (c_int, [c_void_p]),
+    "nz_engine_save_state": (c_int, [c_void_p, c_char_p, c_size_t]),
+    "nz_engine_load_state": (c_int, [c_void_p, c_char_p]),
     "nz_kernel_launch_count": (c_uint64, []),
     "nz_planner_run_trace": (c_int, [c_char_p, c_char_p, c_size_t]),
     "nz_emulate_fold": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64, c_uint64,

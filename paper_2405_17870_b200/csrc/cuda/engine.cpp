@@ -693,6 +693,23 @@ int nz_engine_rail_stats(nz_engine_t* eng, int rail_id, uint64_t* ops, double* t
   });
 }
 
+int nz_engine_save_state(nz_engine_t* eng, char* out, size_t cap) {
+  std::string s;
+  const int rc = guarded([&] {
+    if (!eng) fail(NZ_ERR_INVALID, "null engine");
+    s = eng->bal->saveState();
+  });
+  return rc != NZ_OK ? rc : copyOut(s, out, cap);
+}
+
+int nz_engine_load_state(nz_engine_t* eng, const char* json) {
+  return guarded([&] {
+    if (!eng || !json) fail(NZ_ERR_INVALID, "null argument");
+    eng->synchronize();
+    eng->bal->loadState(json);
+  });
+}
+
 int nz_engine_stats_reset(nz_engine_t* eng) {
   if (!eng) return NZ_ERR_INVALID;
   eng->stats.assign(eng->specs.size(), nz_engine::RailStat{});

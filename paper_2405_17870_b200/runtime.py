@@ -235,6 +235,13 @@ class Engine:
     def stats_reset(self) -> None:
         check(lib().nz_engine_stats_reset(self.handle), "nz_engine_stats_reset")
 
+    def save_state(self) -> str:
+        """AllocationTable + profiles as JSON (SPEC.md:355, --balancer-state)."""
+        return json.dumps(self._json(lib().nz_engine_save_state))
+
+    def load_state(self, text: str) -> None:
+        check(lib().nz_engine_load_state(self.handle, text.encode()), "nz_engine_load_state")
+
     def close(self) -> None:
         if self.handle:
             check(lib().nz_engine_destroy(self.handle), "nz_engine_destroy")

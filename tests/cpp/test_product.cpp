@@ -166,3 +166,27 @@ sm_budget = 16
   CHECK(rails[1].rail_id == 1);
   CHECK_THROWS_AS(toml::parse("a = 1\na = 2\n"), std::runtime_error);
 }
+
+TEST_CASE("AllocationTable persists and restores (SPEC.md:355)") {
+  RailProfile a{.rail_id = 0, .t_setup_us = 10, .bandwidth_bps = 6e11};
+  RailProfile b{.rail_id = 1, .t_setup_us = 30, .bandwidth_bps = 5e11};
+  BalancerConfig cfg;
+  cfg.window = 2;
+  cfg.sync_overhead_us = 2;
+  Balancer bal({a, b}, cfg);
+  const Bytes S = 256ull << 20;
+  for (int op = 0; op < 20; ++op) {
+    auto p = bal.allocate(S);
+    std::vector<std::pair<int, Micros>> lat;
+    for (auto& rs : p.segments) lat.emplace_back(rs.rail_id, rs.rail_id == 0 ? 700.0 : 400.0 + op);
+    bal.recordOp(p, lat);
+  }
+  const std::string saved = bal.saveState();
+  Balancer fresh({a, b}, cfg);
+  fresh.loadState(saved);
+  CHECK(fresh.tableJson().substr(fresh.tableJson().find("\"threshold\"")) ==
+        bal.tableJson().substr(bal.tableJson().find("\"threshold\"")));
+  CHECK(fresh.allocate(S).segments == bal.allocate(S).segments);
+  CHECK(fresh.saveState() == saved);
+  CHECK_THROWS_AS(fresh.loadState("{\"version\":2}"), std::invalid_argument);
+}
