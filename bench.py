@@ -424,6 +424,7 @@ def main():
             if fo:
                 out["failover"] = {"failed_rail": kinds[fo["failed_rail"]], "target_rail": kinds[fo["target_rail"]],
                                    "orphan_bytes": fo["orphan_length"], "detect_us": round(fo["detect_us"], 2),
+                                   "host_detect_us": round(fo["host_detect_us"], 2),
                                    "resume_us": round(fo["resume_us"], 2), "done_us": round(fo["done_us"], 2),
                                    "payload": "bf16 256 MiB"}
                 # failover = device fault stamp -> orphan fully reduced on the survivor

@@ -183,6 +183,8 @@ typedef struct {
   double detect_us;   /* device fault stamp -> host monitor saw it */
   double resume_us;   /* device fault stamp -> survivor started the orphan */
   double done_us;     /* device fault stamp -> orphan complete */
+  double host_detect_us; /* device fault stamp -> host monitor saw the record
+                            (host clock mapped onto %globaltimer, +-~2 us) */
 } nz_failover_report_t;
 /* Last completed failover (returns NZ_ERR_INVALID when none happened). */
 int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep);

@@ -107,6 +107,7 @@ class FailoverReport(ctypes.Structure):
         ("detect_us", c_double),
         ("resume_us", c_double),
         ("done_us", c_double),
+        ("host_detect_us", c_double),
     ]
 
 

@@ -54,6 +54,8 @@ struct nz_engine {
   nz_buf* ub_in = nullptr;
   nz_buf* ub_out = nullptr;
   std::vector<std::string> last_plans;  // JSON of each piece of the last call
+  int64_t clock_offset_ns = 0;          // %globaltimer - CLOCK_REALTIME
+  int64_t host_seen_ns = 0;             // host monitor saw the last fault record
   struct RailStat {
     uint64_t ops = 0;
     double us = 0;
@@ -138,6 +140,7 @@ struct nz_engine {
     fo.detect_us = (static_cast<double>(s[0]) - f) / 1000.0;
     fo.resume_us = (static_cast<double>(s[1]) - f) / 1000.0;
     fo.done_us = (static_cast<double>(s[2]) - f) / 1000.0;
+    fo.host_detect_us = (static_cast<double>(host_seen_ns + clock_offset_ns) - f) / 1000.0;
     have_fo = true;
     fo_pending = false;
   }
@@ -223,6 +226,29 @@ struct nz_engine {
   // Exception handler: wait for the device's fault record,
   // mark the rail Failed, pick the target (P9) and run the orphan chunks on
   // it with the failed segment's geometry (P10), after its current task.
+  static int64_t realtimeNs() {
+    timespec ts;
+    clock_gettime(CLOCK_REALTIME, &ts);
+    return static_cast<int64_t>(ts.tv_sec) * 1000000000LL + ts.tv_nsec;
+  }
+
+  // %globaltimer vs host CLOCK_REALTIME: best of 5 stamp round trips. Lets
+  // the report place the host monitor's detection on the device timeline.
+  void calibrateClock() {
+    int64_t best = INT64_MAX;
+    for (int i = 0; i < 5; ++i) {
+      stamps_host[0] = 0;
+      const int64_t t0 = realtimeNs();
+      nz::launchStamp(stamps_dev + 0, ctrl);
+      NZ_CUDA(cudaStreamSynchronize(ctrl));
+      const int64_t t1 = realtimeNs();
+      if (t1 - t0 < best) {
+        best = t1 - t0;
+        clock_offset_ns = static_cast<int64_t>(stamps_host[0]) - (t0 + t1) / 2;
+      }
+    }
+  }
+
   void handoff(Pending& p, const nezha::Plan& plan, const nezha::Segment& seg, int rid, uint64_t k, nz_buf* in,
                nz_buf* out, uint64_t base, int dtype) {
     nz_rail* fr = rails[index(rid)];
@@ -236,6 +262,7 @@ struct nz_engine {
         rec.chunk = f->chunk;
         rec.t_fail_ns = f->t_fail_ns;
         f->valid = 0;
+        host_seen_ns = realtimeNs();
         break;
       }
       if (*reinterpret_cast<volatile int*>(fr->wd_host)) fail(NZ_ERR_TIMEOUT, "rail watchdog fired while waiting for a fault");
@@ -574,6 +601,7 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     NZ_CUDA(cudaHostAlloc(&eng->stamps_host, 4 * sizeof(uint64_t), cudaHostAllocMapped));
     std::memset(eng->stamps_host, 0, 4 * sizeof(uint64_t));
     NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eng->stamps_dev), eng->stamps_host, 0));
+    eng->calibrateClock();
     if (!all_profiles || c.sync_overhead_us < 0) eng->calibrate();
     NZ_CUDA(cudaDeviceSynchronize());
     *out = eng.release();

@@ -12,8 +12,6 @@ UnboundBuffer, all-reduced by the rails, copied back and averaged — all on the
 current CUDA stream, so DDP's own stream ordering covers it. torch is only the
 caller here; the reduction is the C ABI.
 """
-from __future__ import annotations
-
 import os
 from dataclasses import dataclass
 
@@ -58,7 +56,7 @@ class NezhaHookState:
         self.comm.close()
 
 
-def nezha_allreduce_hook(state: NezhaHookState, bucket) -> torch.futures.Future:
+def nezha_allreduce_hook(state: NezhaHookState, bucket) -> torch.futures.Future[torch.Tensor]:
     """DDP comm hook: mean all-reduce of `bucket.buffer()` through the engine."""
     t = bucket.buffer()
     dtype = _DTYPES.get(t.dtype)
