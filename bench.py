@@ -6,8 +6,9 @@
 
 Metric (BASELINE.json): 8-GPU allreduce busbw GB/s vs size (4KB-1GB); 8KB p50
 latency; failover ms. A "step" is one engine allreduce of the headline payload
-(1 GiB fp32, synthetic) on the configured rails (default configs[1]: NVLS +
-copy-engine rails, load balanced). `value` = busbw = ringVolume(N, S) / t with
+(1 GiB fp32, synthetic) on the configured rails (default: the configs[2]
+rail set NVLS + copy-engine + SM under the cold/hot state machine, swept
+4 KiB-1 GiB as configs[1] specifies; `--rails nvls,ce` is configs[1] itself). `value` = busbw = ringVolume(N, S) / t with
 t the max over ranks of the device time per step (N = 1: algbw S / t, no
 NVLink exchange exists). Inputs are 1 GiB, larger than the 126 MB L2, so no
 flush is needed between steps. Rank 0 prints one JSON line.
@@ -167,7 +168,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rails", default="nvls,ce", help="comma list of nvls|ce|sm (configs[1] = nvls,ce)")
+    ap.add_argument("--rails", default="nvls,ce,sm",
+                    help="comma list of nvls|ce|sm (configs[1] = nvls,ce; configs[2] = nvls,ce,sm)")
     ap.add_argument("--bytes", type=int, default=GiB)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
     ap.add_argument("--tune-ops", type=int, default=200, help="balancer convergence ops before timing")
@@ -299,7 +301,7 @@ def main():
     out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-           "config": {"workload": f"configs[1]: {'+'.join(kinds)} rails, load-balanced {args.dtype} allreduce of "
+           "config": {"workload": f"multi-rail ({'+'.join(kinds)}) state-machine {args.dtype} allreduce of "
                                   f"{S} B per rank (value = busbw at this size; N=1: algbw)",
                       "global_batch": S, "seq_len": 0, "parallelism": f"dp{world}",
                       "l2": "inputs (1 GiB) larger than the 126 MB L2; no flush",

@@ -669,6 +669,7 @@ int nz_engine_inject_failure(nz_engine_t* eng, uint32_t op_seq, int rail_id, uin
     eng->index(rail_id);
     if (op_seq < eng->op_seq) fail(NZ_ERR_INVALID, "op already issued");
     eng->inject[op_seq] = {rail_id, chunk};
+    eng->calibrateClock();  // %globaltimer drifts against the host clock: re-anchor next to the op
   });
 }
 
