@@ -89,7 +89,7 @@ void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_
   }
 }
 
-constexpr uint64_t kLLMaxBytes = 1024 * 1024;  // SM rail one-shot LL path up to this payload
+constexpr uint64_t kLLMaxBytes = 2048 * 1024;  // SM rail one-shot LL path up to this payload
 
 // LL pays 2 wire bytes per payload byte times N receivers; beyond ~4 MiB / N
 // the two-shot kernels win (measured crossover, profiles/README.md).
@@ -388,7 +388,7 @@ int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rai
     NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
     if ((kind == NZ_RAIL_SM || kind == NZ_RAIL_NVLS) && comm->world > 1) {
       // LL slots: [parity 2][rank N][kLLMaxBytes / 4 words] x 8 bytes, zeroed on every rank first.
-      r->ll_slot_words = nz::kLLMaxBytes / 4;
+      r->ll_slot_words = (nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS) + 7) / 4;
       r->ll = nz::allocSymmetric(comm, 2 * comm->world * r->ll_slot_words * sizeof(uint64_t));
       NZ_CUDA(cudaMemset(r->ll->ptrs[comm->rank], 0, r->ll->mapped));
       NZ_CUDA(cudaDeviceSynchronize());

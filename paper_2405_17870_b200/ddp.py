@@ -72,6 +72,8 @@ def nezha_allreduce_hook(state: NezhaHookState, bucket) -> torch.futures.Future[
         state.ub_out.read(t.data_ptr() + done, n, stream=stream)
         done += n
     t.div_(state.world)
-    fut = torch.futures.Future()
+    # A CUDA-aware future: set_result records an event on the current stream and
+    # DDP's consumers wait on it, so nothing reads the bucket before the rails finish.
+    fut = torch.futures.Future(devices=[t.device])
     fut.set_result(t)
     return fut

@@ -88,17 +88,33 @@ def test_engine_failover_reroute(fail_rail):
         pytest.skip("needs 2 GPUs")
     spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3,
             "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 3, "fail": [fail_rail, 3], "fail_rep": 1},
-                      {"dtype": "i32", "nbytes": 64 << 20, "reps": 2}]}
+                      {"dtype": "i32", "nbytes": 64 << 20, "reps": 2},
+                      {"dtype": "i32", "nbytes": 96 << 20, "reps": 1, "readmit": True}]}
     res = _run(world, spec, timeout=900)
     for rk in res:
         fo = [r for r in rk["results"] if "failover" in r][0]["failover"]
         assert fo is not None and fo["failed_rail"] == fail_rail
         assert fo["target_rail"] != fail_rail and fo["orphan_length"] > 0
-        # After the failure the rail carries nothing.
+        assert fo["done_us"] > 0
+        # After the failure the rail carries nothing until it is readmitted.
         later = [r for r in rk["results"] if r["case"] == 0 and r["rep"] == 2] + \
-                [r for r in rk["results"] if r["case"] == 1]
+                [r for r in rk["results"] if r["case"] in (1, 2)]
         for r in later:
             assert all(s[0] != fail_rail for s in r["segs"]), r
+
+
+@pytest.mark.multigpu
+def test_engine_failover_int32_every_rail_exact():
+    """Config 4 rerun as int32: bit-exact on every rail, NVLS included (P2)."""
+    world = 4 if gpu_count() >= 4 else 2
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cases = []
+    for rail in (0, 1, 2):
+        cases.append({"dtype": "i32", "nbytes": 256 << 20, "reps": 1, "fail": [rail, 2], "readmit": True})
+    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "cases": cases}, timeout=900)
+    for rk in res:
+        assert len([r for r in rk["results"] if r.get("failover")]) == 3
 
 
 @pytest.mark.multigpu

@@ -104,6 +104,8 @@ def main():
             if failing:
                 rec["failover"] = fo
             out.append(rec)
+        if c.get("readmit") and c.get("fail"):
+            eng.readmit(c["fail"][0])
     state = eng.state()
     eng.close()
     bin_.free()
