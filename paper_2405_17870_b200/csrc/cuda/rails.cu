@@ -388,7 +388,8 @@ int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rai
     NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
     if ((kind == NZ_RAIL_SM || kind == NZ_RAIL_NVLS) && comm->world > 1) {
       // LL slots: [parity 2][rank N][kLLMaxBytes / 4 words] x 8 bytes, zeroed on every rank first.
-      r->ll_slot_words = (nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS) + 7) / 4;
+      // Even word count: every slot starts 16-byte aligned for the v4 pushes.
+      r->ll_slot_words = ((nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS) + 7) / 4 + 1) & ~uint64_t{1};
       r->ll = nz::allocSymmetric(comm, 2 * comm->world * r->ll_slot_words * sizeof(uint64_t));
       NZ_CUDA(cudaMemset(r->ll->ptrs[comm->rank], 0, r->ll->mapped));
       NZ_CUDA(cudaDeviceSynchronize());
