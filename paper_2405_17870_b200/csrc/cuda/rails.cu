@@ -198,6 +198,12 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     for (int p = 0; p < N; ++p) a.peer[p] = reinterpret_cast<uint64_t*>(r->ll->ptrs[p]);
     a.local = reinterpret_cast<uint64_t*>(r->ll->ptrs[me]);
     a.mc = reinterpret_cast<uint64_t*>(r->ll->mc_ptr);
+    // Every 16-byte push (unicast v4 or multimem.st) must be 16-byte aligned:
+    // a misaligned multimem store is not a clean trap on NVSwitch.
+    if ((r->ll_slot_words & 1u) != 0 || reinterpret_cast<uintptr_t>(r->ll->ptrs[me]) % 16 != 0 ||
+        (a.mc && reinterpret_cast<uintptr_t>(a.mc) % 16 != 0)) {
+      fail(NZ_ERR_INVALID, "LL slots are not 16-byte aligned");
+    }
     a.lo = lo;
     a.hi = hi;
     a.words = (hi - lo + 3) / 4;
@@ -240,6 +246,9 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
   if (r->kind == NZ_RAIL_NVLS) {
     if (!in->mc_ptr || !out->mc_ptr) fail(NZ_ERR_UNSUPPORTED, "NVLS rail needs multicast-bound buffers");
     NvlsArgs a{};
+    if (reinterpret_cast<uintptr_t>(in->mc_ptr) % 16 != 0 || reinterpret_cast<uintptr_t>(out->mc_ptr) % 16 != 0) {
+      fail(NZ_ERR_INVALID, "multicast windows must be 16-byte aligned");
+    }
     a.mc_in = in->mc_ptr;
     a.mc_out = out->mc_ptr;
     for (int p = 0; p < N; ++p) {

@@ -26,11 +26,14 @@ def spawn(world: int, script: str, args: list[str] | None = None, timeout: float
             env.update(extra_env)
         procs.append(subprocess.Popen([sys.executable, script] + (args or []), cwd=ROOT, env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
+    import time
+
     outs = []
     failed = False
+    deadline = time.monotonic() + timeout  # one deadline for the whole job
     for p in procs:
         try:
-            o, e = p.communicate(timeout=timeout)
+            o, e = p.communicate(timeout=max(1.0, deadline - time.monotonic()))
         except subprocess.TimeoutExpired:
             p.kill()
             o, e = p.communicate()

@@ -29,7 +29,7 @@ bandwidth_bps = 5.0e11
 """
 
 
-def _run(world, spec, timeout=600):
+def _run(world, spec, timeout=420):
     res = spawn(world, WORKER, [json.dumps(spec)], timeout=timeout)
     for rk in res:
         for r in rk["results"]:
@@ -60,7 +60,7 @@ def test_engine_multirail_parity(world):
                 {"dtype": "f32", "nbytes": 8192, "reps": 3},
                 {"dtype": "f32", "nbytes": 1 << 20, "reps": 2, "host": True},
             ]}
-    res = _run(world, spec, timeout=900)
+    res = _run(world, spec, timeout=420)
     # Every rank ran the same plans (the table is agreed across ranks).
     plans = [[r["segs"] for r in rk["results"]] for rk in res]
     assert all(p == plans[0] for p in plans)
@@ -74,7 +74,7 @@ def test_engine_oversized_split():
     n = (1 << 30) + (64 << 20)
     spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "calibrate_max_bytes": 1 << 20,
             "cases": [{"dtype": "f32", "nbytes": n}]}
-    res = _run(2, spec, timeout=900)
+    res = _run(2, spec, timeout=420)
     r = res[0]["results"][0]
     assert max(s[1] + s[2] for s in r["segs"]) == n
     assert len({(s[1] // (256 << 20)) for s in r["segs"]}) == 5
@@ -90,7 +90,7 @@ def test_engine_failover_reroute(fail_rail):
             "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 3, "fail": [fail_rail, 3], "fail_rep": 1},
                       {"dtype": "i32", "nbytes": 64 << 20, "reps": 2},
                       {"dtype": "i32", "nbytes": 96 << 20, "reps": 1, "readmit": True}]}
-    res = _run(world, spec, timeout=900)
+    res = _run(world, spec, timeout=420)
     for rk in res:
         fo = [r for r in rk["results"] if "failover" in r][0]["failover"]
         assert fo is not None and fo["failed_rail"] == fail_rail
@@ -112,7 +112,7 @@ def test_engine_failover_int32_every_rail_exact():
     cases = []
     for rail in (0, 1, 2):
         cases.append({"dtype": "i32", "nbytes": 256 << 20, "reps": 1, "fail": [rail, 2], "readmit": True})
-    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "cases": cases}, timeout=900)
+    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "cases": cases}, timeout=420)
     for rk in res:
         assert len([r for r in rk["results"] if r.get("failover")]) == 3
 

@@ -138,7 +138,7 @@ MULTI = [
 def test_multi_gpu_rails(world):
     if gpu_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(MULTI)], timeout=600)
+    res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(MULTI)], timeout=300)
     for rank_res in res:
         for r in rank_res["results"]:
             assert r["watchdog"] == 0, r
