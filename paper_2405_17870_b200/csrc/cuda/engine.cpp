@@ -293,16 +293,42 @@ struct nz_engine {
     fo_pending = true;
   }
 
+  // Collective point: every rank calls it at the same place in its op stream.
   void synchronize() {
-    for (auto* r : rails) {
-      for (auto s : r->side) NZ_CUDA(cudaStreamSynchronize(s));
-      NZ_CUDA(cudaStreamSynchronize(r->stream));
+    NZ_CUDA(cudaDeviceSynchronize());  // rail streams and cold ops on callers' streams
+    // Asynchronous failure path: a rail kernel whose barrier / LL poll timed
+    // out (a peer never arrived) sets its watchdog word and exits. Ranks
+    // agree (any rank saw it) and the rail goes Failed everywhere, so the
+    // tables stay identical; the caller learns the results since the last
+    // synchronize are not to be trusted (ChannelDownError, error.hpp:22-27).
+    std::vector<int32_t> flags(rails.size(), 0);
+    for (size_t i = 0; i < rails.size(); ++i) {
+      volatile int* w = rails[i]->wd_host;
+      flags[i] = *w;
+      *w = 0;
     }
-    NZ_CUDA(cudaStreamSynchronize(ctrl));
-    for (auto* r : rails)
-      if (*reinterpret_cast<volatile int*>(r->wd_host)) fail(NZ_ERR_TIMEOUT, "rail watchdog fired (a peer never arrived)");
+    if (comm->world > 1) {
+      const auto msgs = nz::exchange(comm, flags.data(), flags.size() * sizeof(int32_t), {});
+      for (const auto& m : msgs) {
+        const int32_t* v = reinterpret_cast<const int32_t*>(m.data.data());
+        for (size_t i = 0; i < flags.size(); ++i) flags[i] |= v[i];
+      }
+    }
+    std::string down;
+    for (size_t i = 0; i < rails.size(); ++i) {
+      if (!flags[i]) continue;
+      down += (down.empty() ? "" : ",") + std::to_string(specs[i].rail_id);
+      if (health->state(specs[i].rail_id).status != nezha::HealthStatus::Failed) {
+        health->channelDown(specs[i].rail_id);
+        bal->markFailed(specs[i].rail_id);
+      }
+    }
     finishFailoverReport();
-    drainTimer();  // collective point: every rank harvests the same ops here
+    drainTimer();  // every rank harvests the same ops here
+    if (!down.empty()) {
+      fail(NZ_ERR_RAIL_DOWN, "rail watchdog fired on rail(s) " + down +
+                                 ": marked Failed and excluded; results since the last synchronize are invalid");
+    }
   }
 
   void ensureUnbound(uint64_t bytes) {

@@ -207,10 +207,31 @@ ops 40 8388608
 """
 
 
+CASCADE = """
+world 4
+config sync_us 1 window 3
+rail 0 nvls 5 6e11
+rail 1 ce 20 5e11
+rail 2 sm 6 5e11
+truth 0 5 6e11 0.01
+truth 1 20 5e11 0.01
+truth 2 6 5e11 0.01
+seed 21
+ops 12 536870912
+fail 3 2 1
+fail 6 0 5
+ops 3 4096
+fail 9 1 0
+ops 4 1048576
+readmit 14 2
+ops 4 1048576
+"""
+
+
 @needs_lib
 @pytest.mark.parametrize("name,scenario", [("two_homog", TWO_HOMOG), ("three_hetero", THREE_HETERO),
                                            ("failover", FAILOVER), ("gated", GATED), ("ring", RING_ALGO),
-                                           ("shared_links", SHARED_LINKS)])
+                                           ("shared_links", SHARED_LINKS), ("cascade", CASCADE)])
 def test_trace_parity_byte_exact(name, scenario):
     got = run_trace(scenario)
     want = P.run(scenario)
