@@ -38,6 +38,7 @@ struct BarrierArgs {
   uint32_t* peer[kDevMaxRanks];
   uint32_t epoch;
   int* watchdog;  // host-mapped; set when a wait times out
+  uint64_t timeout_ns;  // give up after this long (NEZHA_WATCHDOG_MS, default 20 s)
 };
 
 struct FaultPost {
@@ -96,7 +97,6 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
 // Per-CTA barrier across ranks. Returns false (and flags the watchdog) if a
 // peer never arrived, so the kernel can exit instead of hanging the GPU.
@@ -120,7 +120,7 @@ __device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch
         const uint64_t now = globaltimer();
         if (t0 == 0) {
           t0 = now;
-        } else if (now - t0 > kWatchdogNs) {
+        } else if (now - t0 > b.timeout_ns) {
           atomicExch_system(b.watchdog, 1);
           s_ok = 0;
           break;
@@ -472,6 +472,7 @@ struct LLArgs {
   int parity;
   int rank;
   int* watchdog;
+  uint64_t timeout_ns;
   FaultPost post;
 };
 
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
           const uint64_t now = globaltimer();
           if (t0 == 0) {
             t0 = now;
-          } else if (now - t0 > kWatchdogNs) {
+          } else if (now - t0 > a.timeout_ns) {
             atomicExch_system(a.watchdog, 1);
             return;
           }

@@ -41,12 +41,24 @@ void shardOf(uint64_t lo, uint64_t hi, int rank, int world, uint64_t* s, uint64_
   *e = rank == world - 1 ? hi : A + 16 * (V * (rank + 1) / world);
 }
 
+// Device wait budget before a kernel gives up on a peer (watchdog).
+// NEZHA_WATCHDOG_MS overrides the 20 s default (tests use a short one).
+uint64_t watchdogNs() {
+  static const uint64_t ns = [] {
+    const char* e = getenv("NEZHA_WATCHDOG_MS");
+    const long long ms = e ? atoll(e) : 20000;
+    return static_cast<uint64_t>(ms > 0 ? ms : 20000) * 1000000ull;
+  }();
+  return ns;
+}
+
 BarrierArgs barrierArgs(nz_rail* r, uint32_t epoch) {
   BarrierArgs b{};
   b.local = r->pad_local;
   for (int p = 0; p < r->comm->world; ++p) b.peer[p] = r->pad_peer[p];
   b.epoch = epoch;
   b.watchdog = r->wd_dev;
+  b.timeout_ns = watchdogNs();
   return b;
 }
 
@@ -214,6 +226,7 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.parity = static_cast<int>(r->ll_flag & 1u);
     a.rank = me;
     a.watchdog = r->wd_dev;
+    a.timeout_ns = watchdogNs();
     a.post = post;
     const uint64_t threads = (a.words + 1) / 2 > a.words ? (a.words + 1) / 2 : a.words;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads,

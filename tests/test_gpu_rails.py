@@ -149,3 +149,15 @@ def test_multi_gpu_rails(world):
                 assert r["fault"] is not None and r["fault"]["chunk"] == case["fail_chunk"], r
             else:
                 assert r["fault"] is None, r
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("kind", ["sm", "nvls"])
+def test_watchdog_instead_of_hang(kind):
+    """A peer that never arrives: the kernel exits after the watchdog budget."""
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = spawn(2, os.path.join(ROOT, "tests", "workers", "watchdog_worker.py"), [kind], timeout=120,
+                extra_env={"NEZHA_WATCHDOG_MS": "300"})
+    r0 = [r for r in res if r["rank"] == 0][0]
+    assert r0["watchdog"] == 1 and r0["seconds"] < 30
