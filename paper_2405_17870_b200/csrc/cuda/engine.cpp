@@ -662,7 +662,10 @@ int nz_engine_allreduce(nz_engine_t* eng, nz_buf_t* in, nz_buf_t* out, uint64_t 
     if (bytes > in->size || bytes > out->size) fail(NZ_ERR_INVALID, "payload exceeds the buffers");
     if (bytes == 0) return;
     NZ_CUDA(cudaSetDevice(eng->comm->device));
-    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    // NULL is the legacy default stream; pass it explicitly, since a NULL
+    // stream given to a rail means "the rail's own stream" (nz_rail_allreduce)
+    // and the cold path would then run unordered with the caller's copies.
+    cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
     eng->last_plans.clear();
     for (const auto& piece : nezha::splitOversized(bytes)) {
       eng->op(in, out, piece.offset, piece.length, dtype, user);
