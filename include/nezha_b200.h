@@ -229,6 +229,11 @@ int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void
                     uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
                     void* stream);
 
+/* Same, for the SM rail's TMA-pipelined fold (ndst must equal world >= 2). */
+int nz_emulate_fold_tma(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
+                        uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
+                        void* stream);
+
 /* ----------------------------------------------------------------- core --- */
 uint64_t nz_core_ring_volume(int node_count, uint64_t payload);
 int nz_core_bucket_of(uint64_t size);

@@ -163,6 +163,8 @@ _SIGS = {
     "nz_planner_run_trace": (c_int, [c_char_p, c_char_p, c_size_t]),
     "nz_emulate_fold": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64, c_uint64,
                                 c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
+    "nz_emulate_fold_tma": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64,
+                                    c_uint64, c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
     "nz_core_ring_volume": (c_uint64, [c_int, c_uint64]),
     "nz_core_bucket_of": (c_int, [c_uint64]),
     "nz_core_default_chunk_bytes": (c_uint64, [c_uint64, c_int, c_int]),

@@ -567,6 +567,145 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
   post_fault(a.post);
 }
 
+// ------------------------------------------------- SM rail, TMA pipeline --
+// K3t: the SM rail's two-shot fold with the peer traffic moved by the Tensor
+// Memory Accelerator. One elected thread streams 1-D bulk tiles of the shard
+// from every rank's `in` (cp.async.bulk global -> shared over NVLink,
+// completion on an mbarrier) through a kTmaStages-deep ring; all threads fold
+// the N staged tiles in ring order (P1) into an output tile; the elected
+// thread then bulk-stores that tile to every rank's `out`
+// (cp.async.bulk shared -> global). Few instructions keep many NVLink bytes
+// in flight, which the LDG/STG version needs a full CTA of threads for.
+constexpr uint32_t kTmaTile = 4096;  // bytes per source per stage
+constexpr int kTmaStages = 3;
+
+__host__ __device__ constexpr size_t tma_smem_bytes(int n) {
+  return static_cast<size_t>(kTmaStages) * (n + 1) * kTmaTile + kTmaStages * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <typename DT, int N>
+__global__ void __launch_bounds__(256, 1) sm_tma_kernel(const __grid_constant__ FoldArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* tiles = smem;                                            // [stage][rank][kTmaTile]
+  unsigned char* outs = smem + static_cast<size_t>(kTmaStages) * N * kTmaTile;  // [stage][kTmaTile]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(outs + static_cast<size_t>(kTmaStages) * kTmaTile);
+
+  if (a.use_barrier && !cta_barrier<N, false>(a.bar, a.bar.epoch, a.rank)) return;
+  const uint64_t vs = (a.s + 15) & ~15ull;
+  const uint64_t ve = a.e & ~15ull;
+  if (vs >= ve) {
+    fold_scalar_range<DT, N>(a, N, a.s, a.e);
+  } else {
+    fold_scalar_range<DT, N>(a, N, a.s, vs);
+    fold_scalar_range<DT, N>(a, N, ve, a.e);
+    const uint64_t nvec = (ve - vs) / 16;
+    const uint64_t cb = vs + 16 * (nvec * blockIdx.x / gridDim.x);
+    const uint64_t ce = vs + 16 * (nvec * (blockIdx.x + 1) / gridDim.x);
+    const uint64_t ntiles = (ce - cb + kTmaTile - 1) / kTmaTile;
+    const bool leader = threadIdx.x == 0;
+    if (leader) {
+      for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint64_t i) {
+      const int s = static_cast<int>(i % kTmaStages);
+      const uint64_t x = cb + i * kTmaTile;
+      const uint32_t len = static_cast<uint32_t>(ce - x < kTmaTile ? ce - x : kTmaTile);
+      mbar_expect_tx(&bars[s], len * N);
+#pragma unroll
+      for (int r = 0; r < N; ++r) tma_load(tiles + (static_cast<size_t>(s) * N + r) * kTmaTile, a.src[r] + x, len, &bars[s]);
+    };
+    if (leader)
+      for (uint64_t i = 0; i < ntiles && i < static_cast<uint64_t>(kTmaStages); ++i) issue(i);
+    for (uint64_t i = 0; i < ntiles; ++i) {
+      const int s = static_cast<int>(i % kTmaStages);
+      const uint64_t x = cb + i * kTmaTile;
+      const uint32_t len = static_cast<uint32_t>(ce - x < kTmaTile ? ce - x : kTmaTile);
+      // The bulk stores of tile i - kTmaStages must have finished reading outs[s].
+      if (leader && i >= static_cast<uint64_t>(kTmaStages))
+        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
+      mbar_wait(&bars[s], static_cast<uint32_t>((i / kTmaStages) & 1));
+      __syncthreads();
+      const unsigned char* st = tiles + static_cast<size_t>(s) * N * kTmaTile;
+      unsigned char* ot = outs + static_cast<size_t>(s) * kTmaTile;
+      for (uint32_t v = threadIdx.x * 16; v < len; v += blockDim.x * 16) {
+        const uint64_t xv = x + v;
+        uint64_t run_end;
+        const int b = block_at<N, DT::kElem>(a.g, xv, &run_end);
+        if (run_end >= xv + 16) {
+          typename DT::Acc acc = DT::load(*reinterpret_cast<const uint4*>(st + static_cast<size_t>(b) * kTmaTile + v));
+#pragma unroll
+          for (int j = 1; j < N; ++j)
+            DT::add(acc, *reinterpret_cast<const uint4*>(st + static_cast<size_t>((b + j) % N) * kTmaTile + v));
+          *reinterpret_cast<uint4*>(ot + v) = DT::store(acc);
+        } else {
+          // Vector straddles a ring-block boundary: fold element by element.
+          for (uint32_t k = 0; k < 16; k += DT::kElem) {
+            uint64_t re;
+            const int be = block_at<N, DT::kElem>(a.g, xv + k, &re);
+            typename DT::Scalar acc = DT::sload(reinterpret_cast<const char*>(st + static_cast<size_t>(be) * kTmaTile + v + k));
+            for (int j = 1; j < N; ++j)
+              acc = DT::sadd(acc, DT::sload(reinterpret_cast<const char*>(st + static_cast<size_t>((be + j) % N) * kTmaTile + v + k)));
+            DT::sstore(reinterpret_cast<char*>(ot + v + k), acc);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+      __syncthreads();
+      if (leader) {
+#pragma unroll
+        for (int r = 0; r < N; ++r) tma_store(a.dst[r] + x, ot, len);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (i + kTmaStages < ntiles) issue(i + kTmaStages);  // tiles[s] is free: every thread folded it
+      }
+    }
+    if (leader) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // all peer stores performed
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // ... and ordered before the release below
+    }
+  }
+  if (a.use_barrier && !cta_barrier<N, true>(a.bar, a.bar.epoch + 1, a.rank)) return;
+  post_fault(a.post);
+}
+
 // CE rail: start / end barriers around the DMA phases, and the fault post.
 template <int N>
 __global__ void barrier_kernel(const __grid_constant__ BarrierArgs b, int rank, FaultPost post) {

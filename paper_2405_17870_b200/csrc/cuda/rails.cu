@@ -91,6 +91,41 @@ void dispatchFoldDT(int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
   }
 }
 
+// SM-rail TMA pipeline (K3t). Opt-in with NEZHA_SM_TMA=1 until its sweep is
+// committed; nz_emulate_fold_tma runs it on one GPU for the parity tests.
+bool smTmaEnabled() {
+  static const bool on = [] {
+    const char* e = getenv("NEZHA_SM_TMA");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
+template <typename DT, int N>
+void launchTmaDT(const FoldArgs& a, int grid, cudaStream_t st) {
+  static bool configured = false;  // opt in to > 48 KiB of dynamic shared memory once
+  const size_t smem = tma_smem_bytes(N);
+  if (!configured) {
+    NZ_CUDA(cudaFuncSetAttribute(sm_tma_kernel<DT, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    configured = true;
+  }
+  sm_tma_kernel<DT, N><<<grid, 256, smem, st>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void dispatchTma(int world, int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
+  switch (world) {
+#define NZ_CASE(n)                                                    \
+  case n:                                                             \
+    if (dtype == NZ_F32) return launchTmaDT<F32, n>(a, grid, st);     \
+    if (dtype == NZ_BF16) return launchTmaDT<BF16, n>(a, grid, st);   \
+    return launchTmaDT<I32, n>(a, grid, st);
+    NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
+#undef NZ_CASE
+  }
+}
+
 template <int NDST_IS_N>
 void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
   switch (world) {
@@ -250,8 +285,14 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.use_barrier = N > 1;
     a.rank = me;
     a.post = post;
-    const int grid = gridFor(r, hi - lo, N, 2);
-    dispatchFold<1>(N, dtype, a, grid, st);
+    if (N > 1 && smTmaEnabled()) {
+      const uint64_t tiles = (hi - lo) / N / kTmaTile + 1;
+      const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, gridFor(r, hi - lo, N, 2))));
+      dispatchTma(N, dtype, a, grid, st);
+    } else {
+      const int grid = gridFor(r, hi - lo, N, 2);
+      dispatchFold<1>(N, dtype, a, grid, st);
+    }
     NZ_CUDA(cudaGetLastError());
     return;
   }
@@ -476,10 +517,11 @@ int nz_rail_allreduce(nz_rail_t* rail, nz_buf_t* in, nz_buf_t* out, uint64_t seg
   });
 }
 
-int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
-                    uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
-                    void* stream) {
+namespace {
+int emulateFold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst, uint64_t seg_off,
+                uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid, void* stream, bool tma) {
   return guarded([&] {
+    if (tma && (ndst != world || world < 2)) fail(NZ_ERR_INVALID, "TMA emulation needs ndst == world >= 2");
     if (world < 1 || world > nz::kMaxRanks || rank < 0 || rank >= world) fail(NZ_ERR_INVALID, "bad world/rank");
     if (!src || !dst || (ndst != 1 && ndst != world)) fail(NZ_ERR_INVALID, "bad src/dst");
     const int es = nz::elemSize(dtype);
@@ -503,12 +545,27 @@ int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void
       grid = static_cast<int>(std::min<uint64_t>(sms, (per_rank_vec + 2 * nz::kThreads - 1) / (2 * nz::kThreads)));
       grid = std::max(grid, 1);
     }
-    if (ndst == 1)
+    if (tma)
+      nz::dispatchTma(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
+    else if (ndst == 1)
       nz::dispatchFold<0>(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
     else
       nz::dispatchFold<1>(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
     NZ_CUDA(cudaGetLastError());
   });
+}
+}  // namespace
+
+int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
+                    uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
+                    void* stream) {
+  return emulateFold(world, rank, dtype, src, dst, ndst, seg_off, seg_len, chunk_bytes, lo, hi, grid, stream, false);
+}
+
+int nz_emulate_fold_tma(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
+                        uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
+                        void* stream) {
+  return emulateFold(world, rank, dtype, src, dst, ndst, seg_off, seg_len, chunk_bytes, lo, hi, grid, stream, true);
 }
 
 int nz_rail_poll_fault(nz_rail_t* r, nz_fault_record_t* rec, int consume) {

@@ -267,9 +267,10 @@ def run_trace(scenario: str) -> str:
 
 
 def emulate_fold(world: int, rank: int, dtype: int, srcs: list[int], dsts: list[int], seg_off: int, seg_len: int,
-                 chunk_bytes: int, lo: int, hi: int, grid: int = 0, stream=None) -> None:
-    """Single-GPU emulation of one rank of the SM / CE rail kernels (nz_emulate_fold)."""
+                 chunk_bytes: int, lo: int, hi: int, grid: int = 0, stream=None, tma: bool = False) -> None:
+    """Single-GPU emulation of one rank of the SM / CE rail kernels (nz_emulate_fold[_tma])."""
     s = (c_void_p * len(srcs))(*srcs)
     d = (c_void_p * len(dsts))(*dsts)
-    check(lib().nz_emulate_fold(world, rank, dtype, s, d, len(dsts), seg_off, seg_len, chunk_bytes, lo, hi, grid,
-                                _stream(stream)), "nz_emulate_fold")
+    fn = lib().nz_emulate_fold_tma if tma else lib().nz_emulate_fold
+    check(fn(world, rank, dtype, s, d, len(dsts), seg_off, seg_len, chunk_bytes, lo, hi, grid, _stream(stream)),
+          "nz_emulate_fold")

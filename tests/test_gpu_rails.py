@@ -55,7 +55,7 @@ EMU_CASES = [
 
 
 @pytest.mark.parametrize("world,dtype,nbytes,seg_off,seg_len,chunked", EMU_CASES)
-@pytest.mark.parametrize("mode", ["sm", "ce"])
+@pytest.mark.parametrize("mode", ["sm", "ce", "tma"])
 def test_emulated_rail_fold_bit_exact(world, dtype, nbytes, seg_off, seg_len, chunked, mode):
     torch = pytest.importorskip("torch")
     if gpu_count() < 1:
@@ -71,13 +71,14 @@ def test_emulated_rail_fold_bit_exact(world, dtype, nbytes, seg_off, seg_len, ch
     chunk = oracle.default_chunk_bytes(seg_len, world, chunked)
     lo, hi = seg_off, seg_off + seg_len
     for r in range(world):
-        dst = [d.data_ptr() for d in douts] if mode == "sm" else [douts[r].data_ptr()]
-        emulate_fold(world, r, dtype, [d.data_ptr() for d in dins], dst, seg_off, seg_len, chunk, lo, hi)
+        dst = [d.data_ptr() for d in douts] if mode in ("sm", "tma") else [douts[r].data_ptr()]
+        emulate_fold(world, r, dtype, [d.data_ptr() for d in dins], dst, seg_off, seg_len, chunk, lo, hi,
+                     tma=mode == "tma")
     torch.cuda.synchronize()
     want = oracle.reduce_range(inputs, dtype, seg_off, seg_len, chunk, lo, hi)
     for r in range(world):
         got = douts[r].cpu().numpy().view(want.dtype)
-        if mode == "sm":
+        if mode in ("sm", "tma"):
             np.testing.assert_array_equal(_bits(got), _bits(want), err_msg=f"rank {r}")
         else:
             s, e = shard_of(lo, hi, r, world)
