@@ -36,3 +36,15 @@ def test_product_cpp_api(tmp_path):
 def test_reference_suites_against_our_headers(tmp_path, suite, extra):
     out = _build_run(tmp_path, suite[:-4], [os.path.join(REF_TESTS, suite), *SRCS, *extra])
     assert "0 failed" in out
+
+
+def test_gpu_header_compiles_and_maps_errors(tmp_path):
+    lib_dir = os.path.join(ROOT, "paper_2405_17870_b200")
+    if not os.path.exists(os.path.join(lib_dir, "libnezha_b200.so")):
+        pytest.skip("library not built")
+    exe = str(tmp_path / "test_gpu_header")
+    r = subprocess.run([shutil.which("g++"), *FLAGS, "-o", exe, os.path.join(ROOT, "tests", "cpp", "test_gpu_header.cpp"),
+                        f"-L{lib_dir}", "-lnezha_b200", f"-Wl,-rpath,{lib_dir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
