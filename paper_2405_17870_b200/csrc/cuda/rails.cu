@@ -271,7 +271,17 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     return;
   }
 
-  if (N == 1 || r->kind == NZ_RAIL_SM) {
+  if (N == 1) {  // identity allreduce: every rail is a local HBM copy
+    const uint64_t vec = (hi - lo) / 16 + 1;
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((vec + kThreads * 8 - 1) / (kThreads * 8), 2ull * c->sm_count)));
+    copy_kernel<<<grid, kThreads, 0, st>>>(in->ptrs[0], out->ptrs[0], lo, hi, post);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    NZ_CUDA(cudaGetLastError());
+    return;
+  }
+
+  if (r->kind == NZ_RAIL_SM) {
     FoldArgs a{};
     for (int p = 0; p < N; ++p) {
       a.src[p] = in->ptrs[p];
