@@ -178,6 +178,7 @@ class Balancer {
  private:
   void rebuild();
   std::vector<double> modelAlpha(int bucket) const;
+  std::vector<double> computeModelAlpha(int bucket) const;
   std::vector<double> restrictToHealthy(std::vector<double> a) const;
   std::vector<RailProfile> healthyProfiles(std::vector<int>* idx, bool concurrent = false) const;
   double hotMinusCold(Bytes S) const;
@@ -192,6 +193,10 @@ class Balancer {
   std::map<int, std::vector<double>> saved_alpha_;  // alpha snapshot at the last failure
   std::map<int, std::vector<LatencyWindow>> windows_;  // bucket -> per rail index
   Agreement agree_;
+  std::uint64_t profile_version_ = 0;  // bumped when rails_ / concurrent_ change
+  mutable std::map<int, std::vector<double>> model_cache_;
+  mutable std::vector<bool> model_cache_healthy_;
+  mutable std::uint64_t model_cache_version_ = ~std::uint64_t{0};
 };
 
 std::string formatDouble(double v);  // "%.17g", shared by every JSON writer

@@ -198,6 +198,8 @@ class Table:
         self.saved = {}
         self.win = {}  # bucket -> {index: [samples]}
         self.conc = []
+        self.pver = 0  # profile version (model alpha cache key)
+        self._mcache, self._mkey = {}, None
         self._rebuild()
 
     @property
@@ -207,6 +209,7 @@ class Table:
 
     def set_concurrent(self, rails):
         self.conc = sorted(rails, key=lambda r: r.rail_id)
+        self.pver += 1
         self._rebuild()
 
     # -- helpers
@@ -232,12 +235,29 @@ class Table:
         return [1.0 / h if self.ok[i] else 0.0 for i in range(len(a))]
 
     def model_alpha(self, k):
+        """P11: Eq. 8 on the model's uniform-split latencies, then up to
+        max_iters Eq. 7 steps on the model's own latencies (cached)."""
+        key = (tuple(self.ok), self.pver)
+        if key != self._mkey:
+            self._mcache, self._mkey = {}, key
+        if k in self._mcache:
+            return list(self._mcache[k])
         H = self.healthy()
-        share = max((1 << k) // len(H), 1)
-        init = eq8([self.hot_rails[i].latency(share) for i in H])
+        hp = [self.hot_rails[i] for i in H]
+        S = 1 << k
+        share = max(S // len(H), 1)
+        ah = eq8([r.latency(share) for r in hp])
+        if len(hp) > 1:
+            for _ in range(self.cfg["max_iters"]):
+                lens = split(ah, S)
+                t = [hp[j].latency(lens[j]) if lens[j] > 0 else 0.0 for j in range(len(hp))]
+                ah, conv = eq7(ah, t, self.cfg["eta"], self.cfg["eps"])
+                if conv:
+                    break
         a = [0.0] * len(self.rails)
         for j, i in enumerate(H):
-            a[i] = init[j]
+            a[i] = ah[j]
+        self._mcache[k] = list(a)
         return a
 
     @staticmethod

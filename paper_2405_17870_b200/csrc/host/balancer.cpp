@@ -239,6 +239,21 @@ std::vector<double> Balancer::restrictToHealthy(std::vector<double> a) const {
 
 // P11: Eq. 8 applied to the calibrated model's uniform-split latencies.
 std::vector<double> Balancer::modelAlpha(int bucket) const {
+  // Depends only on the profiles and the healthy set: cached per bucket.
+  std::vector<bool> key = healthy_;
+  if (key != model_cache_healthy_ || model_cache_version_ != profile_version_) {
+    model_cache_.clear();
+    model_cache_healthy_ = key;
+    model_cache_version_ = profile_version_;
+  }
+  auto it = model_cache_.find(bucket);
+  if (it != model_cache_.end()) return it->second;
+  auto a = computeModelAlpha(bucket);
+  model_cache_[bucket] = a;
+  return a;
+}
+
+std::vector<double> Balancer::computeModelAlpha(int bucket) const {
   std::vector<int> idx;
   const auto hp = healthyProfiles(&idx, /*concurrent=*/true);
   std::vector<double> a(rails_.size(), 0.0);
@@ -246,8 +261,20 @@ std::vector<double> Balancer::modelAlpha(int bucket) const {
   const Bytes share = std::max<Bytes>(S / hp.size(), 1);
   std::vector<Micros> T;
   for (const auto& p : hp) T.push_back(p.messageLatency(share));
-  const auto init = initCoefficients(T);
-  for (size_t j = 0; j < idx.size(); ++j) a[idx[j]] = init[j];
+  std::vector<double> ah = initCoefficients(T);
+  // P11: then the same Eq. 7 descent the Timer would run, on the model's own
+  // latencies (up to max_iters virtual flushes), so an unmeasured bucket is
+  // judged hot or cold on a converged split, not on the Eq. 8 first guess.
+  for (int it = 0; it < cfg_.max_iters && hp.size() > 1; ++it) {
+    const auto len = splitLengths(ah, S);
+    std::vector<Micros> t(hp.size(), 0.0);
+    for (size_t j = 0; j < hp.size(); ++j)
+      if (len[j] > 0) t[j] = hp[j].messageLatency(len[j]);
+    bool conv = false;
+    ah = updateCoefficients(ah, t, cfg_.eta, cfg_.convergence_eps, &conv);
+    if (conv) break;
+  }
+  for (size_t j = 0; j < idx.size(); ++j) a[idx[j]] = ah[j];
   return a;
 }
 
@@ -441,6 +468,7 @@ void Balancer::setProfiles(std::vector<RailProfile> rails) {
     if (rails[i].rail_id != rails_[i].rail_id) throw std::invalid_argument("setProfiles: rail ids changed");
   }
   rails_ = std::move(rails);
+  ++profile_version_;
   rebuild();
 }
 
@@ -454,6 +482,7 @@ void Balancer::setConcurrentProfiles(std::vector<RailProfile> rails) {
     }
   }
   concurrent_ = std::move(rails);
+  ++profile_version_;
   rebuild();
 }
 

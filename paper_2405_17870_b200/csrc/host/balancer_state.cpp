@@ -75,6 +75,7 @@ void Balancer::loadState(const std::string& text) {
   }
   rails_ = prof;
   concurrent_ = conc;
+  ++profile_version_;
   cfg_.sync_overhead_us = root.doubleOr("sync_overhead_us", cfg_.sync_overhead_us);
   for (auto& [k, e] : table_.buckets) {
     e.measured = false;

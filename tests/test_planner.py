@@ -275,3 +275,57 @@ def test_trace_failover_tickets():
     for l in lines:
         if "segs" in l and 20 < l["op"] < 70:
             assert all(s[0] != 0 for s in l["segs"])
+
+
+@needs_lib
+def test_acceptance_balancer_convergence():
+    """SPEC.md:537 (acceptance 3): 20 random 2-3 rail profile sets with rho <= 5;
+    the table converges to within 5% of the 0.001-grid optimum of T_hot in <= 100
+    flushes (one flush per op here: window 1)."""
+    import json
+    import random
+
+    rnd = random.Random(2405)
+    done = 0
+    while done < 20:
+        R = rnd.choice([2, 3])
+        rails = [(rnd.uniform(5, 60), rnd.uniform(1e11, 6e11)) for _ in range(R)]
+        S = 256 << 20
+        thr = sorted(S / (t + S / b * 1e6) for t, b in rails)
+        if thr[-1] / thr[0] > 5:
+            continue
+        done += 1
+        lines = ["world 8", "config sync_us 0 window 1 eta 0.2 eps 0.001 max_iters 100"]
+        for i, (t, b) in enumerate(rails):
+            lines += [f"rail {i} tcp {t} {b}", f"truth {i} {t} {b} 0"]
+        lines += ["seed 1", f"ops 101 {S}"]
+        out = [json.loads(l) for l in run_trace("\n".join(lines)).splitlines()]
+        final = [l for l in out if "segs" in l][-1]
+        T = max(t + n / b * 1e6 for (t, b), (_, _, n) in zip([rails[s[0]] for s in final["segs"]], final["segs"]))
+        profs = [P.Rail(i, t, b) for i, (t, b) in enumerate(rails)]
+        best = float("inf")
+        if R == 2:
+            for k in range(1, 1000):
+                a = k / 1000
+                best = min(best, P.hot(profs, [a, 1 - a], S, 0.0))
+        else:
+            for k in range(1, 200):
+                for m in range(1, 200 - k):
+                    a = [k / 200, m / 200, 1 - (k + m) / 200]
+                    best = min(best, P.hot(profs, a, S, 0.0))
+        assert T <= 1.05 * best, (rails, T, best)
+
+
+@needs_lib
+def test_acceptance_rho_gate():
+    """SPEC.md:538 (acceptance 4): throughput ratio > 5 -> single rail; <= 5 -> split."""
+    import json
+
+    def plan(bw1):
+        sc = "\n".join(["world 4", "config sync_us 0 window 50",
+                        "rail 0 tcp 0 5e9", f"rail 1 tcp 0 {bw1}", "truth 0 0 5e9 0", f"truth 1 0 {bw1} 0",
+                        "seed 1", "ops 1 67108864"])
+        return [json.loads(l) for l in run_trace(sc).splitlines() if '"segs"' in l][0]
+
+    assert len(plan(0.9e9)["segs"]) == 1  # ratio ~5.6 at the model split
+    assert len(plan(2.5e9)["segs"]) == 2  # ratio ~2
