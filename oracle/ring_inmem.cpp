@@ -177,7 +177,7 @@ class Executor {
                 off + blkBegin(sb) * es_);
       const uint64_t n = blkEnd(rb) - blkBegin(rb);
       tmp.resize(n);
-      if (n) recvBlock(prev, reinterpret_cast<uint8_t*>(tmp.data()), n * 4);
+      recvBlock(prev, reinterpret_cast<uint8_t*>(tmp.data()), n * 4);  // an empty block still travels as one frame
       uint32_t* dst = acc.data() + blkBegin(rb);
       for (uint64_t i = 0; i < n; ++i) {
         if (job_.dtype == I32) {
@@ -213,7 +213,7 @@ class Executor {
       const int rb = ((r_ - s) % N_ + N_) % N_;
       sendBlock(next, fin.data() + blkBegin(sb) * es_, (blkEnd(sb) - blkBegin(sb)) * es_, off + blkBegin(sb) * es_);
       const uint64_t n = blkEnd(rb) - blkBegin(rb);
-      if (n) recvBlock(prev, fin.data() + blkBegin(rb) * es_, n * es_);
+      recvBlock(prev, fin.data() + blkBegin(rb) * es_, n * es_);
     }
     std::memcpy(static_cast<uint8_t*>(job_.out[r_]) + off, fin.data(), len);  // commit the whole chunk at once
   }

@@ -106,3 +106,42 @@ def test_handoff_exactly_once(fail_chunk, dtype):
     want = oracle.reduce_segments(inputs, dtype, [(o, l, oracle.default_chunk_bytes(l, world)) for _, o, l in segs])
     for r in range(world):
         np.testing.assert_array_equal(bits(outs[r]), bits(want))
+
+
+def test_acceptance_correctness_vs_direct_sum():
+    """SPEC.md:535 (acceptance 1): ring-order fold = direct sum within 1e-5
+    relative, N in {2, 4, 8}, random fp32 tensors, both algorithms."""
+    rng = np.random.default_rng(535)
+    for case in range(200):
+        world = int(rng.choice([2, 4, 8]))
+        n = int(rng.integers(1, 200_000))
+        chunked = bool(rng.integers(0, 2))
+        inputs = [rng.uniform(-1, 1, n).astype(np.float32) for _ in range(world)]
+        chunk = oracle.default_chunk_bytes(4 * n, world, chunked)
+        got = oracle.reduce_range(inputs, oracle.F32, 0, 4 * n, chunk, 0, 4 * n)
+        exact = np.sum([x.astype(np.float64) for x in inputs], axis=0)
+        scale = np.sum([np.abs(x.astype(np.float64)) for x in inputs], axis=0)
+        assert np.all(np.abs(got - exact) <= 1e-5 * np.maximum(scale, 1e-30)), case
+
+
+@needs_ref
+def test_acceptance_failover_exactly_once_random_trials():
+    """SPEC.md:539 / :409 (acceptance 5, correctness half): random single-rail
+    failures at random chunks on the reference fabric; the final tensor always
+    equals the oracle (no lost or double-reduced segment)."""
+    rng = np.random.default_rng(409)
+    for trial in range(30):
+        world = int(rng.choice([2, 3, 4]))
+        nrails = int(rng.choice([2, 3]))
+        S = 4 * int(rng.integers(40_000, 400_000))
+        cuts = sorted(4 * int(x) for x in rng.integers(1, S // 4, nrails - 1))
+        bounds = [0] + cuts + [S]
+        segs = [(r, bounds[r], bounds[r + 1] - bounds[r]) for r in range(nrails) if bounds[r + 1] > bounds[r]]
+        fail = int(rng.integers(0, nrails))
+        chunk = int(rng.integers(0, 6))
+        inputs = [oracle.synthetic_input(oracle.F32, r, S, seed_base=trial * 31) for r in range(world)]
+        outs, _, _ = oracle.inmem_allreduce(inputs, oracle.F32, segs, nrails, fail_rail=fail, fail_chunk=chunk)
+        want = oracle.reduce_segments(inputs, oracle.F32,
+                                      [(o, l, oracle.default_chunk_bytes(l, world)) for _, o, l in segs])
+        for r in range(world):
+            np.testing.assert_array_equal(bits(outs[r]), bits(want), err_msg=f"trial {trial} rank {r}")
