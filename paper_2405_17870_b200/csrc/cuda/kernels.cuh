@@ -595,16 +595,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+// Bounded wait: false after ~timeout_ns so a lost transfer cannot hang the GPU.
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, uint64_t timeout_ns) {
+  uint64_t t0 = 0;
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return true;
+    const uint64_t now = globaltimer();
+    if (t0 == 0) {
+      t0 = now;
+    } else if (now - t0 > timeout_ns) {
+      return false;
+    }
+  }
 }
 
 __device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -662,8 +674,13 @@ __global__ void __launch_bounds__(256, 1) sm_tma_kernel(const __grid_constant__ 
       // The bulk stores of tile i - kTmaStages must have finished reading outs[s].
       if (leader && i >= static_cast<uint64_t>(kTmaStages))
         asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
-      mbar_wait(&bars[s], static_cast<uint32_t>((i / kTmaStages) & 1));
-      __syncthreads();
+      const uint64_t budget = a.bar.timeout_ns ? a.bar.timeout_ns : 20ull * 1000 * 1000 * 1000;
+      const int ok = mbar_wait(&bars[s], static_cast<uint32_t>((i / kTmaStages) & 1), budget) ? 1 : 0;
+      if (!__syncthreads_and(ok)) {
+        if (leader && a.bar.watchdog) atomicExch_system(a.bar.watchdog, 1);
+        if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        return;  // a tile never arrived: give up rather than hang
+      }
       const unsigned char* st = tiles + static_cast<size_t>(s) * N * kTmaTile;
       unsigned char* ot = outs + static_cast<size_t>(s) * kTmaTile;
       for (uint32_t v = threadIdx.x * 16; v < len; v += blockDim.x * 16) {

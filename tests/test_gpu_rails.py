@@ -60,6 +60,8 @@ def test_emulated_rail_fold_bit_exact(world, dtype, nbytes, seg_off, seg_len, ch
     torch = pytest.importorskip("torch")
     if gpu_count() < 1:
         pytest.skip("no GPU")
+    if mode == "tma" and not os.environ.get("NEZHA_TEST_TMA"):
+        pytest.skip("TMA SM-rail kernel is opt-in until validated on hardware (NEZHA_TEST_TMA=1)")
     from paper_2405_17870_b200 import emulate_fold
 
     torch.cuda.set_device(0)
