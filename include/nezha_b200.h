@@ -22,6 +22,8 @@
  *                  per-rail executors -> join -> Timer -> balancer -> handoff.
  *   nz_planner_*   the balancer + faults decisions alone,
  *                  trace driven, CPU only; what the parity tests diff.
+ *   nz_pool_*      ComputePool: per-phase
+ *                  compute tokens; on B200 the tokens are SMs (P14).
  *   nz_core_*      core cost model (proj/include/nezha/core/math.hpp:9-17,
  *                  types.hpp:26-44) for FFI callers without C++.
  */
@@ -152,6 +154,9 @@ typedef struct {
   int calibrate_iters;       /* ops per size during startup calibration */
   uint64_t calibrate_max_bytes; /* largest calibrated size (default 1 GiB) */
   int timer_lag;             /* op k is sampled when op k + lag is issued (default 2) */
+  int compute_pool;          /* SM arbitration of concurrent rails (P14):
+                                0 off (default), 1 block (SPEC ComputePool), 2 shrink */
+  int pool_tokens;           /* ComputePool total_tokens; 0 = the GPU's SM count */
 } nz_engine_config_t;
 
 void nz_engine_config_default(nz_engine_config_t* cfg);
@@ -233,6 +238,25 @@ int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void
 int nz_emulate_fold_tma(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
                         uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
                         void* stream);
+
+/* ----------------------------------------------------------------- pool --- */
+/* Host ComputePool with the semantics pinned in include/nezha/compute_pool.hpp.
+ * phase: 0 io, 1 communication, 2 computation. nz_pool_acquire blocks when
+ * `blocking`, else sets *grant = -1 when it would block. */
+typedef struct nz_pool nz_pool_t;
+int nz_pool_create(int total_tokens, nz_pool_t** out);
+int nz_pool_destroy(nz_pool_t* pool);
+int nz_pool_declare(nz_pool_t* pool, int rail_id, int io, int communication, int computation);
+int nz_pool_acquire(nz_pool_t* pool, int rail_id, int phase, int blocking, int* grant);
+int nz_pool_release(nz_pool_t* pool, int rail_id, int phase);
+/* Computation tokens outstanding, or a negative error code. */
+int nz_pool_outstanding(const nz_pool_t* pool);
+int nz_pool_waiting(const nz_pool_t* pool);
+/* The engine's stream-order arbitration of one op (planComputeGrants):
+ * mode 0 off, 1 block (SPEC), 2 shrink. For each of the n rails (in order)
+ * writes its grant and a bitmask of the rail ids (< 32) it waits for. */
+int nz_pool_plan(int total_tokens, int mode, int n, const int* rail_ids, const int* demands, int* grants,
+                 uint32_t* wait_masks);
 
 /* ----------------------------------------------------------------- core --- */
 uint64_t nz_core_ring_volume(int node_count, uint64_t payload);

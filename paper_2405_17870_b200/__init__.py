@@ -5,7 +5,7 @@ include/nezha/*.hpp). This package is the Python mirror of that ABI used by
 the tests and bench.py.
 """
 from ._lib import BF16, CE, F32, I32, NVLS, SM, NezhaError, lib  # noqa: F401
-from .runtime import Comm, Engine, Rail, SymmetricBuffer, default_engine_config, emulate_fold, run_trace  # noqa: F401
+from .runtime import Comm, ComputePool, Engine, Rail, SymmetricBuffer, default_engine_config, emulate_fold, run_trace  # noqa: F401
 
-__all__ = ["Comm", "Engine", "Rail", "SymmetricBuffer", "default_engine_config", "emulate_fold", "run_trace",
+__all__ = ["Comm", "ComputePool", "Engine", "Rail", "SymmetricBuffer", "default_engine_config", "emulate_fold", "run_trace",
            "F32", "BF16", "I32", "NVLS", "CE", "SM", "NezhaError", "lib"]

@@ -94,6 +94,8 @@ class EngineConfig(ctypes.Structure):
         ("calibrate_iters", c_int),
         ("calibrate_max_bytes", c_uint64),
         ("timer_lag", c_int),
+        ("compute_pool", c_int),
+        ("pool_tokens", c_int),
     ]
 
 
@@ -165,6 +167,14 @@ _SIGS = {
                                 c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
     "nz_emulate_fold_tma": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64,
                                     c_uint64, c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
+    "nz_pool_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "nz_pool_destroy": (c_int, [c_void_p]),
+    "nz_pool_declare": (c_int, [c_void_p, c_int, c_int, c_int, c_int]),
+    "nz_pool_acquire": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_int)]),
+    "nz_pool_release": (c_int, [c_void_p, c_int, c_int]),
+    "nz_pool_outstanding": (c_int, [c_void_p]),
+    "nz_pool_waiting": (c_int, [c_void_p]),
+    "nz_pool_plan": (c_int, [c_int, c_int, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_uint32)]),
     "nz_core_ring_volume": (c_uint64, [c_int, c_uint64]),
     "nz_core_bucket_of": (c_int, [c_uint64]),
     "nz_core_default_chunk_bytes": (c_uint64, [c_uint64, c_int, c_int]),

@@ -14,6 +14,7 @@
 #include "internal.h"
 #include "nezha/balancer.hpp"
 #include "nezha/collective.hpp"
+#include "nezha/compute_pool.hpp"
 #include "nezha/core/error.hpp"
 #include "nezha/core/math.hpp"
 #include "nezha/engine.hpp"
@@ -62,6 +63,14 @@ struct nz_engine {
     uint64_t bytes = 0;
   };
   std::vector<RailStat> stats;  // parallel to specs
+  // ComputePool over this GPU's SMs (P14), driven in stream order.
+  std::unique_ptr<nezha::ComputePool> cpool;
+  nezha::PoolMode pool_mode = nezha::PoolMode::Off;
+  struct PoolStats {
+    uint64_t ops = 0;     // hot ops arbitrated
+    uint64_t waits = 0;   // computation phases ordered after an earlier holder
+    uint64_t shrunk = 0;  // grants below demand
+  } pool_stats;
 
   int index(int rail_id) const {
     for (size_t i = 0; i < specs.size(); ++i)
@@ -145,6 +154,41 @@ struct nz_engine {
     fo_pending = false;
   }
 
+  // Computation-phase gates of one concurrent launch of `segs` (rail_id,
+  // length) in rail order; empty when the pool is off. The release events go
+  // back to the event pool once the launch is enqueued (waits are captured at
+  // cudaStreamWaitEvent time).
+  std::vector<nz::ComputeGate> gatesFor(const std::vector<std::pair<int, uint64_t>>& segs, std::string* log) {
+    std::vector<nz::ComputeGate> gates(segs.size());
+    if (pool_mode == nezha::PoolMode::Off || segs.size() < 2) return gates;
+    std::vector<std::pair<int, int>> demands;
+    for (const auto& [rid, len] : segs) demands.emplace_back(rid, nz::railComputeCtas(rails[index(rid)], len));
+    const auto grants = nezha::planComputeGrants(*cpool, pool_mode, demands);
+    std::map<int, cudaEvent_t> released;
+    pool_stats.ops += 1;
+    std::ostringstream o;
+    for (size_t i = 0; i < grants.size(); ++i) {
+      const auto& g = grants[i];
+      gates[i].max_ctas = g.grant;
+      for (int w : g.waits) gates[i].waits.push_back(released.at(w));
+      gates[i].release = event();
+      released[g.rail_id] = gates[i].release;
+      pool_pending.push_back(gates[i].release);
+      pool_stats.waits += g.waits.empty() ? 0 : 1;
+      pool_stats.shrunk += g.grant < g.demand ? 1 : 0;
+      o << (i ? "," : "") << "[" << g.rail_id << "," << g.demand << "," << g.grant << ",[";
+      for (size_t j = 0; j < g.waits.size(); ++j) o << (j ? "," : "") << g.waits[j];
+      o << "]]";
+    }
+    if (log) *log = o.str();
+    return gates;
+  }
+  std::vector<cudaEvent_t> pool_pending;  // gate events of the launch being enqueued
+  void recycleGates() {
+    for (auto e : pool_pending) pool.push_back(e);
+    pool_pending.clear();
+  }
+
   // One op (piece) of at most 1 GiB at byte offset `base`.
   void op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dtype, cudaStream_t user) {
     const uint32_t seq = op_seq++;
@@ -173,7 +217,12 @@ struct nz_engine {
     const nezha::Segment* failed_seg = nullptr;
     int failed_rail = -1;
     uint64_t failed_chunk = 0;
-    for (const auto& rs : plan.segments) {
+    std::vector<std::pair<int, uint64_t>> segs;
+    for (const auto& rs : plan.segments) segs.emplace_back(rs.rail_id, rs.segment.length);
+    std::string grant_log;
+    auto gates = gatesFor(segs, &grant_log);
+    for (size_t si = 0; si < plan.segments.size(); ++si) {
+      const auto& rs = plan.segments[si];
       nz_rail* r = rails[index(rs.rail_id)];
       NZ_CUDA(cudaStreamWaitEvent(r->stream, p.start, 0));
       const uint64_t C = nezha::defaultChunkBytes(rs.segment.length, world, algo);
@@ -188,7 +237,7 @@ struct nz_engine {
         }
       }
       nz::railAllreduce(r, in, out, base + rs.segment.offset, rs.segment.length, C, 0, UINT64_MAX, dtype, seq,
-                        fail_chunk, r->stream);
+                        fail_chunk, r->stream, &gates[si]);
       cudaEvent_t e = event();
       NZ_CUDA(cudaEventRecord(e, r->stream));
       p.ends.emplace_back(rs.rail_id, e);
@@ -206,11 +255,12 @@ struct nz_engine {
       }
     }
     for (auto& [id, e] : p.ends) NZ_CUDA(cudaStreamWaitEvent(user, e, 0));
-    recordPlan(seq, base, len, plan);
+    recycleGates();
+    recordPlan(seq, base, len, plan, grant_log);
     pending.push_back(std::move(p));
   }
 
-  void recordPlan(uint32_t seq, uint64_t base, uint64_t len, const nezha::Plan& plan) {
+  void recordPlan(uint32_t seq, uint64_t base, uint64_t len, const nezha::Plan& plan, const std::string& grants = "") {
     std::ostringstream o;
     o << "{\"op\":" << seq << ",\"offset\":" << base << ",\"length\":" << len << ",\"hot\":" << (plan.hot ? "true" : "false")
       << ",\"segs\":[";
@@ -219,7 +269,9 @@ struct nz_engine {
       o << (i ? "," : "") << "[" << rs.rail_id << "," << base + rs.segment.offset << "," << rs.segment.length << ","
         << nezha::defaultChunkBytes(rs.segment.length, comm->world, algo) << "]";
     }
-    o << "]}";
+    o << "]";
+    if (!grants.empty()) o << ",\"grants\":[" << grants << "]";  // [rail, demand, grant, [waits]]
+    o << "}";
     last_plans.push_back(o.str());
   }
 
@@ -448,16 +500,20 @@ struct nz_engine {
       shares.push_back(share);
       const int iters = S <= (1u << 20) ? std::max(cfg.calibrate_iters, 4) : std::max(cfg.calibrate_iters / 4, 2);
       std::vector<double> acc(R, 0.0);
+      std::vector<std::pair<int, uint64_t>> segs;
+      for (size_t i = 0; i < R; ++i) segs.emplace_back(specs[i].rail_id, share);
       for (int it = 0; it < iters + 1; ++it) {
         NZ_CUDA(cudaEventRecord(start, io));
+        auto gates = gatesFor(segs, nullptr);  // the profiles see the same SM arbitration as the ops
         for (size_t i = 0; i < R; ++i) {
           NZ_CUDA(cudaStreamWaitEvent(rails[i]->stream, start, 0));
           const uint64_t C = nezha::defaultChunkBytes(share, world, algo);
           nz::railAllreduce(rails[i], ub_in, ub_out, share * i, share, C, 0, UINT64_MAX, NZ_F32, 0, -1,
-                            rails[i]->stream);
+                            rails[i]->stream, &gates[i]);
           NZ_CUDA(cudaEventRecord(ends[i], rails[i]->stream));
           NZ_CUDA(cudaStreamWaitEvent(io, ends[i], 0));
         }
+        recycleGates();
         NZ_CUDA(cudaStreamSynchronize(io));
         if (it == 0) continue;  // warm-up
         for (size_t i = 0; i < R; ++i) {
@@ -520,7 +576,10 @@ struct nz_engine {
           << nezha::formatDouble(conc[i].efficiency_points[j].second) << "]";
       o << "]}";
     }
-    o << "],\"table\":" << bal->tableJson() << "}";
+    o << "],\"compute_pool\":{\"mode\":" << static_cast<int>(pool_mode) << ",\"tokens\":"
+      << (cpool ? cpool->totalTokens() : 0) << ",\"ops\":" << pool_stats.ops << ",\"waits\":" << pool_stats.waits
+      << ",\"shrunk\":" << pool_stats.shrunk << "}";
+    o << ",\"table\":" << bal->tableJson() << "}";
     return o.str();
   }
 };
@@ -572,6 +631,10 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     }
     auto& c = eng->cfg;
     if (c.timer_lag < 1) c.timer_lag = 1;
+    if (c.compute_pool < 0 || c.compute_pool > 2) fail(NZ_ERR_INVALID, "compute_pool must be 0 (off), 1 (block) or 2 (shrink)");
+    if (c.pool_tokens < 0) fail(NZ_ERR_INVALID, "pool_tokens must be >= 0");
+    eng->pool_mode = static_cast<nezha::PoolMode>(c.compute_pool);
+    eng->cpool = std::make_unique<nezha::ComputePool>(c.pool_tokens > 0 ? c.pool_tokens : std::max(1, comm->sm_count));
     eng->algo = c.algorithm == NZ_ALGO_RING ? nezha::Algorithm::Ring : nezha::Algorithm::RingChunked;
     if (c.rails_toml) {
       eng->specs = nezha::parseRailsToml(c.rails_toml);

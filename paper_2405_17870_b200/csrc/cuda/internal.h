@@ -130,8 +130,23 @@ nz_buf* allocSymmetric(nz_comm* c, size_t bytes);
 void freeSymmetric(nz_buf* b);
 int elemSizeOf(int dtype);
 // rails.cu
+// Computation-phase gate from the engine's ComputePool arbitration
+// (include/nezha/compute_pool.hpp, P14): the rail's SM-driven
+// kernel is capped at `max_ctas`, waits for `waits` (earlier holders' phase
+// exits) and records `release` as soon as it retires; the CE rail's DMA
+// phases stay outside the gate.
+struct ComputeGate {
+  int max_ctas = 0;  // 0: no cap
+  std::vector<cudaEvent_t> waits;
+  cudaEvent_t release = nullptr;
+  bool entered = false;
+  bool exited = false;
+};
 void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes,
                    uint64_t chunk_begin, uint64_t chunk_end, int dtype, uint32_t op_seq, int64_t fail_chunk,
-                   cudaStream_t st);
+                   cudaStream_t st, ComputeGate* gate = nullptr);
+// CTAs of the rail's computation-phase kernel for a whole segment of
+// `seg_len` bytes (the ComputePool demand); 0 when it launches none.
+int railComputeCtas(nz_rail* r, uint64_t seg_len);
 void launchStamp(uint64_t* dst, cudaStream_t st);
 }  // namespace nz

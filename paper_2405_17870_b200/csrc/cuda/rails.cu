@@ -225,9 +225,55 @@ void ensureStaging(nz_rail* r, size_t slot) {
   r->staging_slot = want;
 }
 
+void gateEnter(ComputeGate* gate, cudaStream_t st) {
+  if (!gate || gate->entered) return;
+  for (cudaEvent_t e : gate->waits) NZ_CUDA(cudaStreamWaitEvent(st, e, 0));
+  gate->entered = true;
+}
+
+void gateExit(ComputeGate* gate, cudaStream_t st) {
+  if (!gate || gate->exited) return;
+  gateEnter(gate, st);  // a rail with nothing to compute still orders after its waits
+  if (gate->release) NZ_CUDA(cudaEventRecord(gate->release, st));
+  gate->exited = true;
+}
+
+int gated(int grid, const ComputeGate* gate) {
+  return gate && gate->max_ctas > 0 ? std::max(1, std::min(grid, gate->max_ctas)) : grid;
+}
+
+bool llPath(nz_rail* r, uint64_t lo, uint64_t hi) {
+  const int N = r->comm->world;
+  const bool mc_ll = r->kind == NZ_RAIL_NVLS;
+  return N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= llMaxBytes(N, mc_ll) && lo % 4 == 0 &&
+         (!mc_ll || r->ll->mc_ptr);
+}
+
+int llGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
+  const uint64_t words = (hi - lo + 3) / 4;
+  const uint64_t threads = (words + 1) / 2 > words ? (words + 1) / 2 : words;
+  return static_cast<int>(
+      std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads, r->comm->sm_count)));
+}
+
+int copyGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
+  const uint64_t vec = (hi - lo) / 16 + 1;
+  return static_cast<int>(
+      std::max<uint64_t>(1, std::min<uint64_t>((vec + kThreads * 8 - 1) / (kThreads * 8), 2ull * r->comm->sm_count)));
+}
+
+int smGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
+  const int N = r->comm->world;
+  if (smTmaEnabled()) {
+    const uint64_t tiles = (hi - lo) / N / kTmaTile + 1;
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, gridFor(r, hi - lo, N, 2))));
+  }
+  return gridFor(r, hi - lo, N, 2);
+}
+
 // One rail op over [lo, hi) with order geometry g. `post` is posted after.
 void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const Geometry& g, int dtype, FaultPost post,
-            cudaStream_t st) {
+            cudaStream_t st, ComputeGate* gate) {
   nz_comm* c = r->comm;
   const int N = c->world;
   const int me = c->rank;
@@ -237,8 +283,7 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
   r->epoch += 2;  // start + end barrier; identical on every rank
 
   const bool mc_ll = r->kind == NZ_RAIL_NVLS;
-  if (N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= llMaxBytes(N, mc_ll) && lo % 4 == 0 &&
-      (!mc_ll || r->ll->mc_ptr)) {
+  if (llPath(r, lo, hi)) {
     LLArgs a{};
     a.in = in->ptrs[me];
     a.out = out->ptrs[me];
@@ -263,21 +308,19 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.watchdog = r->wd_dev;
     a.timeout_ns = watchdogNs();
     a.post = post;
-    const uint64_t threads = (a.words + 1) / 2 > a.words ? (a.words + 1) / 2 : a.words;
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads,
-                                                                              c->sm_count)));
-    dispatchLL(N, dtype, mc_ll, a, grid, st);
+    gateEnter(gate, st);
+    dispatchLL(N, dtype, mc_ll, a, gated(llGrid(r, lo, hi), gate), st);
     NZ_CUDA(cudaGetLastError());
+    gateExit(gate, st);
     return;
   }
 
   if (N == 1) {  // identity allreduce: every rail is a local HBM copy
-    const uint64_t vec = (hi - lo) / 16 + 1;
-    const int grid = static_cast<int>(std::max<uint64_t>(
-        1, std::min<uint64_t>((vec + kThreads * 8 - 1) / (kThreads * 8), 2ull * c->sm_count)));
-    copy_kernel<<<grid, kThreads, 0, st>>>(in->ptrs[0], out->ptrs[0], lo, hi, post);
+    gateEnter(gate, st);
+    copy_kernel<<<gated(copyGrid(r, lo, hi), gate), kThreads, 0, st>>>(in->ptrs[0], out->ptrs[0], lo, hi, post);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     NZ_CUDA(cudaGetLastError());
+    gateExit(gate, st);
     return;
   }
 
@@ -295,15 +338,15 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.use_barrier = N > 1;
     a.rank = me;
     a.post = post;
-    if (N > 1 && smTmaEnabled()) {
-      const uint64_t tiles = (hi - lo) / N / kTmaTile + 1;
-      const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, gridFor(r, hi - lo, N, 2))));
+    gateEnter(gate, st);
+    const int grid = gated(smGrid(r, lo, hi), gate);
+    if (smTmaEnabled()) {
       dispatchTma(N, dtype, a, grid, st);
     } else {
-      const int grid = gridFor(r, hi - lo, N, 2);
       dispatchFold<1>(N, dtype, a, grid, st);
     }
     NZ_CUDA(cudaGetLastError());
+    gateExit(gate, st);
     return;
   }
 
@@ -327,9 +370,10 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.f.use_barrier = 1;
     a.f.rank = me;
     a.f.post = post;
-    const int grid = gridFor(r, hi - lo, N, 4);
-    dispatchNvls(N, dtype, a, grid, st);
+    gateEnter(gate, st);
+    dispatchNvls(N, dtype, a, gated(gridFor(r, hi - lo, N, 4), gate), st);
     NZ_CUDA(cudaGetLastError());
+    gateExit(gate, st);
     return;
   }
 
@@ -364,9 +408,10 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.g = g;
     a.use_barrier = 0;
     a.rank = me;
-    const int grid = gridFor(r, hi - lo, N, 2);
-    dispatchFold<0>(N, dtype, a, grid, st);
+    gateEnter(gate, st);  // computation phase: the local fold
+    dispatchFold<0>(N, dtype, a, gated(gridFor(r, hi - lo, N, 2), gate), st);
     NZ_CUDA(cudaGetLastError());
+    gateExit(gate, st);
     NZ_CUDA(cudaEventRecord(r->fork, st));
     for (int j = 1; j < N; ++j) {
       const int p = (me + j) % N;
@@ -379,6 +424,7 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
   }
   launchBarrier(r, epoch + 1, post, st);
   NZ_CUDA(cudaGetLastError());
+  gateExit(gate, st);  // empty shard: nothing was folded
 }
 
 }  // namespace
@@ -399,7 +445,7 @@ void launchStamp(uint64_t* dst, cudaStream_t st) {
 // Used by the engine (engine.cpp) without going through the C ABI.
 void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes,
                    uint64_t chunk_begin, uint64_t chunk_end, int dtype, uint32_t op_seq, int64_t fail_chunk,
-                   cudaStream_t st) {
+                   cudaStream_t st, ComputeGate* gate) {
   const int es = elemSize(dtype);
   if (chunk_bytes == 0 || chunk_bytes % es || seg_off % es || seg_len % es) {
     fail(NZ_ERR_INVALID, "segment geometry not element aligned");
@@ -422,11 +468,20 @@ void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64
   if (!st) st = r->stream;
   NZ_CUDA(cudaSetDevice(r->comm->device));
   if (hi > lo) {
-    railOp(r, in, out, lo, hi, Geometry{seg_off, seg_len, chunk_bytes}, dtype, post, st);
+    railOp(r, in, out, lo, hi, Geometry{seg_off, seg_len, chunk_bytes}, dtype, post, st, gate);
   } else if (post.rec) {
     launchBarrier(r, r->epoch + 1, post, st);
     r->epoch += 2;
   }
+  gateExit(gate, st);
+}
+
+int railComputeCtas(nz_rail* r, uint64_t seg_len) {
+  if (seg_len == 0) return 0;
+  if (llPath(r, 0, seg_len)) return llGrid(r, 0, seg_len);
+  if (r->comm->world == 1) return copyGrid(r, 0, seg_len);
+  if (r->kind == NZ_RAIL_SM) return smGrid(r, 0, seg_len);
+  return gridFor(r, seg_len, r->comm->world, r->kind == NZ_RAIL_NVLS ? 4 : 2);
 }
 
 }  // namespace nz

@@ -274,3 +274,68 @@ def emulate_fold(world: int, rank: int, dtype: int, srcs: list[int], dsts: list[
     fn = lib().nz_emulate_fold_tma if tma else lib().nz_emulate_fold
     check(fn(world, rank, dtype, s, d, len(dsts), seg_off, seg_len, chunk_bytes, lo, hi, grid, _stream(stream)),
           "nz_emulate_fold")
+
+
+class ComputePool:
+    """Per-phase compute tokens (nz_pool_*, include/nezha/compute_pool.hpp).
+
+    Mirrors acquire_phase_tokens / release_phase_tokens: phase 0 io, 1
+    communication, 2 computation. ``try_acquire`` returns None when
+    ``acquire`` would block."""
+
+    IO, COMMUNICATION, COMPUTATION = 0, 1, 2
+
+    def __init__(self, total_tokens: int):
+        self._h = None
+        h = c_void_p()
+        check(lib().nz_pool_create(total_tokens, ctypes.byref(h)), "nz_pool_create")
+        self._h = h
+
+    def close(self) -> None:
+        if self._h:
+            lib().nz_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def declare(self, rail_id: int, computation: int, io: int = 1, communication: int = 1) -> None:
+        check(lib().nz_pool_declare(self._h, rail_id, io, communication, computation), "nz_pool_declare")
+
+    def _acquire(self, rail_id: int, phase: int, blocking: int) -> int:
+        g = ctypes.c_int(0)
+        check(lib().nz_pool_acquire(self._h, rail_id, phase, blocking, ctypes.byref(g)), "nz_pool_acquire")
+        return g.value
+
+    def acquire(self, rail_id: int, phase: int) -> int:
+        return self._acquire(rail_id, phase, 1)
+
+    def try_acquire(self, rail_id: int, phase: int) -> int | None:
+        g = self._acquire(rail_id, phase, 0)
+        return None if g < 0 else g
+
+    def release(self, rail_id: int, phase: int) -> None:
+        check(lib().nz_pool_release(self._h, rail_id, phase), "nz_pool_release")
+
+    @property
+    def outstanding(self) -> int:
+        return check(lib().nz_pool_outstanding(self._h), "nz_pool_outstanding")
+
+    @property
+    def waiting(self) -> int:
+        return check(lib().nz_pool_waiting(self._h), "nz_pool_waiting")
+
+
+def plan_compute_grants(total_tokens: int, mode: int, demands: list[tuple[int, int]]) -> list[dict]:
+    """The engine's per-op SM arbitration (nz_pool_plan): per rail {rail, demand, grant, waits}."""
+    n = len(demands)
+    ids = (ctypes.c_int * max(n, 1))(*[r for r, _ in demands])
+    dem = (ctypes.c_int * max(n, 1))(*[d for _, d in demands])
+    grants = (ctypes.c_int * max(n, 1))()
+    masks = (ctypes.c_uint32 * max(n, 1))()
+    check(lib().nz_pool_plan(total_tokens, mode, n, ids, dem, grants, masks), "nz_pool_plan")
+    out = []
+    for i, (r, d) in enumerate(demands):
+        waits = [rr for rr, _ in demands[:i] if masks[i] >> rr & 1]
+        out.append({"rail": r, "demand": d, "grant": grants[i], "waits": waits})
+    return out

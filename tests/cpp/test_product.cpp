@@ -5,10 +5,15 @@
 
 #include "nezha/balancer.hpp"
 #include "nezha/collective.hpp"
+#include "nezha/compute_pool.hpp"
 #include "nezha/core/error.hpp"
 #include "nezha/engine.hpp"
 #include "nezha/faults.hpp"
 #include "nezha/util/toml.hpp"
+
+#include <atomic>
+#include <chrono>
+#include <thread>
 
 using namespace nezha;
 
@@ -189,4 +194,82 @@ TEST_CASE("AllocationTable persists and restores (SPEC.md:355)") {
   CHECK(fresh.allocate(S).segments == bal.allocate(S).segments);
   CHECK(fresh.saveState() == saved);
   CHECK_THROWS_AS(fresh.loadState("{\"version\":2}"), std::invalid_argument);
+}
+
+TEST_CASE("ComputePool: io/communication immediate, computation capped (SPEC.md:333-336)") {
+  ComputePool p(8);
+  p.declare(0, PhaseDemand{1, 1, 20});
+  p.declare(1, PhaseDemand{1, 1, 8});
+  CHECK(p.acquire(0, Phase::Computation) == 8);  // demand > total -> capped
+  CHECK(p.outstanding() == 8);
+  CHECK(p.tryAcquire(1, Phase::Io).value() == 1);  // io: immediate grant of 1
+  p.release(1, Phase::Io);
+  CHECK(!p.tryAcquire(1, Phase::Computation).has_value());
+  CHECK_THROWS_AS(p.acquire(0, Phase::Io), std::invalid_argument);  // single grant per rail
+  CHECK_THROWS_AS(p.release(1, Phase::Computation), std::invalid_argument);
+  CHECK_THROWS_AS(p.declare(0, PhaseDemand{1, 1, 1}), std::invalid_argument);
+  CHECK_THROWS_AS(p.tryAcquire(7, Phase::Io), std::invalid_argument);
+  p.release(0, Phase::Computation);
+  CHECK(p.tryAcquire(1, Phase::Computation).value() == 8);
+  CHECK_THROWS_AS(ComputePool(0), std::invalid_argument);
+}
+
+// Rails loop io -> communication -> computation; returns the peak number of
+// rails inside their computation phase at once.
+static int runRails(int total, const std::vector<int>& demand, int rounds) {
+  ComputePool p(total);
+  for (size_t r = 0; r < demand.size(); ++r) p.declare(static_cast<int>(r), PhaseDemand{1, 1, demand[r]});
+  std::atomic<int> inside{0}, peak{0}, over{0};
+  std::vector<std::thread> th;
+  for (size_t r = 0; r < demand.size(); ++r) {
+    th.emplace_back([&, r] {
+      const int id = static_cast<int>(r);
+      for (int k = 0; k < rounds; ++k) {
+        p.acquire(id, Phase::Io);
+        p.release(id, Phase::Io);
+        p.acquire(id, Phase::Communication);
+        p.release(id, Phase::Communication);
+        p.acquire(id, Phase::Computation);
+        const int now = ++inside;
+        int pk = peak.load();
+        while (now > pk && !peak.compare_exchange_weak(pk, now)) {}
+        if (p.outstanding() > total) ++over;
+        std::this_thread::sleep_for(std::chrono::microseconds(300));
+        --inside;
+        p.release(id, Phase::Computation);
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  CHECK(over.load() == 0);
+  CHECK(p.outstanding() == 0);
+  CHECK(p.peakOutstanding() <= total);
+  return peak.load();
+}
+
+TEST_CASE("ComputePool: contention examples (SPEC.md:334-336)") {
+  CHECK(runRails(8, {8, 8}, 40) == 1);        // serialized computation phases
+  CHECK(runRails(6, {3, 3, 3}, 40) <= 2);     // at most two compute concurrently
+  CHECK(runRails(148, {32, 64, 148}, 20) <= 2);  // B200 default budgets: CE fold never overlaps both
+}
+
+TEST_CASE("planComputeGrants: stream-order arbitration (DESIGN.md P14)") {
+  ComputePool p(148);
+  auto off = planComputeGrants(p, PoolMode::Off, {{0, 32}, {1, 148}, {2, 64}});
+  CHECK(off[1].grant == 148);
+  CHECK(off[1].waits.empty());
+  auto blk = planComputeGrants(p, PoolMode::Block, {{0, 32}, {1, 148}, {2, 64}});
+  CHECK(blk[0].grant == 32);
+  CHECK(blk[1].grant == 148);
+  CHECK(blk[1].waits == std::vector<int>{0});
+  CHECK(blk[2].waits == std::vector<int>{1});
+  CHECK(p.outstanding() == 0);
+  auto shr = planComputeGrants(p, PoolMode::Shrink, {{0, 32}, {1, 148}, {2, 64}});
+  CHECK(shr[1].grant == 116);
+  CHECK(shr[1].waits.empty());
+  CHECK(shr[2].grant == 32);  // free reaches 32 once rail 0 exits; shrink to it
+  CHECK(shr[2].waits == std::vector<int>{0});
+  auto fit = planComputeGrants(p, PoolMode::Block, {{0, 32}, {2, 64}});
+  CHECK(fit[1].waits.empty());
+  CHECK(p.outstanding() == 0);
 }

@@ -67,6 +67,34 @@ def test_engine_multirail_parity(world):
 
 
 @pytest.mark.multigpu
+@pytest.mark.parametrize("mode", [1, 2])
+def test_engine_compute_pool_parity(mode):
+    """SM arbitration of concurrent rails (ComputePool, P14): the
+    result is unchanged and every op's grants are the oracle's for its demands."""
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from oracle.compute_pool import plan_grants
+
+    tokens = 100
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4, "compute_pool": mode,
+            "pool_tokens": tokens,
+            "cases": [{"dtype": "f32", "nbytes": 64 << 20, "reps": 6},
+                      {"dtype": "bf16", "nbytes": 24 << 20, "reps": 2},
+                      {"dtype": "i32", "nbytes": 16 << 20, "reps": 2}]}
+    res = _run(2, spec, timeout=420)
+    arbitrated = 0
+    for rk in res:
+        assert rk["state"]["compute_pool"]["mode"] == mode
+        for r in rk["results"]:
+            for g in r["grants"]:
+                demands = [(x[0], x[1]) for x in g]
+                want = plan_grants(tokens, mode, demands)
+                assert [[w["rail"], w["demand"], w["grant"], w["waits"]] for w in want] == g, r
+                arbitrated += 1
+    assert arbitrated > 0
+
+
+@pytest.mark.multigpu
 def test_engine_oversized_split():
     """Payloads above 1 GiB run as 256 MiB pieces."""
     if gpu_count() < 2:

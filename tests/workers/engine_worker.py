@@ -55,7 +55,7 @@ def main():
     rank, world = comm.rank, comm.world
     kinds = spec["rails"]
     over = {"kinds": kinds}
-    for k in ("window", "eta", "demote_after", "calibrate_max_bytes", "calibrate_iters"):
+    for k in ("window", "eta", "demote_after", "calibrate_max_bytes", "calibrate_iters", "compute_pool", "pool_tokens"):
         if k in spec:
             over[k] = spec[k]
     if "rails_toml" in spec:
@@ -100,7 +100,8 @@ def main():
                     else:
                         bad += check_segment(kind, dt, got, inputs, off, length, chunk)
                     segs.append([rail_id, off, length, chunk])
-            rec = {"case": ci, "rep": rep, "dtype": c["dtype"], "nbytes": n, "mismatch": bad, "segs": segs}
+            rec = {"case": ci, "rep": rep, "dtype": c["dtype"], "nbytes": n, "mismatch": bad, "segs": segs,
+                   "grants": [p["grants"] for p in plans if "grants" in p]}
             if failing:
                 rec["failover"] = fo
             out.append(rec)
@@ -112,7 +113,8 @@ def main():
     bout.free()
     comm.close()
     print(json.dumps({"rank": rank, "results": out, "state": {"sync": state["sync_overhead_us"],
-                                                               "rails": state["rails"]}}))
+                                                               "rails": state["rails"],
+                                                               "compute_pool": state.get("compute_pool")}}))
 
 
 if __name__ == "__main__":
