@@ -124,6 +124,24 @@ int nz_rail_allreduce(nz_rail_t* rail, nz_buf_t* in, nz_buf_t* out, uint64_t seg
                       uint64_t chunk_bytes, uint64_t chunk_begin, uint64_t chunk_end, int dtype,
                       uint32_t op_seq, int64_t fail_chunk, void* stream);
 
+/* Trace-form failure for the rail's next nz_rail_allreduce on this rank: the
+ * same as passing fail_chunk = chunk to it (InMemoryFabric::failRailAtFrame,
+ * inmem.hpp:22-24). Every rank arms the same chunk. */
+int nz_rail_inject_failure(nz_rail_t* rail, uint64_t chunk);
+/* Chunks of the last nz_rail_allreduce that are complete on this rank. A
+ * rail folds all chunks of a call in one kernel, so the count moves from
+ * chunk_begin to its stop chunk (chunk_end, or the injected failure chunk)
+ * when that call's work retires on the device. Non-blocking. */
+int nz_rail_progress(nz_rail_t* rail, uint64_t* chunks_done);
+/* Kills the rail on this rank (InMemoryFabric::killRail, inmem.cpp:214-233):
+ * later nz_rail_allreduce calls fail with NZ_ERR_RAIL_DOWN. Work already on
+ * the device cannot be preempted: it completes, or its cross-rank waits are
+ * bounded by the watchdog when a peer never arrives. */
+int nz_rail_abort(nz_rail_t* rail);
+/* Elapsed microseconds between two recorded cudaEvent_t (e.g. around a rail
+ * call on its stream), for FFI callers without the CUDA runtime. */
+int nz_event_elapsed_us(void* start_event, void* end_event, double* us);
+
 typedef struct {
   uint32_t valid;      /* 1 once the device posted a fault */
   uint32_t op_seq;

@@ -144,6 +144,10 @@ _SIGS = {
                                   c_int, c_uint32, c_int64, c_void_p]),
     "nz_rail_poll_fault": (c_int, [c_void_p, POINTER(FaultRecord), c_int]),
     "nz_rail_watchdog": (c_int, [c_void_p]),
+    "nz_rail_inject_failure": (c_int, [c_void_p, c_uint64]),
+    "nz_rail_progress": (c_int, [c_void_p, POINTER(c_uint64)]),
+    "nz_rail_abort": (c_int, [c_void_p]),
+    "nz_event_elapsed_us": (c_int, [c_void_p, c_void_p, POINTER(c_double)]),
     "nz_engine_config_default": (None, [POINTER(EngineConfig)]),
     "nz_engine_create": (c_int, [c_void_p, POINTER(EngineConfig), POINTER(c_void_p)]),
     "nz_engine_destroy": (c_int, [c_void_p]),

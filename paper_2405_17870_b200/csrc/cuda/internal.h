@@ -120,6 +120,14 @@ struct nz_rail {
   nz_buf* ll = nullptr;     // SM: one-shot LL slots [parity][rank][slot_words] of {data, flag}
   uint64_t ll_slot_words = 0;
   uint32_t ll_flag = 0;
+  // C-ABI bookkeeping (nz_rail_inject_failure / _progress / _abort); the
+  // engine drives rails through nz::railAllreduce and does not touch these.
+  int64_t armed_fail = -1;      // failure armed for the next nz_rail_allreduce
+  bool aborted = false;         // nz_rail_abort: the rail takes no more work
+  cudaEvent_t done = nullptr;   // end of the last nz_rail_allreduce
+  uint64_t prog_begin = 0;      // its first chunk
+  uint64_t prog_stop = 0;       // chunks complete once `done` fired
+  bool prog_valid = false;
 };
 
 namespace nz {

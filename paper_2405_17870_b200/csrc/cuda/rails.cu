@@ -556,6 +556,7 @@ int nz_rail_destroy(nz_rail_t* r) {
     if (r->ll) nz::freeSymmetric(r->ll);
     if (r->fault_host) cudaFreeHost(r->fault_host);
     if (r->wd_host) cudaFreeHost(r->wd_host);
+    if (r->done) cudaEventDestroy(r->done);
     delete r;
   });
 }
@@ -577,8 +578,65 @@ int nz_rail_allreduce(nz_rail_t* rail, nz_buf_t* in, nz_buf_t* out, uint64_t seg
                       int64_t fail_chunk, void* stream) {
   return guarded([&] {
     if (!rail || !in || !out) fail(NZ_ERR_INVALID, "null argument");
+    if (rail->aborted) fail(NZ_ERR_RAIL_DOWN, "rail " + std::to_string(rail->rail_id) + " was aborted");
+    if (fail_chunk < 0 && rail->armed_fail >= 0) fail_chunk = rail->armed_fail;
+    rail->armed_fail = -1;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rail->stream;
     nz::railAllreduce(rail, in, out, seg_off, seg_len, chunk_bytes, chunk_begin, chunk_end, dtype, op_seq, fail_chunk,
-                      static_cast<cudaStream_t>(stream));
+                      st);
+    const uint64_t nch = chunk_bytes ? (seg_len + chunk_bytes - 1) / chunk_bytes : 0;
+    const uint64_t end = std::min(chunk_end, nch);
+    rail->prog_begin = std::min(chunk_begin, end);
+    rail->prog_stop = fail_chunk >= 0 && static_cast<uint64_t>(fail_chunk) >= rail->prog_begin &&
+                              static_cast<uint64_t>(fail_chunk) < end
+                          ? static_cast<uint64_t>(fail_chunk)
+                          : end;
+    if (!rail->done) NZ_CUDA(cudaEventCreateWithFlags(&rail->done, cudaEventDisableTiming));
+    NZ_CUDA(cudaEventRecord(rail->done, st));
+    rail->prog_valid = true;
+  });
+}
+
+int nz_rail_inject_failure(nz_rail_t* rail, uint64_t chunk) {
+  return guarded([&] {
+    if (!rail) fail(NZ_ERR_INVALID, "null rail");
+    if (chunk > static_cast<uint64_t>(INT64_MAX)) fail(NZ_ERR_INVALID, "chunk out of range");
+    rail->armed_fail = static_cast<int64_t>(chunk);
+  });
+}
+
+int nz_rail_progress(nz_rail_t* rail, uint64_t* chunks_done) {
+  return guarded([&] {
+    if (!rail || !chunks_done) fail(NZ_ERR_INVALID, "null argument");
+    if (!rail->prog_valid) {
+      *chunks_done = 0;
+      return;
+    }
+    NZ_CUDA(cudaSetDevice(rail->comm->device));
+    const cudaError_t q = cudaEventQuery(rail->done);
+    if (q == cudaErrorNotReady) {
+      *chunks_done = rail->prog_begin;
+      return;
+    }
+    NZ_CUDA(q);
+    *chunks_done = rail->prog_stop;
+  });
+}
+
+int nz_rail_abort(nz_rail_t* rail) {
+  return guarded([&] {
+    if (!rail) fail(NZ_ERR_INVALID, "null rail");
+    rail->aborted = true;
+    rail->armed_fail = -1;
+  });
+}
+
+int nz_event_elapsed_us(void* start, void* end, double* us) {
+  return guarded([&] {
+    if (!start || !end || !us) fail(NZ_ERR_INVALID, "null argument");
+    float ms = 0;
+    NZ_CUDA(cudaEventElapsedTime(&ms, static_cast<cudaEvent_t>(start), static_cast<cudaEvent_t>(end)));
+    *us = static_cast<double>(ms) * 1000.0;
   });
 }
 

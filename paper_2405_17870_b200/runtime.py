@@ -142,6 +142,20 @@ class Rail:
     def watchdog(self) -> int:
         return lib().nz_rail_watchdog(self.handle)
 
+    def inject_failure(self, chunk: int) -> None:
+        """Arms a failure at `chunk` for this rank's next allreduce (nz_rail_inject_failure)."""
+        check(lib().nz_rail_inject_failure(self.handle, chunk), "nz_rail_inject_failure")
+
+    def progress(self) -> int:
+        """Chunks of the last allreduce complete on this rank (nz_rail_progress)."""
+        v = ctypes.c_uint64(0)
+        check(lib().nz_rail_progress(self.handle, byref(v)), "nz_rail_progress")
+        return v.value
+
+    def abort(self) -> None:
+        """Kills the rail on this rank (nz_rail_abort); later calls raise ChannelDownError."""
+        check(lib().nz_rail_abort(self.handle), "nz_rail_abort")
+
     def close(self) -> None:
         if self.handle:
             check(lib().nz_rail_destroy(self.handle), "nz_rail_destroy")

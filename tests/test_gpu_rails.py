@@ -133,6 +133,9 @@ MULTI = [
     {"kind": "sm", "dtype": "bf16", "nbytes": 8 << 20, "chunk_begin": 1, "chunk_end": 3},
     {"kind": "ce", "dtype": "f32", "nbytes": 16 << 20, "chunk_begin": 3},
     {"kind": "nvls", "dtype": "i32", "nbytes": 16 << 20, "fail_chunk": 2},
+    {"kind": "sm", "dtype": "f32", "nbytes": 32 << 20, "fail_chunk": 3, "armed": True},  # nz_rail_inject_failure
+    {"kind": "ce", "dtype": "f32", "nbytes": 4 << 20, "fail_chunk": 1, "armed": True},
+    {"kind": "sm", "dtype": "f32", "nbytes": 4096, "abort": True},  # nz_rail_abort: later calls refused
 ]
 
 
@@ -147,7 +150,10 @@ def test_multi_gpu_rails(world):
             assert r["watchdog"] == 0, r
             assert r["outside_nonzero"] == 0, r
             assert r["mismatch"] == 0, r
+            assert r["progress"] == r["stop"], r  # nz_rail_progress after the call retired
             case = MULTI[r["case"]]
+            if case.get("abort"):
+                assert r["abort_refused"], r
             if case.get("fail_chunk", -1) >= 0:
                 assert r["fault"] is not None and r["fault"]["chunk"] == case["fail_chunk"], r
             else:

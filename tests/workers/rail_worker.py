@@ -73,13 +73,19 @@ def main():
         cb, ce = c.get("chunk_begin", 0), min(c.get("chunk_end", nch), nch)
         fail = c.get("fail_chunk", -1)
         comm.barrier()
-        rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce,
-                       fail_chunk=fail)
+        if c.get("armed") and fail >= 0:  # nz_rail_inject_failure instead of the fail_chunk argument
+            rail.inject_failure(fail)
+            rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce)
+        else:
+            rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce,
+                           fail_chunk=fail)
         rail.synchronize()
         wd = rail.watchdog()
+        progress = rail.progress()
         stop = fail if 0 <= fail < ce and fail >= cb else ce
         lo, hi = seg_off + min(seg_len, cb * chunk), seg_off + min(seg_len, stop * chunk)
-        res = {"case": ci, "kind": kind, "dtype": c["dtype"], "nbytes": nbytes, "lo": lo, "hi": hi, "watchdog": wd}
+        res = {"case": ci, "kind": kind, "dtype": c["dtype"], "nbytes": nbytes, "lo": lo, "hi": hi, "watchdog": wd,
+               "progress": progress, "stop": min(stop, nch)}
         if check:
             got = np.zeros(nbytes // es, dtype=oracle.NP_DTYPE[dt])
             bout.read(got, nbytes)
@@ -110,6 +116,17 @@ def main():
             res["us"] = t * 1e6
             res["busbw_GBs"] = 2 * (world - 1) / world * seg_len / t / 1e9 if world > 1 else 0.0
             res["algbw_GBs"] = seg_len / t / 1e9
+        if c.get("abort"):
+            from paper_2405_17870_b200 import NezhaError
+            rail.abort()
+            try:
+                rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci)
+                res["abort_refused"] = False
+            except NezhaError:
+                res["abort_refused"] = True
+            rails[key] = Rail(comm, RAIL_KINDS[kind], len(rails) + 10, c.get("sm_budget", 0))
+            r_old = rail
+            r_old.close()
         results.append(res)
     for r in rails.values():
         r.close()
