@@ -54,7 +54,15 @@ struct nz_engine {
   cudaStream_t io = nullptr;
   nz_buf* ub_in = nullptr;
   nz_buf* ub_out = nullptr;
-  std::vector<std::string> last_plans;  // JSON of each piece of the last call
+  // Plans of each piece of the last call; rendered to JSON only on request
+  // (nz_engine_last_plan_json) so the per-op host path builds no strings.
+  struct PlanRecord {
+    uint32_t seq = 0;
+    uint64_t base = 0, len = 0;
+    nezha::Plan plan;
+    std::string grants;  // [rail, demand, grant, [waits]]... when the ComputePool is on
+  };
+  std::vector<PlanRecord> last_plans;
   int64_t clock_offset_ns = 0;          // %globaltimer - CLOCK_REALTIME
   int64_t host_seen_ns = 0;             // host monitor saw the last fault record
   struct RailStat {
@@ -205,7 +213,7 @@ struct nz_engine {
       const uint64_t C = nezha::defaultChunkBytes(rs.segment.length, world, algo);
       nz::railAllreduce(r, in, out, base + rs.segment.offset, rs.segment.length, C, 0, UINT64_MAX, dtype, seq, -1,
                         user);
-      recordPlan(seq, base, len, plan);
+      recordPlan(seq, base, len, std::move(plan));
       return;
     }
     Pending p;
@@ -256,23 +264,27 @@ struct nz_engine {
     }
     for (auto& [id, e] : p.ends) NZ_CUDA(cudaStreamWaitEvent(user, e, 0));
     recycleGates();
-    recordPlan(seq, base, len, plan, grant_log);
     pending.push_back(std::move(p));
+    recordPlan(seq, base, len, std::move(plan), std::move(grant_log));
   }
 
-  void recordPlan(uint32_t seq, uint64_t base, uint64_t len, const nezha::Plan& plan, const std::string& grants = "") {
+  void recordPlan(uint32_t seq, uint64_t base, uint64_t len, nezha::Plan&& plan, std::string&& grants = {}) {
+    last_plans.push_back(PlanRecord{seq, base, len, std::move(plan), std::move(grants)});
+  }
+
+  std::string planRecordJson(const PlanRecord& r) const {
     std::ostringstream o;
-    o << "{\"op\":" << seq << ",\"offset\":" << base << ",\"length\":" << len << ",\"hot\":" << (plan.hot ? "true" : "false")
-      << ",\"segs\":[";
-    for (size_t i = 0; i < plan.segments.size(); ++i) {
-      const auto& rs = plan.segments[i];
-      o << (i ? "," : "") << "[" << rs.rail_id << "," << base + rs.segment.offset << "," << rs.segment.length << ","
-        << nezha::defaultChunkBytes(rs.segment.length, comm->world, algo) << "]";
+    o << "{\"op\":" << r.seq << ",\"offset\":" << r.base << ",\"length\":" << r.len
+      << ",\"hot\":" << (r.plan.hot ? "true" : "false") << ",\"segs\":[";
+    for (size_t i = 0; i < r.plan.segments.size(); ++i) {
+      const auto& rs = r.plan.segments[i];
+      o << (i ? "," : "") << "[" << rs.rail_id << "," << r.base + rs.segment.offset << "," << rs.segment.length
+        << "," << nezha::defaultChunkBytes(rs.segment.length, comm->world, algo) << "]";
     }
     o << "]";
-    if (!grants.empty()) o << ",\"grants\":[" << grants << "]";  // [rail, demand, grant, [waits]]
+    if (!r.grants.empty()) o << ",\"grants\":[" << r.grants << "]";
     o << "}";
-    last_plans.push_back(o.str());
+    return o.str();
   }
 
   // Exception handler: wait for the device's fault record,
@@ -840,7 +852,7 @@ int nz_engine_stats_reset(nz_engine_t* eng) {
 int nz_engine_last_plan_json(nz_engine_t* eng, char* out, size_t cap) {
   if (!eng) return NZ_ERR_INVALID;
   std::string s = "[";
-  for (size_t i = 0; i < eng->last_plans.size(); ++i) s += (i ? "," : "") + eng->last_plans[i];
+  for (size_t i = 0; i < eng->last_plans.size(); ++i) s += (i ? "," : "") + eng->planRecordJson(eng->last_plans[i]);
   s += "]";
   return copyOut(s, out, cap);
 }
