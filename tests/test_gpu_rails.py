@@ -170,3 +170,39 @@ def test_watchdog_instead_of_hang(kind):
                 extra_env={"NEZHA_WATCHDOG_MS": "300"})
     r0 = [r for r in res if r["rank"] == 0][0]
     assert r0["watchdog"] == 1 and r0["seconds"] < 30
+
+
+@pytest.mark.parametrize("mode", ["sm", "ce"])
+def test_config1_hash_emulated(mode):
+    """Config 1 (8 ranks, 2 rails of 32 MiB, Ring) through the production fold
+    kernels for 8 virtual ranks on one GPU: the output hash equals the golden
+    generated from the reference's InMemoryFabric ring."""
+    import hashlib
+
+    torch = pytest.importorskip("torch")
+    if gpu_count() < 1:
+        pytest.skip("no GPU")
+    from paper_2405_17870_b200 import emulate_fold
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "config1_hash.json")))
+    world, n = g["world"], g["bytes"]
+    torch.cuda.set_device(0)
+    dins = [torch.from_numpy(oracle.synthetic_input(oracle.F32, r, n).view(np.uint8).copy()).cuda()
+            for r in range(world)]
+    douts = [torch.zeros(n, dtype=torch.uint8, device="cuda") for _ in range(world)]
+    for _, off, length in g["segments"]:
+        for r in range(world):
+            dst = [d.data_ptr() for d in douts] if mode == "sm" else [douts[r].data_ptr()]
+            emulate_fold(world, r, oracle.F32, [d.data_ptr() for d in dins], dst, off, length, length, off,
+                         off + length)
+    torch.cuda.synchronize()
+    if mode == "sm":
+        for r in range(world):
+            assert hashlib.sha256(douts[r].cpu().numpy().tobytes()).hexdigest() == g["sha256"], r
+    else:  # each virtual rank wrote its own shard of each segment: stitch them
+        full = np.zeros(n, dtype=np.uint8)
+        for _, off, length in g["segments"]:
+            for r in range(world):
+                s, e = shard_of(off, off + length, r, world)
+                full[s:e] = douts[r][s:e].cpu().numpy()
+        assert hashlib.sha256(full.tobytes()).hexdigest() == g["sha256"]

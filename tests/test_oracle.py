@@ -145,3 +145,14 @@ def test_acceptance_failover_exactly_once_random_trials():
                                       [(o, l, oracle.default_chunk_bytes(l, world)) for _, o, l in segs])
         for r in range(world):
             np.testing.assert_array_equal(bits(outs[r]), bits(want), err_msg=f"trial {trial} rank {r}")
+
+
+def test_config1_output_hash_golden():
+    """SURVEY.md §8c golden: the 64 MiB config-1 output hash, generated from
+    the reference's InMemoryFabric ring (tests/golden/make_config1_hash.py)."""
+    import hashlib
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "config1_hash.json")))
+    xs = [oracle.synthetic_input(oracle.F32, r, g["bytes"]) for r in range(g["world"])]
+    out = oracle.reduce_segments(xs, oracle.F32, [(o, l, l) for _, o, l in g["segments"]])
+    assert hashlib.sha256(out.tobytes()).hexdigest() == g["sha256"]
