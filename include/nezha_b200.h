@@ -280,6 +280,10 @@ int nz_pool_plan(int total_tokens, int mode, int n, const int* rail_ids, const i
 uint64_t nz_core_ring_volume(int node_count, uint64_t payload);
 int nz_core_bucket_of(uint64_t size);
 uint64_t nz_core_default_chunk_bytes(uint64_t seg_len, int world, int algorithm);
+/* calibrate(samples) -> CalibratedProfile (P15):
+ * *interpolated = 1 when the samples had to become an interpolation table. */
+int nz_core_calibrate(const uint64_t* sizes, const double* lat_us, int n, double* t_setup_us, double* bandwidth_bps,
+                      int* interpolated, double* max_rel_residual);
 
 #ifdef __cplusplus
 }

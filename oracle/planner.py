@@ -178,6 +178,37 @@ def threshold(f, lo, hi):
     return a
 
 
+def calibrate(samples):
+    """SPEC.md:434-446 calibrate(samples) with DESIGN.md P15's pins: relative
+    least squares of t + c*S; kept if t >= 0, c > 0 and every residual <= 10 %,
+    else the samples become an interpolation table. Returns
+    (t_setup_us, bandwidth_bps, interpolated, max_rel_residual)."""
+    pts = sorted(samples)
+    if len(pts) < 2 or any(y <= 0 for _, y in pts) or len({x for x, _ in pts}) != len(pts):
+        raise ValueError("bad samples")
+    # Minimise sum(((t + c x - y) / y)^2): the 2x2 weighted normal equations,
+    # w = 1/y^2, accumulated in sample order with the product's operation
+    # order so the doubles agree bit for bit (DESIGN.md §6).
+    a11 = a12 = a22 = b1 = b2 = 0.0
+    for x, y in pts:
+        x = float(x)
+        w = 1.0 / (y * y)
+        a11 += w
+        a12 += w * x
+        a22 += w * x * x
+        b1 += w * y
+        b2 += w * x * y
+    det = a11 * a22 - a12 * a12
+    t, c = (-1.0, -1.0) if det <= 0 else ((a22 * b1 - a12 * b2) / det, (a11 * b2 - a12 * b1) / det)
+    worst = max(abs(t + c * x - y) / y for x, y in pts)
+    if t >= 0 and c > 0 and worst <= 0.10:
+        return t, 1e6 / c, False, worst
+    if any(pts[i][1] <= pts[i - 1][1] for i in range(1, len(pts))):
+        raise ValueError("interpolation table not increasing")
+    dx, dy = pts[-1][0] - pts[0][0], pts[-1][1] - pts[0][1]
+    return pts[0][1], dx / (dy * 1e-6), True, 0.0
+
+
 def chunk_bytes(seg_len, world, chunked=True):
     """P10."""
     if not chunked:

@@ -182,6 +182,8 @@ _SIGS = {
     "nz_core_ring_volume": (c_uint64, [c_int, c_uint64]),
     "nz_core_bucket_of": (c_int, [c_uint64]),
     "nz_core_default_chunk_bytes": (c_uint64, [c_uint64, c_int, c_int]),
+    "nz_core_calibrate": (c_int, [POINTER(c_uint64), POINTER(c_double), c_int, POINTER(c_double), POINTER(c_double),
+                                  POINTER(c_int), POINTER(c_double)]),
 }
 
 _lib = None

@@ -13,6 +13,7 @@
 #include "../host/planner_trace.hpp"
 #include "internal.h"
 #include "nezha/balancer.hpp"
+#include "nezha/calibration.hpp"
 #include "nezha/collective.hpp"
 #include "nezha/compute_pool.hpp"
 #include "nezha/core/error.hpp"
@@ -451,8 +452,11 @@ struct nz_engine {
       p.rail_id = specs[i].rail_id;
       p.efficiency_points.clear();
       for (size_t j = 0; j < sizes.size(); ++j) p.efficiency_points.emplace_back(sizes[j], lat[j]);
-      p.t_setup_us = lat.front();
-      p.bandwidth_bps = static_cast<double>(sizes.back() - sizes.front()) / ((lat.back() - lat.front()) * 1e-6);
+      // (t_setup, B) from calibrate(); the measured
+      // points stay as the interpolation table messageLatency() uses.
+      const nezha::CalibratedProfile cal = nezha::calibrate(p.rail_id, p.protocol, p.efficiency_points);
+      p.t_setup_us = cal.profile.t_setup_us;
+      p.bandwidth_bps = cal.profile.bandwidth_bps;
       profiles.push_back(p);
       specs[i].profile = p;
       specs[i].has_profile = true;

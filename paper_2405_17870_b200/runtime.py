@@ -353,3 +353,15 @@ def plan_compute_grants(total_tokens: int, mode: int, demands: list[tuple[int, i
         waits = [rr for rr, _ in demands[:i] if masks[i] >> rr & 1]
         out.append({"rail": r, "demand": d, "grant": grants[i], "waits": waits})
     return out
+
+
+def calibrate(samples: list[tuple[int, float]]) -> dict:
+    """calibrate(samples) -> CalibratedProfile (nz_core_calibrate, SPEC.md:434-446)."""
+    n = len(samples)
+    xs = (ctypes.c_uint64 * max(n, 1))(*[int(x) for x, _ in samples])
+    ys = (ctypes.c_double * max(n, 1))(*[float(y) for _, y in samples])
+    t, bw, mr = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    it = ctypes.c_int()
+    check(lib().nz_core_calibrate(xs, ys, n, byref(t), byref(bw), byref(it), byref(mr)), "nz_core_calibrate")
+    return {"t_setup_us": t.value, "bandwidth_bps": bw.value, "interpolated": bool(it.value),
+            "max_rel_residual": mr.value}

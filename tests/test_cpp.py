@@ -11,7 +11,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HOST = os.path.join(ROOT, "paper_2405_17870_b200", "csrc", "host")
-SRCS = [os.path.join(HOST, f) for f in ("core.cpp", "collective.cpp", "balancer.cpp", "faults.cpp", "toml.cpp", "rails_config.cpp", "balancer_state.cpp", "json.cpp", "compute_pool.cpp")]
+SRCS = [os.path.join(HOST, f) for f in ("core.cpp", "collective.cpp", "balancer.cpp", "faults.cpp", "toml.cpp", "rails_config.cpp", "balancer_state.cpp", "json.cpp", "compute_pool.cpp", "calibration.cpp")]
 REF_TESTS = "/root/reference/proj/tests"
 FLAGS = ["-std=c++20", "-O1", "-pthread", "-ffp-contract=off", f"-I{ROOT}/include", f"-I{ROOT}/oracle/shim"]
 
