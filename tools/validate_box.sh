@@ -1,0 +1,30 @@
+#!/bin/bash
+# One gpurun call that validates the tree on a box (development aid).
+#   gpurun --gpus 2 --timeout 2400 -- 'bash tools/validate_box.sh'
+# Every step runs under its own timeout and logs to gpurun_out/val_*.log;
+# a failing step does not stop the later ones. Summary: gpurun_out/val_summary.txt
+set -u
+mkdir -p gpurun_out
+S=gpurun_out/val_summary.txt
+: > $S
+step() {  # step NAME SECONDS CMD...
+  local name=$1 secs=$2
+  shift 2
+  local t0=$(date +%s)
+  timeout --kill-after=20 "$secs" bash -c "$*" > "gpurun_out/val_${name}.log" 2>&1
+  local rc=$?
+  echo "$name rc=$rc $(( $(date +%s) - t0 ))s" | tee -a $S
+}
+nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/val_gpus.csv 2>&1
+step build 300 "python -c 'import __graft_entry__ as g; g.build()'"
+step smoke 300 "python -c 'import __graft_entry__ as g; g.smoke()'"
+step pytest_gpu 1500 "python -m pytest tests -m gpu -x -q -p no:cacheprovider"
+step ddp 300 "python tools/run_spawn.py 2 tools/debug_ddp.py"
+step bench1 600 "python bench.py --steps 5 --warmup 3"
+if [ "$(nvidia-smi -L | wc -l)" -ge 2 ]; then
+  step bench2 900 "python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3"
+  for m in 0 1 2; do
+    step pool$m 300 "python tools/run_spawn.py 2 tools/engine_hot_probe.py nvls,ce,sm 0.33 $m"
+  done
+fi
+cat $S
