@@ -32,7 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "8-GPU allreduce busbw GB/s vs size (4KB–1GB); 8KB p50 latency; failover ms"
-NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (nominal); BASELINE.md roofline
+NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
 GiB = 1 << 30
 
 
@@ -50,6 +50,26 @@ def measured_peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def ncu_traffic(kernel: str, per_launch_bytes: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` summary (profiles/ncu_traffic.json), when it
+    was captured at this launch size; else None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[kernel]
+    except Exception:
+        return None
+    return t["dram_bytes"] if t.get("per_launch_bytes") == per_launch_bytes else None
+
+
+def wire_bytes(kind: str, world: int, seg: int) -> int:
+    """Bytes one GPU must send over NVLink per op of `seg` bytes on a rail (per
+    direction): ring-equivalent rails 2(N-1)/N*S (Eq. 1); NVLS (N+1)/N*S — the
+    switch reads every rank's copy once and multicasts the reduced shards."""
+    if kind == "nvls":
+        return (world + 1) * seg // world
+    return ring_volume(world, seg)
 
 
 # --------------------------------------------------------------------- clocks
@@ -282,18 +302,21 @@ def main():
         t_rail = max_over_ranks(st["total_us"] / st["ops"] * 1e-6)
         seg = st["bytes"] / st["ops"]
         if world > 1:
-            ach = ring_volume(world, int(seg)) / t_rail / 1e9
+            wb = wire_bytes(kinds[dom], world, int(seg))
+            ach = wb / t_rail / 1e9
             roofline = {"bound": "nvlink", "kernel": f"{kinds[dom]} rail", "achieved": round(ach, 1),
                         "peak": NVLINK_GBS, "unit": "GB/s", "frac": round(ach / NVLINK_GBS, 4), "traffic": None,
-                        "per_launch_bytes": ring_volume(world, int(seg)),
-                        "note": "achieved = ringVolume(N, segment) / rail time per op (CUDA events on the rail "
-                                "stream); peak = NVLink 5 900 GB/s per direction (nominal; measured peer copy "
-                                "770, B200_PROFILING.md)"}
+                        "per_launch_bytes": wb,
+                        "note": "achieved = NVLink bytes one GPU must send per op (ring rails 2(N-1)/N*S, NVLS "
+                                "(N+1)/N*S) / rail time per op (CUDA events on the rail stream); peak = measured "
+                                "peer copy 770 GB/s per direction (B200_PROFILING.md; 900 nominal). traffic: ncu "
+                                "cannot replay kernels with cross-GPU barriers (profiles/README.md)"}
         else:
             hbm = peaks.get("hbm_gbs", 6650.0)
             ach = 2 * seg / t_rail / 1e9
             roofline = {"bound": "hbm", "kernel": f"{kinds[dom]} rail (N=1 copy)", "achieved": round(ach, 1),
-                        "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                        "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                        "traffic": ncu_traffic("copy_kernel", int(2 * seg)),
                         "per_launch_bytes": int(2 * seg),
                         "note": "N=1: the allreduce is a copy in->out, 2S HBM bytes; peak = MEASURED_PEAKS.json "
                                 "hbm_gbs" + ("" if "hbm_gbs" in peaks else " (fallback)")}

@@ -21,6 +21,7 @@ step smoke 300 "python -c 'import __graft_entry__ as g; g.smoke()'"
 step pytest_gpu 1500 "python -m pytest tests -m gpu -x -q -p no:cacheprovider"
 step ddp 300 "python tools/run_spawn.py 2 tools/debug_ddp.py"
 step bench1 600 "python bench.py --steps 5 --warmup 3"
+step ncu_copy 900 "ncu --set full --clock-control none --import-source on -k regex:copy_kernel -s 1 -c 1 -f -o gpurun_out/ncu_copy_n1 python tools/ncu_copy_n1.py"
 if [ "$(nvidia-smi -L | wc -l)" -ge 2 ]; then
   step bench2 900 "python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3"
   for m in 0 1 2; do
