@@ -14,6 +14,7 @@ step() {  # step NAME SECONDS CMD...
   timeout --kill-after=20 "$secs" bash -c "$*" > "gpurun_out/val_${name}.log" 2>&1
   local rc=$?
   echo "$name rc=$rc $(( $(date +%s) - t0 ))s" | tee -a $S
+  return $rc
 }
 nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/val_gpus.csv 2>&1
 step build 300 "python -c 'import __graft_entry__ as g; g.build()'"
@@ -21,7 +22,8 @@ step smoke 300 "python -c 'import __graft_entry__ as g; g.smoke()'"
 step pytest_gpu 1500 "python -m pytest tests -m gpu -x -q -p no:cacheprovider"
 step ddp 300 "python tools/run_spawn.py 2 tools/debug_ddp.py"
 step bench1 600 "python bench.py --steps 5 --warmup 3"
-step ncu_copy 900 "ncu --set full --clock-control none --import-source on -k regex:copy_kernel -s 1 -c 1 -f -o gpurun_out/ncu_copy_n1 python tools/ncu_copy_n1.py"
+step copy_plain 300 "python tools/ncu_copy_n1.py" && \
+  step ncu_copy 900 "ncu --set full --clock-control none --import-source on -k regex:copy_kernel -s 1 -c 1 -f -o gpurun_out/ncu_copy_n1 python tools/ncu_copy_n1.py"
 if [ "$(nvidia-smi -L | wc -l)" -ge 2 ]; then
   step bench2 900 "python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3"
   for m in 0 1 2; do
