@@ -39,6 +39,7 @@ struct BarrierArgs {
   uint32_t epoch;
   int* watchdog;  // host-mapped; set when a wait times out
   uint64_t timeout_ns;  // give up after this long (NEZHA_WATCHDOG_MS, default 20 s)
+  int relaxed_poll;     // 1: poll ld.relaxed.sys, one fence.acq_rel.sys after (PTX acquire pattern)
 };
 
 struct FaultPost {
@@ -84,6 +85,12 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint4 ld_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -114,7 +121,8 @@ __device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch
     const uint32_t* slot = b.local + blockIdx.x * kDevMaxRanks + t;
     uint64_t t0 = 0;
     int spins = 0;
-    while (static_cast<int32_t>(ld_acquire_sys(slot) - epoch) < 0) {
+    const bool relaxed = b.relaxed_poll != 0;
+    while (static_cast<int32_t>((relaxed ? ld_relaxed_sys(slot) : ld_acquire_sys(slot)) - epoch) < 0) {
       if (++spins == 64) {
         spins = 0;
         const uint64_t now = globaltimer();
@@ -127,6 +135,7 @@ __device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch
         }
       }
     }
+    if (relaxed) fence_acq_rel_sys();  // relaxed observation + fence = acquire pattern
   }
   __syncthreads();
   return s_ok != 0;

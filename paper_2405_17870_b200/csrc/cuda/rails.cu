@@ -52,6 +52,16 @@ uint64_t watchdogNs() {
   return ns;
 }
 
+// NEZHA_BARRIER_POLL=relaxed: barrier waits poll with relaxed loads and fence
+// once (A/B knob; the default acquire-load poll is the validated one).
+bool barrierRelaxedPoll() {
+  static const bool on = [] {
+    const char* e = getenv("NEZHA_BARRIER_POLL");
+    return e && strcmp(e, "relaxed") == 0;
+  }();
+  return on;
+}
+
 BarrierArgs barrierArgs(nz_rail* r, uint32_t epoch) {
   BarrierArgs b{};
   b.local = r->pad_local;
@@ -59,6 +69,7 @@ BarrierArgs barrierArgs(nz_rail* r, uint32_t epoch) {
   b.epoch = epoch;
   b.watchdog = r->wd_dev;
   b.timeout_ns = watchdogNs();
+  b.relaxed_poll = barrierRelaxedPoll() ? 1 : 0;
   return b;
 }
 
