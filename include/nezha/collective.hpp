@@ -66,4 +66,11 @@ inline int ringBlockOf(std::uint64_t elem, std::uint64_t chunk_elems, int world)
 // contiguous pieces of at most 256 MiB; everything else is one piece.
 std::vector<Segment> splitOversized(Bytes payload);
 
+// Pieces of the host-memory allreduce pipeline (nz_engine_allreduce_host,
+// DESIGN.md §4c): below 8 MiB one piece; else pieces of
+// clamp(roundup(S / 16, 64 KiB), 4 MiB, 64 MiB), the last one shorter.
+// A function of S alone, so every rank cuts the same pieces; `elem_size`
+// only validates that S is whole elements.
+std::vector<Segment> hostPipelinePieces(Bytes payload, int elem_size);
+
 }  // namespace nezha

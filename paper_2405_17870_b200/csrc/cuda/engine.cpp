@@ -53,6 +53,8 @@ struct nz_engine {
   uint64_t* stamps_dev = nullptr;
   cudaStream_t ctrl = nullptr;
   cudaStream_t io = nullptr;
+  cudaStream_t h2d = nullptr;  // host path: uploads of the next piece
+  cudaStream_t d2h = nullptr;  // host path: downloads of the previous piece
   nz_buf* ub_in = nullptr;
   nz_buf* ub_out = nullptr;
   // Plans of each piece of the last call; rendered to JSON only on request
@@ -703,6 +705,8 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     eng->health = std::make_unique<nezha::HealthMonitor>(ids);
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->ctrl, cudaStreamNonBlocking));
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->io, cudaStreamNonBlocking));
+    NZ_CUDA(cudaStreamCreateWithFlags(&eng->h2d, cudaStreamNonBlocking));
+    NZ_CUDA(cudaStreamCreateWithFlags(&eng->d2h, cudaStreamNonBlocking));
     NZ_CUDA(cudaHostAlloc(&eng->stamps_host, 4 * sizeof(uint64_t), cudaHostAllocMapped));
     std::memset(eng->stamps_host, 0, 4 * sizeof(uint64_t));
     NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eng->stamps_dev), eng->stamps_host, 0));
@@ -728,6 +732,8 @@ int nz_engine_destroy(nz_engine_t* eng) {
     if (eng->ub_out) nz::freeSymmetric(eng->ub_out);
     if (eng->ctrl) cudaStreamDestroy(eng->ctrl);
     if (eng->io) cudaStreamDestroy(eng->io);
+    if (eng->h2d) cudaStreamDestroy(eng->h2d);
+    if (eng->d2h) cudaStreamDestroy(eng->d2h);
     if (eng->stamps_host) cudaFreeHost(eng->stamps_host);
     delete eng;
   });
@@ -760,12 +766,33 @@ int nz_engine_allreduce_host(nz_engine_t* eng, const void* host_in, void* host_o
     eng->ensureUnbound(bytes);
     nz_buf* in = eng->ub_in;
     nz_buf* out = eng->ub_out;
-    NZ_CUDA(cudaMemcpyAsync(in->ptrs[eng->comm->rank], host_in, bytes, cudaMemcpyHostToDevice, eng->io));
+    const int me = eng->comm->rank;
+    const char* src = static_cast<const char*>(host_in);
+    char* dst = static_cast<char*>(host_out);
+    // Three-stage pipeline over pieces: upload piece i+1 on
+    // h2d while the rails reduce piece i on io and d2h downloads piece i-1, so
+    // the PCIe directions overlap each other and the NVLink work. Pieces are
+    // independent allreduces, each with its own recorded plan, exactly like
+    // split_oversized pieces; the piece size is a function of `bytes` alone,
+    // so every rank cuts the same pieces.
     eng->last_plans.clear();
-    for (const auto& piece : nezha::splitOversized(bytes)) {
+    const auto pieces = nezha::hostPipelinePieces(bytes, nz::elemSizeOf(dtype));
+    for (const auto& piece : pieces) {
+      NZ_CUDA(cudaMemcpyAsync(in->ptrs[me] + piece.offset, src + piece.offset, piece.length, cudaMemcpyHostToDevice,
+                              eng->h2d));
+      cudaEvent_t up = eng->event();
+      NZ_CUDA(cudaEventRecord(up, eng->h2d));
+      NZ_CUDA(cudaStreamWaitEvent(eng->io, up, 0));
       eng->op(in, out, piece.offset, piece.length, dtype, eng->io);
+      cudaEvent_t red = eng->event();
+      NZ_CUDA(cudaEventRecord(red, eng->io));
+      NZ_CUDA(cudaStreamWaitEvent(eng->d2h, red, 0));
+      NZ_CUDA(cudaMemcpyAsync(dst + piece.offset, out->ptrs[me] + piece.offset, piece.length, cudaMemcpyDeviceToHost,
+                              eng->d2h));
+      eng->pool.push_back(up);  // waits captured at enqueue time: safe to recycle
+      eng->pool.push_back(red);
     }
-    NZ_CUDA(cudaMemcpyAsync(host_out, out->ptrs[eng->comm->rank], bytes, cudaMemcpyDeviceToHost, eng->io));
+    NZ_CUDA(cudaStreamSynchronize(eng->d2h));
     NZ_CUDA(cudaStreamSynchronize(eng->io));
     eng->finishFailoverReport();
   });

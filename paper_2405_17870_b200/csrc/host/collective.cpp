@@ -37,4 +37,17 @@ std::vector<Segment> splitOversized(Bytes payload) {
   return out;
 }
 
+std::vector<Segment> hostPipelinePieces(Bytes payload, int elem_size) {
+  if (payload == 0) throw std::invalid_argument("hostPipelinePieces: payload must be positive");
+  if (elem_size <= 0 || payload % static_cast<Bytes>(elem_size) != 0) {
+    throw std::invalid_argument("hostPipelinePieces: payload is not whole elements");
+  }
+  constexpr Bytes kMin = Bytes{4} << 20, kMax = Bytes{64} << 20, kAlign = Bytes{64} << 10;
+  if (payload < 2 * kMin) return {Segment{0, payload}};
+  const Bytes piece = std::clamp((payload / 16 + kAlign - 1) / kAlign * kAlign, kMin, kMax);
+  std::vector<Segment> out;
+  for (Bytes off = 0; off < payload; off += piece) out.push_back(Segment{off, std::min(piece, payload - off)});
+  return out;
+}
+
 }  // namespace nezha

@@ -27,6 +27,20 @@ TEST_CASE("split_oversized (SPEC.md:212-214)") {
   CHECK_THROWS_AS(splitOversized(0), std::invalid_argument);
 }
 
+TEST_CASE("host pipeline pieces (DESIGN.md 4c)") {
+  CHECK(hostPipelinePieces(4096, 4).size() == 1);
+  CHECK(hostPipelinePieces((8ull << 20) - 4, 4).size() == 1);
+  auto p = hostPipelinePieces(1ull << 30, 4);
+  CHECK(p.size() == 16);
+  CHECK(p[0].length == (64ull << 20));
+  std::vector<Segment> segs(p.begin(), p.end());
+  CHECK(segmentsCoverExactly(segs, 1ull << 30));
+  auto q = hostPipelinePieces((100ull << 20) + 2, 2);
+  CHECK(segmentsCoverExactly(q, (100ull << 20) + 2));
+  CHECK(q.front().length == (25ull << 18));  // roundup(S / 16, 64 KiB) = 6.25 MiB
+  CHECK_THROWS_AS(hostPipelinePieces(6, 4), std::invalid_argument);
+}
+
 TEST_CASE("chunk geometry (P10)") {
   CHECK(defaultChunkBytes(64ull << 20, 8, Algorithm::RingChunked) == (4ull << 20));
   CHECK(defaultChunkBytes(1 << 20, 8, Algorithm::RingChunked) == 65536);

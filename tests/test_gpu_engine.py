@@ -59,6 +59,7 @@ def test_engine_multirail_parity(world):
                 {"dtype": "i32", "nbytes": (32 << 20) + 12, "reps": 2},
                 {"dtype": "f32", "nbytes": 8192, "reps": 3},
                 {"dtype": "f32", "nbytes": 1 << 20, "reps": 2, "host": True},
+                {"dtype": "bf16", "nbytes": (24 << 20) + 2, "reps": 1, "host": True},  # pipelined pieces
             ]}
     res = _run(world, spec, timeout=420)
     # Every rank ran the same plans (the table is agreed across ranks).
