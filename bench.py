@@ -390,7 +390,7 @@ def main():
         out["sweep"] = sweep
 
     # ---- 8 KiB p50 latency: engine (cold start) vs each rail alone vs NCCL --
-    def p50_host(fn, n=300):
+    def p50_host(fn, n=1000):
         lat = []
         for _ in range(n):
             comm.barrier()
