@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--no-failover", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep-max", type=int, default=GiB)
+    ap.add_argument("--nccl-algos", action="store_true",
+                    help="also time NCCL with NCCL_ALGO=NVLS and =Ring (SURVEY.md 8d) at a few sizes")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -351,16 +353,16 @@ def main():
             os.dup2(saved, 1)
             os.close(saved)
 
-    def nccl_time(nbytes, iters):
+    def nccl_time(nbytes, iters, group=None):
         t = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
         for _ in range(5):
-            pg.all_reduce(t)
+            pg.all_reduce(t, group=group)
         torch.cuda.synchronize()
         pg.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(iters):
-            pg.all_reduce(t)
+            pg.all_reduce(t, group=group)
         b.record()
         b.synchronize()
         return max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
@@ -369,6 +371,25 @@ def main():
         tn = nccl_time(S, max(5, args.steps // 2))
         nccl["busbw_headline"] = round(ring_volume(world, S) / tn / 1e9, 2)
         out["nccl_busbw_GBs"] = nccl["busbw_headline"]
+        if args.nccl_algos:
+            # NCCL reads NCCL_ALGO when a communicator is created: one group per algorithm.
+            algos = {}
+            for algo in ("NVLS", "Ring"):
+                old = os.environ.get("NCCL_ALGO")
+                os.environ["NCCL_ALGO"] = algo
+                try:
+                    g = pg.new_group(backend="nccl")
+                    algos[algo] = {str(sz): round(ring_volume(world, sz) / nccl_time(sz, 20 if sz > (64 << 20) else 100,
+                                                                                       g) / 1e9, 2)
+                                   for sz in (8192, 1 << 20, 64 << 20, S)}
+                except Exception as e:  # pragma: no cover
+                    algos[algo] = {"error": str(e)[:160]}
+                finally:
+                    if old is None:
+                        os.environ.pop("NCCL_ALGO", None)
+                    else:
+                        os.environ["NCCL_ALGO"] = old
+            out["nccl_algos_busbw_GBs"] = algos
 
     # ---- sweep 4 KiB .. 1 GiB ----------------------------------------------
     if not args.no_sweep:
