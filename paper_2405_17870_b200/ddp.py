@@ -8,9 +8,12 @@ reduce its gradient buckets through libnezha_b200.so instead of NCCL:
     ddp_model.register_comm_hook(state, nezha_allreduce_hook)
 
 Each bucket is copied (device to device) into the engine's symmetric
-UnboundBuffer, all-reduced by the rails, copied back and averaged — all on the
-current CUDA stream, so DDP's own stream ordering covers it. torch is only the
-caller here; the reduction is the C ABI.
+UnboundBuffer, all-reduced by the rails, copied back and averaged on the
+hook's own communication stream, which first waits for the stream that
+produced the gradients; the returned CUDA-aware future carries an event on
+that communication stream, so backward compute of the next buckets overlaps
+the reduction (as with NCCL's stream) and DDP's consumers wait for it.
+torch is only the caller here; the reduction is the C ABI.
 """
 import os
 from dataclasses import dataclass
@@ -31,6 +34,7 @@ class NezhaHookState:
     ub_out: SymmetricBuffer
     capacity: int
     world: int
+    stream: torch.cuda.Stream = None
 
     @classmethod
     def create(cls, process_group=None, capacity: int = 256 << 20, rails=("nvls", "ce", "sm"),
@@ -47,7 +51,8 @@ class NezhaHookState:
         if world > 1 and not comm.multicast:
             rails = tuple(r for r in rails if r != "nvls") or ("sm",)
         engine = Engine(comm, kinds=list(rails), **engine_overrides)
-        return cls(comm, engine, SymmetricBuffer(comm, capacity), SymmetricBuffer(comm, capacity), capacity, world)
+        return cls(comm, engine, SymmetricBuffer(comm, capacity), SymmetricBuffer(comm, capacity), capacity, world,
+                   torch.cuda.Stream(priority=-1))
 
     def close(self) -> None:
         self.engine.close()
@@ -63,17 +68,19 @@ def nezha_allreduce_hook(state: NezhaHookState, bucket) -> torch.futures.Future[
     if dtype is None:
         raise TypeError(f"nezha hook: unsupported gradient dtype {t.dtype}")
     nbytes = t.numel() * t.element_size()
-    stream = torch.cuda.current_stream()
-    done = 0
-    while done < nbytes:  # buckets larger than the UnboundBuffer go in pieces
-        n = min(state.capacity, nbytes - done)
-        state.ub_in.write(t.data_ptr() + done, n, stream=stream)
-        state.engine.allreduce(state.ub_in, state.ub_out, n, dtype, stream)
-        state.ub_out.read(t.data_ptr() + done, n, stream=stream)
-        done += n
-    t.div_(state.world)
-    # A CUDA-aware future: set_result records an event on the current stream and
-    # DDP's consumers wait on it, so nothing reads the bucket before the rails finish.
-    fut = torch.futures.Future(devices=[t.device])
-    fut.set_result(t)
+    stream = state.stream or torch.cuda.current_stream()
+    stream.wait_stream(torch.cuda.current_stream())  # the gradients of this bucket are written
+    with torch.cuda.stream(stream):
+        done = 0
+        while done < nbytes:  # buckets larger than the UnboundBuffer go in pieces
+            n = min(state.capacity, nbytes - done)
+            state.ub_in.write(t.data_ptr() + done, n, stream=stream)
+            state.engine.allreduce(state.ub_in, state.ub_out, n, dtype, stream)
+            state.ub_out.read(t.data_ptr() + done, n, stream=stream)
+            done += n
+        t.div_(state.world)
+        # CUDA-aware future: set_result records an event on the communication
+        # stream; DDP's consumers wait on it before reading the bucket.
+        fut = torch.futures.Future(devices=[t.device])
+        fut.set_result(t)
     return fut
