@@ -241,6 +241,24 @@ int nz_engine_last_plan_json(nz_engine_t* eng, char* out, size_t cap);
  * oracle/planner.py. */
 int nz_planner_run_trace(const char* scenario, char* out, size_t cap);
 
+/* The planner driven op by op: the engine's nezha::Balancer with the rails
+ * and profiles of a rails TOML (every rail needs a profile). The
+ * engine's multi-rank flush agreement is the caller's `agree` callback: it
+ * receives this rank's per-rail window means (in rail_id order) and must
+ * replace them in place with the values every rank applies (the engine uses
+ * the max over ranks); return 0 on success. Without a callback, identity. */
+typedef struct nz_balancer nz_balancer_t;
+typedef int (*nz_agree_fn)(void* ctx, int bucket, int n, const int* rail_ids, double* means);
+int nz_balancer_create(const char* rails_toml, double tau, double eta, double sync_overhead_us, int window,
+                       int demote_after, nz_balancer_t** out);
+int nz_balancer_destroy(nz_balancer_t* b);
+int nz_balancer_set_agreement(nz_balancer_t* b, nz_agree_fn fn, void* ctx);
+/* Plans one op of `bytes` (JSON as in the planner trace) and keeps it
+ * pending until nz_balancer_record reports its per-rail latencies. */
+int nz_balancer_allocate(nz_balancer_t* b, uint64_t bytes, char* plan_json, size_t cap);
+int nz_balancer_record(nz_balancer_t* b, int n, const int* rail_ids, const double* us, int* flushed);
+int nz_balancer_table_json(nz_balancer_t* b, char* out, size_t cap);
+
 /* ------------------------------------------------------------ emulation --- */
 /* Single-GPU emulation of one rank of the SM rail (ndst == world: fold and
  * store to every rank's output) or of the CE rail's local reduce (ndst == 1)

@@ -113,6 +113,8 @@ class FailoverReport(ctypes.Structure):
     ]
 
 
+AGREE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_int, c_int, POINTER(c_int), POINTER(c_double))
+
 _SIGS = {
     "nz_last_error": (c_char_p, []),
     "nz_abi_version": (c_int, []),
@@ -171,6 +173,12 @@ _SIGS = {
                                 c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
     "nz_emulate_fold_tma": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64,
                                     c_uint64, c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
+    "nz_balancer_create": (c_int, [c_char_p, c_double, c_double, c_double, c_int, c_int, POINTER(c_void_p)]),
+    "nz_balancer_destroy": (c_int, [c_void_p]),
+    "nz_balancer_set_agreement": (c_int, [c_void_p, AGREE_FN, c_void_p]),
+    "nz_balancer_allocate": (c_int, [c_void_p, c_uint64, c_char_p, c_size_t]),
+    "nz_balancer_record": (c_int, [c_void_p, c_int, POINTER(c_int), POINTER(c_double), POINTER(c_int)]),
+    "nz_balancer_table_json": (c_int, [c_void_p, c_char_p, c_size_t]),
     "nz_pool_create": (c_int, [c_int, POINTER(c_void_p)]),
     "nz_pool_destroy": (c_int, [c_void_p]),
     "nz_pool_declare": (c_int, [c_void_p, c_int, c_int, c_int, c_int]),

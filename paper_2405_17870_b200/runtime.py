@@ -365,3 +365,57 @@ def calibrate(samples: list[tuple[int, float]]) -> dict:
     check(lib().nz_core_calibrate(xs, ys, n, byref(t), byref(bw), byref(it), byref(mr)), "nz_core_calibrate")
     return {"t_setup_us": t.value, "bandwidth_bps": bw.value, "interpolated": bool(it.value),
             "max_rel_residual": mr.value}
+
+
+class Planner:
+    """The engine's balancer driven op by op (nz_balancer_*), no GPU.
+
+    ``agree(bucket, rail_ids, means) -> means`` is the multi-rank flush
+    agreement (the engine: max over ranks); None = single process."""
+
+    def __init__(self, rails_toml: str, tau: float = 5.0, eta: float = 0.05, sync_overhead_us: float = 0.0,
+                 window: int = 100, demote_after: int = 0, agree=None):
+        self._h = None
+        h = c_void_p()
+        self._toml = rails_toml.encode()
+        check(lib().nz_balancer_create(self._toml, tau, eta, sync_overhead_us, window, demote_after, byref(h)),
+              "nz_balancer_create")
+        self._h = h
+        self._cb = None
+        if agree is not None:
+            def _cb(_ctx, bucket, n, ids, means):
+                try:
+                    new = agree(bucket, [ids[i] for i in range(n)], [means[i] for i in range(n)])
+                    for i in range(n):
+                        means[i] = float(new[i])
+                    return 0
+                except Exception:  # pragma: no cover - surfaced as NZ_ERR_SYSTEM by the library
+                    return 1
+            self._cb = _lib.AGREE_FN(_cb)
+            check(lib().nz_balancer_set_agreement(self._h, self._cb, None), "nz_balancer_set_agreement")
+
+    def close(self) -> None:
+        if self._h:
+            lib().nz_balancer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def allocate(self, nbytes: int) -> dict:
+        buf = ctypes.create_string_buffer(1 << 16)
+        check(lib().nz_balancer_allocate(self._h, nbytes, buf, len(buf)), "nz_balancer_allocate")
+        return json.loads(buf.value.decode())
+
+    def record(self, latencies: dict) -> bool:
+        ids = sorted(latencies)
+        arr_i = (ctypes.c_int * max(len(ids), 1))(*ids)
+        arr_d = (ctypes.c_double * max(len(ids), 1))(*[latencies[i] for i in ids])
+        fl = ctypes.c_int(0)
+        check(lib().nz_balancer_record(self._h, len(ids), arr_i, arr_d, byref(fl)), "nz_balancer_record")
+        return bool(fl.value)
+
+    def table(self) -> dict:
+        buf = ctypes.create_string_buffer(1 << 20)
+        check(lib().nz_balancer_table_json(self._h, buf, len(buf)), "nz_balancer_table_json")
+        return json.loads(buf.value.decode())
