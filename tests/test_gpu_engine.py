@@ -60,6 +60,10 @@ def test_engine_multirail_parity(world):
                 {"dtype": "f32", "nbytes": 8192, "reps": 3},
                 {"dtype": "f32", "nbytes": 1 << 20, "reps": 2, "host": True},
                 {"dtype": "bf16", "nbytes": (24 << 20) + 2, "reps": 1, "host": True},  # pipelined pieces
+                {"dtype": "f32", "nbytes": 4, "reps": 2},     # one element, fewer than ranks
+                {"dtype": "bf16", "nbytes": 2, "reps": 2},
+                {"dtype": "i32", "nbytes": 12, "reps": 1, "host": True},
+                {"dtype": "bf16", "nbytes": 4_194_306, "reps": 2},  # odd bf16 count near the LL ceiling
             ]}
     res = _run(world, spec, timeout=420)
     # Every rank ran the same plans (the table is agreed across ranks).
