@@ -217,6 +217,8 @@ def main():
     session = f"bench-{os.environ.get('MASTER_PORT', '0')}-{os.environ.get('TORCHELASTIC_RUN_ID', str(os.getppid()))}"
     comm = Comm(rank, world, local, session)
     kinds = args.rails.split(",")
+    if world > 1 and not comm.multicast and "nvls" in kinds:  # no NVSwitch multicast on this box
+        kinds = [k for k in kinds if k != "nvls"] or ["sm"]
     dt = DTYPES[args.dtype]
     S = args.bytes
     eng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=min(GiB, max(S, 1 << 20)))
