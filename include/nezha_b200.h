@@ -175,6 +175,8 @@ typedef struct {
   int compute_pool;          /* SM arbitration of concurrent rails (P14):
                                 0 off (default), 1 block (SPEC ComputePool), 2 shrink */
   int pool_tokens;           /* ComputePool total_tokens; 0 = the GPU's SM count */
+  int tune_budgets;          /* 1 (default): measure the NVLS / SM rails' CTA budget at
+                                startup for rails whose sm_budget is 0 */
 } nz_engine_config_t;
 
 void nz_engine_config_default(nz_engine_config_t* cfg);

@@ -96,6 +96,7 @@ class EngineConfig(ctypes.Structure):
         ("timer_lag", c_int),
         ("compute_pool", c_int),
         ("pool_tokens", c_int),
+        ("tune_budgets", c_int),
     ]
 
 

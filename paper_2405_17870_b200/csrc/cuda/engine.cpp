@@ -410,6 +410,47 @@ struct nz_engine {
 
   // Startup calibration: each rail alone over a size sweep, then the
   // coordination cost of a fork/join over all rails.
+  // CTA budget of the SM-driven rails, measured instead of assumed: each
+  // candidate grid runs the two-shot path at one large size, ranks agree on
+  // the times (max), the fastest wins (ties within 3 % go to the smaller
+  // grid). Rails whose budget the config pins are left alone. The chosen
+  // grids then hold for calibration and every op, identically on all ranks.
+  void tuneBudgets(uint64_t maxb, cudaEvent_t e0, cudaEvent_t e1) {
+    if (comm->world == 1) return;
+    const uint64_t s = std::min<uint64_t>(uint64_t{64} << 20, maxb) & ~uint64_t{4095};
+    if (s <= (uint64_t{4} << 20)) return;  // must be past the one-shot (LL) ceiling
+    for (size_t i = 0; i < rails.size(); ++i) {
+      nz_rail* r = rails[i];
+      if (specs[i].sm_budget > 0) continue;
+      std::vector<int> cands;
+      if (r->kind == NZ_RAIL_NVLS) cands = {16, 32, 64};
+      if (r->kind == NZ_RAIL_SM) cands = {32, 64, 128};
+      if (cands.empty()) continue;
+      const uint64_t C = nezha::defaultChunkBytes(s, comm->world, algo);
+      std::vector<double> t(cands.size());
+      for (size_t k = 0; k < cands.size(); ++k) {
+        r->sm_budget = std::min(cands[k], comm->sm_count);
+        for (int w = 0; w < 2; ++w) nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
+        NZ_CUDA(cudaEventRecord(e0, r->stream));
+        for (int it = 0; it < 5; ++it) nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
+        NZ_CUDA(cudaEventRecord(e1, r->stream));
+        NZ_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        NZ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        t[k] = ms;
+      }
+      const auto msgs = nz::exchange(comm, t.data(), t.size() * sizeof(double), {});
+      for (int rk = 0; rk < comm->world; ++rk) {
+        const double* v = reinterpret_cast<const double*>(msgs[rk].data.data());
+        for (size_t k = 0; k < t.size(); ++k) t[k] = std::max(t[k], v[k]);
+      }
+      size_t best = 0;
+      for (size_t k = 1; k < t.size(); ++k)
+        if (t[k] < t[best] * 0.97) best = k;
+      r->sm_budget = std::min(cands[best], comm->sm_count);
+    }
+  }
+
   void calibrate() {
     const uint64_t maxb = std::max<uint64_t>(cfg.calibrate_max_bytes, 1 << 16);
     ensureUnbound(maxb);
@@ -417,6 +458,7 @@ struct nz_engine {
     std::vector<uint64_t> sizes;
     for (uint64_t s = 4096; s <= maxb; s *= 4) sizes.push_back(s);
     cudaEvent_t e0 = event(), e1 = event();
+    if (cfg.tune_budgets) tuneBudgets(maxb, e0, e1);
     std::vector<nezha::RailProfile> profiles;
     bool measured_any = false;
     for (size_t i = 0; i < specs.size(); ++i) {
@@ -576,7 +618,7 @@ struct nz_engine {
       const auto& p = bal->rails()[i];
       o << (i ? "," : "") << "{\"rail_id\":" << specs[i].rail_id << ",\"kind\":\""
         << (specs[i].kind == NZ_RAIL_NVLS ? "nvls" : specs[i].kind == NZ_RAIL_CE ? "ce" : "sm")
-        << "\",\"protocol\":\"" << nezha::toString(p.protocol) << "\",\"health\":\""
+        << "\",\"sm_budget\":" << rails[i]->sm_budget << ",\"protocol\":\"" << nezha::toString(p.protocol) << "\",\"health\":\""
         << nezha::toString(health->state(specs[i].rail_id).status) << "\",\"t_setup_us\":"
         << nezha::formatDouble(p.t_setup_us) << ",\"bandwidth_bps\":" << nezha::formatDouble(p.bandwidth_bps)
         << ",\"calibration\":[";
@@ -635,6 +677,7 @@ void nz_engine_config_default(nz_engine_config_t* c) {
   c->calibrate_iters = 20;
   c->calibrate_max_bytes = uint64_t{1} << 30;
   c->timer_lag = 2;
+  c->tune_budgets = 1;
 }
 
 int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t** out) {
