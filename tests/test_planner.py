@@ -329,3 +329,27 @@ def test_acceptance_rho_gate():
 
     assert len(plan(0.9e9)["segs"]) == 1  # ratio ~5.6 at the model split
     assert len(plan(2.5e9)["segs"]) == 2  # ratio ~2
+
+
+def test_acceptance_8_cold_start_threshold_shrinks_with_nodes():
+    """SPEC.md:541 (acceptance 8): under the SPEC's ring-step model
+    (2(N-1) steps of t_setup + (S/N)/B) the Eq. 6 threshold
+    strictly decreases when the node count doubles, and below it the plan is
+    a single rail, i.e. dual-rail latency = the best single rail's."""
+    from paper_2405_17870_b200.runtime import Planner
+
+    def toml(n):
+        t_step, b = 5.0, 25e9
+        rail = f"t_setup_us = {2 * (n - 1) * t_step}\nbandwidth_bps = {b * n / (2 * (n - 1))}\n"
+        return f'[[rail]]\nprotocol = "tcp"\n{rail}[[rail]]\nprotocol = "glex"\n{rail}'
+
+    thr = {}
+    for n in (2, 4, 8, 16):
+        p = Planner(toml(n), sync_overhead_us=50.0)
+        thr[n] = p.table()["threshold"]
+        below = p.allocate(max(4096, thr[n] // 2))
+        assert len(below["segs"]) == 1 and not below["hot"]
+        above = p.allocate(min(1 << 30, thr[n] * 4))
+        assert above["hot"] and len(above["segs"]) == 2
+        p.close()
+    assert thr[2] > thr[4] > thr[8] > thr[16], thr
