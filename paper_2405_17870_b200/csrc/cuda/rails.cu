@@ -253,6 +253,19 @@ int gated(int grid, const ComputeGate* gate) {
   return gate && gate->max_ctas > 0 ? std::max(1, std::min(grid, gate->max_ctas)) : grid;
 }
 
+// NVLS-LL (one-shot multicast push) is opt-in: NEZHA_NVLS_LL=1. The only
+// NVLink error incident of this project came from a multicast store path
+// (profiles/README.md); until its fixed form has a clean hardware record the
+// NVLS rail runs small payloads two-shot, and the planner sends them to the
+// SM rail's unicast LL path, which is as fast.
+bool nvlsLLEnabled() {
+  static const bool on = [] {
+    const char* e = getenv("NEZHA_NVLS_LL");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool llPath(nz_rail* r, uint64_t lo, uint64_t hi) {
   const int N = r->comm->world;
   const bool mc_ll = r->kind == NZ_RAIL_NVLS;
@@ -525,7 +538,7 @@ int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rai
     for (int p = 0; p < comm->world; ++p) r->pad_peer[p] = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[p] + pad_off);
     NZ_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
     NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
-    if ((kind == NZ_RAIL_SM || kind == NZ_RAIL_NVLS) && comm->world > 1) {
+    if ((kind == NZ_RAIL_SM || (kind == NZ_RAIL_NVLS && nz::nvlsLLEnabled())) && comm->world > 1) {
       // LL slots: [parity 2][rank N][kLLMaxBytes / 4 words] x 8 bytes, zeroed on every rank first.
       // Even word count: every slot starts 16-byte aligned for the v4 pushes.
       r->ll_slot_words = ((nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS) + 7) / 4 + 1) & ~uint64_t{1};

@@ -161,6 +161,22 @@ def test_multi_gpu_rails(world):
 
 
 @pytest.mark.multigpu
+def test_multi_gpu_nvls_ll_opt_in():
+    """NVLS-LL (multicast push one-shot) is opt-in (NEZHA_NVLS_LL=1, rails.cu);
+    its parity cases run only when NEZHA_TEST_NVLS_LL=1 asks for them."""
+    if not os.environ.get("NEZHA_TEST_NVLS_LL"):
+        pytest.skip("NVLS-LL is opt-in (NEZHA_TEST_NVLS_LL=1)")
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cases = [c for c in MULTI if c["kind"] == "nvls" and c["nbytes"] <= (512 << 10)]
+    res = spawn(2, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(cases)], timeout=300,
+                extra_env={"NEZHA_NVLS_LL": "1"})
+    for rank_res in res:
+        for r in rank_res["results"]:
+            assert r["watchdog"] == 0 and r["mismatch"] == 0 and r["outside_nonzero"] == 0, r
+
+
+@pytest.mark.multigpu
 @pytest.mark.parametrize("kind", ["sm", "nvls"])
 def test_watchdog_instead_of_hang(kind):
     """A peer that never arrives: the kernel exits after the watchdog budget."""
