@@ -190,8 +190,14 @@ int nz_engine_destroy(nz_engine_t* eng);
  * rails fork from it and join back into it. Asynchronous. */
 int nz_engine_allreduce(nz_engine_t* eng, nz_buf_t* in, nz_buf_t* out, uint64_t bytes, int dtype, void* stream);
 /* End to end from host memory (pinned or pageable): H2D into the engine's
- * UnboundBuffer, multi-rail allreduce, D2H into host_out. Synchronous. */
+ * UnboundBuffer, multi-rail allreduce, D2H into host_out, pipelined over
+ * pieces. Synchronous. */
 int nz_engine_allreduce_host(nz_engine_t* eng, const void* host_in, void* host_out, uint64_t bytes, int dtype);
+/* Same pipeline for device memory the caller owns (not symmetric), e.g. a
+ * PyTorch gradient bucket: staged through the engine's UnboundBuffer in
+ * pieces, asynchronous on `stream` (NULL = legacy default); src == dst is
+ * allowed. */
+int nz_engine_allreduce_device(nz_engine_t* eng, const void* src, void* dst, uint64_t bytes, int dtype, void* stream);
 /* Arms a failure of `rail_id` at `chunk` of op `op_seq` (trace form P10). */
 int nz_engine_inject_failure(nz_engine_t* eng, uint32_t op_seq, int rail_id, uint64_t chunk);
 /* Readmits a previously failed rail. */

@@ -156,6 +156,7 @@ _SIGS = {
     "nz_engine_destroy": (c_int, [c_void_p]),
     "nz_engine_allreduce": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64, c_int, c_void_p]),
     "nz_engine_allreduce_host": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64, c_int]),
+    "nz_engine_allreduce_device": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64, c_int, c_void_p]),
     "nz_engine_inject_failure": (c_int, [c_void_p, c_uint32, c_int, c_uint64]),
     "nz_engine_readmit": (c_int, [c_void_p, c_int]),
     "nz_engine_synchronize": (c_int, [c_void_p]),

@@ -360,6 +360,49 @@ struct nz_engine {
     fo_pending = true;
   }
 
+  // Allreduce of memory outside the symmetric heap (host, or device memory
+  // the caller owns): a three-stage pipeline over pieces.
+  // Piece i+1 is staged into the UnboundBuffer on h2d while the rails reduce
+  // piece i on io and piece i-1 is copied out on d2h, so the copies overlap
+  // each other and the NVLink work. Each piece is an independent allreduce
+  // with its own recorded plan (like split_oversized pieces); the pieces are
+  // a function of `bytes` alone, so every rank cuts the same ones. `user`
+  // (device variant): the staging waits for it first and it waits for the
+  // last copy-out; nullptr (host variant): the caller synchronizes.
+  void staged(const char* src, char* dst, uint64_t bytes, int dtype, cudaMemcpyKind kin, cudaMemcpyKind kout,
+              cudaStream_t user) {
+    ensureUnbound(bytes);
+    nz_buf* in = ub_in;
+    nz_buf* out = ub_out;
+    const int me = comm->rank;
+    if (user) {
+      cudaEvent_t ready = event();
+      NZ_CUDA(cudaEventRecord(ready, user));
+      NZ_CUDA(cudaStreamWaitEvent(h2d, ready, 0));
+      pool.push_back(ready);
+    }
+    last_plans.clear();
+    for (const auto& piece : nezha::hostPipelinePieces(bytes, nz::elemSizeOf(dtype))) {
+      NZ_CUDA(cudaMemcpyAsync(in->ptrs[me] + piece.offset, src + piece.offset, piece.length, kin, h2d));
+      cudaEvent_t up = event();
+      NZ_CUDA(cudaEventRecord(up, h2d));
+      NZ_CUDA(cudaStreamWaitEvent(io, up, 0));
+      op(in, out, piece.offset, piece.length, dtype, io);
+      cudaEvent_t red = event();
+      NZ_CUDA(cudaEventRecord(red, io));
+      NZ_CUDA(cudaStreamWaitEvent(d2h, red, 0));
+      NZ_CUDA(cudaMemcpyAsync(dst + piece.offset, out->ptrs[me] + piece.offset, piece.length, kout, d2h));
+      pool.push_back(up);  // waits are captured at enqueue time: safe to recycle
+      pool.push_back(red);
+    }
+    if (user) {
+      cudaEvent_t done = event();
+      NZ_CUDA(cudaEventRecord(done, d2h));
+      NZ_CUDA(cudaStreamWaitEvent(user, done, 0));
+      pool.push_back(done);
+    }
+  }
+
   // Collective point: every rank calls it at the same place in its op stream.
   void synchronize() {
     NZ_CUDA(cudaDeviceSynchronize());  // rail streams and cold ops on callers' streams
@@ -806,38 +849,23 @@ int nz_engine_allreduce_host(nz_engine_t* eng, const void* host_in, void* host_o
     if (!eng || !host_in || !host_out) fail(NZ_ERR_INVALID, "null argument");
     if (bytes == 0) return;
     NZ_CUDA(cudaSetDevice(eng->comm->device));
-    eng->ensureUnbound(bytes);
-    nz_buf* in = eng->ub_in;
-    nz_buf* out = eng->ub_out;
-    const int me = eng->comm->rank;
-    const char* src = static_cast<const char*>(host_in);
-    char* dst = static_cast<char*>(host_out);
-    // Three-stage pipeline over pieces: upload piece i+1 on
-    // h2d while the rails reduce piece i on io and d2h downloads piece i-1, so
-    // the PCIe directions overlap each other and the NVLink work. Pieces are
-    // independent allreduces, each with its own recorded plan, exactly like
-    // split_oversized pieces; the piece size is a function of `bytes` alone,
-    // so every rank cuts the same pieces.
-    eng->last_plans.clear();
-    const auto pieces = nezha::hostPipelinePieces(bytes, nz::elemSizeOf(dtype));
-    for (const auto& piece : pieces) {
-      NZ_CUDA(cudaMemcpyAsync(in->ptrs[me] + piece.offset, src + piece.offset, piece.length, cudaMemcpyHostToDevice,
-                              eng->h2d));
-      cudaEvent_t up = eng->event();
-      NZ_CUDA(cudaEventRecord(up, eng->h2d));
-      NZ_CUDA(cudaStreamWaitEvent(eng->io, up, 0));
-      eng->op(in, out, piece.offset, piece.length, dtype, eng->io);
-      cudaEvent_t red = eng->event();
-      NZ_CUDA(cudaEventRecord(red, eng->io));
-      NZ_CUDA(cudaStreamWaitEvent(eng->d2h, red, 0));
-      NZ_CUDA(cudaMemcpyAsync(dst + piece.offset, out->ptrs[me] + piece.offset, piece.length, cudaMemcpyDeviceToHost,
-                              eng->d2h));
-      eng->pool.push_back(up);  // waits captured at enqueue time: safe to recycle
-      eng->pool.push_back(red);
-    }
+    eng->staged(static_cast<const char*>(host_in), static_cast<char*>(host_out), bytes, dtype, cudaMemcpyHostToDevice,
+                cudaMemcpyDeviceToHost, nullptr);
     NZ_CUDA(cudaStreamSynchronize(eng->d2h));
     NZ_CUDA(cudaStreamSynchronize(eng->io));
     eng->finishFailoverReport();
+  });
+}
+
+int nz_engine_allreduce_device(nz_engine_t* eng, const void* src, void* dst, uint64_t bytes, int dtype,
+                               void* stream) {
+  return guarded([&] {
+    if (!eng || !src || !dst) fail(NZ_ERR_INVALID, "null argument");
+    if (bytes == 0) return;
+    NZ_CUDA(cudaSetDevice(eng->comm->device));
+    cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    eng->staged(static_cast<const char*>(src), static_cast<char*>(dst), bytes, dtype, cudaMemcpyDeviceToDevice,
+                cudaMemcpyDeviceToDevice, user);
   });
 }
 

@@ -7,10 +7,11 @@ reduce its gradient buckets through libnezha_b200.so instead of NCCL:
     state = NezhaHookState.create(process_group)      # one Engine per rank
     ddp_model.register_comm_hook(state, nezha_allreduce_hook)
 
-Each bucket is copied (device to device) into the engine's symmetric
-UnboundBuffer, all-reduced by the rails, copied back and averaged on the
-hook's own communication stream, which first waits for the stream that
-produced the gradients; the returned CUDA-aware future carries an event on
+Each bucket goes through nz_engine_allreduce_device: staged piecewise into
+the engine's symmetric UnboundBuffer, all-reduced by the rails and copied
+back with the copies pipelined against the NVLink work, then averaged — all
+on the hook's own communication stream, which first waits for the stream that
+produced the gradients. The returned CUDA-aware future carries an event on
 that communication stream, so backward compute of the next buckets overlaps
 the reduction (as with NCCL's stream) and DDP's consumers wait for it.
 torch is only the caller here; the reduction is the C ABI.
@@ -21,7 +22,7 @@ from dataclasses import dataclass
 import torch
 
 from ._lib import BF16, F32, I32
-from .runtime import Comm, Engine, SymmetricBuffer
+from .runtime import Comm, Engine
 
 _DTYPES = {torch.float32: F32, torch.bfloat16: BF16, torch.int32: I32}
 
@@ -30,15 +31,14 @@ _DTYPES = {torch.float32: F32, torch.bfloat16: BF16, torch.int32: I32}
 class NezhaHookState:
     comm: Comm
     engine: Engine
-    ub_in: SymmetricBuffer
-    ub_out: SymmetricBuffer
-    capacity: int
     world: int
     stream: torch.cuda.Stream = None
 
     @classmethod
     def create(cls, process_group=None, capacity: int = 256 << 20, rails=("nvls", "ce", "sm"),
                **engine_overrides) -> "NezhaHookState":
+        """`capacity` sizes the startup calibration (and so the first staging
+        buffer) unless `calibrate_max_bytes` is given; larger buckets grow it."""
         import torch.distributed as dist
 
         rank = dist.get_rank(process_group)
@@ -50,14 +50,12 @@ class NezhaHookState:
         comm = Comm(rank, world, device, token[0])
         if world > 1 and not comm.multicast:
             rails = tuple(r for r in rails if r != "nvls") or ("sm",)
+        engine_overrides.setdefault("calibrate_max_bytes", capacity)
         engine = Engine(comm, kinds=list(rails), **engine_overrides)
-        return cls(comm, engine, SymmetricBuffer(comm, capacity), SymmetricBuffer(comm, capacity), capacity, world,
-                   torch.cuda.Stream(priority=-1))
+        return cls(comm, engine, world, torch.cuda.Stream(priority=-1))
 
     def close(self) -> None:
         self.engine.close()
-        self.ub_in.free()
-        self.ub_out.free()
         self.comm.close()
 
 
@@ -71,13 +69,7 @@ def nezha_allreduce_hook(state: NezhaHookState, bucket) -> torch.futures.Future[
     stream = state.stream or torch.cuda.current_stream()
     stream.wait_stream(torch.cuda.current_stream())  # the gradients of this bucket are written
     with torch.cuda.stream(stream):
-        done = 0
-        while done < nbytes:  # buckets larger than the UnboundBuffer go in pieces
-            n = min(state.capacity, nbytes - done)
-            state.ub_in.write(t.data_ptr() + done, n, stream=stream)
-            state.engine.allreduce(state.ub_in, state.ub_out, n, dtype, stream)
-            state.ub_out.read(t.data_ptr() + done, n, stream=stream)
-            done += n
+        state.engine.allreduce_device(t, t, nbytes, dtype, stream)
         t.div_(state.world)
         # CUDA-aware future: set_result records an event on the communication
         # stream; DDP's consumers wait on it before reading the bucket.

@@ -199,6 +199,11 @@ class Engine:
         check(lib().nz_engine_allreduce_host(self.handle, _ptr(host_in), _ptr(host_out), nbytes, dtype),
               "nz_engine_allreduce_host")
 
+    def allreduce_device(self, src, dst, nbytes: int, dtype: int, stream=None) -> None:
+        """Allreduce of caller-owned device memory (nz_engine_allreduce_device); src may equal dst."""
+        check(lib().nz_engine_allreduce_device(self.handle, _ptr(src), _ptr(dst), nbytes, dtype, _stream(stream)),
+              "nz_engine_allreduce_device")
+
     def inject_failure(self, op_seq: int, rail_id: int, chunk: int) -> None:
         check(lib().nz_engine_inject_failure(self.handle, op_seq, rail_id, chunk), "nz_engine_inject_failure")
 

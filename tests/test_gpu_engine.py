@@ -64,6 +64,8 @@ def test_engine_multirail_parity(world):
                 {"dtype": "bf16", "nbytes": 2, "reps": 2},
                 {"dtype": "i32", "nbytes": 12, "reps": 1, "host": True},
                 {"dtype": "bf16", "nbytes": 4_194_306, "reps": 2},  # odd bf16 count near the LL ceiling
+                {"dtype": "f32", "nbytes": (40 << 20) + 4, "reps": 2, "device": True},  # staged pipeline
+                {"dtype": "i32", "nbytes": 4096, "reps": 1, "device": True},
             ]}
     res = _run(world, spec, timeout=420)
     # Every rank ran the same plans (the table is agreed across ranks).

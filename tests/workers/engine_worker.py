@@ -74,6 +74,14 @@ def main():
             got = np.zeros(n // ES[dt], dtype=oracle.NP_DTYPE[dt])
             if c.get("host"):
                 eng.allreduce_host(inputs[rank], got, n, dt)
+            elif c.get("device"):  # caller-owned device memory, in place (nz_engine_allreduce_device)
+                import torch
+                torch.cuda.set_device(comm.device)
+                dev = torch.from_numpy(inputs[rank].view(np.uint8).copy()).cuda()
+                comm.barrier()
+                eng.allreduce_device(dev, dev, n, dt)
+                eng.synchronize()
+                got = dev.cpu().numpy().view(got.dtype).copy()
             else:
                 bin_.write(inputs[rank], n)
                 bout.zero()
