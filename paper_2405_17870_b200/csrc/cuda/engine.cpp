@@ -375,9 +375,12 @@ struct nz_engine {
     nz_buf* in = ub_in;
     nz_buf* out = ub_out;
     const int me = comm->rank;
-    if (user) {
+    // The UnboundBuffer is reused call after call: staging waits for the
+    // previous call's reductions and copy-outs, and for the caller's stream.
+    for (cudaStream_t prev : {io, d2h, user}) {
+      if (!prev) continue;
       cudaEvent_t ready = event();
-      NZ_CUDA(cudaEventRecord(ready, user));
+      NZ_CUDA(cudaEventRecord(ready, prev));
       NZ_CUDA(cudaStreamWaitEvent(h2d, ready, 0));
       pool.push_back(ready);
     }
