@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--no-failover", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep-max", type=int, default=GiB)
+    ap.add_argument("--nccl-graph", action="store_true",
+                    help="also time NCCL at <= 1 MiB from a captured CUDA graph (no host launch overhead)")
     ap.add_argument("--nccl-algos", action="store_true",
                     help="also time NCCL with NCCL_ALGO=NVLS and =Ring (SURVEY.md 8d) at a few sizes")
     args = ap.parse_args()
@@ -369,6 +371,31 @@ def main():
         b.synchronize()
         return max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
 
+    def nccl_graph_time(nbytes, per_graph=50, replays=10):
+        """NCCL device time per op: `per_graph` allreduces captured in one CUDA
+        graph, replayed; excludes the Python / launch overhead of nccl_time."""
+        t = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                pg.all_reduce(t)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(per_graph):
+                pg.all_reduce(t)
+        g.replay()
+        torch.cuda.synchronize()
+        pg.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(replays):
+            g.replay()
+        b.record()
+        b.synchronize()
+        return max_over_ranks(a.elapsed_time(b) / 1e3 / (replays * per_graph))
+
     if pg is not None:
         tn = nccl_time(S, max(5, args.steps // 2))
         nccl["busbw_headline"] = round(ring_volume(world, S) / tn / 1e9, 2)
@@ -408,6 +435,11 @@ def main():
                 tn = nccl_time(s, it)
                 row["nccl_busbw_GBs"] = round(ring_volume(world, s) / tn / 1e9, 2)
                 row["nccl_us"] = round(tn * 1e6, 2)
+                if args.nccl_graph and s <= (1 << 20):
+                    try:
+                        row["nccl_graph_us"] = round(nccl_graph_time(s) * 1e6, 2)
+                    except Exception as e:  # pragma: no cover
+                        row["nccl_graph_error"] = str(e)[:120]
             sweep.append(row)
             s *= 2
         out["sweep"] = sweep
