@@ -95,6 +95,10 @@ class Engine {
     out.values.resize(in.values.size());
     check(nz_engine_allreduce_host(h_, in.data(), out.data(), in.byteLength(), NZ_F32));
   }
+  // Caller-owned device memory (not symmetric), asynchronous on `stream`.
+  void allreduceDevice(const void* src, void* dst, Bytes bytes, nz_dtype_t dtype, void* stream = nullptr) {
+    check(nz_engine_allreduce_device(h_, src, dst, bytes, dtype, stream));
+  }
   // InMemoryFabric::failRailAtFrame (inmem.hpp:22-24) in trace form.
   void failRailAt(std::uint32_t op_seq, int rail, std::uint64_t chunk) {
     check(nz_engine_inject_failure(h_, op_seq, rail, chunk));
