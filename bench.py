@@ -446,14 +446,24 @@ def main():
 
     # ---- 8 KiB p50 latency: engine (cold start) vs each rail alone vs NCCL --
     def p50_host(fn, n=1000):
+        """Per op: every rank issues at one agreed CLOCK_MONOTONIC instant (the
+        clock is system-wide, so one box shares it) and stops when its result
+        is on the host's side of a synchronize; the op's latency is the max over
+        ranks of (done - start), i.e. issued on all GPUs -> complete on all GPUs
+        (SURVEY.md 8d). p50 over n ops. Removes the skew a plain barrier leaves."""
+        import struct
         lat = []
         for _ in range(n):
-            comm.barrier()
-            t0 = time.perf_counter()
+            prop = time.perf_counter() + 1e-3  # well past the exchange itself
+            start = max(struct.unpack("d", b)[0] for b in comm.allgather_bytes(struct.pack("d", prop)))
+            while time.perf_counter() < start:
+                pass
             fn()
             torch.cuda.synchronize()
-            lat.append(time.perf_counter() - t0)
-        return max_over_ranks(statistics.median(lat) * 1e6)
+            lat.append(time.perf_counter() - start)
+        mine = struct.pack(f"{n}d", *lat)
+        per_op = [max(v) for v in zip(*[struct.unpack(f"{n}d", b) for b in comm.allgather_bytes(mine)])]
+        return statistics.median(per_op) * 1e6
 
     lat = {}
     lat["engine_us"] = round(p50_host(lambda: eng.allreduce(bin_, bout, 8192, dt, stream)), 2)
