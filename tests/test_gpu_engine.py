@@ -71,6 +71,11 @@ def test_engine_multirail_parity(world):
     # Every rank ran the same plans (the table is agreed across ranks).
     plans = [[r["segs"] for r in rk["results"]] for rk in res]
     assert all(p == plans[0] for p in plans)
+    # Startup budget tuning picked a candidate grid, the same on every rank.
+    budgets = [[(x["kind"], x["sm_budget"]) for x in rk["state"]["rails"]] for rk in res]
+    assert all(b == budgets[0] for b in budgets)
+    cands = {"nvls": {16, 32, 64}, "sm": {32, 64, 128}, "ce": {0}}
+    assert all(v in cands[k] for k, v in budgets[0]), budgets[0]
 
 
 @pytest.mark.multigpu
