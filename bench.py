@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--no-failover", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep-max", type=int, default=GiB)
+    ap.add_argument("--graph", action="store_true",
+                    help="small sizes replayed from CUDA graphs: a graph_safe engine vs NCCL (device time per op)")
     ap.add_argument("--nccl-graph", action="store_true",
                     help="also time NCCL at <= 1 MiB from a captured CUDA graph (no host launch overhead)")
     ap.add_argument("--nccl-algos", action="store_true",
@@ -479,6 +481,39 @@ def main():
             t8 = torch.empty(2048, dtype=torch.float32, device="cuda")
             lat["nccl_us"] = round(p50_host(lambda: pg.all_reduce(t8)), 2)
     out["latency_8k_p50_us"] = lat
+
+    # ---- small sizes from CUDA graphs (no host launch cost on either side) --
+    if args.graph and world > 1:
+        geng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=1 << 22,
+                      graph_safe=1)
+        rows = {}
+        for sz in (8192, 65536, 1 << 20):
+            try:
+                geng.allreduce(bin_, bout, sz, dt)  # warm-up
+                geng.synchronize()
+                g = torch.cuda.CUDAGraph()
+                per_graph, replays = 50, 10
+                with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+                    for _ in range(per_graph):
+                        geng.allreduce(bin_, bout, sz, dt, torch.cuda.current_stream())
+                g.replay()
+                torch.cuda.synchronize()
+                comm.barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                for _ in range(replays):
+                    g.replay()
+                b.record()
+                b.synchronize()
+                row = {"ours_us": round(max_over_ranks(a.elapsed_time(b) * 1e3 / (replays * per_graph)), 2),
+                       "rails": sorted({seg[0] for p in geng.last_plans() for seg in p["segs"]})}
+                if pg is not None:
+                    row["nccl_us"] = round(nccl_graph_time(sz) * 1e6, 2)
+                rows[str(sz)] = row
+            except Exception as e:  # pragma: no cover
+                rows[str(sz)] = {"error": str(e)[:160]}
+        geng.close()
+        out["graph_replay_us"] = rows
 
     # ---- e2e through the public host API (H2D + allreduce + D2H) ------------
     if not args.no_e2e:

@@ -106,6 +106,14 @@ int nz_buffer_fill_zero(nz_buf_t* buf, void* stream);
 /* A rail owns a CUDA stream on this rank, its barrier pads and (CE) staging.
  * `sm_budget` caps the CTAs its kernels use (0 = all SMs). */
 int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rail_t** out);
+/* NZ_RAIL_FLAG_GRAPH_SAFE: the rail's kernels take their barrier epochs and
+ * LL flags from a device counter (advanced by the last CTA of each launch)
+ * instead of launch arguments, so its launches can be captured in a CUDA
+ * graph and replayed any number of times, mixed with eager calls. Collective
+ * (all ranks pass the same flags). Warm up once before capturing (the CE rail
+ * sizes its staging buffer on first use). */
+#define NZ_RAIL_FLAG_GRAPH_SAFE 1
+int nz_rail_create_ex(nz_comm_t* comm, int kind, int rail_id, int sm_budget, int flags, nz_rail_t** out);
 int nz_rail_destroy(nz_rail_t* rail);
 int nz_rail_kind(const nz_rail_t* rail);
 /* Blocks the host until all work enqueued on the rail's own streams is done. */
@@ -177,6 +185,9 @@ typedef struct {
   int pool_tokens;           /* ComputePool total_tokens; 0 = the GPU's SM count */
   int tune_budgets;          /* 1 (default): measure the NVLS / SM rails' CTA budget at
                                 startup for rails whose sm_budget is 0 */
+  int graph_safe;            /* 1: rails created with NZ_RAIL_FLAG_GRAPH_SAFE, so engine
+                                allreduces can be captured in CUDA graphs (captured
+                                ops are not Timer samples) */
 } nz_engine_config_t;
 
 void nz_engine_config_default(nz_engine_config_t* cfg);

@@ -97,6 +97,7 @@ class EngineConfig(ctypes.Structure):
         ("compute_pool", c_int),
         ("pool_tokens", c_int),
         ("tune_budgets", c_int),
+        ("graph_safe", c_int),
     ]
 
 
@@ -139,6 +140,7 @@ _SIGS = {
     "nz_buffer_read": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64, c_void_p]),
     "nz_buffer_fill_zero": (c_int, [c_void_p, c_void_p]),
     "nz_rail_create": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "nz_rail_create_ex": (c_int, [c_void_p, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
     "nz_rail_destroy": (c_int, [c_void_p]),
     "nz_rail_kind": (c_int, [c_void_p]),
     "nz_rail_stream": (c_void_p, [c_void_p]),

@@ -203,7 +203,17 @@ struct nz_engine {
   // One op (piece) of at most 1 GiB at byte offset `base`.
   void op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dtype, cudaStream_t user) {
     const uint32_t seq = op_seq++;
-    harvest(seq);
+    // Inside a CUDA graph capture (graph-safe rails only) nothing may wait on
+    // the device: no Timer harvest, no Timer sample, no failure injection.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    NZ_CUDA(cudaStreamIsCapturing(user, &cap));
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    if (capturing) {
+      if (!cfg.graph_safe) fail(NZ_ERR_INVALID, "graph capture needs an engine created with graph_safe = 1");
+      if (inject.count(seq)) fail(NZ_ERR_INVALID, "failure injection inside a graph capture");
+    } else {
+      harvest(seq);
+    }
     nezha::Plan plan = bal->allocate(len);
     const int world = comm->world;
     if (!plan.hot && inject.find(seq) == inject.end()) {
@@ -267,7 +277,12 @@ struct nz_engine {
     }
     for (auto& [id, e] : p.ends) NZ_CUDA(cudaStreamWaitEvent(user, e, 0));
     recycleGates();
-    pending.push_back(std::move(p));
+    if (capturing) {  // the captured records become graph edges: the events are free again
+      for (auto& [id, e] : p.ends) pool.push_back(e);
+      pool.push_back(p.start);
+    } else {
+      pending.push_back(std::move(p));
+    }
     recordPlan(seq, base, len, std::move(plan), std::move(grant_log));
   }
 
@@ -371,6 +386,13 @@ struct nz_engine {
   // last copy-out; nullptr (host variant): the caller synchronizes.
   void staged(const char* src, char* dst, uint64_t bytes, int dtype, cudaMemcpyKind kin, cudaMemcpyKind kout,
               cudaStream_t user) {
+    if (user) {
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      NZ_CUDA(cudaStreamIsCapturing(user, &cap));
+      if (cap != cudaStreamCaptureStatusNone) {
+        fail(NZ_ERR_INVALID, "staged allreduce cannot be captured: capture nz_engine_allreduce on symmetric buffers");
+      }
+    }
     ensureUnbound(bytes);
     nz_buf* in = ub_in;
     nz_buf* out = ub_out;
@@ -763,7 +785,8 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     NZ_CUDA(cudaSetDevice(comm->device));
     for (auto& s : eng->specs) {
       nz_rail_t* r = nullptr;
-      const int rc = nz_rail_create(comm, s.kind, s.rail_id, s.sm_budget, &r);
+      const int rc = nz_rail_create_ex(comm, s.kind, s.rail_id, s.sm_budget, c.graph_safe ? NZ_RAIL_FLAG_GRAPH_SAFE : 0,
+                                       &r);
       if (rc != NZ_OK) fail(rc, nz_last_error());
       eng->rails.push_back(r);
     }

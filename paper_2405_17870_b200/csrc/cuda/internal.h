@@ -120,6 +120,7 @@ struct nz_rail {
   nz_buf* ll = nullptr;     // SM: one-shot LL slots [parity][rank][slot_words] of {data, flag}
   uint64_t ll_slot_words = 0;
   uint32_t ll_flag = 0;
+  uint32_t* seq_dev = nullptr;  // graph-safe rails: device [op counter, CTAs retired]
   // C-ABI bookkeeping (nz_rail_inject_failure / _progress / _abort); the
   // engine drives rails through nz::railAllreduce and does not touch these.
   int64_t armed_fail = -1;      // failure armed for the next nz_rail_allreduce

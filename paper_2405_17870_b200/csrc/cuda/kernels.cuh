@@ -40,6 +40,7 @@ struct BarrierArgs {
   int* watchdog;  // host-mapped; set when a wait times out
   uint64_t timeout_ns;  // give up after this long (NEZHA_WATCHDOG_MS, default 20 s)
   int relaxed_poll;     // 1: poll ld.relaxed.sys, one fence.acq_rel.sys after (PTX acquire pattern)
+  uint32_t* seq;        // graph-safe rails: device [op counter, CTAs retired]; nullptr = host `epoch`
 };
 
 struct FaultPost {
@@ -104,6 +105,31 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
+
+// Graph-safe rails (NZ_RAIL_FLAG_GRAPH_SAFE) take their barrier epochs and
+// LL flags from a device counter instead of kernel arguments, so a launch
+// captured in a CUDA graph stays valid on every replay. Every CTA reads the
+// counter on entry; the last CTA to retire advances it. A rail's launches are
+// stream ordered, so the next one sees the advanced value.
+__device__ __forceinline__ uint32_t seq_read(const uint32_t* seq) {
+  return *reinterpret_cast<const volatile uint32_t*>(seq);
+}
+
+__device__ __forceinline__ void seq_retire(uint32_t* seq) {
+  if (!seq) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(seq + 1, 1u) == gridDim.x - 1) {
+      atomicExch(seq + 1, 0u);
+      atomicAdd(seq, 1u);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t op_epoch(const BarrierArgs& b) {
+  return b.seq ? 2u * seq_read(b.seq) + 1u : b.epoch;
+}
 
 // Per-CTA barrier across ranks. Returns false (and flags the watchdog) if a
 // peer never arrived, so the kernel can exit instead of hanging the GPU.
@@ -346,10 +372,12 @@ __device__ __forceinline__ void fold_shard(const FoldArgs& a) {
 
 template <typename DT, int N, int NDST>
 __global__ void __launch_bounds__(512, 2) fold_kernel(const __grid_constant__ FoldArgs a) {
-  if (a.use_barrier && !cta_barrier<N, false>(a.bar, a.bar.epoch, a.rank)) return;
+  const uint32_t ep = op_epoch(a.bar);
+  if (a.use_barrier && !cta_barrier<N, false>(a.bar, ep, a.rank)) return seq_retire(a.bar.seq);
   fold_shard<DT, N, NDST>(a);
-  if (a.use_barrier && !cta_barrier<N, true>(a.bar, a.bar.epoch + 1, a.rank)) return;
+  if (a.use_barrier && !cta_barrier<N, true>(a.bar, ep + 1, a.rank)) return seq_retire(a.bar.seq);
   post_fault(a.post);
+  seq_retire(a.bar.seq);
 }
 
 // ------------------------------------------------------------------ NVLS --
@@ -432,7 +460,8 @@ __device__ __forceinline__ void mm_st(char* p, uint4 v) {
 
 template <typename DT, int N, int U, bool WEAK>
 __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ NvlsArgs a) {
-  if (!cta_barrier<N, false>(a.f.bar, a.f.bar.epoch, a.f.rank)) return;
+  const uint32_t ep = op_epoch(a.f.bar);
+  if (!cta_barrier<N, false>(a.f.bar, ep, a.f.rank)) return seq_retire(a.f.bar.seq);
   const uint64_t vs = (a.f.s + 15) & ~15ull;
   const uint64_t ve = a.f.e & ~15ull;
   if (vs >= ve) {
@@ -456,8 +485,9 @@ __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ Nv
       }
     }
   }
-  if (!cta_barrier<N, true>(a.f.bar, a.f.bar.epoch + 1, a.f.rank)) return;
+  if (!cta_barrier<N, true>(a.f.bar, ep + 1, a.f.rank)) return seq_retire(a.f.bar.seq);
   post_fault(a.f.post);
+  seq_retire(a.f.bar.seq);
 }
 
 // --------------------------------------------------------- LL (one-shot) --
@@ -483,6 +513,7 @@ struct LLArgs {
   int* watchdog;
   uint64_t timeout_ns;
   FaultPost post;
+  uint32_t* seq;  // graph-safe rails: flag / parity from the device counter (see seq_retire)
 };
 
 __device__ __forceinline__ uint32_t ll_load_word(const char* base, uint64_t x, uint64_t hi) {
@@ -529,35 +560,44 @@ template <typename DT, int N, bool MC>
 __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs a) {
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const uint64_t my_slot = (static_cast<uint64_t>(a.parity) * N + a.rank) * a.slot_words;
+  uint32_t flag = a.flag;
+  int parity = a.parity;
+  if (a.seq) {
+    flag = seq_read(a.seq) + 1u;
+    if (flag == 0) flag = 1;  // 0 means "never written"
+    parity = static_cast<int>(flag & 1u);
+  }
+  const uint64_t my_slot = (static_cast<uint64_t>(parity) * N + a.rank) * a.slot_words;
   const uint64_t pairs = (a.words + 1) / 2;
   for (uint64_t p = tid; p < pairs; p += stride) {
     const uint64_t x = a.lo + 8 * p;
     const uint32_t d0 = ll_load_word(a.in, x, a.hi);
     const uint32_t d1 = x + 4 < a.hi ? ll_load_word(a.in, x + 4, a.hi) : 0u;
     if (MC) {
-      mm_st<false>(reinterpret_cast<char*>(a.mc + my_slot + 2 * p), make_uint4(d0, a.flag, d1, a.flag));
+      mm_st<false>(reinterpret_cast<char*>(a.mc + my_slot + 2 * p), make_uint4(d0, flag, d1, flag));
     } else {
 #pragma unroll
       for (int r = 0; r < N; ++r) {
         uint64_t* dst = a.peer[r] + my_slot + 2 * p;
-        asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(a.flag), "r"(d1),
-                     "r"(a.flag)
+        asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(flag), "r"(d1),
+                     "r"(flag)
                      : "memory");
       }
     }
   }
-  for (uint64_t w = tid; w < a.words; w += stride) {
+  bool bail = false;  // a peer's words never arrived (watchdog)
+  for (uint64_t w = tid; w < a.words && !bail; w += stride) {
     uint32_t v[N];
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      const uint64_t* src = a.local + (static_cast<uint64_t>(a.parity) * N + r) * a.slot_words + w;
-      uint32_t d, f;
+      if (bail) break;
+      const uint64_t* src = a.local + (static_cast<uint64_t>(parity) * N + r) * a.slot_words + w;
+      uint32_t d = 0, f;
       int spins = 0;
       uint64_t t0 = 0;
       for (;;) {
         asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(d), "=r"(f) : "l"(src) : "memory");
-        if (f == a.flag) break;
+        if (f == flag) break;
         if (++spins == 256) {
           spins = 0;
           const uint64_t now = globaltimer();
@@ -565,13 +605,20 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
             t0 = now;
           } else if (now - t0 > a.timeout_ns) {
             atomicExch_system(a.watchdog, 1);
-            return;
+            bail = true;
+            break;
           }
         }
       }
       v[r] = d;
     }
-    ll_fold_word<DT, N>(a, v, a.lo + 4 * w);
+    if (!bail) ll_fold_word<DT, N>(a, v, a.lo + 4 * w);
+  }
+  if (a.seq) {
+    seq_retire(a.seq);  // every thread gets here (no early return): the barrier inside is safe
+    if (bail) return;
+  } else if (bail) {
+    return;
   }
   post_fault(a.post);
 }
@@ -648,7 +695,8 @@ __global__ void __launch_bounds__(256, 1) sm_tma_kernel(const __grid_constant__ 
   unsigned char* outs = smem + static_cast<size_t>(kTmaStages) * N * kTmaTile;  // [stage][kTmaTile]
   uint64_t* bars = reinterpret_cast<uint64_t*>(outs + static_cast<size_t>(kTmaStages) * kTmaTile);
 
-  if (a.use_barrier && !cta_barrier<N, false>(a.bar, a.bar.epoch, a.rank)) return;
+  const uint32_t ep = op_epoch(a.bar);
+  if (a.use_barrier && !cta_barrier<N, false>(a.bar, ep, a.rank)) return seq_retire(a.bar.seq);
   const uint64_t vs = (a.s + 15) & ~15ull;
   const uint64_t ve = a.e & ~15ull;
   if (vs >= ve) {
@@ -688,7 +736,7 @@ __global__ void __launch_bounds__(256, 1) sm_tma_kernel(const __grid_constant__ 
       if (!__syncthreads_and(ok)) {
         if (leader && a.bar.watchdog) atomicExch_system(a.bar.watchdog, 1);
         if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        return;  // a tile never arrived: give up rather than hang
+        return seq_retire(a.bar.seq);  // a tile never arrived: give up rather than hang
       }
       const unsigned char* st = tiles + static_cast<size_t>(s) * N * kTmaTile;
       unsigned char* ot = outs + static_cast<size_t>(s) * kTmaTile;
@@ -728,8 +776,9 @@ __global__ void __launch_bounds__(256, 1) sm_tma_kernel(const __grid_constant__ 
       asm volatile("fence.proxy.async.global;" ::: "memory");   // ... and ordered before the release below
     }
   }
-  if (a.use_barrier && !cta_barrier<N, true>(a.bar, a.bar.epoch + 1, a.rank)) return;
+  if (a.use_barrier && !cta_barrier<N, true>(a.bar, ep + 1, a.rank)) return seq_retire(a.bar.seq);
   post_fault(a.post);
+  seq_retire(a.bar.seq);
 }
 
 // N = 1: the allreduce is the identity, i.e. a copy in -> out (HBM-bound).
@@ -770,8 +819,9 @@ __global__ void __launch_bounds__(512, 2) copy_kernel(const char* __restrict__ s
 // CE rail: start / end barriers around the DMA phases, and the fault post.
 template <int N>
 __global__ void barrier_kernel(const __grid_constant__ BarrierArgs b, int rank, FaultPost post) {
-  if (!cta_barrier<N, true>(b, b.epoch, rank)) return;
+  if (!cta_barrier<N, true>(b, op_epoch(b), rank)) return seq_retire(b.seq);
   post_fault(post);
+  seq_retire(b.seq);
 }
 
 }  // namespace nz

@@ -70,6 +70,7 @@ BarrierArgs barrierArgs(nz_rail* r, uint32_t epoch) {
   b.watchdog = r->wd_dev;
   b.timeout_ns = watchdogNs();
   b.relaxed_poll = barrierRelaxedPoll() ? 1 : 0;
+  b.seq = r->seq_dev;
   return b;
 }
 
@@ -332,6 +333,7 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.watchdog = r->wd_dev;
     a.timeout_ns = watchdogNs();
     a.post = post;
+    a.seq = r->seq_dev;
     gateEnter(gate, st);
     dispatchLL(N, dtype, mc_ll, a, gated(llGrid(r, lo, hi), gate), st);
     NZ_CUDA(cudaGetLastError());
@@ -520,8 +522,13 @@ int nz_has_cuda_kernels(void) { return 1; }
 uint64_t nz_kernel_launch_count(void) { return nz::g_launches.load(); }
 
 int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rail_t** out) {
+  return nz_rail_create_ex(comm, kind, rail_id, sm_budget, 0, out);
+}
+
+int nz_rail_create_ex(nz_comm_t* comm, int kind, int rail_id, int sm_budget, int flags, nz_rail_t** out) {
   return guarded([&] {
     if (!comm || !out) fail(NZ_ERR_INVALID, "null argument");
+    if (flags & ~NZ_RAIL_FLAG_GRAPH_SAFE) fail(NZ_ERR_INVALID, "unknown rail flags");
     if (kind < NZ_RAIL_NVLS || kind > NZ_RAIL_SM) fail(NZ_ERR_INVALID, "unknown rail kind");
     if (kind == NZ_RAIL_NVLS && comm->world > 1 && !comm->multicast) {
       fail(NZ_ERR_UNSUPPORTED, "NVLS rail requires NVSwitch multicast support");
@@ -532,6 +539,10 @@ int nz_rail_create(nz_comm_t* comm, int kind, int rail_id, int sm_budget, nz_rai
     r->comm = comm;
     r->kind = kind;
     r->rail_id = rail_id;
+    if (flags & NZ_RAIL_FLAG_GRAPH_SAFE) {  // device op counter (kernels.cuh seq_retire), zero on every rank
+      NZ_CUDA(cudaMalloc(&r->seq_dev, 2 * sizeof(uint32_t)));
+      NZ_CUDA(cudaMemset(r->seq_dev, 0, 2 * sizeof(uint32_t)));
+    }
     r->sm_budget = sm_budget;
     const size_t pad_off = nz::kPadBytes * comm->next_pad++;
     r->pad_local = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[comm->rank] + pad_off);
@@ -581,6 +592,7 @@ int nz_rail_destroy(nz_rail_t* r) {
     if (r->fault_host) cudaFreeHost(r->fault_host);
     if (r->wd_host) cudaFreeHost(r->wd_host);
     if (r->done) cudaEventDestroy(r->done);
+    if (r->seq_dev) cudaFree(r->seq_dev);
     delete r;
   });
 }

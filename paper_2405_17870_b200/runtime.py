@@ -114,9 +114,10 @@ class SymmetricBuffer:
 class Rail:
     """One rail's executor on this rank (nz_rail_create)."""
 
-    def __init__(self, comm: Comm, kind: int, rail_id: int, sm_budget: int = 0):
+    def __init__(self, comm: Comm, kind: int, rail_id: int, sm_budget: int = 0, graph_safe: bool = False):
         h = c_void_p()
-        check(lib().nz_rail_create(comm.handle, kind, rail_id, sm_budget, byref(h)), "nz_rail_create")
+        check(lib().nz_rail_create_ex(comm.handle, kind, rail_id, sm_budget, 1 if graph_safe else 0, byref(h)),
+              "nz_rail_create_ex")
         self.handle = h
         self.kind = kind
         self.rail_id = rail_id

@@ -107,6 +107,20 @@ def test_engine_compute_pool_parity(mode):
 
 
 @pytest.mark.multigpu
+def test_engine_graph_capture():
+    """graph_safe engine (device op counters in the rails): allreduces captured
+    in a CUDA graph and replayed give the oracle's result on every plan kind."""
+    if gpu_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4, "graph_safe": 1,
+            "cases": [{"dtype": "f32", "nbytes": 64 << 20, "reps": 8},     # converges to a hot split
+                      {"dtype": "f32", "nbytes": 64 << 20, "reps": 1, "graph": 3},
+                      {"dtype": "bf16", "nbytes": 8192, "reps": 1, "graph": 4},
+                      {"dtype": "i32", "nbytes": 3 << 20, "reps": 1, "graph": 2}]}
+    _run(2, spec, timeout=420)
+
+
+@pytest.mark.multigpu
 def test_engine_oversized_split():
     """Payloads above 1 GiB run as 256 MiB pieces."""
     if gpu_count() < 2:

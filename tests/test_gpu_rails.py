@@ -136,6 +136,11 @@ MULTI = [
     {"kind": "sm", "dtype": "f32", "nbytes": 32 << 20, "fail_chunk": 3, "armed": True},  # nz_rail_inject_failure
     {"kind": "ce", "dtype": "f32", "nbytes": 4 << 20, "fail_chunk": 1, "armed": True},
     {"kind": "sm", "dtype": "f32", "nbytes": 4096, "abort": True},  # nz_rail_abort: later calls refused
+    # Graph-safe rails (device op counter): captured ops replayed, mixed with eager ones.
+    {"kind": "sm", "dtype": "f32", "nbytes": 8192, "graph": 3},             # LL path
+    {"kind": "sm", "dtype": "bf16", "nbytes": 8 << 20, "graph": 2},         # two-shot fold
+    {"kind": "nvls", "dtype": "f32", "nbytes": 16 << 20, "graph": 2},
+    {"kind": "ce", "dtype": "i32", "nbytes": 4 << 20, "graph": 2},
 ]
 
 
@@ -154,6 +159,8 @@ def test_multi_gpu_rails(world):
             case = MULTI[r["case"]]
             if case.get("abort"):
                 assert r["abort_refused"], r
+            if case.get("graph"):
+                assert r["graph_mismatch"] == 0, r
             if case.get("fail_chunk", -1) >= 0:
                 assert r["fault"] is not None and r["fault"]["chunk"] == case["fail_chunk"], r
             else:

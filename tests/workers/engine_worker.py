@@ -55,7 +55,8 @@ def main():
     rank, world = comm.rank, comm.world
     kinds = spec["rails"]
     over = {"kinds": kinds}
-    for k in ("window", "eta", "demote_after", "calibrate_max_bytes", "calibrate_iters", "compute_pool", "pool_tokens"):
+    for k in ("window", "eta", "demote_after", "calibrate_max_bytes", "calibrate_iters", "compute_pool", "pool_tokens",
+              "graph_safe"):
         if k in spec:
             over[k] = spec[k]
     if "rails_toml" in spec:
@@ -74,6 +75,25 @@ def main():
             got = np.zeros(n // ES[dt], dtype=oracle.NP_DTYPE[dt])
             if c.get("host"):
                 eng.allreduce_host(inputs[rank], got, n, dt)
+            elif c.get("graph"):  # graph-safe engine: capture `graph` allreduces, replay, check
+                import torch
+                torch.cuda.set_device(comm.device)
+                bin_.write(inputs[rank], n)
+                comm.barrier()
+                eng.allreduce(bin_, bout, n, dt)  # eager warm-up (sizes CE staging)
+                eng.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+                    for _ in range(c["graph"]):
+                        eng.allreduce(bin_, bout, n, dt, torch.cuda.current_stream())
+                bout.zero()
+                torch.cuda.synchronize()
+                comm.barrier()
+                g.replay()
+                g.replay()
+                torch.cuda.synchronize()
+                eng.synchronize()
+                bout.read(got, n)
             elif c.get("device"):  # caller-owned device memory, in place (nz_engine_allreduce_device)
                 import torch
                 torch.cuda.set_device(comm.device)

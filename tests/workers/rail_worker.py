@@ -52,9 +52,9 @@ def main():
     results = []
     for ci, c in enumerate(cases):
         kind = c["kind"]
-        key = (kind, c.get("sm_budget", 0))
+        key = (kind, c.get("sm_budget", 0), bool(c.get("graph")))
         if key not in rails:
-            rails[key] = Rail(comm, RAIL_KINDS[kind], len(rails), c.get("sm_budget", 0))
+            rails[key] = Rail(comm, RAIL_KINDS[kind], len(rails), c.get("sm_budget", 0), graph_safe=bool(c.get("graph")))
         rail = rails[key]
         dt = DTYPES[c["dtype"]]
         es = 2 if dt == oracle.BF16 else 4
@@ -97,6 +97,33 @@ def main():
             res["outside_nonzero"] = int(np.count_nonzero(outside))
         rec = rail.poll_fault()
         res["fault"] = None if rec is None else {"op_seq": rec.op_seq, "chunk": rec.chunk}
+        if c.get("graph") and check:
+            # Graph-safe rail: capture `graph` ops (the eager op above was the
+            # warm-up), replay three times, then one more eager op; every
+            # result must equal the oracle.
+            import torch
+            torch.cuda.set_device(comm.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=torch.cuda.Stream()):
+                for _ in range(c["graph"]):
+                    rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce,
+                                   stream=torch.cuda.current_stream())
+            bad = 0
+            for rep in range(4):
+                bout.zero()
+                torch.cuda.synchronize()
+                comm.barrier()
+                if rep < 3:
+                    g.replay()
+                else:
+                    rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce)
+                    rail.synchronize()
+                torch.cuda.synchronize()
+                got = np.zeros(nbytes // es, dtype=oracle.NP_DTYPE[dt])
+                bout.read(got, nbytes)
+                bad += compare(kind, dt, got, want, inputs, lo, hi, es)["mismatch"]
+            res["graph_mismatch"] = bad
+            res["watchdog"] = max(res["watchdog"], rail.watchdog())
         iters = c.get("iters", 0)
         if iters:
             import torch
