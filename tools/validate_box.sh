@@ -19,7 +19,7 @@ step() {  # step NAME SECONDS CMD...
 nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/val_gpus.csv 2>&1
 step build 300 "python -c 'import __graft_entry__ as g; g.build()'"
 step smoke 300 "python -c 'import __graft_entry__ as g; g.smoke()'"
-step pytest_gpu 1500 "python -m pytest tests -m gpu -x -q -p no:cacheprovider"
+step pytest_gpu 2400 "python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 -rfE"
 step ddp 300 "python tools/run_spawn.py 2 tools/debug_ddp.py"
 step bench1 600 "python bench.py --steps 5 --warmup 3"
 step copy_plain 300 "python tools/ncu_copy_n1.py" && \
