@@ -121,6 +121,8 @@ struct nz_rail {
   uint64_t ll_slot_words = 0;
   uint32_t ll_flag = 0;
   uint32_t* seq_dev = nullptr;  // graph-safe rails: device [op counter, CTAs retired]
+  nz_buf* os = nullptr;         // SM one-shot staging [parity 2][rank N][os_slot bytes] (NEZHA_SM_ONESHOT)
+  uint64_t os_slot = 0;
   // C-ABI bookkeeping (nz_rail_inject_failure / _progress / _abort); the
   // engine drives rails through nz::railAllreduce and does not touch these.
   int64_t armed_fail = -1;      // failure armed for the next nz_rail_allreduce

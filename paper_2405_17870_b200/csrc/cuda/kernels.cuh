@@ -623,6 +623,76 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
   post_fault(a.post);
 }
 
+// ------------------------------------------------- SM rail, one-shot ------
+// K7: mid-size payloads on the SM rail. Every rank pushes its whole range
+// into slot [parity][rank] of every peer's staging buffer, one per-CTA
+// barrier publishes the pushes, then every rank folds all N copies locally in
+// P1 order (its own from `in`) into its own `out`. One barrier instead of the
+// two-shot's two, (N-1)·L wire bytes instead of 2(N-1)/N·L: it wins where
+// latency dominates. CTA c pushes exactly the bytes it later folds (same
+// partition as fold_shard over [lo, hi)), so its own barrier slot suffices.
+// Parity alternates with the epoch; a rank can only reuse a parity after an
+// op every rank joined, i.e. after every rank finished reading it.
+struct OneShotArgs {
+  const char* in;
+  char* stg_peer[kDevMaxRanks];  // rank p's staging buffer (where I push)
+  uint64_t lo, hi;               // reduced byte range
+  uint64_t lo16;                 // lo rounded down to 16: slot offset 0
+  uint64_t slot_bytes;
+  BarrierArgs bar;
+  int rank;
+  FaultPost post;
+  FoldArgs f[2];  // the local fold per staging parity (sources: my `in` + my staging slots), built on the host
+};
+
+template <int N, int ES>
+__device__ __forceinline__ void oneshot_push_scalar(const OneShotArgs& a, uint64_t off, uint64_t x) {
+  if (ES == 4) {
+    const uint32_t v = *reinterpret_cast<const uint32_t*>(a.in + x);
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+      if (r != a.rank) *reinterpret_cast<uint32_t*>(a.stg_peer[r] + off + (x - a.lo16)) = v;
+  } else {
+    const unsigned short v = *reinterpret_cast<const unsigned short*>(a.in + x);
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+      if (r != a.rank) *reinterpret_cast<unsigned short*>(a.stg_peer[r] + off + (x - a.lo16)) = v;
+  }
+}
+
+template <typename DT, int N>
+__global__ void __launch_bounds__(512, 2) oneshot_kernel(const __grid_constant__ OneShotArgs a) {
+  const uint32_t ep = op_epoch(a.bar);
+  const int parity = static_cast<int>((ep >> 1) & 1u);
+  const uint64_t off = (static_cast<uint64_t>(parity) * N + a.rank) * a.slot_bytes;  // my slot in every peer
+  // Push: the same element / vector partition fold_shard uses below.
+  const uint64_t vs = (a.lo + 15) & ~15ull;
+  const uint64_t ve = a.hi & ~15ull;
+  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * blockDim.x * DT::kElem;
+  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (vs >= ve) {
+    for (uint64_t x = a.lo + gtid * DT::kElem; x < a.hi; x += gstride) oneshot_push_scalar<N, DT::kElem>(a, off, x);
+  } else {
+    for (uint64_t x = a.lo + gtid * DT::kElem; x < vs; x += gstride) oneshot_push_scalar<N, DT::kElem>(a, off, x);
+    for (uint64_t x = ve + gtid * DT::kElem; x < a.hi; x += gstride) oneshot_push_scalar<N, DT::kElem>(a, off, x);
+    const uint64_t nvec = (ve - vs) / 16;
+    const uint64_t cb = vs + 16 * (nvec * blockIdx.x / gridDim.x);
+    const uint64_t ce = vs + 16 * (nvec * (blockIdx.x + 1) / gridDim.x);
+    for (uint64_t x = cb + threadIdx.x * 16ull; x < ce; x += static_cast<uint64_t>(blockDim.x) * 16) {
+      const uint4 v = ld_v4(a.in + x);
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+        if (r != a.rank) st_v4(a.stg_peer[r] + off + (x - a.lo16), v);
+    }
+  }
+  if (!cta_barrier<N, true>(a.bar, ep, a.rank)) return seq_retire(a.bar.seq);
+  // Fold every rank's copy of this CTA's part, P1 order, into my `out`
+  // (param-space FoldArgs: no local-memory copy).
+  fold_shard<DT, N, 1>(a.f[parity]);
+  post_fault(a.post);
+  seq_retire(a.bar.seq);
+}
+
 // ------------------------------------------------- SM rail, TMA pipeline --
 // K3t: the SM rail's two-shot fold with the peer traffic moved by the Tensor
 // Memory Accelerator. One elected thread streams 1-D bulk tiles of the shard

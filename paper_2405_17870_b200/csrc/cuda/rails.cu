@@ -156,7 +156,14 @@ constexpr uint64_t kLLMaxBytes = 2048 * 1024;  // SM rail one-shot LL path up to
 // N = 4 it is 9.1 us at 256 KiB but 24.8 us at 1 MiB vs 20 us two-shot.
 uint64_t llMaxBytes(int world, bool mc) {
   const uint64_t cap = mc ? (uint64_t{512} << 10) : kLLMaxBytes;
-  return std::min<uint64_t>(cap, (uint64_t{4} << 20) / world);
+  // NEZHA_LL_MAX (bytes) lowers the ceiling for sweeps; it never raises it
+  // (the LL buffers are sized by this function at rail creation).
+  static const long long env = [] {
+    const char* e = getenv("NEZHA_LL_MAX");
+    return e ? atoll(e) : -1LL;
+  }();
+  const uint64_t def = std::min<uint64_t>(cap, (uint64_t{4} << 20) / world);
+  return env >= 0 ? std::min<uint64_t>(def, static_cast<uint64_t>(env)) : def;
 }
 
 template <int N, bool MC>
@@ -267,6 +274,48 @@ bool nvlsLLEnabled() {
   return on;
 }
 
+// SM-rail one-shot (K7) for payloads between the LL ceiling and
+// min(4 MiB, 8 MiB / N): opt-in with NEZHA_SM_ONESHOT=1 until its sweep is in
+// profiles/. NEZHA_SM_ONESHOT_MAX overrides the ceiling (bytes).
+bool oneshotEnabled() {
+  static const bool on = [] {
+    const char* e = getenv("NEZHA_SM_ONESHOT");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
+uint64_t oneshotMaxBytes(int world) {
+  static const long long env = [] {
+    const char* e = getenv("NEZHA_SM_ONESHOT_MAX");
+    return e ? atoll(e) : 0LL;
+  }();
+  const uint64_t def = std::min<uint64_t>(uint64_t{4} << 20, (uint64_t{8} << 20) / world);
+  return env > 0 ? std::min<uint64_t>(static_cast<uint64_t>(env), uint64_t{16} << 20) : def;
+}
+
+bool oneshotPath(nz_rail* r, uint64_t lo, uint64_t hi) {
+  return r->comm->world > 1 && r->kind == NZ_RAIL_SM && r->os && hi > lo && hi - (lo & ~15ull) <= r->os_slot;
+}
+
+int oneshotGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
+  const int budget = std::min(r->sm_budget > 0 ? r->sm_budget : 64, r->comm->sm_count);
+  const uint64_t vec = (hi - lo) / 16 + 1;
+  const uint64_t g = (vec + 2 * kThreads - 1) / (2 * kThreads);
+  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, std::min(budget, kMaxCtas))));
+}
+
+template <typename DT>
+void launchOneshotDT(int world, const OneShotArgs& a, int grid, cudaStream_t st) {
+  switch (world) {
+#define NZ_CASE(n) \
+  case n: oneshot_kernel<DT, n><<<grid, kThreads, 0, st>>>(a); break;
+    NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
+#undef NZ_CASE
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
 bool llPath(nz_rail* r, uint64_t lo, uint64_t hi) {
   const int N = r->comm->world;
   const bool mc_ll = r->kind == NZ_RAIL_NVLS;
@@ -336,6 +385,40 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.seq = r->seq_dev;
     gateEnter(gate, st);
     dispatchLL(N, dtype, mc_ll, a, gated(llGrid(r, lo, hi), gate), st);
+    NZ_CUDA(cudaGetLastError());
+    gateExit(gate, st);
+    return;
+  }
+
+  if (oneshotPath(r, lo, hi)) {
+    OneShotArgs a{};
+    a.in = in->ptrs[me];
+    for (int p = 0; p < N; ++p) a.stg_peer[p] = r->os->ptrs[p];
+    a.lo = lo;
+    a.hi = hi;
+    a.lo16 = lo & ~15ull;
+    a.slot_bytes = r->os_slot;
+    a.bar = barrierArgs(r, epoch);
+    a.rank = me;
+    a.post = post;
+    for (int par = 0; par < 2; ++par) {
+      FoldArgs& f = a.f[par];
+      for (int p = 0; p < N; ++p) {
+        f.src[p] = p == me ? in->ptrs[me]
+                           : r->os->ptrs[me] + (static_cast<uint64_t>(par) * N + p) * r->os_slot - a.lo16;
+      }
+      f.dst[0] = out->ptrs[me];
+      f.s = lo;
+      f.e = hi;
+      f.range_bytes = hi - lo;
+      f.g = g;
+      f.rank = me;
+    }
+    gateEnter(gate, st);
+    const int grid = gated(oneshotGrid(r, lo, hi), gate);
+    if (dtype == NZ_F32) launchOneshotDT<F32>(N, a, grid, st);
+    else if (dtype == NZ_BF16) launchOneshotDT<BF16>(N, a, grid, st);
+    else launchOneshotDT<I32>(N, a, grid, st);
     NZ_CUDA(cudaGetLastError());
     gateExit(gate, st);
     return;
@@ -505,6 +588,7 @@ void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64
 int railComputeCtas(nz_rail* r, uint64_t seg_len) {
   if (seg_len == 0) return 0;
   if (llPath(r, 0, seg_len)) return llGrid(r, 0, seg_len);
+  if (oneshotPath(r, 0, seg_len)) return oneshotGrid(r, 0, seg_len);
   if (r->comm->world == 1) return copyGrid(r, 0, seg_len);
   if (r->kind == NZ_RAIL_SM) return smGrid(r, 0, seg_len);
   return gridFor(r, seg_len, r->comm->world, r->kind == NZ_RAIL_NVLS ? 4 : 2);
@@ -558,6 +642,10 @@ int nz_rail_create_ex(nz_comm_t* comm, int kind, int rail_id, int sm_budget, int
       NZ_CUDA(cudaDeviceSynchronize());
       nz::exchange(comm, nullptr, 0, {});
     }
+    if (kind == NZ_RAIL_SM && comm->world > 1 && nz::oneshotEnabled()) {
+      r->os_slot = (nz::oneshotMaxBytes(comm->world) + 16 + 255) & ~uint64_t{255};
+      r->os = nz::allocSymmetric(comm, 2 * comm->world * r->os_slot);
+    }
     if (kind == NZ_RAIL_CE) {
       for (int j = 1; j < comm->world; ++j) {
         cudaStream_t s;
@@ -593,6 +681,7 @@ int nz_rail_destroy(nz_rail_t* r) {
     if (r->wd_host) cudaFreeHost(r->wd_host);
     if (r->done) cudaEventDestroy(r->done);
     if (r->seq_dev) cudaFree(r->seq_dev);
+    if (r->os) nz::freeSymmetric(r->os);
     delete r;
   });
 }

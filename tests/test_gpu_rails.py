@@ -167,6 +167,36 @@ def test_multi_gpu_rails(world):
                 assert r["fault"] is None, r
 
 
+ONESHOT = [  # SM one-shot (K7) between the LL ceiling and NEZHA_SM_ONESHOT_MAX, mixed with LL and two-shot ops
+    {"kind": "sm", "dtype": "f32", "nbytes": 3 << 20},
+    {"kind": "sm", "dtype": "bf16", "nbytes": 5_000_002, "seg_off": 2, "seg_len": 5_000_000},
+    {"kind": "sm", "dtype": "f32", "nbytes": 8192},                       # LL in between
+    {"kind": "sm", "dtype": "i32", "nbytes": 6 << 20},
+    {"kind": "sm", "dtype": "f32", "nbytes": 4 << 20, "seg_off": 1 << 20, "seg_len": 3_000_004},
+    {"kind": "sm", "dtype": "f32", "nbytes": 16 << 20},                   # two-shot in between
+    {"kind": "sm", "dtype": "f32", "nbytes": 3 << 20, "fail_chunk": 2},
+    {"kind": "sm", "dtype": "bf16", "nbytes": 4 << 20, "chunk_begin": 1, "chunk_end": 3},
+    {"kind": "sm", "dtype": "f32", "nbytes": 3 << 20, "graph": 2},
+]
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_sm_oneshot(world):
+    """The SM rail's one-shot path (NEZHA_SM_ONESHOT=1): bit-exact to the oracle."""
+    if gpu_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(ONESHOT)], timeout=300,
+                extra_env={"NEZHA_SM_ONESHOT": "1", "NEZHA_SM_ONESHOT_MAX": str(8 << 20)})
+    for rank_res in res:
+        for r in rank_res["results"]:
+            case = ONESHOT[r["case"]]
+            assert r["watchdog"] == 0 and r["mismatch"] == 0 and r["outside_nonzero"] == 0, r
+            assert r.get("graph_mismatch", 0) == 0, r
+            if case.get("fail_chunk", -1) >= 0:
+                assert r["fault"] is not None and r["fault"]["chunk"] == case["fail_chunk"], r
+
+
 @pytest.mark.multigpu
 def test_multi_gpu_nvls_ll_opt_in():
     """NVLS-LL (multicast push one-shot) is opt-in (NEZHA_NVLS_LL=1, rails.cu);

@@ -28,6 +28,9 @@ if [ "$(nvidia-smi -L | wc -l)" -ge 2 ]; then
   step bench2 900 "python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3"
   step bench2x 900 "python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29518 bench.py --gpus 2 --steps 5 --warmup 3 --graph --nccl-graph --nccl-algos --no-failover --no-e2e"
   step train2 900 "python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29519 tools/ddp_train_bench.py resnet50,bert 20"
+  for v in "" "NEZHA_LL_MAX=0" "NEZHA_LL_MAX=0 NEZHA_SM_ONESHOT=1 NEZHA_SM_ONESHOT_MAX=8388608"; do
+    step "smpaths_${#v}" 400 "$v python tools/rail_perf.py 2 sm 65536,262144,1048576,2097152,4194304,8388608"
+  done
   for p in acquire relaxed; do
     step barrier_$p 400 "NEZHA_BARRIER_POLL=$p python tools/rail_perf.py 2 nvls,sm,ce 8192,1048576,16777216,268435456"
   done
