@@ -519,6 +519,67 @@ struct nz_engine {
     }
   }
 
+  // Which protocol a rail uses at which size, measured instead of assumed:
+  // for rails with more than one path (SM: one-shot LL, optional one-shot
+  // staging, two-shot) every path is timed at sizes 64 KiB .. 4 MiB, ranks
+  // agree on the times (max), and each ceiling becomes the largest size of
+  // the contiguous run of sizes where that path was fastest. Per rail, the
+  // same on every rank; the startup profiles are then measured with it.
+  void tunePaths(uint64_t maxb, cudaEvent_t e0, cudaEvent_t e1) {
+    if (comm->world == 1) return;
+    for (size_t i = 0; i < rails.size(); ++i) {
+      nz_rail* r = rails[i];
+      if (r->ll_cap == 0 && r->os_cap == 0) continue;
+      std::vector<uint64_t> sizes;
+      for (uint64_t sz = 64 << 10; sz <= std::min<uint64_t>(uint64_t{4} << 20, maxb); sz *= 2) sizes.push_back(sz);
+      if (sizes.empty()) continue;
+      // times[k][v]: v = 0 LL, 1 one-shot, 2 two-shot; huge when not applicable.
+      std::vector<double> t(sizes.size() * 3, 1e30);
+      for (size_t k = 0; k < sizes.size(); ++k) {
+        const uint64_t s = sizes[k];
+        const uint64_t C = nezha::defaultChunkBytes(s, comm->world, algo);
+        for (int v = 0; v < 3; ++v) {
+          if ((v == 0 && s > r->ll_cap) || (v == 1 && s > r->os_cap)) continue;
+          r->ll_max = v == 0 ? r->ll_cap : 0;
+          r->os_max = v == 1 ? r->os_cap : 0;
+          for (int w = 0; w < 3; ++w) nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
+          NZ_CUDA(cudaEventRecord(e0, r->stream));
+          for (int it = 0; it < 20; ++it) nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
+          NZ_CUDA(cudaEventRecord(e1, r->stream));
+          NZ_CUDA(cudaEventSynchronize(e1));
+          float ms = 0;
+          NZ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+          t[k * 3 + v] = ms;
+        }
+      }
+      const auto msgs = nz::exchange(comm, t.data(), t.size() * sizeof(double), {});
+      for (int rk = 0; rk < comm->world; ++rk) {
+        const double* v = reinterpret_cast<const double*>(msgs[rk].data.data());
+        for (size_t j = 0; j < t.size(); ++j) t[j] = std::max(t[j], v[j]);
+      }
+      auto best = [&](size_t k) {
+        int b = 2;
+        for (int v = 0; v < 2; ++v)
+          if (t[k * 3 + v] < t[k * 3 + b]) b = v;
+        return b;
+      };
+      uint64_t ll_max = 0, os_max = 0;
+      size_t k = 0;
+      if (r->ll_cap) {
+        ll_max = std::min<uint64_t>(r->ll_cap, sizes[0] / 2);  // below the sweep: LL as before
+        for (; k < sizes.size() && best(k) == 0; ++k) ll_max = sizes[k];
+        if (k == sizes.size()) ll_max = r->ll_cap;  // LL won everywhere measured: keep its full range
+      }
+      if (r->os_cap) {
+        os_max = ll_max;
+        for (; k < sizes.size() && best(k) == 1; ++k) os_max = sizes[k];
+        if (k == sizes.size()) os_max = std::max(os_max, r->os_cap);
+      }
+      r->ll_max = ll_max;
+      r->os_max = os_max;
+    }
+  }
+
   void calibrate() {
     const uint64_t maxb = std::max<uint64_t>(cfg.calibrate_max_bytes, 1 << 16);
     ensureUnbound(maxb);
@@ -526,7 +587,10 @@ struct nz_engine {
     std::vector<uint64_t> sizes;
     for (uint64_t s = 4096; s <= maxb; s *= 4) sizes.push_back(s);
     cudaEvent_t e0 = event(), e1 = event();
-    if (cfg.tune_budgets) tuneBudgets(maxb, e0, e1);
+    if (cfg.tune_budgets) {
+      tuneBudgets(maxb, e0, e1);
+      tunePaths(maxb, e0, e1);
+    }
     std::vector<nezha::RailProfile> profiles;
     bool measured_any = false;
     for (size_t i = 0; i < specs.size(); ++i) {
@@ -686,7 +750,8 @@ struct nz_engine {
       const auto& p = bal->rails()[i];
       o << (i ? "," : "") << "{\"rail_id\":" << specs[i].rail_id << ",\"kind\":\""
         << (specs[i].kind == NZ_RAIL_NVLS ? "nvls" : specs[i].kind == NZ_RAIL_CE ? "ce" : "sm")
-        << "\",\"sm_budget\":" << rails[i]->sm_budget << ",\"protocol\":\"" << nezha::toString(p.protocol) << "\",\"health\":\""
+        << "\",\"sm_budget\":" << rails[i]->sm_budget << ",\"ll_max\":" << rails[i]->ll_max
+        << ",\"oneshot_max\":" << rails[i]->os_max << ",\"protocol\":\"" << nezha::toString(p.protocol) << "\",\"health\":\""
         << nezha::toString(health->state(specs[i].rail_id).status) << "\",\"t_setup_us\":"
         << nezha::formatDouble(p.t_setup_us) << ",\"bandwidth_bps\":" << nezha::formatDouble(p.bandwidth_bps)
         << ",\"calibration\":[";

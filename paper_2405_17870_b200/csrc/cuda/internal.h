@@ -123,6 +123,13 @@ struct nz_rail {
   uint32_t* seq_dev = nullptr;  // graph-safe rails: device [op counter, CTAs retired]
   nz_buf* os = nullptr;         // SM one-shot staging [parity 2][rank N][os_slot bytes] (NEZHA_SM_ONESHOT)
   uint64_t os_slot = 0;
+  // Path ceilings (bytes): LL up to ll_max, one-shot up to os_max, two-shot
+  // above. Set to the buffer capacities at creation; the engine re-measures
+  // the crossovers at startup (same on every rank).
+  uint64_t ll_max = 0;
+  uint64_t os_max = 0;
+  uint64_t ll_cap = 0;
+  uint64_t os_cap = 0;
   // C-ABI bookkeeping (nz_rail_inject_failure / _progress / _abort); the
   // engine drives rails through nz::railAllreduce and does not touch these.
   int64_t armed_fail = -1;      // failure armed for the next nz_rail_allreduce

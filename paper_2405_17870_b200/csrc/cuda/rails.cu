@@ -295,7 +295,8 @@ uint64_t oneshotMaxBytes(int world) {
 }
 
 bool oneshotPath(nz_rail* r, uint64_t lo, uint64_t hi) {
-  return r->comm->world > 1 && r->kind == NZ_RAIL_SM && r->os && hi > lo && hi - (lo & ~15ull) <= r->os_slot;
+  return r->comm->world > 1 && r->kind == NZ_RAIL_SM && r->os && hi > lo && hi - lo <= r->os_max &&
+         hi - (lo & ~15ull) <= r->os_slot;
 }
 
 int oneshotGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
@@ -319,7 +320,7 @@ void launchOneshotDT(int world, const OneShotArgs& a, int grid, cudaStream_t st)
 bool llPath(nz_rail* r, uint64_t lo, uint64_t hi) {
   const int N = r->comm->world;
   const bool mc_ll = r->kind == NZ_RAIL_NVLS;
-  return N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= llMaxBytes(N, mc_ll) && lo % 4 == 0 &&
+  return N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= r->ll_max && lo % 4 == 0 &&
          (!mc_ll || r->ll->mc_ptr);
 }
 
@@ -638,6 +639,7 @@ int nz_rail_create_ex(nz_comm_t* comm, int kind, int rail_id, int sm_budget, int
       // Even word count: every slot starts 16-byte aligned for the v4 pushes.
       r->ll_slot_words = ((nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS) + 7) / 4 + 1) & ~uint64_t{1};
       r->ll = nz::allocSymmetric(comm, 2 * comm->world * r->ll_slot_words * sizeof(uint64_t));
+      r->ll_cap = r->ll_max = nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS);
       NZ_CUDA(cudaMemset(r->ll->ptrs[comm->rank], 0, r->ll->mapped));
       NZ_CUDA(cudaDeviceSynchronize());
       nz::exchange(comm, nullptr, 0, {});
@@ -645,6 +647,7 @@ int nz_rail_create_ex(nz_comm_t* comm, int kind, int rail_id, int sm_budget, int
     if (kind == NZ_RAIL_SM && comm->world > 1 && nz::oneshotEnabled()) {
       r->os_slot = (nz::oneshotMaxBytes(comm->world) + 16 + 255) & ~uint64_t{255};
       r->os = nz::allocSymmetric(comm, 2 * comm->world * r->os_slot);
+      r->os_cap = r->os_max = nz::oneshotMaxBytes(comm->world);
     }
     if (kind == NZ_RAIL_CE) {
       for (int j = 1; j < comm->world; ++j) {
