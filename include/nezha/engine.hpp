@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "nezha/balancer.hpp"
@@ -37,5 +38,15 @@ struct RailSpec {
 // calibration = [[size, latency_us], ...] / sm_budget. protocol maps
 // sharp|nvls -> NVLS, glex|ce -> CE, tcp|sm -> SM.
 std::vector<RailSpec> parseRailsToml(const std::string& text);
+
+// Protocol ceilings of one rail from a startup sweep (engine tunePaths):
+// times[3k + v] is the (rank-agreed) time of path v at sizes[k] (v = 0 LL,
+// 1 staged one-shot, 2 two-shot; >= 1e30 = not applicable), sizes ascending.
+// LL keeps the contiguous run of sizes it won from the smallest (its full
+// capacity if it won all, half the smallest size if it won none); one-shot
+// the run right after it. Returns {ll_max, oneshot_max}.
+std::pair<std::uint64_t, std::uint64_t> choosePathCeilings(const std::vector<std::uint64_t>& sizes,
+                                                           const std::vector<double>& times, std::uint64_t ll_cap,
+                                                           std::uint64_t os_cap);
 
 }  // namespace nezha

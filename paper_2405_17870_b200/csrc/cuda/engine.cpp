@@ -557,24 +557,7 @@ struct nz_engine {
         const double* v = reinterpret_cast<const double*>(msgs[rk].data.data());
         for (size_t j = 0; j < t.size(); ++j) t[j] = std::max(t[j], v[j]);
       }
-      auto best = [&](size_t k) {
-        int b = 2;
-        for (int v = 0; v < 2; ++v)
-          if (t[k * 3 + v] < t[k * 3 + b]) b = v;
-        return b;
-      };
-      uint64_t ll_max = 0, os_max = 0;
-      size_t k = 0;
-      if (r->ll_cap) {
-        ll_max = std::min<uint64_t>(r->ll_cap, sizes[0] / 2);  // below the sweep: LL as before
-        for (; k < sizes.size() && best(k) == 0; ++k) ll_max = sizes[k];
-        if (k == sizes.size()) ll_max = r->ll_cap;  // LL won everywhere measured: keep its full range
-      }
-      if (r->os_cap) {
-        os_max = ll_max;
-        for (; k < sizes.size() && best(k) == 1; ++k) os_max = sizes[k];
-        if (k == sizes.size()) os_max = std::max(os_max, r->os_cap);
-      }
+      const auto [ll_max, os_max] = nezha::choosePathCeilings(sizes, t, r->ll_cap, r->os_cap);
       r->ll_max = ll_max;
       r->os_max = os_max;
     }

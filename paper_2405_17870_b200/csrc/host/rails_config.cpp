@@ -37,4 +37,29 @@ std::vector<RailSpec> parseRailsToml(const std::string& text) {
   return out;
 }
 
+std::pair<std::uint64_t, std::uint64_t> choosePathCeilings(const std::vector<std::uint64_t>& sizes,
+                                                           const std::vector<double>& times, std::uint64_t ll_cap,
+                                                           std::uint64_t os_cap) {
+  if (times.size() != 3 * sizes.size()) throw std::invalid_argument("choosePathCeilings: 3 times per size");
+  auto best = [&](size_t k) {
+    int b = 2;
+    for (int v = 0; v < 2; ++v)
+      if (times[k * 3 + v] < times[k * 3 + b]) b = v;
+    return b;
+  };
+  std::uint64_t ll_max = 0, os_max = 0;
+  size_t k = 0;
+  if (ll_cap) {
+    ll_max = sizes.empty() ? ll_cap : std::min<std::uint64_t>(ll_cap, sizes[0] / 2);
+    for (; k < sizes.size() && best(k) == 0; ++k) ll_max = sizes[k];
+    if (k == sizes.size()) ll_max = ll_cap;
+  }
+  if (os_cap) {
+    os_max = ll_max;
+    for (; k < sizes.size() && best(k) == 1; ++k) os_max = sizes[k];
+    if (k == sizes.size()) os_max = std::max(os_max, os_cap);
+  }
+  return {ll_max, os_max};
+}
+
 }  // namespace nezha

@@ -287,3 +287,20 @@ TEST_CASE("planComputeGrants: stream-order arbitration (DESIGN.md P14)") {
   CHECK(fit[1].waits.empty());
   CHECK(p.outstanding() == 0);
 }
+
+TEST_CASE("choosePathCeilings: contiguous runs from the smallest size") {
+  const std::vector<std::uint64_t> sz = {64 << 10, 128 << 10, 256 << 10, 512 << 10, 1 << 20};
+  const double X = 1e30;
+  // LL wins 64K..256K, one-shot 512K, two-shot 1M.
+  auto c = choosePathCeilings(sz, {5, 9, 12, 6, 9, 12, 8, 9, 12, 14, 11, 13, 25, 22, 20}, 1 << 20, 2 << 20);
+  CHECK(c.first == (256u << 10));
+  CHECK(c.second == (512u << 10));
+  // LL everywhere it applies, no one-shot staging.
+  c = choosePathCeilings(sz, {5, X, 9, 6, X, 9, 7, X, 9, 8, X, 9, 9, X, 9.5}, 1 << 20, 0);
+  CHECK(c.first == (1u << 20));
+  CHECK(c.second == 0);
+  // LL loses already at 64K: below the sweep only.
+  c = choosePathCeilings(sz, {9, X, 8, 9, X, 8, 9, X, 8, 9, X, 8, 9, X, 8}, 1 << 20, 0);
+  CHECK(c.first == (32u << 10));
+  CHECK_THROWS_AS(choosePathCeilings(sz, {1, 2}, 1, 1), std::invalid_argument);
+}
