@@ -883,6 +883,7 @@ int nz_engine_destroy(nz_engine_t* eng) {
     cudaSetDevice(eng->comm->device);
     cudaDeviceSynchronize();
     for (auto e : eng->pool) cudaEventDestroy(e);
+    for (auto e : eng->pool_pending) cudaEventDestroy(e);
     for (auto& p : eng->pending) {
       cudaEventDestroy(p.start);
       for (auto& pr : p.ends) cudaEventDestroy(pr.second);
