@@ -71,7 +71,8 @@ def main():
         inputs = [oracle.synthetic_input(dt, r, n, seed_base=oracle.SEED_BASE + 131 * ci) for r in range(world)]
         for rep in range(c.get("reps", 1)):
             if c.get("fail") and rep == c.get("fail_rep", 0):
-                eng.inject_failure(eng.op_seq, c["fail"][0], c["fail"][1])
+                inj_seq = eng.op_seq
+                eng.inject_failure(inj_seq, c["fail"][0], c["fail"][1])
             got = np.zeros(n // ES[dt], dtype=oracle.NP_DTYPE[dt])
             if c.get("host"):
                 eng.allreduce_host(inputs[rank], got, n, dt)
@@ -112,6 +113,8 @@ def main():
             plans = eng.last_plans()
             failing = c.get("fail") and rep == c.get("fail_rep", 0)
             fo = eng.last_failover() if failing else None
+            if fo is not None and fo["op_seq"] != inj_seq:
+                fo = None  # the failed rail carried nothing of this op (idle failure): no reroute
             bad = 0
             segs = []
             for p in plans:
