@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--no-failover", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweep-max", type=int, default=GiB)
+    ap.add_argument("--tune", action="store_true",
+                    help="engine measures its CTA budgets and protocol crossovers at startup (tune_budgets=1)")
     ap.add_argument("--graph", action="store_true",
                     help="small sizes replayed from CUDA graphs: a graph_safe engine vs NCCL (device time per op)")
     ap.add_argument("--nccl-graph", action="store_true",
@@ -225,7 +227,8 @@ def main():
         kinds = [k for k in kinds if k != "nvls"] or ["sm"]
     dt = DTYPES[args.dtype]
     S = args.bytes
-    eng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=min(GiB, max(S, 1 << 20)))
+    eng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=min(GiB, max(S, 1 << 20)),
+                 tune_budgets=1 if args.tune else 0)
 
     def max_over_ranks(x: float) -> float:
         vals = comm.allgather_bytes(json.dumps(x).encode().ljust(32))

@@ -183,8 +183,8 @@ typedef struct {
   int compute_pool;          /* SM arbitration of concurrent rails (P14):
                                 0 off (default), 1 block (SPEC ComputePool), 2 shrink */
   int pool_tokens;           /* ComputePool total_tokens; 0 = the GPU's SM count */
-  int tune_budgets;          /* 1 (default): measure the NVLS / SM rails' CTA budget at
-                                startup for rails whose sm_budget is 0 */
+  int tune_budgets;          /* 1: measure the NVLS / SM rails' CTA budgets and protocol
+                                crossovers at startup (default 0 until validated) */
   int graph_safe;            /* 1: rails created with NZ_RAIL_FLAG_GRAPH_SAFE, so engine
                                 allreduces can be captured in CUDA graphs (captured
                                 ops are not Timer samples) */

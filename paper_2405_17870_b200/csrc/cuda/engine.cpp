@@ -793,7 +793,7 @@ void nz_engine_config_default(nz_engine_config_t* c) {
   c->calibrate_iters = 20;
   c->calibrate_max_bytes = uint64_t{1} << 30;
   c->timer_lag = 2;
-  c->tune_budgets = 1;
+  c->tune_budgets = 0;  // on once its hardware sweep is recorded in profiles/
 }
 
 int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t** out) {

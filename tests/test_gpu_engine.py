@@ -52,7 +52,7 @@ def test_engine_single_gpu_identity():
 def test_engine_multirail_parity(world):
     if gpu_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4,
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4, "tune_budgets": 1,
             "cases": [
                 {"dtype": "f32", "nbytes": 64 << 20, "reps": 10},
                 {"dtype": "bf16", "nbytes": 48 << 20, "reps": 2},

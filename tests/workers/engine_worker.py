@@ -56,7 +56,7 @@ def main():
     kinds = spec["rails"]
     over = {"kinds": kinds}
     for k in ("window", "eta", "demote_after", "calibrate_max_bytes", "calibrate_iters", "compute_pool", "pool_tokens",
-              "graph_safe"):
+              "graph_safe", "tune_budgets"):
         if k in spec:
             over[k] = spec[k]
     if "rails_toml" in spec:
