@@ -174,7 +174,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": round(ring_volume(world_sim, nbytes) / (v * 1e9) * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"CPU allreduce, {world_sim} simulated ranks, 2 rails 50/50, 64 MiB fp32 sample",
-                       "global_batch": nbytes, "seq_len": 0, "parallelism": f"dp{world_sim} (threads)"},
+                       "bytes_per_rank": nbytes, "ranks": f"{world_sim} simulated (threads)"},
             "cpu_baseline": res,
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -337,7 +337,7 @@ def main():
            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
            "config": {"workload": f"multi-rail ({'+'.join(kinds)}) state-machine {args.dtype} allreduce of "
                                   f"{S} B per rank (value = busbw at this size; N=1: algbw)",
-                      "global_batch": S, "seq_len": 0, "parallelism": f"dp{world}",
+                      "bytes_per_rank": S, "ranks": world,
                       "l2": "inputs (1 GiB) larger than the 126 MB L2; no flush",
                       "algbw_GBs": round(algbw, 2), "busbw_GBs": round(busbw, 2), "plan": plan},
            "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary()}
