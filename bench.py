@@ -598,9 +598,8 @@ def main():
 
     # ---- config 5: DDP gradient-bucket traces ----------------
     if not args.no_sweep:
-        traces = {"resnet50": [8196000, 31502336, 26255360, 26550272, 9724160],
-                  "bert_large": [4214792, 37903592] + [33591296, 29396992, 37781504] * 11 +
-                                [33591296, 29396992, 131330048]}
+        # torch 2.11's own DDP bucketing of the two models (tests/golden/make_ddp_buckets.py).
+        traces = json.load(open(os.path.join(ROOT, "tests", "golden", "ddp_buckets.json")))
         c5 = {}
         for name, buckets in traces.items():
             offs, o = [], 0

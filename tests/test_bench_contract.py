@@ -40,3 +40,21 @@ def test_bench_our_arm_requires_the_cuda_library():
     if has_gpu:
         pytest.skip("GPU present")
     assert r.returncode != 0
+
+
+def test_ddp_bucket_traces_match_torch():
+    """Config 5's bucket sizes (tests/golden/ddp_buckets.json, read by bench.py)
+    are torch's own DDP bucketing of ResNet-50 and BERT-large; the byte sums
+    equal params x 4."""
+    pytest.importorskip("torchvision")
+    pytest.importorskip("transformers")
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("mk", os.path.join(ROOT, "tests", "golden", "make_ddp_buckets.py"))
+    mk = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mk)
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "ddp_buckets.json")))
+    for name, model in mk.models():
+        assert mk.buckets(model) == golden[name], name
+        assert sum(golden[name]) == 4 * sum(p.numel() for p in model.parameters())
+    assert sum(golden["resnet50"]) == 25_557_032 * 4 and sum(golden["bert_large"]) == 336_226_108 * 4
