@@ -481,6 +481,9 @@ def parse(text):
                 v = float(val)
                 sc["cfg"][keys[name]] = int(v) if name in ("window", "max_iters", "demote_after") else v
         elif k in ("rail", "concurrent"):
+            # Protocol names of the reference (types.cpp protocolKindFromString) + the B200 aliases.
+            if a[1] not in ("tcp", "sharp", "glex", "custom", "nvls", "ce", "sm"):
+                raise ValueError(f"unknown protocol kind: {a[1]}")
             pts = []
             if len(a) > 4:
                 assert a[4] == "cal"

@@ -353,3 +353,79 @@ def test_acceptance_8_cold_start_threshold_shrinks_with_nodes():
         assert above["hot"] and len(above["segs"]) == 2
         p.close()
     assert thr[2] > thr[4] > thr[8] > thr[16], thr
+
+
+# ------------------------------------------------------------ randomized parity
+def random_scenario(seed):
+    """A random planner scenario: 2-8 ranks, Ring or RingChunked, 2-3 rails of
+    any protocol with parametric or calibrated profiles, optional concurrent
+    profiles, jittered truth, fixed and log-uniform op blocks, failures and
+    readmissions at random ops / chunks."""
+    import random as _random
+
+    return _gen(_random.Random(seed))
+
+
+def _gen(R):
+    world = R.choice([2, 4, 8])
+    lines = [f"world {world}"]
+    if R.random() < 0.3:
+        lines.append("algorithm ring")
+    cfg = f"config sync_us {R.choice([0, 1, 3, 6, 20])} window {R.randint(2, 15)}"
+    if R.random() < 0.5: cfg += f" eta {R.choice([0.05, 0.1, 0.2, 0.3])}"
+    if R.random() < 0.4: cfg += f" demote_after {R.randint(1, 3)}"
+    if R.random() < 0.3: cfg += f" tau {R.choice([2, 5, 10])}"
+    lines.append(cfg)
+    nr = R.choice([2, 3])
+    protos = ["nvls", "ce", "sm", "tcp", "sharp", "glex"]
+    for r in range(nr):
+        t = R.choice([0, 1, 5, 12, 30, 45, 200])
+        b = R.choice([0.06e9, 1e9, 1.25e9, 3e11, 5e11, 7e11])
+        l = f"rail {r} {R.choice(protos)} {t} {b:.6g}"
+        if R.random() < 0.3:
+            base = t + 1
+            l += f" cal 4096:{base} 1048576:{base + 2 + R.random() * 5:.3f} 67108864:{base + 100 + R.random() * 50:.3f}"
+        lines.append(l)
+    if R.random() < 0.3:
+        for r in range(nr):
+            lines.append(f"concurrent {r} {R.choice(protos)} {R.choice([5, 15, 40])} {R.choice([2e11, 4e11]):.6g}")
+    for r in range(nr):
+        lines.append(f"truth {r} {R.choice([1, 5, 14, 40])} {R.choice([1e9, 3e11, 6e11]):.6g} {R.choice([0, 0.02, 0.1])}")
+    lines.append(f"truth_sync {R.choice([0, 2, 5])}")
+    lines.append(f"seed {R.randint(0, 1000)}")
+    total = 0
+    for _ in range(R.randint(1, 4)):
+        n = R.randint(5, 120)
+        if R.random() < 0.3:
+            lines.append(f"ops_loguniform {n} 8192 {R.choice([1 << 20, 1 << 24, 1 << 30])}")
+        else:
+            lines.append(f"ops {n} {R.choice([4096, 8192, 65536, 1 << 20, 8 << 20, 64 << 20, 256 << 20, 1 << 30, 3 << 29])}")
+        total += n
+    fails = []
+    for _ in range(R.randint(0, 3)):
+        op = R.randint(0, max(0, total - 1)); rail = R.randrange(nr)
+        fails.append((op, rail))
+        lines.append(f"fail {op} {rail} {R.randint(0, 7)}")
+    for op, rail in fails:
+        if R.random() < 0.5 and op + 2 < total:
+            lines.append(f"readmit {R.randint(op + 1, total - 1)} {rail}")
+    return "\n".join(lines) + "\n"
+
+
+
+@needs_lib
+def test_trace_parity_randomized():
+    """200 random scenarios: product and oracle decision logs identical byte for
+    byte (or both reject the scenario)."""
+    for seed in range(200):
+        sc = random_scenario(seed)
+        try:
+            want, werr = P.run(sc), None
+        except Exception as e:  # noqa: BLE001
+            want, werr = None, e
+        try:
+            got, gerr = run_trace(sc), None
+        except Exception as e:  # noqa: BLE001
+            got, gerr = None, e
+        assert (werr is None) == (gerr is None), (seed, werr, gerr, sc)
+        assert got == want, (seed, sc)
