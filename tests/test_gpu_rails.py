@@ -259,3 +259,40 @@ def test_config1_hash_emulated(mode):
                 s, e = shard_of(off, off + length, r, world)
                 full[s:e] = douts[r][s:e].cpu().numpy()
         assert hashlib.sha256(full.tobytes()).hexdigest() == g["sha256"]
+
+
+def random_rail_cases(seed, n=24):
+    """Random single-rail geometries: rail kind, dtype, ragged offsets and
+    lengths across every protocol path (LL, two-shot, CE), chunk windows and
+    injected failures."""
+    import random
+
+    rng = random.Random(seed)
+    cases = []
+    for _ in range(n):
+        dtype = rng.choice(["f32", "bf16", "i32"])
+        es = 2 if dtype == "bf16" else 4
+        nbytes = es * rng.choice([rng.randint(1, 4096), rng.randint(4096, 600_000), rng.randint(600_000, 6_000_000)])
+        seg_off = es * rng.randint(0, min(64, nbytes // es - 1))
+        seg_len = es * rng.randint(1, nbytes // es - seg_off // es)
+        c = {"kind": rng.choice(["sm", "ce", "nvls"]), "dtype": dtype, "nbytes": nbytes, "seg_off": seg_off,
+             "seg_len": seg_len}
+        r = rng.random()
+        if r < 0.2:
+            c["fail_chunk"] = rng.randint(0, 3)
+        elif r < 0.35:
+            c["chunk_begin"] = rng.randint(0, 2)
+        cases.append(c)
+    return cases
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_rails_randomized(world):
+    if gpu_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cases = random_rail_cases(100 + world)
+    res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(cases)], timeout=300)
+    for rank_res in res:
+        for r in rank_res["results"]:
+            assert r["watchdog"] == 0 and r["mismatch"] == 0 and r["outside_nonzero"] == 0, (r, cases[r["case"]])
