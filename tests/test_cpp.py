@@ -48,3 +48,18 @@ def test_gpu_header_compiles_and_maps_errors(tmp_path):
     assert r.returncode == 0, r.stderr[-3000:]
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_product_host_code_under_tsan(tmp_path):
+    """The product's host C++ (planner, faults, ComputePool incl. its blocking
+    multi-threaded tests) under ThreadSanitizer."""
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else shutil.which("g++")
+    exe = str(tmp_path / "test_product_tsan")
+    r = subprocess.run([cxx, *FLAGS, "-g", "-fsanitize=thread", "-o", exe,
+                        os.path.join(ROOT, "tests", "cpp", "test_product.cpp"), *SRCS], capture_output=True, text=True)
+    if r.returncode != 0 and "tsan" in r.stderr:
+        pytest.skip("no ThreadSanitizer runtime")
+    assert r.returncode == 0, r.stderr[-3000:]
+    run = subprocess.run([exe], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, TSAN_OPTIONS="halt_on_error=1"))
+    assert run.returncode == 0 and "ThreadSanitizer" not in run.stdout + run.stderr, (run.stdout + run.stderr)[-3000:]

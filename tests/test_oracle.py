@@ -179,3 +179,22 @@ def test_closed_form_equals_literal_ring_randomized():
                                       [(o, l, oracle.default_chunk_bytes(l, world, chunked)) for _, o, l in segs])
         for r in range(world):
             np.testing.assert_array_equal(bits(outs[r]), bits(want), err_msg=f"trial {trial} rank {r}")
+
+
+@needs_ref
+def test_literal_ring_is_race_free_under_tsan():
+    """the oracle's threads (rank executors, per-rail executors,
+    failure gate, handoff mailbox) on the reference fabric under
+    ThreadSanitizer, multi-rail and failover configurations."""
+    import shutil
+    import subprocess
+
+    if not os.path.exists("/usr/bin/g++") and not shutil.which("g++"):
+        pytest.skip("no compiler")
+    r = subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "tsan"], capture_output=True, text=True, timeout=600)
+    if r.returncode != 0 and "tsan" in r.stderr:
+        pytest.skip("no ThreadSanitizer runtime: " + r.stderr[-200:])
+    assert r.returncode == 0, r.stderr[-2000:]
+    run = subprocess.run([os.path.join(ROOT, "oracle", "_ref", "tsan_ring")], capture_output=True, text=True,
+                         timeout=600, env=dict(os.environ, TSAN_OPTIONS="halt_on_error=1"))
+    assert run.returncode == 0 and "ThreadSanitizer" not in run.stderr, run.stderr[-3000:]
