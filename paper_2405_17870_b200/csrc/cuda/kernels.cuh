@@ -521,6 +521,18 @@ __device__ __forceinline__ uint32_t ll_load_word(const char* base, uint64_t x, u
   return static_cast<uint32_t>(*reinterpret_cast<const unsigned short*>(base + x));  // bf16 tail
 }
 
+// v[(b + j) mod N] without a runtime index into the register array (which
+// would put v in local memory: the N = 4 / 5 instances spilled): an unrolled
+// select over the N registers.
+template <int N>
+__device__ __forceinline__ uint32_t ll_pick(const uint32_t (&v)[N], int b, int j) {
+  const int i = b + j < N ? b + j : b + j - N;
+  uint32_t r = v[0];
+#pragma unroll
+  for (int q = 1; q < N; ++q) r = i == q ? v[q] : r;
+  return r;
+}
+
 template <typename DT, int N>
 __device__ __forceinline__ void ll_fold_word(const LLArgs& a, const uint32_t (&v)[N], uint64_t x) {
   constexpr int per = 4 / DT::kElem;
@@ -532,21 +544,22 @@ __device__ __forceinline__ void ll_fold_word(const LLArgs& a, const uint32_t (&v
     const int b = block_at<N, DT::kElem>(a.g, xe, &run_end);
     if (DT::kElem == 4) {
       typename DT::Scalar acc;
-      uint32_t w = v[b];
+      uint32_t w = ll_pick<N>(v, b, 0);
       memcpy(&acc, &w, 4);
 #pragma unroll
       for (int j = 1; j < N; ++j) {
         typename DT::Scalar t;
-        uint32_t wj = v[(b + j) % N];
+        uint32_t wj = ll_pick<N>(v, b, j);
         memcpy(&t, &wj, 4);
         acc = DT::sadd(acc, t);
       }
       DT::sstore(a.out + xe, acc);
     } else {
-      float acc = __uint_as_float(k == 0 ? (v[b] << 16) : (v[b] & 0xffff0000u));
+      const uint32_t wb = ll_pick<N>(v, b, 0);
+      float acc = __uint_as_float(k == 0 ? (wb << 16) : (wb & 0xffff0000u));
 #pragma unroll
       for (int j = 1; j < N; ++j) {
-        const uint32_t wj = v[(b + j) % N];
+        const uint32_t wj = ll_pick<N>(v, b, j);
         acc = acc + __uint_as_float(k == 0 ? (wj << 16) : (wj & 0xffff0000u));
       }
       DT::sstore(a.out + xe, acc);
