@@ -256,12 +256,20 @@ struct I32 {
   __device__ static uint32_t sadd(uint32_t a, uint32_t b) { return a + b; }
 };
 
+// a / b through the 32-bit divider when both fit (always for segments of at
+// most 1 GiB, split_oversized): the same quotient without a call to the 64-bit
+// division subroutine, whose caller-saved registers were the kernels' spills.
+__device__ __forceinline__ uint64_t udiv(uint64_t a, uint64_t b) {
+  if (((a | b) >> 32) == 0) return static_cast<uint32_t>(a) / static_cast<uint32_t>(b);
+  return a / b;
+}
+
 // Ring block (fold start rank) of the element at absolute byte offset x,
 // plus the absolute end of that run. Mirrors nezha::ringBlockOf.
 template <int N, int ES>
 __device__ __forceinline__ int block_at(const Geometry& g, uint64_t x, uint64_t* run_end) {
   const uint64_t rel = x - g.seg_off;
-  const uint64_t c = rel / g.chunk;
+  const uint64_t c = udiv(rel, g.chunk);
   const uint64_t cbeg = c * g.chunk;
   const uint64_t rem = g.seg_len - cbeg;
   const uint64_t clen = rem < g.chunk ? rem : g.chunk;
@@ -270,7 +278,7 @@ __device__ __forceinline__ int block_at(const Geometry& g, uint64_t x, uint64_t*
   if (q == 0) {
     b = N - 1;
   } else {
-    const uint64_t bb = ((rel - cbeg) / ES) / q;
+    const uint64_t bb = udiv((rel - cbeg) / ES, q);
     b = bb >= static_cast<uint64_t>(N) ? N - 1 : static_cast<int>(bb);
   }
   *run_end = g.seg_off + cbeg + (b == N - 1 ? clen : static_cast<uint64_t>(b + 1) * q * ES);
