@@ -3,7 +3,9 @@
  *
  * Plain C: opaque handles, plain pointers and sizes, int return codes
  * (0 = ok, < 0 = error, message in nz_last_error()). Nothing throws across
- * this boundary and no torch type appears in it. One process drives one GPU.
+ * this boundary and no torch type appears in it. One process drives one GPU,
+ * or (nz_comm_init_loopback) one host thread drives one virtual rank of a job
+ * whose ranks all live on one GPU.
  *
  * Which reference interface each group replaces (file:line under
  * /root/reference):
@@ -37,7 +39,7 @@
 extern "C" {
 #endif
 
-#define NZ_ABI_VERSION 1
+#define NZ_ABI_VERSION 2
 
 enum {
   NZ_OK = 0,
@@ -75,6 +77,16 @@ int nz_has_cuda_kernels(void);
  * unix sockets, the FileStore analogue. Blocks until all ranks arrive or
  * `timeout_ms` passes (NZ_ERR_TIMEOUT). */
 int nz_comm_init(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out);
+/* Loopback bootstrap of one VIRTUAL rank: `world` ranks of one job live in
+ * this process on the same `device`, one host thread per rank, each calling
+ * this with the same `session`. Buffers are per-rank allocations on that GPU
+ * whose pointers are exchanged in process; every cross-rank kernel runs all
+ * virtual ranks in one grid (blockIdx.y = rank) sized to be co-resident, so
+ * the rails' exact protocols (barriers, LL flags, copy-engine DMA between
+ * ranks' memory, failure detection) run on a single B200. No multicast, so
+ * no NVLS rail. Every other entry point is used exactly as with nz_comm_init. */
+int nz_comm_init_loopback(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out);
+int nz_comm_is_loopback(const nz_comm_t* comm);
 int nz_comm_destroy(nz_comm_t* comm);
 int nz_comm_rank(const nz_comm_t* comm);
 int nz_comm_world(const nz_comm_t* comm);
@@ -136,10 +148,12 @@ int nz_rail_allreduce(nz_rail_t* rail, nz_buf_t* in, nz_buf_t* out, uint64_t seg
  * same as passing fail_chunk = chunk to it (InMemoryFabric::failRailAtFrame,
  * inmem.hpp:22-24). Every rank arms the same chunk. */
 int nz_rail_inject_failure(nz_rail_t* rail, uint64_t chunk);
-/* Chunks of the last nz_rail_allreduce that are complete on this rank. A
- * rail folds all chunks of a call in one kernel, so the count moves from
- * chunk_begin to its stop chunk (chunk_end, or the injected failure chunk)
- * when that call's work retires on the device. Non-blocking. */
+/* Chunks of the last nz_rail_allreduce that are complete on this rank, from
+ * the device progress record: a call runs as waves of consecutive chunks
+ * (one launch each, >= 32 MiB apiece) and each wave that succeeds publishes
+ * its end chunk, so the count moves from chunk_begin through the wave ends to
+ * the stop chunk (chunk_end, or the injected trace-form failure chunk).
+ * Non-blocking. */
 int nz_rail_progress(nz_rail_t* rail, uint64_t* chunks_done);
 /* Kills the rail on this rank (InMemoryFabric::killRail, inmem.cpp:214-233):
  * later nz_rail_allreduce calls fail with NZ_ERR_RAIL_DOWN. Work already on
@@ -156,6 +170,34 @@ typedef struct {
   uint64_t chunk;      /* first chunk NOT completed */
   uint64_t t_fail_ns;  /* %globaltimer when the rail stopped */
 } nz_fault_record_t;
+
+/* Launch status of a rail on this rank, written by its kernels into mapped
+ * host memory (the engine's monitor reads it). Tags number
+ * the rail's op entries (one per nz_rail_allreduce call / engine op). */
+typedef struct {
+  uint32_t ok_tag;      /* last entry whose every launch succeeded on this rank */
+  uint32_t prog_tag;    /* entry of prog_chunk */
+  uint64_t prog_chunk;  /* chunks [chunk_begin, prog_chunk) of that entry done on this rank */
+  uint32_t start_tag;   /* last launch that started on the device */
+  uint32_t fail_tag;    /* entry in which an injected dead link stopped this rank */
+  uint64_t t_start_ns;  /* %globaltimer of that start */
+  uint64_t t_fail_ns;   /* %globaltimer of that stop */
+  uint32_t det_tag;     /* entry whose cross-rank wait timed out / was aborted here */
+  uint32_t abort;       /* host -> device: stop waiting on peers (rail declared Failed) */
+  uint64_t t_det_ns;    /* %globaltimer of that detection */
+} nz_rail_status_t;
+int nz_rail_status(const nz_rail_t* rail, nz_rail_status_t* out);
+/* Unplanned failure injection: THIS rank's link of the rail
+ * dies at `chunk` of its next nz_rail_allreduce — its kernels arrive at the
+ * start barrier of the launch that covers that chunk and stop there, posting
+ * nothing to the peers, and every later launch on this rank exits at once.
+ * Peers are not told: their end-barrier waits time out (nz_rail_set_detect_us)
+ * and their launches fail too. nz_rail_revive (on every rank) clears it. */
+int nz_rail_inject_stall(nz_rail_t* rail, uint64_t chunk);
+int nz_rail_revive(nz_rail_t* rail);
+/* End-barrier budget of the rail's launches (failure detection), microseconds;
+ * 0 restores the default (NEZHA_DETECT_US, else max(2000, 2 x range / 100 GB/s)). */
+int nz_rail_set_detect_us(nz_rail_t* rail, double us);
 
 /* Non-blocking read of the rail's mapped fault word; clears it when `consume`. */
 int nz_rail_poll_fault(nz_rail_t* rail, nz_fault_record_t* rec, int consume);
@@ -187,7 +229,13 @@ typedef struct {
                                 crossovers at startup (default 0 until validated) */
   int graph_safe;            /* 1: rails created with NZ_RAIL_FLAG_GRAPH_SAFE, so engine
                                 allreduces can be captured in CUDA graphs (captured
-                                ops are not Timer samples) */
+                                ops are not Timer samples and are not monitored) */
+  int monitor;               /* 1 (default): failure monitor thread + stream gates
+                                (DESIGN.md §6b); 0: none (a failed rail raises at
+                                nz_engine_synchronize) */
+  double detect_us;          /* end-barrier budget floor; <= 0: default */
+  double heartbeat_us;       /* monitor heartbeat interval, default 50000 */
+  double readmit_hold_us;    /* healthy probes needed before readmit, default 1e6 */
 } nz_engine_config_t;
 
 void nz_engine_config_default(nz_engine_config_t* cfg);
@@ -209,9 +257,14 @@ int nz_engine_allreduce_host(nz_engine_t* eng, const void* host_in, void* host_o
  * pieces, asynchronous on `stream` (NULL = legacy default); src == dst is
  * allowed. */
 int nz_engine_allreduce_device(nz_engine_t* eng, const void* src, void* dst, uint64_t bytes, int dtype, void* stream);
-/* Arms a failure of `rail_id` at `chunk` of op `op_seq` (trace form P10). */
+/* Unplanned failure: THIS rank's link of `rail_id` dies at `chunk` of op
+ * `op_seq` (nz_rail_inject_stall semantics). Call it on one rank only: the
+ * others are not told and must detect it; every rank's monitor then agrees on
+ * the orphan (min over ranks of completed chunks) and reroutes it (P9/P10). */
 int nz_engine_inject_failure(nz_engine_t* eng, uint32_t op_seq, int rail_id, uint64_t chunk);
-/* Readmits a previously failed rail. */
+/* Readmits a previously failed rail: collective; probes the
+ * rail until it has been healthy for readmit_hold_us, then re-enters it at
+ * its last converged split. */
 int nz_engine_readmit(nz_engine_t* eng, int rail_id);
 int nz_engine_synchronize(nz_engine_t* eng);
 uint32_t nz_engine_op_seq(const nz_engine_t* eng);
@@ -225,11 +278,20 @@ typedef struct {
   double detect_us;   /* device fault stamp -> host monitor saw it */
   double resume_us;   /* device fault stamp -> survivor started the orphan */
   double done_us;     /* device fault stamp -> orphan complete */
-  double host_detect_us; /* device fault stamp -> host monitor saw the record
+  double host_detect_us; /* device fault stamp -> this rank's monitor saw the failure
                             (host clock mapped onto %globaltimer, +-~2 us) */
+  double device_detect_us; /* device fault stamp -> this rank's kernel gave up waiting
+                              (0 on the rank whose link died) */
+  double resume_after_detect_us; /* monitor saw the failure -> survivor started the orphan */
+  uint64_t orphan_chunk;  /* first chunk rerouted = min over ranks of completed chunks */
+  int stalled_here;       /* 1 on the rank whose link died */
 } nz_failover_report_t;
-/* Last completed failover (returns NZ_ERR_INVALID when none happened). */
+/* Last completed failover (returns NZ_ERR_INVALID when none happened).
+ * `t_fail` is the dead rank's device stamp, shared by the agreement. */
 int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep);
+/* Every failover so far, in order: count, and the i-th report. */
+int nz_engine_failover_count(nz_engine_t* eng);
+int nz_engine_failover_get(nz_engine_t* eng, int i, nz_failover_report_t* rep);
 
 /* Warm restart: the allocation table, calibrated profiles and
  * sync overhead as JSON; load it on every rank (same text) to skip
@@ -289,10 +351,6 @@ int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void
                     uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
                     void* stream);
 
-/* Same, for the SM rail's TMA-pipelined fold (ndst must equal world >= 2). */
-int nz_emulate_fold_tma(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
-                        uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
-                        void* stream);
 
 /* ----------------------------------------------------------------- pool --- */
 /* Host ComputePool with the semantics pinned in include/nezha/compute_pool.hpp.

@@ -98,6 +98,10 @@ class EngineConfig(ctypes.Structure):
         ("pool_tokens", c_int),
         ("tune_budgets", c_int),
         ("graph_safe", c_int),
+        ("monitor", c_int),
+        ("detect_us", c_double),
+        ("heartbeat_us", c_double),
+        ("readmit_hold_us", c_double),
     ]
 
 
@@ -112,6 +116,27 @@ class FailoverReport(ctypes.Structure):
         ("resume_us", c_double),
         ("done_us", c_double),
         ("host_detect_us", c_double),
+        ("device_detect_us", c_double),
+        ("resume_after_detect_us", c_double),
+        ("orphan_chunk", c_uint64),
+        ("stalled_here", c_int),
+    ]
+
+
+class RailStatus(ctypes.Structure):
+    """nz_rail_status_t: launch status a rail's kernels publish."""
+
+    _fields_ = [
+        ("ok_tag", c_uint32),
+        ("prog_tag", c_uint32),
+        ("prog_chunk", c_uint64),
+        ("start_tag", c_uint32),
+        ("fail_tag", c_uint32),
+        ("t_start_ns", c_uint64),
+        ("t_fail_ns", c_uint64),
+        ("det_tag", c_uint32),
+        ("abort", c_uint32),
+        ("t_det_ns", c_uint64),
     ]
 
 
@@ -122,6 +147,8 @@ _SIGS = {
     "nz_abi_version": (c_int, []),
     "nz_has_cuda_kernels": (c_int, []),
     "nz_comm_init": (c_int, [c_int, c_int, c_int, c_char_p, c_int, POINTER(c_void_p)]),
+    "nz_comm_init_loopback": (c_int, [c_int, c_int, c_int, c_char_p, c_int, POINTER(c_void_p)]),
+    "nz_comm_is_loopback": (c_int, [c_void_p]),
     "nz_comm_destroy": (c_int, [c_void_p]),
     "nz_comm_rank": (c_int, [c_void_p]),
     "nz_comm_world": (c_int, [c_void_p]),
@@ -152,6 +179,10 @@ _SIGS = {
     "nz_rail_inject_failure": (c_int, [c_void_p, c_uint64]),
     "nz_rail_progress": (c_int, [c_void_p, POINTER(c_uint64)]),
     "nz_rail_abort": (c_int, [c_void_p]),
+    "nz_rail_status": (c_int, [c_void_p, c_void_p]),
+    "nz_rail_inject_stall": (c_int, [c_void_p, c_uint64]),
+    "nz_rail_revive": (c_int, [c_void_p]),
+    "nz_rail_set_detect_us": (c_int, [c_void_p, c_double]),
     "nz_event_elapsed_us": (c_int, [c_void_p, c_void_p, POINTER(c_double)]),
     "nz_engine_config_default": (None, [POINTER(EngineConfig)]),
     "nz_engine_create": (c_int, [c_void_p, POINTER(EngineConfig), POINTER(c_void_p)]),
@@ -164,6 +195,8 @@ _SIGS = {
     "nz_engine_synchronize": (c_int, [c_void_p]),
     "nz_engine_op_seq": (c_uint32, [c_void_p]),
     "nz_engine_last_failover": (c_int, [c_void_p, POINTER(FailoverReport)]),
+    "nz_engine_failover_count": (c_int, [c_void_p]),
+    "nz_engine_failover_get": (c_int, [c_void_p, c_int, POINTER(FailoverReport)]),
     "nz_engine_state_json": (c_int, [c_void_p, c_char_p, c_size_t]),
     "nz_engine_plan_json": (c_int, [c_void_p, c_uint64, c_char_p, c_size_t]),
     "nz_engine_last_plan_json": (c_int, [c_void_p, c_char_p, c_size_t]),
@@ -175,8 +208,6 @@ _SIGS = {
     "nz_planner_run_trace": (c_int, [c_char_p, c_char_p, c_size_t]),
     "nz_emulate_fold": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64, c_uint64,
                                 c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
-    "nz_emulate_fold_tma": (c_int, [c_int, c_int, c_int, POINTER(c_void_p), POINTER(c_void_p), c_int, c_uint64,
-                                    c_uint64, c_uint64, c_uint64, c_uint64, c_int, c_void_p]),
     "nz_balancer_create": (c_int, [c_char_p, c_double, c_double, c_double, c_int, c_int, POINTER(c_void_p)]),
     "nz_balancer_destroy": (c_int, [c_void_p]),
     "nz_balancer_set_agreement": (c_int, [c_void_p, AGREE_FN, c_void_p]),

@@ -76,7 +76,21 @@ nz_buf* allocSymmetric(nz_comm* c, size_t bytes) {
     NZ_CU(NZ_DRV(cuMemCreate)(&b->local, b->mapped, &prop, 0));
     b->ptrs[c->rank] = mapHandle(b->local, b->mapped, gran, c->device);
 
-    if (c->world > 1) {
+    if (c->loop) {
+      // Virtual ranks share this process's address space and GPU: the peers'
+      // mappings are their own, passed by pointer (no import, no multicast).
+      struct {
+        uint64_t mapped;
+        uint64_t va;
+      } mine{b->mapped, reinterpret_cast<uint64_t>(b->ptrs[c->rank])};
+      const auto msgs = exchange(c, &mine, sizeof(mine), {});
+      for (int p = 0; p < c->world; ++p) {
+        decltype(mine) theirs{};
+        memcpy(&theirs, msgs[p].data.data(), sizeof(theirs));
+        if (theirs.mapped != b->mapped) fail(NZ_ERR_INVALID, "asymmetric buffer allocation");
+        b->ptrs[p] = reinterpret_cast<char*>(theirs.va);
+      }
+    } else if (c->world > 1) {
       int fd = -1;
       NZ_CU(NZ_DRV(cuMemExportToShareableHandle)(&fd, b->local, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
       uint64_t mine = b->mapped;
@@ -136,6 +150,14 @@ void freeSymmetric(nz_buf* b) {
   if (!b) return;
   nz_comm* c = b->comm;
   cudaSetDevice(c->device);
+  if (c->loop) {
+    // A virtual rank's memory is its peers' too: free it only once every rank
+    // stopped using it (all ranks free in the same order).
+    try {
+      exchange(c, nullptr, 0, {});
+    } catch (...) {
+    }
+  }
   cudaDeviceSynchronize();
   if (b->mc_ptr) unmap(b->mc_ptr, b->mapped);
   if (b->mc) {
@@ -143,7 +165,8 @@ void freeSymmetric(nz_buf* b) {
     if (NZ_DRV(cuDeviceGet)(&dev, c->device) == CUDA_SUCCESS) NZ_DRV(cuMulticastUnbind)(b->mc, dev, 0, b->mapped);
     NZ_DRV(cuMemRelease)(b->mc);
   }
-  for (int p = 0; p < static_cast<int>(b->ptrs.size()); ++p) unmap(b->ptrs[p], b->mapped);
+  for (int p = 0; p < static_cast<int>(b->ptrs.size()); ++p)
+    if (!c->loop || p == c->rank) unmap(b->ptrs[p], b->mapped);
   for (auto h : b->imported)
     if (h) NZ_DRV(cuMemRelease)(h);
   if (b->local) NZ_DRV(cuMemRelease)(b->local);
@@ -168,7 +191,7 @@ int nz_buffer_free(nz_buf_t* buf) {
   return guarded([&] {
     if (!buf) return;
     // Collective: nobody unmaps while a peer may still touch the memory.
-    if (buf->comm->world > 1) {
+    if (buf->comm->world > 1 && !buf->comm->loop) {
       cudaSetDevice(buf->comm->device);
       cudaDeviceSynchronize();
       nz::exchange(buf->comm, nullptr, 0, {});

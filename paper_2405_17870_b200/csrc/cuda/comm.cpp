@@ -7,7 +7,12 @@
 // mappings, so what has to travel between the rank processes is file
 // descriptors of VMM allocations and of the NVSwitch multicast object. They
 // travel over abstract unix sockets (SCM_RIGHTS), one short connection per
-// message, named after the job's session string.
+// message, named after the job's session string. Each rank has two control
+// channels (the issuing thread's and the failure monitor's), so the monitor
+// can agree with its peers while the issuing thread is inside an exchange.
+//
+// Loopback ranks (nz_comm_init_loopback) are threads of one process on one
+// GPU: their exchanges meet in an in-process mailbox instead.
 #include <fcntl.h>
 #include <poll.h>
 #include <sys/socket.h>
@@ -37,10 +42,10 @@ struct WireHeader {
 constexpr size_t kMaxMsg = 60 * 1024;
 constexpr int kMaxFds = 16;
 
-sockaddr_un socketName(const std::string& session, int rank, socklen_t* len) {
+sockaddr_un socketName(const std::string& session, int channel, int rank, socklen_t* len) {
   sockaddr_un a{};
   a.sun_family = AF_UNIX;
-  const std::string name = "nezha-b200-" + session + "-" + std::to_string(rank);
+  const std::string name = "nezha-b200-" + session + (channel ? "-mon-" : "-") + std::to_string(rank);
   if (name.size() + 1 >= sizeof(a.sun_path)) fail(NZ_ERR_INVALID, "session name too long");
   a.sun_path[0] = '\0';  // abstract namespace: nothing on disk to clean up
   memcpy(a.sun_path + 1, name.data(), name.size());
@@ -50,9 +55,10 @@ sockaddr_un socketName(const std::string& session, int rank, socklen_t* len) {
 
 using Clock = std::chrono::steady_clock;
 
-void sendTo(nz_comm* c, int peer, uint64_t seq, const void* data, size_t bytes, const std::vector<int>& fds) {
+void sendTo(nz_comm* c, int channel, int peer, uint64_t seq, const void* data, size_t bytes,
+            const std::vector<int>& fds) {
   socklen_t len;
-  sockaddr_un addr = socketName(c->session, peer, &len);
+  sockaddr_un addr = socketName(c->session, channel, peer, &len);
   const auto deadline = Clock::now() + std::chrono::milliseconds(c->timeout_ms);
   int s = -1;
   while (true) {
@@ -90,13 +96,13 @@ void sendTo(nz_comm* c, int peer, uint64_t seq, const void* data, size_t bytes, 
   if (n != static_cast<ssize_t>(buf.size())) fail(NZ_ERR_SYSTEM, std::string("sendmsg: ") + strerror(errno));
 }
 
-// Accepts one message into the stash. Returns false on timeout.
-bool receiveOne(nz_comm* c, int wait_ms) {
-  pollfd p{c->listen_fd, POLLIN, 0};
+// Accepts one message into the channel's stash. Returns false on timeout.
+bool receiveOne(Channel& ch, int wait_ms) {
+  pollfd p{ch.listen_fd, POLLIN, 0};
   const int r = poll(&p, 1, wait_ms);
   if (r == 0) return false;
   if (r < 0) fail(NZ_ERR_SYSTEM, std::string("poll: ") + strerror(errno));
-  const int s = accept4(c->listen_fd, nullptr, nullptr, SOCK_CLOEXEC);
+  const int s = accept4(ch.listen_fd, nullptr, nullptr, SOCK_CLOEXEC);
   if (s < 0) fail(NZ_ERR_SYSTEM, std::string("accept: ") + strerror(errno));
   std::vector<char> buf(sizeof(WireHeader) + kMaxMsg);
   iovec iov{buf.data(), buf.size()};
@@ -112,7 +118,7 @@ bool receiveOne(nz_comm* c, int wait_ms) {
   WireHeader h;
   memcpy(&h, buf.data(), sizeof(h));
   if (h.bytes + sizeof(h) != static_cast<size_t>(n)) fail(NZ_ERR_SYSTEM, "truncated rendezvous message");
-  nz_comm::Msg msg;
+  Msg msg;
   msg.data.assign(buf.data() + sizeof(h), buf.data() + n);
   for (cmsghdr* cm = CMSG_FIRSTHDR(&m); cm; cm = CMSG_NXTHDR(&m, cm)) {
     if (cm->cmsg_level == SOL_SOCKET && cm->cmsg_type == SCM_RIGHTS) {
@@ -122,10 +128,66 @@ bool receiveOne(nz_comm* c, int wait_ms) {
     }
   }
   if (msg.fds.size() != h.nfds) fail(NZ_ERR_SYSTEM, "fd count mismatch in rendezvous message");
-  c->stash[{h.seq, h.from}] = std::move(msg);
+  ch.stash[{h.seq, h.from}] = std::move(msg);
   return true;
 }
+
+int openListener(nz_comm* c, int channel) {
+  const int fd = socket(AF_UNIX, SOCK_SEQPACKET | SOCK_CLOEXEC, 0);
+  if (fd < 0) fail(NZ_ERR_SYSTEM, std::string("socket: ") + strerror(errno));
+  socklen_t len;
+  sockaddr_un addr = socketName(c->session, channel, c->rank, &len);
+  if (bind(fd, reinterpret_cast<sockaddr*>(&addr), len) != 0) {
+    const int err = errno;
+    close(fd);
+    fail(NZ_ERR_SYSTEM, std::string("bind rendezvous socket: ") + strerror(err));
+  }
+  if (listen(fd, 256) != 0) {
+    const int err = errno;
+    close(fd);
+    fail(NZ_ERR_SYSTEM, std::string("listen: ") + strerror(err));
+  }
+  return fd;
+}
+
+// Loopback exchange: the messages of one (channel, sequence) meet in the
+// group's mailbox; the last reader clears them.
+std::vector<Msg> loopExchange(nz_comm* c, int channel, uint64_t seq, const void* data, size_t bytes) {
+  LoopGroup& g = *c->loop;
+  std::vector<Msg> out(c->world);
+  std::unique_lock<std::mutex> lk(g.m);
+  g.box[{channel, seq, c->rank}].assign(static_cast<const char*>(data), static_cast<const char*>(data) + bytes);
+  g.cv.notify_all();
+  const auto deadline = Clock::now() + std::chrono::milliseconds(c->timeout_ms);
+  for (int p = 0; p < c->world; ++p) {
+    while (g.box.find({channel, seq, p}) == g.box.end()) {
+      if (g.cv.wait_until(lk, deadline) == std::cv_status::timeout && g.box.find({channel, seq, p}) == g.box.end()) {
+        fail(NZ_ERR_TIMEOUT, "loopback rendezvous timeout waiting for virtual rank " + std::to_string(p));
+      }
+    }
+    out[p].data = g.box[{channel, seq, p}];
+  }
+  if (++g.reads[{channel, seq}] == c->world) {
+    for (int p = 0; p < c->world; ++p) g.box.erase({channel, seq, p});
+    g.reads.erase({channel, seq});
+  }
+  return out;
+}
+
+std::mutex g_groups_mu;
+std::map<std::string, std::weak_ptr<LoopGroup>> g_groups;
+
 }  // namespace
+
+LoopGroup::~LoopGroup() {
+  for (auto& kv : rails) {
+    if (kv.second->stream) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(kv.second->stream);
+      cudaStreamDestroy(kv.second->stream);
+    }
+  }
+}
 
 const DriverApi& drv() {
   static const DriverApi api = [] {
@@ -160,28 +222,105 @@ void checkCu(CUresult e, const char* what) {
   }
 }
 
-std::vector<nz_comm::Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std::vector<int>& fds) {
+std::vector<Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std::vector<int>& fds, int channel) {
   if (bytes > kMaxMsg) fail(NZ_ERR_INVALID, "exchange payload too large");
   if (fds.size() > static_cast<size_t>(kMaxFds)) fail(NZ_ERR_INVALID, "too many fds in one exchange");
-  const uint64_t seq = c->xchg_seq++;
-  std::vector<nz_comm::Msg> out(c->world);
+  if (channel < 0 || channel >= kChannels) fail(NZ_ERR_INVALID, "bad exchange channel");
+  Channel& ch = c->chan[channel];
+  const uint64_t seq = ch.seq++;
+  if (c->loop) {
+    if (!fds.empty()) fail(NZ_ERR_INVALID, "loopback ranks exchange no file descriptors");
+    return loopExchange(c, channel, seq, data, bytes);
+  }
+  std::vector<Msg> out(c->world);
   out[c->rank].data.assign(static_cast<const char*>(data), static_cast<const char*>(data) + bytes);
-  for (int k = 1; k < c->world; ++k) sendTo(c, (c->rank + k) % c->world, seq, data, bytes, fds);
+  if (c->world == 1) return out;
+  for (int k = 1; k < c->world; ++k) sendTo(c, channel, (c->rank + k) % c->world, seq, data, bytes, fds);
   const auto deadline = Clock::now() + std::chrono::milliseconds(c->timeout_ms);
   for (int p = 0; p < c->world; ++p) {
     if (p == c->rank) continue;
-    while (c->stash.find({seq, p}) == c->stash.end()) {
+    while (ch.stash.find({seq, p}) == ch.stash.end()) {
       const auto left = std::chrono::duration_cast<std::chrono::milliseconds>(deadline - Clock::now()).count();
-      if (left <= 0 || !receiveOne(c, static_cast<int>(std::min<long long>(left, 1000)))) {
+      if (left <= 0 || !receiveOne(ch, static_cast<int>(std::min<long long>(left, 1000)))) {
         if (Clock::now() > deadline) fail(NZ_ERR_TIMEOUT, "rendezvous timeout waiting for rank " + std::to_string(p));
       }
     }
-    auto it = c->stash.find({seq, p});
+    auto it = ch.stash.find({seq, p});
     out[p] = std::move(it->second);
-    c->stash.erase(it);
+    ch.stash.erase(it);
   }
   return out;
 }
+
+namespace {
+
+int commInit(int rank, int world, int device, const char* session, int timeout_ms, bool loopback, nz_comm_t** out) {
+  return guarded([&] {
+    if (!out || !session) fail(NZ_ERR_INVALID, "nz_comm_init: null argument");
+    if (world < 1 || world > kMaxRanks) fail(NZ_ERR_INVALID, "world must be in [1, 8]");
+    if (rank < 0 || rank >= world) fail(NZ_ERR_INVALID, "rank out of range");
+    auto* c = new nz_comm();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->session = session;
+    c->timeout_ms = timeout_ms > 0 ? timeout_ms : 60000;
+    try {
+      NZ_CUDA(cudaSetDevice(device));
+      NZ_CUDA(cudaFree(nullptr));  // create the primary context
+      if (!drv().cuMulticastBindMem || !drv().cuMemCreate) fail(NZ_ERR_CUDA, "CUDA driver entry points unavailable");
+      NZ_CU(NZ_DRV(cuInit)(0));
+      CUdevice dev;
+      NZ_CU(NZ_DRV(cuDeviceGet)(&dev, device));
+      int mc = 0;
+      NZ_CU(NZ_DRV(cuDeviceGetAttribute)(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+      NZ_CU(NZ_DRV(cuDeviceGetAttribute)(&c->sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev));
+      if (loopback) {
+        std::lock_guard<std::mutex> lk(g_groups_mu);
+        auto& w = g_groups[c->session];
+        auto g = w.lock();
+        if (!g) {
+          g = std::make_shared<LoopGroup>();
+          g->world = world;
+          g->device = device;
+          w = g;
+        }
+        if (g->world != world || g->device != device) fail(NZ_ERR_INVALID, "loopback ranks disagree on world / device");
+        if (g->joined & (1u << rank)) fail(NZ_ERR_INVALID, "loopback rank joined twice");
+        g->joined |= 1u << rank;
+        c->loop = g;
+        c->multicast = false;  // one GPU: no NVSwitch multicast team
+      } else if (world > 1) {
+        for (int ch = 0; ch < kChannels; ++ch) c->chan[ch].listen_fd = openListener(c, ch);
+        // Every rank must agree on multicast before any buffer is built.
+        const auto all = exchange(c, &mc, sizeof(mc), {});
+        int agreed = 1;
+        for (const auto& m : all) {
+          int v = 0;
+          memcpy(&v, m.data.data(), sizeof(v));
+          agreed &= (v != 0);
+        }
+        c->multicast = agreed && getenv("NEZHA_DISABLE_MULTICAST") == nullptr;
+      }
+      c->ctrl = allocSymmetric(c, kPadBytes * kMaxRails);
+      NZ_CUDA(cudaMemset(c->ctrl->ptrs[rank], 0, c->ctrl->mapped));
+      NZ_CUDA(cudaDeviceSynchronize());
+      exchange(c, nullptr, 0, {});  // pads are zero everywhere before first use
+    } catch (...) {
+      for (auto& ch : c->chan)
+        if (ch.listen_fd >= 0) close(ch.listen_fd);
+      if (c->loop) {
+        std::lock_guard<std::mutex> lk(g_groups_mu);
+        c->loop->joined &= ~(1u << rank);
+      }
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+}  // namespace
 
 }  // namespace nz
 
@@ -194,67 +333,29 @@ const char* nz_last_error(void) { return nz::lastError(); }
 int nz_abi_version(void) { return NZ_ABI_VERSION; }
 
 int nz_comm_init(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out) {
-  return guarded([&] {
-    if (!out || !session) fail(NZ_ERR_INVALID, "nz_comm_init: null argument");
-    if (world < 1 || world > nz::kMaxRanks) fail(NZ_ERR_INVALID, "world must be in [1, 8]");
-    if (rank < 0 || rank >= world) fail(NZ_ERR_INVALID, "rank out of range");
-    auto* c = new nz_comm();
-    c->rank = rank;
-    c->world = world;
-    c->device = device;
-    c->session = session;
-    c->timeout_ms = timeout_ms > 0 ? timeout_ms : 60000;
-    try {
-      NZ_CUDA(cudaSetDevice(device));
-      NZ_CUDA(cudaFree(nullptr));  // create the primary context
-      if (!nz::drv().cuMulticastBindMem || !nz::drv().cuMemCreate) fail(NZ_ERR_CUDA, "CUDA driver entry points unavailable");
-      NZ_CU(NZ_DRV(cuInit)(0));
-      CUdevice dev;
-      NZ_CU(NZ_DRV(cuDeviceGet)(&dev, device));
-      int mc = 0;
-      NZ_CU(NZ_DRV(cuDeviceGetAttribute)(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
-      NZ_CU(NZ_DRV(cuDeviceGetAttribute)(&c->sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev));
-      if (world > 1) {
-        c->listen_fd = socket(AF_UNIX, SOCK_SEQPACKET | SOCK_CLOEXEC, 0);
-        if (c->listen_fd < 0) fail(NZ_ERR_SYSTEM, std::string("socket: ") + strerror(errno));
-        socklen_t len;
-        sockaddr_un addr = nz::socketName(c->session, rank, &len);
-        if (bind(c->listen_fd, reinterpret_cast<sockaddr*>(&addr), len) != 0) {
-          fail(NZ_ERR_SYSTEM, std::string("bind rendezvous socket: ") + strerror(errno));
-        }
-        if (listen(c->listen_fd, 256) != 0) fail(NZ_ERR_SYSTEM, std::string("listen: ") + strerror(errno));
-        // Every rank must agree on multicast before any buffer is built.
-        const auto all = nz::exchange(c, &mc, sizeof(mc), {});
-        int agreed = 1;
-        for (const auto& m : all) {
-          int v = 0;
-          memcpy(&v, m.data.data(), sizeof(v));
-          agreed &= (v != 0);
-        }
-        c->multicast = agreed && getenv("NEZHA_DISABLE_MULTICAST") == nullptr;
-      }
-      c->ctrl = nz::allocSymmetric(c, nz::kPadBytes * nz::kMaxRails);
-      NZ_CUDA(cudaMemset(c->ctrl->ptrs[rank], 0, c->ctrl->mapped));
-      NZ_CUDA(cudaDeviceSynchronize());
-      nz::exchange(c, nullptr, 0, {});  // pads are zero everywhere before first use
-    } catch (...) {
-      if (c->listen_fd >= 0) close(c->listen_fd);
-      delete c;
-      throw;
-    }
-    *out = c;
-  });
+  return nz::commInit(rank, world, device, session, timeout_ms, false, out);
 }
+
+int nz_comm_init_loopback(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out) {
+  return nz::commInit(rank, world, device, session, timeout_ms, true, out);
+}
+
+int nz_comm_is_loopback(const nz_comm_t* c) { return c ? (c->loop ? 1 : 0) : NZ_ERR_INVALID; }
 
 int nz_comm_destroy(nz_comm_t* comm) {
   return guarded([&] {
     if (!comm) return;
     cudaSetDevice(comm->device);
-    cudaDeviceSynchronize();
-    if (comm->ctrl) nz::freeSymmetric(comm->ctrl);
-    for (auto& kv : comm->stash)
-      for (int fd : kv.second.fds) close(fd);
-    if (comm->listen_fd >= 0) close(comm->listen_fd);
+    if (comm->ctrl) nz::freeSymmetric(comm->ctrl);  // collective: ranks leave together
+    for (auto& ch : comm->chan) {
+      for (auto& kv : ch.stash)
+        for (int fd : kv.second.fds) close(fd);
+      if (ch.listen_fd >= 0) close(ch.listen_fd);
+    }
+    if (comm->loop) {
+      std::lock_guard<std::mutex> lk(nz::g_groups_mu);
+      comm->loop->joined &= ~(1u << comm->rank);
+    }
     delete comm;
   });
 }

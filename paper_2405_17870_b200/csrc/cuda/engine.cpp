@@ -1,7 +1,7 @@
 // Engine: the multi-rail allreduce of one rank (
-// PAPER.md:379 Fig. 6). Planner (Balancer) + rails (rails.cu) + Timer +
-// fault monitor / handoff. See include/nezha/engine.hpp for the contract;
-// startup calibration lives in engine_calibrate.cpp.
+// PAPER.md:379 Fig. 6). Planner (Balancer) + rails (rails.cu) + Timer, with
+// the failure monitor in engine_monitor.cpp. See include/nezha/engine.hpp for
+// the contract; startup calibration lives in engine_calibrate.cpp.
 #include "engine_impl.h"
 
 using nz::fail;
@@ -23,6 +23,11 @@ std::vector<std::pair<int, nezha::Micros>> nz_engine::agree(const std::vector<st
   return out;
 }
 
+// Timer: op k is sampled when op k + timer_lag is issued,
+// the same op on every rank, so every flush (and its cross-rank agreement)
+// happens at the same point of every rank's op stream. The end events are
+// recorded right after each rail's launches, so this never waits on a
+// stream gate, i.e. never on the failure monitor.
 void nz_engine::harvest(uint32_t upto) {
   while (!pending.empty() && pending.front().op + static_cast<uint32_t>(cfg.timer_lag) <= upto) {
     Pending p = std::move(pending.front());
@@ -42,6 +47,12 @@ void nz_engine::harvest(uint32_t upto) {
       pool.push_back(e);
     }
     pool.push_back(p.start);
+    // A rail whose launches failed (on every rank alike) makes the op a
+    // non-sample: its latency is the failure's, not the rail's.
+    for (auto& [ri, tag] : p.tags) {
+      const volatile nz_rail_status_t* s = rails[ri]->status_host;
+      if (static_cast<int32_t>(s->ok_tag - tag) < 0) p.skip = true;
+    }
     if (stats.size() != specs.size()) stats.assign(specs.size(), RailStat{});
     for (auto& [id, us] : lat) {
       RailStat& st = stats[index(id)];
@@ -52,19 +63,6 @@ void nz_engine::harvest(uint32_t upto) {
     }
     if (!p.skip) bal->recordOp(p.plan, lat);
   }
-}
-
-void nz_engine::finishFailoverReport() {
-  if (!fo_pending) return;
-  volatile uint64_t* s = stamps_host;
-  if (s[2] == 0) return;
-  const double f = static_cast<double>(s[3]);
-  fo.detect_us = (static_cast<double>(s[0]) - f) / 1000.0;
-  fo.resume_us = (static_cast<double>(s[1]) - f) / 1000.0;
-  fo.done_us = (static_cast<double>(s[2]) - f) / 1000.0;
-  fo.host_detect_us = (static_cast<double>(host_seen_ns + clock_offset_ns) - f) / 1000.0;
-  have_fo = true;
-  fo_pending = false;
 }
 
 std::vector<nz::ComputeGate> nz_engine::gatesFor(const std::vector<std::pair<int, uint64_t>>& segs, std::string* log) {
@@ -98,10 +96,71 @@ void nz_engine::recycleGates() {
   pool_pending.clear();
 }
 
+void nz_engine::launchSegment(uint32_t seq, const nezha::Plan& plan, const nezha::RailSegment& rs, nz_buf* in,
+                              nz_buf* out, uint64_t base, int dtype, cudaStream_t st, nz::ComputeGate* gate,
+                              bool capturing, cudaStream_t user, cudaEvent_t* end_out, Pending* p) {
+  const int ri = index(rs.rail_id);
+  nz_rail* r = rails[ri];
+  const uint64_t C = nezha::defaultChunkBytes(rs.segment.length, comm->world, algo);
+  nz::RailOp o;
+  o.in = in;
+  o.out = out;
+  o.seg_off = base + rs.segment.offset;
+  o.seg_len = rs.segment.length;
+  o.chunk_bytes = C;
+  o.dtype = dtype;
+  o.op_seq = seq;
+  o.st = st;
+  o.gate = gate;
+  o.status = !capturing;
+  auto inj = inject.find(seq);
+  if (inj != inject.end() && inj->second.first == rs.rail_id) o.stall_chunk = static_cast<int64_t>(inj->second.second);
+  const uint32_t tag = nz::railRun(r, o);
+  if (end_out) {  // Timer end of a hot op's rail
+    *end_out = event();
+    NZ_CUDA(cudaEventRecord(*end_out, st));
+    NZ_CUDA(cudaStreamWaitEvent(user, *end_out, 0));
+  }
+  if (!monitored || capturing || tag == 0) return;
+  // The caller's stream passes this segment only once its gate word holds
+  // the tag: written by the rail's last launch when it succeeded, or by the
+  // monitor's reroute when it did not.
+  NZ_CU(NZ_DRV(cuStreamWaitValue32)(reinterpret_cast<CUstream>(user), nz::railGateAddr(r), tag,
+                                    CU_STREAM_WAIT_VALUE_GEQ));
+  Entry e;
+  e.op = seq;
+  e.rail = ri;
+  e.tag = tag;
+  e.in = in;
+  e.out = out;
+  e.seg_off = o.seg_off;
+  e.seg_len = o.seg_len;
+  e.chunk = C;
+  e.chunk_end = (o.seg_len + C - 1) / C;
+  e.dtype = dtype;
+  e.plan = plan;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!entry_pool.empty()) {
+      e.end = entry_pool.back();
+      entry_pool.pop_back();
+    }
+  }
+  if (!e.end) NZ_CUDA(cudaEventCreateWithFlags(&e.end, cudaEventDisableTiming));
+  NZ_CUDA(cudaEventRecord(e.end, st));
+  if (p) p->tags.emplace_back(ri, tag);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    inflight.push_back(std::move(e));
+  }
+  cv.notify_all();
+}
+
 void nz_engine::op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dtype, cudaStream_t user) {
   const uint32_t seq = op_seq++;
   // Inside a CUDA graph capture (graph-safe rails only) nothing may wait on
-  // the device: no Timer harvest, no Timer sample, no failure injection.
+  // the device: no Timer harvest, no Timer sample, no failure injection, no
+  // monitor entries or gates.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   NZ_CUDA(cudaStreamIsCapturing(user, &cap));
   const bool capturing = cap != cudaStreamCaptureStatusNone;
@@ -111,18 +170,16 @@ void nz_engine::op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dty
   } else {
     harvest(seq);
   }
+  applyTableEvents(seq);
   nezha::Plan plan = bal->allocate(len);
-  const int world = comm->world;
-  if (!plan.hot && inject.find(seq) == inject.end()) {
+  if (!plan.hot) {
     // Cold (or rho-gated) op: one rail, launched straight on the caller's
     // stream — no fork/join, no Timer events. A single-rail sample cannot
     // move the table (a cold flush only records telemetry), so skipping it
     // leaves every decision unchanged (P11).
-    const auto& rs = plan.segments[0];
-    nz_rail* r = rails[index(rs.rail_id)];
-    const uint64_t C = nezha::defaultChunkBytes(rs.segment.length, world, algo);
-    nz::railAllreduce(r, in, out, base + rs.segment.offset, rs.segment.length, C, 0, UINT64_MAX, dtype, seq, -1,
-                      user);
+    launchSegment(seq, plan, plan.segments[0], in, out, base, dtype, user, nullptr, capturing, user, nullptr,
+                  nullptr);
+    inject.erase(seq);
     recordPlan(seq, base, len, std::move(plan));
     return;
   }
@@ -131,10 +188,6 @@ void nz_engine::op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dty
   p.plan = plan;
   p.start = event();
   NZ_CUDA(cudaEventRecord(p.start, user));
-  auto inj = inject.find(seq);
-  const nezha::Segment* failed_seg = nullptr;
-  int failed_rail = -1;
-  uint64_t failed_chunk = 0;
   std::vector<std::pair<int, uint64_t>> segs;
   for (const auto& rs : plan.segments) segs.emplace_back(rs.rail_id, rs.segment.length);
   std::string grant_log;
@@ -143,36 +196,11 @@ void nz_engine::op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dty
     const auto& rs = plan.segments[si];
     nz_rail* r = rails[index(rs.rail_id)];
     NZ_CUDA(cudaStreamWaitEvent(r->stream, p.start, 0));
-    const uint64_t C = nezha::defaultChunkBytes(rs.segment.length, world, algo);
-    int64_t fail_chunk = -1;
-    if (inj != inject.end() && inj->second.first == rs.rail_id) {
-      fail_chunk = static_cast<int64_t>(inj->second.second);
-      const uint64_t nch = (rs.segment.length + C - 1) / C;
-      if (inj->second.second < nch) {
-        failed_seg = &rs.segment;
-        failed_rail = rs.rail_id;
-        failed_chunk = inj->second.second;
-      }
-    }
-    nz::railAllreduce(r, in, out, base + rs.segment.offset, rs.segment.length, C, 0, UINT64_MAX, dtype, seq,
-                      fail_chunk, r->stream, &gates[si]);
-    cudaEvent_t e = event();
-    NZ_CUDA(cudaEventRecord(e, r->stream));
+    cudaEvent_t e = nullptr;
+    launchSegment(seq, plan, rs, in, out, base, dtype, r->stream, &gates[si], capturing, user, &e, &p);
     p.ends.emplace_back(rs.rail_id, e);
   }
-  if (inj != inject.end()) {
-    const int rid = inj->second.first;
-    inject.erase(inj);
-    p.skip = true;
-    if (failed_seg) {
-      handoff(p, plan, *failed_seg, failed_rail, failed_chunk, in, out, base, dtype);
-    } else if (health->state(rid).status != nezha::HealthStatus::Failed) {
-      // Idle failure: the rail carried nothing at / after that chunk.
-      health->channelDown(rid);
-      bal->markFailed(rid);
-    }
-  }
-  for (auto& [id, e] : p.ends) NZ_CUDA(cudaStreamWaitEvent(user, e, 0));
+  if (inject.erase(seq)) p.skip = true;
   recycleGates();
   if (capturing) {  // the captured records become graph edges: the events are free again
     for (auto& [id, e] : p.ends) pool.push_back(e);
@@ -206,65 +234,6 @@ int64_t nz_engine::realtimeNs() {
   timespec ts;
   clock_gettime(CLOCK_REALTIME, &ts);
   return static_cast<int64_t>(ts.tv_sec) * 1000000000LL + ts.tv_nsec;
-}
-
-void nz_engine::calibrateClock() {
-  int64_t best = INT64_MAX;
-  for (int i = 0; i < 5; ++i) {
-    stamps_host[0] = 0;
-    const int64_t t0 = realtimeNs();
-    nz::launchStamp(stamps_dev + 0, ctrl);
-    NZ_CUDA(cudaStreamSynchronize(ctrl));
-    const int64_t t1 = realtimeNs();
-    if (t1 - t0 < best) {
-      best = t1 - t0;
-      clock_offset_ns = static_cast<int64_t>(stamps_host[0]) - (t0 + t1) / 2;
-    }
-  }
-}
-
-void nz_engine::handoff(Pending& p, const nezha::Plan& plan, const nezha::Segment& seg, int rid, uint64_t k,
-                        nz_buf* in, nz_buf* out, uint64_t base, int dtype) {
-  nz_rail* fr = rails[index(rid)];
-  nz_fault_record_t rec{};
-  const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(60);
-  for (;;) {
-    volatile nz_fault_record_t* f = fr->fault_host;
-    if (f->valid) {
-      __sync_synchronize();
-      rec.op_seq = f->op_seq;
-      rec.chunk = f->chunk;
-      rec.t_fail_ns = f->t_fail_ns;
-      f->valid = 0;
-      host_seen_ns = realtimeNs();
-      break;
-    }
-    if (*reinterpret_cast<volatile int*>(fr->wd_host)) fail(NZ_ERR_TIMEOUT, "rail watchdog fired while waiting for a fault");
-    if (std::chrono::steady_clock::now() > deadline) fail(NZ_ERR_TIMEOUT, "fault record never arrived");
-  }
-  std::memset(stamps_host, 0, 4 * sizeof(uint64_t));
-  stamps_host[3] = rec.t_fail_ns;
-  nz::launchStamp(stamps_dev + 0, ctrl);  // detection acknowledged on the device timeline
-  health->channelDown(rid);
-  bal->markFailed(rid);
-  const auto target = nezha::chooseHandoffTarget(plan, rid, healthyIds());
-  if (!target) fail(NZ_ERR_UNRECOVERABLE, "no surviving rail to take over the orphaned segment");
-  const uint64_t C = nezha::defaultChunkBytes(seg.length, comm->world, algo);
-  const nezha::Segment orphan = nezha::orphanOf(seg, C, k);
-  nz_rail* tr = rails[index(*target)];
-  nz::launchStamp(stamps_dev + 1, tr->stream);
-  nz::railAllreduce(tr, in, out, base + seg.offset, seg.length, C, k, UINT64_MAX, dtype, p.op, -1, tr->stream);
-  nz::launchStamp(stamps_dev + 2, tr->stream);
-  cudaEvent_t e = event();
-  NZ_CUDA(cudaEventRecord(e, tr->stream));
-  p.ends.emplace_back(*target, e);
-  fo = nz_failover_report_t{};
-  fo.op_seq = p.op;
-  fo.failed_rail = rid;
-  fo.target_rail = *target;
-  fo.orphan_offset = base + orphan.offset;
-  fo.orphan_length = orphan.length;
-  fo_pending = true;
 }
 
 void nz_engine::staged(const char* src, char* dst, uint64_t bytes, int dtype, cudaMemcpyKind kin,
@@ -312,19 +281,21 @@ void nz_engine::staged(const char* src, char* dst, uint64_t bytes, int dtype, cu
 }
 
 void nz_engine::synchronize() {
-  NZ_CUDA(cudaDeviceSynchronize());  // rail streams and cold ops on callers' streams
-  // Asynchronous failure path: a rail kernel whose barrier / LL poll timed
-  // out (a peer never arrived) sets its watchdog word and exits. Ranks
-  // agree (any rank saw it) and the rail goes Failed everywhere, so the
-  // tables stay identical; the caller learns the results since the last
-  // synchronize are not to be trusted (ChannelDownError, error.hpp:22-27).
+  NZ_CUDA(cudaDeviceSynchronize());  // rail streams, gated caller streams (the monitor releases them)
+  if (monitored) drainMonitor();
+  // Without the monitor a rail kernel whose cross-rank wait timed out sets
+  // its watchdog word and exits: ranks agree (any rank saw it) and the rail
+  // goes Failed everywhere, so the tables stay identical; the caller learns
+  // the results since the last synchronize are not to be trusted
+  // (ChannelDownError, error.hpp:22-27). With the monitor those launches
+  // were rerouted already: the words are just cleared.
   std::vector<int32_t> flags(rails.size(), 0);
   for (size_t i = 0; i < rails.size(); ++i) {
     volatile int* w = rails[i]->wd_host;
-    flags[i] = *w;
+    flags[i] = monitored ? 0 : *w;
     *w = 0;
   }
-  if (comm->world > 1) {
+  if (comm->world > 1 && !monitored) {
     const auto msgs = nz::exchange(comm, flags.data(), flags.size() * sizeof(int32_t), {});
     for (const auto& m : msgs) {
       const int32_t* v = reinterpret_cast<const int32_t*>(m.data.data());
@@ -340,12 +311,17 @@ void nz_engine::synchronize() {
       bal->markFailed(specs[i].rail_id);
     }
   }
-  finishFailoverReport();
   drainTimer();  // every rank harvests the same ops here
   if (!down.empty()) {
     fail(NZ_ERR_RAIL_DOWN, "rail watchdog fired on rail(s) " + down +
                                ": marked Failed and excluded; results since the last synchronize are invalid");
   }
+  std::string err;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    err.swap(mon_error);
+  }
+  if (!err.empty()) fail(NZ_ERR_UNRECOVERABLE, "failure monitor: " + err);
 }
 
 void nz_engine::ensureUnbound(uint64_t bytes) {
@@ -361,16 +337,18 @@ void nz_engine::ensureUnbound(uint64_t bytes) {
 std::string nz_engine::stateJson() {
   std::ostringstream o;
   o << "{\"op_seq\":" << op_seq << ",\"world\":" << comm->world << ",\"rank\":" << comm->rank
+    << ",\"loopback\":" << (comm->loop ? "true" : "false")
     << ",\"sync_overhead_us\":" << nezha::formatDouble(bal->config().sync_overhead_us) << ",\"rails\":[";
+  std::lock_guard<std::mutex> lk(mu);
   for (size_t i = 0; i < specs.size(); ++i) {
     const auto& p = bal->rails()[i];
     o << (i ? "," : "") << "{\"rail_id\":" << specs[i].rail_id << ",\"kind\":\""
       << (specs[i].kind == NZ_RAIL_NVLS ? "nvls" : specs[i].kind == NZ_RAIL_CE ? "ce" : "sm")
-      << "\",\"sm_budget\":" << rails[i]->sm_budget << ",\"ll_max\":" << rails[i]->ll_max
-      << ",\"oneshot_max\":" << rails[i]->os_max << ",\"protocol\":\"" << nezha::toString(p.protocol) << "\",\"health\":\""
-      << nezha::toString(health->state(specs[i].rail_id).status) << "\",\"t_setup_us\":"
-      << nezha::formatDouble(p.t_setup_us) << ",\"bandwidth_bps\":" << nezha::formatDouble(p.bandwidth_bps)
-      << ",\"calibration\":[";
+      << "\",\"sm_budget\":" << rails[i]->sm_budget << ",\"ll_max\":" << rails[i]->ll_max << ",\"protocol\":\""
+      << nezha::toString(p.protocol) << "\",\"health\":\"" << nezha::toString(health->state(specs[i].rail_id).status)
+      << "\",\"planned\":" << (bal->healthy(specs[i].rail_id) ? "true" : "false")
+      << ",\"t_setup_us\":" << nezha::formatDouble(p.t_setup_us)
+      << ",\"bandwidth_bps\":" << nezha::formatDouble(p.bandwidth_bps) << ",\"calibration\":[";
     for (size_t j = 0; j < p.efficiency_points.size(); ++j)
       o << (j ? "," : "") << "[" << p.efficiency_points[j].first << ","
         << nezha::formatDouble(p.efficiency_points[j].second) << "]";
@@ -388,6 +366,14 @@ std::string nz_engine::stateJson() {
   o << "],\"compute_pool\":{\"mode\":" << static_cast<int>(pool_mode) << ",\"tokens\":"
     << (cpool ? cpool->totalTokens() : 0) << ",\"ops\":" << pool_stats.ops << ",\"waits\":" << pool_stats.waits
     << ",\"shrunk\":" << pool_stats.shrunk << "}";
+  o << ",\"monitor\":{\"on\":" << (monitored ? "true" : "false") << ",\"failovers\":" << reports.size()
+    << ",\"inflight\":" << inflight.size() << ",\"failed\":[";
+  bool first = true;
+  for (int id : agreed_failed) {
+    o << (first ? "" : ",") << id;
+    first = false;
+  }
+  o << "]}";
   o << ",\"table\":" << bal->tableJson() << "}";
   return o.str();
 }
@@ -424,8 +410,14 @@ void nz_engine_config_default(nz_engine_config_t* c) {
   c->rails_toml = nullptr;
   c->calibrate_iters = 20;
   c->calibrate_max_bytes = uint64_t{1} << 30;
-  c->timer_lag = 2;
+  // Op k is harvested when op k + 16 is issued: the issuing thread (e.g. a
+  // DDP hook inside backward) runs up to 16 ops ahead of the device.
+  c->timer_lag = 16;
   c->tune_budgets = 0;  // on once its hardware sweep is recorded in profiles/
+  c->monitor = 1;
+  c->detect_us = 0;
+  c->heartbeat_us = 50000;
+  c->readmit_hold_us = 1e6;
 }
 
 int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t** out) {
@@ -440,8 +432,12 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     }
     auto& c = eng->cfg;
     if (c.timer_lag < 1) c.timer_lag = 1;
+    if (!(c.heartbeat_us > 0)) c.heartbeat_us = 50000;
+    if (c.readmit_hold_us < 0) c.readmit_hold_us = 0;
     if (c.compute_pool < 0 || c.compute_pool > 2) fail(NZ_ERR_INVALID, "compute_pool must be 0 (off), 1 (block) or 2 (shrink)");
     if (c.pool_tokens < 0) fail(NZ_ERR_INVALID, "pool_tokens must be >= 0");
+    if (c.graph_safe && comm->loop && comm->world > 1)
+      fail(NZ_ERR_UNSUPPORTED, "graph-safe engines need one process per rank (loopback launches cannot be captured)");
     eng->pool_mode = static_cast<nezha::PoolMode>(c.compute_pool);
     eng->cpool = std::make_unique<nezha::ComputePool>(c.pool_tokens > 0 ? c.pool_tokens : std::max(1, comm->sm_count));
     eng->algo = c.algorithm == NZ_ALGO_RING ? nezha::Algorithm::Ring : nezha::Algorithm::RingChunked;
@@ -463,12 +459,16 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     }
     std::sort(eng->specs.begin(), eng->specs.end(), [](auto& a, auto& b) { return a.rail_id < b.rail_id; });
     NZ_CUDA(cudaSetDevice(comm->device));
+    // Destroys whatever was built if a later step throws.
+    struct Cleanup {
+      std::unique_ptr<nz_engine>* e;
+      ~Cleanup() {
+        if (*e) nz_engine_destroy(e->release());
+      }
+    } cleanup{&eng};
     for (auto& s : eng->specs) {
-      nz_rail_t* r = nullptr;
-      const int rc = nz_rail_create_ex(comm, s.kind, s.rail_id, s.sm_budget, c.graph_safe ? NZ_RAIL_FLAG_GRAPH_SAFE : 0,
-                                       &r);
-      if (rc != NZ_OK) fail(rc, nz_last_error());
-      eng->rails.push_back(r);
+      eng->rails.push_back(nz::railCreate(comm, s.kind, s.rail_id, s.sm_budget, c.graph_safe != 0, false));
+      eng->rails.back()->detect_us = c.detect_us;
     }
     std::vector<int> ids;
     std::vector<nezha::RailProfile> profiles;
@@ -494,17 +494,18 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     eng->bal = std::make_unique<nezha::Balancer>(profiles, bc);
     nz_engine* raw = eng.get();
     eng->bal->setAgreement([raw](int, const std::vector<std::pair<int, nezha::Micros>>& m) { return raw->agree(m); });
-    eng->health = std::make_unique<nezha::HealthMonitor>(ids);
+    eng->health = std::make_unique<nezha::HealthMonitor>(ids, c.heartbeat_us);
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->ctrl, cudaStreamNonBlocking));
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->io, cudaStreamNonBlocking));
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->h2d, cudaStreamNonBlocking));
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->d2h, cudaStreamNonBlocking));
-    NZ_CUDA(cudaHostAlloc(&eng->stamps_host, 4 * sizeof(uint64_t), cudaHostAllocMapped));
-    std::memset(eng->stamps_host, 0, 4 * sizeof(uint64_t));
-    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eng->stamps_dev), eng->stamps_host, 0));
+    NZ_CUDA(cudaHostAlloc(&eng->rec_stamps_host, 4 * sizeof(uint64_t), cudaHostAllocMapped));
+    std::memset(eng->rec_stamps_host, 0, 4 * sizeof(uint64_t));
+    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eng->rec_stamps_dev), eng->rec_stamps_host, 0));
     eng->calibrateClock();
     if (!all_profiles || c.sync_overhead_us < 0) eng->calibrate();
     NZ_CUDA(cudaDeviceSynchronize());
+    eng->startMonitor();
     *out = eng.release();
   });
 }
@@ -514,20 +515,24 @@ int nz_engine_destroy(nz_engine_t* eng) {
     if (!eng) return;
     cudaSetDevice(eng->comm->device);
     cudaDeviceSynchronize();
+    eng->stopMonitor();
     for (auto e : eng->pool) cudaEventDestroy(e);
     for (auto e : eng->pool_pending) cudaEventDestroy(e);
+    for (auto e : eng->entry_pool) cudaEventDestroy(e);
+    for (auto& en : eng->inflight) cudaEventDestroy(en.end);
     for (auto& p : eng->pending) {
       cudaEventDestroy(p.start);
       for (auto& pr : p.ends) cudaEventDestroy(pr.second);
     }
-    for (auto* r : eng->rails) nz_rail_destroy(r);
+    for (auto* r : eng->twins) nz::railDestroy(r);
+    for (auto* r : eng->rails) nz::railDestroy(r);
     if (eng->ub_in) nz::freeSymmetric(eng->ub_in);
     if (eng->ub_out) nz::freeSymmetric(eng->ub_out);
     if (eng->ctrl) cudaStreamDestroy(eng->ctrl);
     if (eng->io) cudaStreamDestroy(eng->io);
     if (eng->h2d) cudaStreamDestroy(eng->h2d);
     if (eng->d2h) cudaStreamDestroy(eng->d2h);
-    if (eng->stamps_host) cudaFreeHost(eng->stamps_host);
+    if (eng->rec_stamps_host) cudaFreeHost(eng->rec_stamps_host);
     delete eng;
   });
 }
@@ -560,7 +565,6 @@ int nz_engine_allreduce_host(nz_engine_t* eng, const void* host_in, void* host_o
                 cudaMemcpyDeviceToHost, nullptr);
     NZ_CUDA(cudaStreamSynchronize(eng->d2h));
     NZ_CUDA(cudaStreamSynchronize(eng->io));
-    eng->finishFailoverReport();
   });
 }
 
@@ -581,19 +585,18 @@ int nz_engine_inject_failure(nz_engine_t* eng, uint32_t op_seq, int rail_id, uin
     if (!eng) fail(NZ_ERR_INVALID, "null engine");
     eng->index(rail_id);
     if (op_seq < eng->op_seq) fail(NZ_ERR_INVALID, "op already issued");
+    if (chunk > static_cast<uint64_t>(INT64_MAX)) fail(NZ_ERR_INVALID, "chunk out of range");
+    if (!eng->monitored && eng->comm->world > 1)
+      fail(NZ_ERR_INVALID, "failure injection needs the failure monitor (config monitor = 1)");
     eng->inject[op_seq] = {rail_id, chunk};
-    eng->calibrateClock();  // %globaltimer drifts against the host clock: re-anchor next to the op
   });
 }
 
 int nz_engine_readmit(nz_engine_t* eng, int rail_id) {
   return guarded([&] {
     if (!eng) fail(NZ_ERR_INVALID, "null engine");
-    eng->synchronize();
-    eng->drainTimer();
-    eng->health->heartbeat(rail_id, 0);
-    eng->health->readmit(rail_id, 0, 0);
-    eng->bal->readmit(rail_id);
+    NZ_CUDA(cudaSetDevice(eng->comm->device));
+    eng->readmit(rail_id);
   });
 }
 
@@ -609,9 +612,23 @@ uint32_t nz_engine_op_seq(const nz_engine_t* eng) { return eng ? eng->op_seq : 0
 
 int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep) {
   if (!eng || !rep) return NZ_ERR_INVALID;
-  eng->finishFailoverReport();
-  if (!eng->have_fo) return NZ_ERR_INVALID;
-  *rep = eng->fo;
+  std::lock_guard<std::mutex> lk(eng->mu);
+  if (eng->reports.empty()) return NZ_ERR_INVALID;
+  *rep = eng->reports.back();
+  return NZ_OK;
+}
+
+int nz_engine_failover_count(nz_engine_t* eng) {
+  if (!eng) return NZ_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(eng->mu);
+  return static_cast<int>(eng->reports.size());
+}
+
+int nz_engine_failover_get(nz_engine_t* eng, int i, nz_failover_report_t* rep) {
+  if (!eng || !rep) return NZ_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(eng->mu);
+  if (i < 0 || i >= static_cast<int>(eng->reports.size())) return NZ_ERR_INVALID;
+  *rep = eng->reports[i];
   return NZ_OK;
 }
 

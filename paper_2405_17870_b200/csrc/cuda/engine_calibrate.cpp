@@ -46,19 +46,19 @@ void nz_engine::tunePaths(uint64_t maxb, cudaEvent_t e0, cudaEvent_t e1) {
   if (comm->world == 1) return;
   for (size_t i = 0; i < rails.size(); ++i) {
     nz_rail* r = rails[i];
-    if (r->ll_cap == 0 && r->os_cap == 0) continue;
+    if (r->ll_cap == 0) continue;
     std::vector<uint64_t> sizes;
     for (uint64_t sz = 64 << 10; sz <= std::min<uint64_t>(uint64_t{4} << 20, maxb); sz *= 2) sizes.push_back(sz);
     if (sizes.empty()) continue;
-    // times[k][v]: v = 0 LL, 1 one-shot, 2 two-shot; huge when not applicable.
+    // times[3k + v]: v = 0 LL, 2 two-shot (1, the staged one-shot of round 1,
+    // is gone: never applicable); huge when not applicable.
     std::vector<double> t(sizes.size() * 3, 1e30);
     for (size_t k = 0; k < sizes.size(); ++k) {
       const uint64_t s = sizes[k];
       const uint64_t C = nezha::defaultChunkBytes(s, comm->world, algo);
-      for (int v = 0; v < 3; ++v) {
-        if ((v == 0 && s > r->ll_cap) || (v == 1 && s > r->os_cap)) continue;
+      for (int v : {0, 2}) {
+        if (v == 0 && s > r->ll_cap) continue;
         r->ll_max = v == 0 ? r->ll_cap : 0;
-        r->os_max = v == 1 ? r->os_cap : 0;
         for (int w = 0; w < 3; ++w) nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
         NZ_CUDA(cudaEventRecord(e0, r->stream));
         for (int it = 0; it < 20; ++it) nz::railAllreduce(r, ub_in, ub_out, 0, s, C, 0, UINT64_MAX, NZ_F32, 0, -1, r->stream);
@@ -74,9 +74,7 @@ void nz_engine::tunePaths(uint64_t maxb, cudaEvent_t e0, cudaEvent_t e1) {
       const double* v = reinterpret_cast<const double*>(msgs[rk].data.data());
       for (size_t j = 0; j < t.size(); ++j) t[j] = std::max(t[j], v[j]);
     }
-    const auto [ll_max, os_max] = nezha::choosePathCeilings(sizes, t, r->ll_cap, r->os_cap);
-    r->ll_max = ll_max;
-    r->os_max = os_max;
+    r->ll_max = nezha::choosePathCeilings(sizes, t, r->ll_cap, 0).first;
   }
 }
 

@@ -1,14 +1,19 @@
 // nz_engine: state and operations of one rank's multi-rail engine, shared by
-// engine.cpp (ops, Timer, faults, C ABI) and engine_calibrate.cpp (startup
-// calibration and tuning). Flow and contract: include/nezha/engine.hpp.
+// engine.cpp (ops, Timer, C ABI), engine_monitor.cpp (failure monitor,
+// reroute, readmit) and engine_calibrate.cpp (startup calibration and
+// tuning). Flow and contract: include/nezha/engine.hpp.
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
 #include <deque>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <sstream>
 #include <thread>
 
@@ -30,25 +35,43 @@ struct nz_engine {
     nezha::Plan plan;
     cudaEvent_t start = nullptr;
     std::vector<std::pair<int, cudaEvent_t>> ends;
+    std::vector<std::pair<int, uint32_t>> tags;  // (rail index, entry tag) of monitored segments
     bool skip = false;  // an op that lost a rail is not a Timer sample
+  };
+
+  // One rail's part of one op, watched by the monitor until it retires
+  // (DESIGN.md §6b). The geometry is what a reroute re-reduces.
+  struct Entry {
+    uint32_t op = 0;
+    int rail = 0;  // index into rails
+    uint32_t tag = 0;
+    nz_buf* in = nullptr;
+    nz_buf* out = nullptr;
+    uint64_t seg_off = 0, seg_len = 0, chunk = 0, chunk_end = 0;
+    int dtype = NZ_F32;
+    nezha::Plan plan;
+    cudaEvent_t end = nullptr;
+  };
+
+  // A table change agreed by every rank, applied before op `activation` is
+  // planned (so every rank plans every op against the same table).
+  struct TableEvent {
+    uint32_t activation = 0;
+    int rail_id = 0;
   };
 
   nz_comm* comm = nullptr;
   nz_engine_config_t cfg{};
   std::vector<nezha::RailSpec> specs;  // sorted by rail_id
   std::vector<nz_rail*> rails;         // parallel to specs
-  std::unique_ptr<nezha::Balancer> bal;
-  std::unique_ptr<nezha::HealthMonitor> health;
+  std::vector<nz_rail*> twins;         // recovery twin per rail (monitor only), parallel to specs
+  std::unique_ptr<nezha::Balancer> bal;  // owned by the issuing thread
+  std::unique_ptr<nezha::HealthMonitor> health;  // owned by the monitor thread (under mu)
   nezha::Algorithm algo = nezha::Algorithm::RingChunked;
   uint32_t op_seq = 0;
   std::deque<Pending> pending;
   std::vector<cudaEvent_t> pool;
   std::map<uint32_t, std::pair<int, uint64_t>> inject;
-  nz_failover_report_t fo{};
-  bool have_fo = false;
-  bool fo_pending = false;
-  uint64_t* stamps_host = nullptr;  // [0] detect, [1] resume, [2] done, [3] fault
-  uint64_t* stamps_dev = nullptr;
   cudaStream_t ctrl = nullptr;
   cudaStream_t io = nullptr;
   cudaStream_t h2d = nullptr;  // host path: uploads of the next piece
@@ -64,8 +87,7 @@ struct nz_engine {
     std::string grants;  // [rail, demand, grant, [waits]]... when the ComputePool is on
   };
   std::vector<PlanRecord> last_plans;
-  int64_t clock_offset_ns = 0;          // %globaltimer - CLOCK_REALTIME
-  int64_t host_seen_ns = 0;             // host monitor saw the last fault record
+  int64_t clock_offset_ns = 0;  // %globaltimer - CLOCK_REALTIME
   struct RailStat {
     uint64_t ops = 0;
     double us = 0;
@@ -80,6 +102,24 @@ struct nz_engine {
     uint64_t waits = 0;   // computation phases ordered after an earlier holder
     uint64_t shrunk = 0;  // grants below demand
   } pool_stats;
+
+  // ---- failure monitor (engine_monitor.cpp) ----
+  bool monitored = false;  // cfg.monitor and world > 1
+  std::mutex mu;           // everything below, shared by the two threads
+  std::condition_variable cv;
+  std::deque<Entry> inflight;                 // issue order
+  std::vector<cudaEvent_t> entry_pool;        // retired entry events
+  std::deque<TableEvent> table_events;        // agreed, not yet applied
+  std::set<int> agreed_failed;                // rail ids failed by agreement
+  std::set<uint32_t> lost_ops;                // ops whose result needed a reroute
+  uint32_t issued = 0;                        // ops planned by the issuing thread
+  bool agreeing = false;                      // the monitor is agreeing: planning waits
+  bool mon_stop = false;
+  std::string mon_error;                      // surfaced at the next synchronize
+  std::vector<nz_failover_report_t> reports;  // every failover, in order
+  std::thread mon;
+  uint64_t* rec_stamps_host = nullptr;  // [0] resume, [1] done of the current reroute
+  uint64_t* rec_stamps_dev = nullptr;
 
   int index(int rail_id) const {
     for (size_t i = 0; i < specs.size(); ++i)
@@ -105,10 +145,6 @@ struct nz_engine {
 
   void drainTimer() { harvest(UINT32_MAX - 8); }
 
-  std::vector<int> healthyIds() const { return health->healthyRails(); }
-
-  void finishFailoverReport();
-
   // Computation-phase gates of one concurrent launch of `segs` (rail_id,
   // length) in rail order; empty when the pool is off. The release events go
   // back to the event pool once the launch is enqueued (waits are captured at
@@ -119,22 +155,20 @@ struct nz_engine {
 
   // One op (piece) of at most 1 GiB at byte offset `base`.
   void op(nz_buf* in, nz_buf* out, uint64_t base, uint64_t len, int dtype, cudaStream_t user);
+  // One rail segment of an op: launches, entry for the monitor, stream gate.
+  void launchSegment(uint32_t seq, const nezha::Plan& plan, const nezha::RailSegment& rs, nz_buf* in, nz_buf* out,
+                     uint64_t base, int dtype, cudaStream_t st, nz::ComputeGate* gate, bool capturing,
+                     cudaStream_t user, cudaEvent_t* end_out, Pending* p);
 
   void recordPlan(uint32_t seq, uint64_t base, uint64_t len, nezha::Plan&& plan, std::string&& grants = {});
 
   std::string planRecordJson(const PlanRecord& r) const;
 
-  // Exception handler: wait for the device's fault record,
-  // mark the rail Failed, pick the target (P9) and run the orphan chunks on
-  // it with the failed segment's geometry (P10), after its current task.
   static int64_t realtimeNs();
 
   // %globaltimer vs host CLOCK_REALTIME: best of 5 stamp round trips. Lets
-  // the report place the host monitor's detection on the device timeline.
+  // the reports place host-side detection on the device timeline.
   void calibrateClock();
-
-  void handoff(Pending& p, const nezha::Plan& plan, const nezha::Segment& seg, int rid, uint64_t k, nz_buf* in,
-               nz_buf* out, uint64_t base, int dtype);
 
   // Allreduce of memory outside the symmetric heap (host, or device memory
   // the caller owns): a three-stage pipeline over pieces.
@@ -153,6 +187,20 @@ struct nz_engine {
 
   void ensureUnbound(uint64_t bytes);
 
+  // ---- monitor thread (engine_monitor.cpp) ----
+  void startMonitor();
+  void stopMonitor();
+  void monitorLoop();
+  // Handles the failed front entry: agreement on the orphan, P9 target,
+  // reroute on the target's twin, gate release, report.
+  void failover(Entry e, int64_t seen_ns);
+  // Applies agreed table events due before planning op `seq` (issuing thread).
+  void applyTableEvents(uint32_t seq);
+  // Waits until every entry issued so far retired or was rerouted.
+  void drainMonitor();
+  // SPEC.md:398-406 with probes on the rail (collective).
+  void readmit(int rail_id);
+
   // Startup calibration: each rail alone over a size sweep, then the
   // coordination cost of a fork/join over all rails.
   // CTA budget of the SM-driven rails, measured instead of assumed: each
@@ -163,11 +211,9 @@ struct nz_engine {
   void tuneBudgets(uint64_t maxb, cudaEvent_t e0, cudaEvent_t e1);
 
   // Which protocol a rail uses at which size, measured instead of assumed:
-  // for rails with more than one path (SM: one-shot LL, optional one-shot
-  // staging, two-shot) every path is timed at sizes 64 KiB .. 4 MiB, ranks
-  // agree on the times (max), and each ceiling becomes the largest size of
-  // the contiguous run of sizes where that path was fastest. Per rail, the
-  // same on every rank; the startup profiles are then measured with it.
+  // for rails with an LL path (SM) both paths are timed at sizes 64 KiB ..
+  // 4 MiB, ranks agree on the times (max), and the LL ceiling becomes the
+  // largest size of the contiguous run of sizes where LL was fastest.
   void tunePaths(uint64_t maxb, cudaEvent_t e0, cudaEvent_t e1);
 
   void calibrate();
@@ -178,4 +224,3 @@ struct nz_engine {
 
   std::string stateJson();
 };
-

@@ -8,12 +8,29 @@
 //   K3 fold_kernel<.., NDST=N> : SM rail, 128-bit peer loads from every rank,
 //                      in-register fold in ring order, 128-bit peer stores of
 //                      the sum to every rank (the "TCP" rail).
+//   K4 barrier_kernel: the copy-engine rail's start / end barriers.
+//   K5 ll_kernel     : SM rail one-shot for small payloads (flag-tagged words).
+//   K6 copy_kernel   : N = 1 (the identity allreduce).
 //
 // Summation order (P1): an element of ring block b of its chunk is
 // folded x_b + x_{b+1} + ... + x_{b-1}. A CTA walks its contiguous share of
 // the shard run by run (a run = one ring block of one chunk), so the
 // rotation is resolved once per run, not per vector; the rare 16-byte vector
 // that straddles a run boundary is folded element by element.
+//
+// Failure handling. Every rail launch carries a RailCtl: the
+// last CTA to retire on a rank publishes the launch's progress and, when the
+// launch completes an op entry, writes the entry's tag into the rail's gate
+// word (the callers' streams wait on it with cuStreamWaitValue32). A launch
+// that fails — a cross-rank wait timed out or was aborted by the host
+// monitor, or an injected dead link — writes nothing, marks the rail failed
+// on this rank (sticky: later launches exit at once without touching peers)
+// and stamps the host-mapped status record the monitor reads.
+//
+// Loopback (nz_comm_init_loopback): the *_vr kernels run every virtual rank
+// of a one-GPU job in one grid, blockIdx.y = rank, each with its own
+// arguments; the cross-rank waits are then between CTAs of that grid, which
+// the host sizes to be co-resident.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -31,16 +48,36 @@ struct Geometry {
   uint64_t chunk;
 };
 
+// Words of a rail's device control block (RailCtl::dev).
+enum : int {
+  kCtlRetired = 0,  // CTAs of the current launch that retired
+  kCtlFailed = 1,   // a CTA of the current launch failed
+  kCtlGate = 2,     // tag of the last op entry completed on this rank
+  kCtlSticky = 3,   // the rail failed on this rank: launches exit at once
+  kCtlSeq = 4,      // launches retired (graph-safe epochs / LL flags)
+  kCtlWords = 8,
+};
+
+struct RailCtl {
+  uint32_t* dev;              // nullptr: launch without status (emulation, CE reduce)
+  nz_rail_status_t* host;     // host-mapped record for the engine's monitor
+  uint32_t tag;               // op entry this launch belongs to
+  int final_wave;             // last launch of the entry: gate on success
+  int stall;                  // injected dead link: stop after the start barrier
+  uint64_t prog_chunk;        // chunks complete once this launch succeeds (~0: none)
+  uint64_t end_timeout_ns;    // budget of the end barrier (failure detection)
+};
+
 // Cross-rank per-CTA barrier pads of one rail: slot [cta][rank] of rank p's
 // pad is written only by `rank`, with monotonically increasing epochs.
 struct BarrierArgs {
   uint32_t* local;
   uint32_t* peer[kDevMaxRanks];
   uint32_t epoch;
-  int* watchdog;  // host-mapped; set when a wait times out
-  uint64_t timeout_ns;  // give up after this long (NEZHA_WATCHDOG_MS, default 20 s)
-  int relaxed_poll;     // 1: poll ld.relaxed.sys, one fence.acq_rel.sys after (PTX acquire pattern)
-  uint32_t* seq;        // graph-safe rails: device [op counter, CTAs retired]; nullptr = host `epoch`
+  int* watchdog;                    // host-mapped; set when a wait times out
+  uint64_t timeout_ns;              // start-of-op budget (NEZHA_WATCHDOG_MS, default 20 s)
+  const uint32_t* seq;              // graph-safe rails: device launch counter; nullptr = host `epoch`
+  const volatile uint32_t* abort;   // host-mapped; nonzero = the monitor gave up on this rail
 };
 
 struct FaultPost {
@@ -59,12 +96,19 @@ struct FoldArgs {
   int use_barrier;
   int rank;
   FaultPost post;
+  RailCtl ctl;
 };
 
 struct NvlsArgs {
   char* mc_in;
   char* mc_out;
   FoldArgs f;  // unicast view for the unaligned head / tail and the barrier
+};
+
+// Arguments of every virtual rank of a loopback job, indexed by blockIdx.y.
+template <typename A>
+struct VPack {
+  A a[kDevMaxRanks];
 };
 
 // ------------------------------------------------------------ primitives --
@@ -86,12 +130,6 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
-__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ uint4 ld_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -105,38 +143,96 @@ __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-
-// Graph-safe rails (NZ_RAIL_FLAG_GRAPH_SAFE) take their barrier epochs and
-// LL flags from a device counter instead of kernel arguments, so a launch
-// captured in a CUDA graph stays valid on every replay. Every CTA reads the
-// counter on entry; the last CTA to retire advances it. A rail's launches are
-// stream ordered, so the next one sees the advanced value.
+// ------------------------------------------------------ launch status ------
 __device__ __forceinline__ uint32_t seq_read(const uint32_t* seq) {
   return *reinterpret_cast<const volatile uint32_t*>(seq);
 }
 
-__device__ __forceinline__ void seq_retire(uint32_t* seq) {
-  if (!seq) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(seq + 1, 1u) == gridDim.x - 1) {
-      atomicExch(seq + 1, 0u);
-      atomicAdd(seq, 1u);
-    }
-  }
-}
-
+// Graph-safe rails (NZ_RAIL_FLAG_GRAPH_SAFE) take their barrier epochs and LL
+// flags from the device launch counter (advanced by the last CTA of every
+// launch in rail_exit) instead of kernel arguments, so a launch captured in a
+// CUDA graph stays valid on every replay. A rail's launches are ordered, so
+// the next one sees the advanced value.
 __device__ __forceinline__ uint32_t op_epoch(const BarrierArgs& b) {
   return b.seq ? 2u * seq_read(b.seq) + 1u : b.epoch;
 }
 
-// Per-CTA barrier across ranks. Returns false (and flags the watchdog) if a
-// peer never arrived, so the kernel can exit instead of hanging the GPU.
-// `publish` = this CTA wrote peer-visible data that must land before peers
-// pass the barrier (each thread fences its own stores at system scope).
+// Entry of every CTA: false (uniformly over the CTA) when the rail failed on
+// this rank in an EARLIER launch, so this launch must not touch peers. The
+// sticky word holds (launch counter + 1) of the failing launch; the counter
+// only moves when a launch retires, so a failure inside the current launch
+// does not stop its other CTAs from arriving at the start barrier. CTA 0
+// stamps the start for the monitor's heartbeat clock.
+__device__ __forceinline__ bool rail_enter(const RailCtl& c) {
+  if (!c.dev) return true;
+  int dead = 0;
+  if (threadIdx.x == 0) {
+    const uint32_t sticky = *reinterpret_cast<const volatile uint32_t*>(c.dev + kCtlSticky);
+    const uint32_t seq = *reinterpret_cast<const volatile uint32_t*>(c.dev + kCtlSeq);
+    dead = sticky != 0 && static_cast<int32_t>(sticky - 1u - seq) < 0;
+    if (c.host && blockIdx.x == 0) {
+      volatile nz_rail_status_t* h = c.host;
+      h->t_start_ns = globaltimer();
+      h->start_tag = c.tag;
+    }
+  }
+  return __syncthreads_or(dead) == 0;
+}
+
+// A cross-rank wait gave up (timeout or host abort): device-side detection time.
+__device__ __forceinline__ void note_detect(const RailCtl* c, uint64_t now) {
+  if (c && c->host) {
+    volatile nz_rail_status_t* h = c->host;
+    h->t_det_ns = now;
+    h->det_tag = c->tag;
+  }
+}
+
+// The injected dead link of this rank stops here.
+__device__ __forceinline__ void note_stall(const RailCtl& c) {
+  if (c.host && blockIdx.x == 0 && threadIdx.x == 0) {
+    volatile nz_rail_status_t* h = c.host;
+    h->t_fail_ns = globaltimer();
+    h->fail_tag = c.tag;
+  }
+}
+
+// Exit of every CTA (every thread calls it; `ok` is uniform over the CTA).
+// The last CTA of the launch on this rank publishes the outcome.
+__device__ __forceinline__ void rail_exit(const RailCtl& c, bool ok) {
+  if (!c.dev) return;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (!ok) {
+    atomicExch(c.dev + kCtlFailed, 1u);
+    atomicExch(c.dev + kCtlSticky, *reinterpret_cast<const volatile uint32_t*>(c.dev + kCtlSeq) + 1u);
+  }
+  __threadfence_system();  // this CTA's stores (peer stores included) before it counts as retired
+  if (atomicAdd(c.dev + kCtlRetired, 1u) != gridDim.x - 1) return;
+  atomicExch(c.dev + kCtlRetired, 0u);
+  const bool failed = atomicExch(c.dev + kCtlFailed, 0u) != 0;
+  if (!failed) {
+    volatile nz_rail_status_t* h = c.host;
+    if (h && c.prog_chunk != ~0ull) {
+      h->prog_chunk = c.prog_chunk;
+      __threadfence_system();
+      h->prog_tag = c.tag;
+    }
+    if (c.final_wave) {
+      st_release_sys(c.dev + kCtlGate, c.tag);
+      if (h) h->ok_tag = c.tag;
+    }
+  }
+  atomicAdd(c.dev + kCtlSeq, 1u);
+}
+
+// Per-CTA barrier across ranks. Returns false (uniformly over the CTA) if a
+// peer did not arrive within `timeout_ns` or the host aborted the rail, so
+// the kernel exits instead of hanging the GPU. `publish` = this CTA wrote
+// peer-visible data that must land before peers pass the barrier.
 template <int N, bool kPublish>
-__device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch, int rank) {
+__device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch, int rank, uint64_t timeout_ns,
+                                            const RailCtl* ctl) {
   __shared__ int s_ok;
   if (threadIdx.x == 0) s_ok = 1;
   if (kPublish) fence_acq_rel_sys();
@@ -147,21 +243,20 @@ __device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch
     const uint32_t* slot = b.local + blockIdx.x * kDevMaxRanks + t;
     uint64_t t0 = 0;
     int spins = 0;
-    const bool relaxed = b.relaxed_poll != 0;
-    while (static_cast<int32_t>((relaxed ? ld_relaxed_sys(slot) : ld_acquire_sys(slot)) - epoch) < 0) {
+    while (static_cast<int32_t>(ld_acquire_sys(slot) - epoch) < 0) {
       if (++spins == 64) {
         spins = 0;
         const uint64_t now = globaltimer();
         if (t0 == 0) {
           t0 = now;
-        } else if (now - t0 > b.timeout_ns) {
-          atomicExch_system(b.watchdog, 1);
+        } else if (now - t0 > timeout_ns || (b.abort && *b.abort)) {
+          if (b.watchdog) atomicExch_system(b.watchdog, 1);
+          note_detect(ctl, now);
           s_ok = 0;
           break;
         }
       }
     }
-    if (relaxed) fence_acq_rel_sys();  // relaxed observation + fence = acquire pattern
   }
   __syncthreads();
   return s_ok != 0;
@@ -176,6 +271,10 @@ __device__ __forceinline__ void post_fault(const FaultPost& p) {
     __threadfence_system();
     r->valid = 1;
   }
+}
+
+__device__ __forceinline__ uint64_t end_budget(const BarrierArgs& b, const RailCtl& c) {
+  return c.end_timeout_ns ? c.end_timeout_ns : b.timeout_ns;
 }
 
 // ------------------------------------------------------------ dtype folds --
@@ -196,7 +295,6 @@ struct F32 {
   __device__ static float sload(const char* p) { return *reinterpret_cast<const float*>(p); }
   __device__ static void sstore(char* p, float v) { *reinterpret_cast<float*>(p) = v; }
   __device__ static float sadd(float a, float b) { return a + b; }
-  __device__ static float sfinal(float a) { return a; }
 };
 
 struct BF16 {
@@ -311,7 +409,7 @@ constexpr int unroll_for() {
 
 // Vectors of [x0, x1) (16-byte aligned, one run: fold start rank b).
 template <typename DT, int N, int NDST>
-__device__ __forceinline__ void fold_run(const FoldArgs& a, int ndst, int b, uint64_t x0, uint64_t x1) {
+__device__ __forceinline__ void fold_run(const FoldArgs& a, int b, uint64_t x0, uint64_t x1) {
   constexpr int U = unroll_for<N>();
   const char* src[N];
 #pragma unroll
@@ -368,7 +466,7 @@ __device__ __forceinline__ void fold_shard(const FoldArgs& a) {
     uint64_t vend = run_end & ~15ull;
     if (vend > ce) vend = ce;
     if (vend > x) {
-      fold_run<DT, N, NDST>(a, ndst, b, x, vend);
+      fold_run<DT, N, NDST>(a, b, x, vend);
       x = vend;
     } else {
       // The vector at x crosses a run boundary: fold its elements one by one.
@@ -378,98 +476,88 @@ __device__ __forceinline__ void fold_shard(const FoldArgs& a) {
   }
 }
 
+// K2 / K3. With the barrier (SM rail): start barrier (inputs of this op are
+// ready on every rank), fold + peer stores, end barrier (every rank's stores
+// to my output landed).
+template <typename DT, int N, int NDST>
+__device__ __forceinline__ void fold_body(const FoldArgs& a) {
+  if (!rail_enter(a.ctl)) return rail_exit(a.ctl, false);
+  const uint32_t ep = op_epoch(a.bar);
+  if (a.use_barrier && !cta_barrier<N, false>(a.bar, ep, a.rank, a.bar.timeout_ns, &a.ctl))
+    return rail_exit(a.ctl, false);
+  if (a.ctl.stall) {
+    note_stall(a.ctl);
+    return rail_exit(a.ctl, false);
+  }
+  fold_shard<DT, N, NDST>(a);
+  if (a.use_barrier && !cta_barrier<N, true>(a.bar, ep + 1, a.rank, end_budget(a.bar, a.ctl), &a.ctl))
+    return rail_exit(a.ctl, false);
+  post_fault(a.post);
+  rail_exit(a.ctl, true);
+}
+
 template <typename DT, int N, int NDST>
 __global__ void __launch_bounds__(512, 2) fold_kernel(const __grid_constant__ FoldArgs a) {
-  const uint32_t ep = op_epoch(a.bar);
-  if (a.use_barrier && !cta_barrier<N, false>(a.bar, ep, a.rank)) return seq_retire(a.bar.seq);
-  fold_shard<DT, N, NDST>(a);
-  if (a.use_barrier && !cta_barrier<N, true>(a.bar, ep + 1, a.rank)) return seq_retire(a.bar.seq);
-  post_fault(a.post);
-  seq_retire(a.bar.seq);
+  fold_body<DT, N, NDST>(a);
+}
+
+template <typename DT, int N, int NDST>
+__global__ void __launch_bounds__(512, 2) fold_kernel_vr(const __grid_constant__ VPack<FoldArgs> p) {
+  fold_body<DT, N, NDST>(p.a[blockIdx.y]);
 }
 
 // ------------------------------------------------------------------ NVLS --
-// WEAK selects .weak instead of .relaxed.sys memory semantics (the barrier
-// around the loop already orders the data); kept as a tuning variant.
-template <typename DT, bool WEAK>
+template <typename DT>
 __device__ __forceinline__ uint4 mm_ld_reduce(const char* p);
 
-#define NZ_MM_LDR(SEM, TY)                                                                                  \
-  asm volatile("multimem.ld_reduce." SEM ".global.add." TY " {%0,%1,%2,%3}, [%4];"                        \
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)                                               \
-               : "l"(p)                                                                                   \
+#define NZ_MM_LDR(TY)                                                                            \
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add." TY " {%0,%1,%2,%3}, [%4];"         \
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)                                    \
+               : "l"(p)                                                                        \
                : "memory")
 
 template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<F32, false>(const char* p) {
+__device__ __forceinline__ uint4 mm_ld_reduce<F32>(const char* p) {
   uint4 r;
-  NZ_MM_LDR("relaxed.sys", "v4.f32");
+  NZ_MM_LDR("v4.f32");
   return r;
 }
 template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<F32, true>(const char* p) {
+__device__ __forceinline__ uint4 mm_ld_reduce<BF16>(const char* p) {
   uint4 r;
-  NZ_MM_LDR("weak", "v4.f32");
-  return r;
-}
-template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<BF16, false>(const char* p) {
-  uint4 r;
-  NZ_MM_LDR("relaxed.sys", "acc::f32.v4.bf16x2");
-  return r;
-}
-template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<BF16, true>(const char* p) {
-  uint4 r;
-  NZ_MM_LDR("weak", "acc::f32.v4.bf16x2");
+  NZ_MM_LDR("acc::f32.v4.bf16x2");
   return r;
 }
 #undef NZ_MM_LDR
 
-template <bool WEAK>
-__device__ __forceinline__ uint4 mm_ld_reduce_i32(const char* p) {
+template <>
+__device__ __forceinline__ uint4 mm_ld_reduce<I32>(const char* p) {
   // ptxas rejects .v4 for integer ld_reduce; four scalar accesses instead.
   uint4 r;
-  if (WEAK) {
-    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
-    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 4) : "memory");
-    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 8) : "memory");
-    asm volatile("multimem.ld_reduce.weak.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 12) : "memory");
-  } else {
-    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
-    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 4) : "memory");
-    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 8) : "memory");
-    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 12) : "memory");
-  }
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.x) : "l"(p) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.y) : "l"(p + 4) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.z) : "l"(p + 8) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(r.w) : "l"(p + 12) : "memory");
   return r;
 }
-template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<I32, false>(const char* p) {
-  return mm_ld_reduce_i32<false>(p);
-}
-template <>
-__device__ __forceinline__ uint4 mm_ld_reduce<I32, true>(const char* p) {
-  return mm_ld_reduce_i32<true>(p);
-}
 
-template <bool WEAK>
 __device__ __forceinline__ void mm_st(char* p, uint4 v) {
   // The store moves bits; .f32 is the only accepted 16-byte form.
-  if (WEAK) {
-    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
-                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
-                 : "memory");
-  } else {
-    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
-                 "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
-                 : "memory");
-  }
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(__uint_as_float(v.x)),
+               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+               : "memory");
 }
 
-template <typename DT, int N, int U, bool WEAK>
+template <typename DT, int N>
 __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ NvlsArgs a) {
+  constexpr int U = 4;
+  if (!rail_enter(a.f.ctl)) return rail_exit(a.f.ctl, false);
   const uint32_t ep = op_epoch(a.f.bar);
-  if (!cta_barrier<N, false>(a.f.bar, ep, a.f.rank)) return seq_retire(a.f.bar.seq);
+  if (!cta_barrier<N, false>(a.f.bar, ep, a.f.rank, a.f.bar.timeout_ns, &a.f.ctl)) return rail_exit(a.f.ctl, false);
+  if (a.f.ctl.stall) {
+    note_stall(a.f.ctl);
+    return rail_exit(a.f.ctl, false);
+  }
   const uint64_t vs = (a.f.s + 15) & ~15ull;
   const uint64_t ve = a.f.e & ~15ull;
   if (vs >= ve) {
@@ -484,18 +572,19 @@ __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ Nv
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t x = base + u * step;
-        if (x < ve) v[u] = mm_ld_reduce<DT, WEAK>(a.mc_in + x);
+        if (x < ve) v[u] = mm_ld_reduce<DT>(a.mc_in + x);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t x = base + u * step;
-        if (x < ve) mm_st<WEAK>(a.mc_out + x, v[u]);
+        if (x < ve) mm_st(a.mc_out + x, v[u]);
       }
     }
   }
-  if (!cta_barrier<N, true>(a.f.bar, ep + 1, a.f.rank)) return seq_retire(a.f.bar.seq);
+  if (!cta_barrier<N, true>(a.f.bar, ep + 1, a.f.rank, end_budget(a.f.bar, a.f.ctl), &a.f.ctl))
+    return rail_exit(a.f.ctl, false);
   post_fault(a.f.post);
-  seq_retire(a.f.bar.seq);
+  rail_exit(a.f.ctl, true);
 }
 
 // --------------------------------------------------------- LL (one-shot) --
@@ -510,7 +599,6 @@ struct LLArgs {
   char* out;       // my output
   uint64_t* peer[kDevMaxRanks];  // each rank's LL buffer (8-byte {data, flag} words)
   uint64_t* local;
-  uint64_t* mc;  // multicast view of the LL buffers (NVLS-LL: one store reaches every rank)
   uint64_t lo, hi;
   uint64_t words;       // ceil((hi - lo) / 4)
   uint64_t slot_words;  // capacity of one (parity, rank) slot
@@ -521,7 +609,9 @@ struct LLArgs {
   int* watchdog;
   uint64_t timeout_ns;
   FaultPost post;
-  uint32_t* seq;  // graph-safe rails: flag / parity from the device counter (see seq_retire)
+  const uint32_t* seq;              // graph-safe rails: flag / parity from the device launch counter
+  const volatile uint32_t* abort;   // host-mapped monitor abort
+  RailCtl ctl;
 };
 
 __device__ __forceinline__ uint32_t ll_load_word(const char* base, uint64_t x, uint64_t hi) {
@@ -530,8 +620,7 @@ __device__ __forceinline__ uint32_t ll_load_word(const char* base, uint64_t x, u
 }
 
 // v[(b + j) mod N] without a runtime index into the register array (which
-// would put v in local memory: the N = 4 / 5 instances spilled): an unrolled
-// select over the N registers.
+// would put v in local memory): an unrolled select over the N registers.
 template <int N>
 __device__ __forceinline__ uint32_t ll_pick(const uint32_t (&v)[N], int b, int j) {
   const int i = b + j < N ? b + j : b + j - N;
@@ -575,10 +664,13 @@ __device__ __forceinline__ void ll_fold_word(const LLArgs& a, const uint32_t (&v
   }
 }
 
-// MC = true is the NVLS-LL variant: the push is one multimem.st to the
-// multicast view, which the switch replicates into every rank's slot.
-template <typename DT, int N, bool MC>
-__global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs a) {
+template <typename DT, int N>
+__device__ __forceinline__ void ll_body(const LLArgs& a) {
+  if (!rail_enter(a.ctl)) return rail_exit(a.ctl, false);
+  if (a.ctl.stall) {  // dead link: nothing of this rank reaches its peers
+    note_stall(a.ctl);
+    return rail_exit(a.ctl, false);
+  }
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   uint32_t flag = a.flag;
@@ -594,19 +686,14 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
     const uint64_t x = a.lo + 8 * p;
     const uint32_t d0 = ll_load_word(a.in, x, a.hi);
     const uint32_t d1 = x + 4 < a.hi ? ll_load_word(a.in, x + 4, a.hi) : 0u;
-    if (MC) {
-      mm_st<false>(reinterpret_cast<char*>(a.mc + my_slot + 2 * p), make_uint4(d0, flag, d1, flag));
-    } else {
 #pragma unroll
-      for (int r = 0; r < N; ++r) {
-        uint64_t* dst = a.peer[r] + my_slot + 2 * p;
-        asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(flag), "r"(d1),
-                     "r"(flag)
-                     : "memory");
-      }
+    for (int r = 0; r < N; ++r) {
+      uint64_t* dst = a.peer[r] + my_slot + 2 * p;
+      asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(flag), "r"(d1), "r"(flag)
+                   : "memory");
     }
   }
-  bool bail = false;  // a peer's words never arrived (watchdog)
+  bool bail = false;  // a peer's words never arrived (watchdog / monitor abort)
   for (uint64_t w = tid; w < a.words && !bail; w += stride) {
     uint32_t v[N];
 #pragma unroll
@@ -624,8 +711,9 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
           const uint64_t now = globaltimer();
           if (t0 == 0) {
             t0 = now;
-          } else if (now - t0 > a.timeout_ns) {
+          } else if (now - t0 > a.timeout_ns || (a.abort && *a.abort)) {
             atomicExch_system(a.watchdog, 1);
+            note_detect(&a.ctl, now);
             bail = true;
             break;
           }
@@ -635,247 +723,30 @@ __global__ void __launch_bounds__(512) ll_kernel(const __grid_constant__ LLArgs 
     }
     if (!bail) ll_fold_word<DT, N>(a, v, a.lo + 4 * w);
   }
-  if (a.seq) {
-    seq_retire(a.seq);  // every thread gets here (no early return): the barrier inside is safe
-    if (bail) return;
-  } else if (bail) {
-    return;
-  }
-  post_fault(a.post);
-}
-
-// ------------------------------------------------- SM rail, one-shot ------
-// K7: mid-size payloads on the SM rail. Every rank pushes its whole range
-// into slot [parity][rank] of every peer's staging buffer, one per-CTA
-// barrier publishes the pushes, then every rank folds all N copies locally in
-// P1 order (its own from `in`) into its own `out`. One barrier instead of the
-// two-shot's two, (N-1)·L wire bytes instead of 2(N-1)/N·L: it wins where
-// latency dominates. CTA c pushes exactly the bytes it later folds (same
-// partition as fold_shard over [lo, hi)), so its own barrier slot suffices.
-// Parity alternates with the epoch; a rank can only reuse a parity after an
-// op every rank joined, i.e. after every rank finished reading it.
-struct OneShotArgs {
-  const char* in;
-  char* stg_peer[kDevMaxRanks];  // rank p's staging buffer (where I push)
-  uint64_t lo, hi;               // reduced byte range
-  uint64_t lo16;                 // lo rounded down to 16: slot offset 0
-  uint64_t slot_bytes;
-  BarrierArgs bar;
-  int rank;
-  FaultPost post;
-  FoldArgs f[2];  // the local fold per staging parity (sources: my `in` + my staging slots), built on the host
-};
-
-template <int N, int ES>
-__device__ __forceinline__ void oneshot_push_scalar(const OneShotArgs& a, uint64_t off, uint64_t x) {
-  if (ES == 4) {
-    const uint32_t v = *reinterpret_cast<const uint32_t*>(a.in + x);
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-      if (r != a.rank) *reinterpret_cast<uint32_t*>(a.stg_peer[r] + off + (x - a.lo16)) = v;
-  } else {
-    const unsigned short v = *reinterpret_cast<const unsigned short*>(a.in + x);
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-      if (r != a.rank) *reinterpret_cast<unsigned short*>(a.stg_peer[r] + off + (x - a.lo16)) = v;
-  }
+  const bool failed = __syncthreads_or(bail) != 0;
+  if (!failed) post_fault(a.post);
+  rail_exit(a.ctl, !failed);
 }
 
 template <typename DT, int N>
-__global__ void __launch_bounds__(512, 2) oneshot_kernel(const __grid_constant__ OneShotArgs a) {
-  const uint32_t ep = op_epoch(a.bar);
-  const int parity = static_cast<int>((ep >> 1) & 1u);
-  const uint64_t off = (static_cast<uint64_t>(parity) * N + a.rank) * a.slot_bytes;  // my slot in every peer
-  // Push: the same element / vector partition fold_shard uses below.
-  const uint64_t vs = (a.lo + 15) & ~15ull;
-  const uint64_t ve = a.hi & ~15ull;
-  const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * blockDim.x * DT::kElem;
-  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (vs >= ve) {
-    for (uint64_t x = a.lo + gtid * DT::kElem; x < a.hi; x += gstride) oneshot_push_scalar<N, DT::kElem>(a, off, x);
-  } else {
-    for (uint64_t x = a.lo + gtid * DT::kElem; x < vs; x += gstride) oneshot_push_scalar<N, DT::kElem>(a, off, x);
-    for (uint64_t x = ve + gtid * DT::kElem; x < a.hi; x += gstride) oneshot_push_scalar<N, DT::kElem>(a, off, x);
-    const uint64_t nvec = (ve - vs) / 16;
-    const uint64_t cb = vs + 16 * (nvec * blockIdx.x / gridDim.x);
-    const uint64_t ce = vs + 16 * (nvec * (blockIdx.x + 1) / gridDim.x);
-    for (uint64_t x = cb + threadIdx.x * 16ull; x < ce; x += static_cast<uint64_t>(blockDim.x) * 16) {
-      const uint4 v = ld_v4(a.in + x);
-#pragma unroll
-      for (int r = 0; r < N; ++r)
-        if (r != a.rank) st_v4(a.stg_peer[r] + off + (x - a.lo16), v);
-    }
-  }
-  if (!cta_barrier<N, true>(a.bar, ep, a.rank)) return seq_retire(a.bar.seq);
-  // Fold every rank's copy of this CTA's part, P1 order, into my `out`
-  // (param-space FoldArgs: no local-memory copy).
-  fold_shard<DT, N, 1>(a.f[parity]);
-  post_fault(a.post);
-  seq_retire(a.bar.seq);
-}
-
-// ------------------------------------------------- SM rail, TMA pipeline --
-// K3t: the SM rail's two-shot fold with the peer traffic moved by the Tensor
-// Memory Accelerator. One elected thread streams 1-D bulk tiles of the shard
-// from every rank's `in` (cp.async.bulk global -> shared over NVLink,
-// completion on an mbarrier) through a kTmaStages-deep ring; all threads fold
-// the N staged tiles in ring order (P1) into an output tile; the elected
-// thread then bulk-stores that tile to every rank's `out`
-// (cp.async.bulk shared -> global). Few instructions keep many NVLink bytes
-// in flight, which the LDG/STG version needs a full CTA of threads for.
-constexpr uint32_t kTmaTile = 4096;  // bytes per source per stage
-constexpr int kTmaStages = 3;
-
-__host__ __device__ constexpr size_t tma_smem_bytes(int n) {
-  return static_cast<size_t>(kTmaStages) * (n + 1) * kTmaTile + kTmaStages * sizeof(uint64_t);
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-// Bounded wait: false after ~timeout_ns so a lost transfer cannot hang the GPU.
-__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, uint64_t timeout_ns) {
-  uint64_t t0 = 0;
-  for (;;) {
-    uint32_t done;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return true;
-    const uint64_t now = globaltimer();
-    if (t0 == 0) {
-      t0 = now;
-    } else if (now - t0 > timeout_ns) {
-      return false;
-    }
-  }
-}
-
-__device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(smem_dst)),
-               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_store(void* gdst, const void* smem_src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
-               "r"(bytes)
-               : "memory");
+__global__ void __launch_bounds__(512, 1) ll_kernel(const __grid_constant__ LLArgs a) {
+  ll_body<DT, N>(a);
 }
 
 template <typename DT, int N>
-__global__ void __launch_bounds__(256, 1) sm_tma_kernel(const __grid_constant__ FoldArgs a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* tiles = smem;                                            // [stage][rank][kTmaTile]
-  unsigned char* outs = smem + static_cast<size_t>(kTmaStages) * N * kTmaTile;  // [stage][kTmaTile]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(outs + static_cast<size_t>(kTmaStages) * kTmaTile);
-
-  const uint32_t ep = op_epoch(a.bar);
-  if (a.use_barrier && !cta_barrier<N, false>(a.bar, ep, a.rank)) return seq_retire(a.bar.seq);
-  const uint64_t vs = (a.s + 15) & ~15ull;
-  const uint64_t ve = a.e & ~15ull;
-  if (vs >= ve) {
-    fold_scalar_range<DT, N>(a, N, a.s, a.e);
-  } else {
-    fold_scalar_range<DT, N>(a, N, a.s, vs);
-    fold_scalar_range<DT, N>(a, N, ve, a.e);
-    const uint64_t nvec = (ve - vs) / 16;
-    const uint64_t cb = vs + 16 * (nvec * blockIdx.x / gridDim.x);
-    const uint64_t ce = vs + 16 * (nvec * (blockIdx.x + 1) / gridDim.x);
-    const uint64_t ntiles = (ce - cb + kTmaTile - 1) / kTmaTile;
-    const bool leader = threadIdx.x == 0;
-    if (leader) {
-      for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto issue = [&](uint64_t i) {
-      const int s = static_cast<int>(i % kTmaStages);
-      const uint64_t x = cb + i * kTmaTile;
-      const uint32_t len = static_cast<uint32_t>(ce - x < kTmaTile ? ce - x : kTmaTile);
-      mbar_expect_tx(&bars[s], len * N);
-#pragma unroll
-      for (int r = 0; r < N; ++r) tma_load(tiles + (static_cast<size_t>(s) * N + r) * kTmaTile, a.src[r] + x, len, &bars[s]);
-    };
-    if (leader)
-      for (uint64_t i = 0; i < ntiles && i < static_cast<uint64_t>(kTmaStages); ++i) issue(i);
-    for (uint64_t i = 0; i < ntiles; ++i) {
-      const int s = static_cast<int>(i % kTmaStages);
-      const uint64_t x = cb + i * kTmaTile;
-      const uint32_t len = static_cast<uint32_t>(ce - x < kTmaTile ? ce - x : kTmaTile);
-      // The bulk stores of tile i - kTmaStages must have finished reading outs[s].
-      if (leader && i >= static_cast<uint64_t>(kTmaStages))
-        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmaStages - 1) : "memory");
-      const uint64_t budget = a.bar.timeout_ns ? a.bar.timeout_ns : 20ull * 1000 * 1000 * 1000;
-      const int ok = mbar_wait(&bars[s], static_cast<uint32_t>((i / kTmaStages) & 1), budget) ? 1 : 0;
-      if (!__syncthreads_and(ok)) {
-        if (leader && a.bar.watchdog) atomicExch_system(a.bar.watchdog, 1);
-        if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        return seq_retire(a.bar.seq);  // a tile never arrived: give up rather than hang
-      }
-      const unsigned char* st = tiles + static_cast<size_t>(s) * N * kTmaTile;
-      unsigned char* ot = outs + static_cast<size_t>(s) * kTmaTile;
-      for (uint32_t v = threadIdx.x * 16; v < len; v += blockDim.x * 16) {
-        const uint64_t xv = x + v;
-        uint64_t run_end;
-        const int b = block_at<N, DT::kElem>(a.g, xv, &run_end);
-        if (run_end >= xv + 16) {
-          typename DT::Acc acc = DT::load(*reinterpret_cast<const uint4*>(st + static_cast<size_t>(b) * kTmaTile + v));
-#pragma unroll
-          for (int j = 1; j < N; ++j)
-            DT::add(acc, *reinterpret_cast<const uint4*>(st + static_cast<size_t>((b + j) % N) * kTmaTile + v));
-          *reinterpret_cast<uint4*>(ot + v) = DT::store(acc);
-        } else {
-          // Vector straddles a ring-block boundary: fold element by element.
-          for (uint32_t k = 0; k < 16; k += DT::kElem) {
-            uint64_t re;
-            const int be = block_at<N, DT::kElem>(a.g, xv + k, &re);
-            typename DT::Scalar acc = DT::sload(reinterpret_cast<const char*>(st + static_cast<size_t>(be) * kTmaTile + v + k));
-            for (int j = 1; j < N; ++j)
-              acc = DT::sadd(acc, DT::sload(reinterpret_cast<const char*>(st + static_cast<size_t>((be + j) % N) * kTmaTile + v + k)));
-            DT::sstore(reinterpret_cast<char*>(ot + v + k), acc);
-          }
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
-      __syncthreads();
-      if (leader) {
-#pragma unroll
-        for (int r = 0; r < N; ++r) tma_store(a.dst[r] + x, ot, len);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if (i + kTmaStages < ntiles) issue(i + kTmaStages);  // tiles[s] is free: every thread folded it
-      }
-    }
-    if (leader) {
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // all peer stores performed
-      asm volatile("fence.proxy.async.global;" ::: "memory");   // ... and ordered before the release below
-    }
-  }
-  if (a.use_barrier && !cta_barrier<N, true>(a.bar, ep + 1, a.rank)) return seq_retire(a.bar.seq);
-  post_fault(a.post);
-  seq_retire(a.bar.seq);
+__global__ void __launch_bounds__(512, 1) ll_kernel_vr(const __grid_constant__ VPack<LLArgs> p) {
+  ll_body<DT, N>(p.a[blockIdx.y]);
 }
 
 // N = 1: the allreduce is the identity, i.e. a copy in -> out (HBM-bound).
 // 8 x 16-byte loads in flight per thread before the stores, no run walking.
-__global__ void __launch_bounds__(512, 2) copy_kernel(const char* __restrict__ src, char* __restrict__ dst, uint64_t lo,
-                                                      uint64_t hi, FaultPost post) {
+static __global__ void __launch_bounds__(512, 2) copy_kernel(const char* __restrict__ src, char* __restrict__ dst, uint64_t lo,
+                                                      uint64_t hi, FaultPost post, RailCtl ctl) {
+  if (!rail_enter(ctl)) return rail_exit(ctl, false);
+  if (ctl.stall) {
+    note_stall(ctl);
+    return rail_exit(ctl, false);
+  }
   const uint64_t vs = (lo + 15) & ~15ull;
   const uint64_t ve = hi & ~15ull;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -905,14 +776,42 @@ __global__ void __launch_bounds__(512, 2) copy_kernel(const char* __restrict__ s
     __syncthreads();
     post_fault(post);
   }
+  rail_exit(ctl, true);
 }
 
-// CE rail: start / end barriers around the DMA phases, and the fault post.
+// CE rail: start / end barriers around the DMA phases (K4). The start
+// barrier orders the peers' inputs before this rank's gather DMAs; the end
+// barrier orders every peer's scatter into this rank's output before the op
+// counts as done, posts the fault record and publishes the launch status.
+struct BarrierKArgs {
+  BarrierArgs bar;
+  int rank;
+  int end;  // 0: start barrier, 1: end barrier
+  FaultPost post;
+  RailCtl ctl;
+};
+
 template <int N>
-__global__ void barrier_kernel(const __grid_constant__ BarrierArgs b, int rank, FaultPost post) {
-  if (!cta_barrier<N, true>(b, op_epoch(b), rank)) return seq_retire(b.seq);
-  post_fault(post);
-  seq_retire(b.seq);
+__device__ __forceinline__ void barrier_body(const BarrierKArgs& k) {
+  if (!rail_enter(k.ctl)) return rail_exit(k.ctl, false);
+  const uint64_t budget = k.end ? end_budget(k.bar, k.ctl) : k.bar.timeout_ns;
+  if (!cta_barrier<N, true>(k.bar, op_epoch(k.bar), k.rank, budget, &k.ctl)) return rail_exit(k.ctl, false);
+  if (!k.end && k.ctl.stall) {
+    note_stall(k.ctl);
+    return rail_exit(k.ctl, false);
+  }
+  post_fault(k.post);
+  rail_exit(k.ctl, true);
+}
+
+template <int N>
+__global__ void barrier_kernel(const __grid_constant__ BarrierKArgs k) {
+  barrier_body<N>(k);
+}
+
+template <int N>
+__global__ void barrier_kernel_vr(const __grid_constant__ VPack<BarrierKArgs> p) {
+  barrier_body<N>(p.a[blockIdx.y]);
 }
 
 }  // namespace nz

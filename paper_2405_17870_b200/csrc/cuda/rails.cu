@@ -1,9 +1,10 @@
 // Host side of the three rails: launch configuration, DMA phases of the
-// copy-engine rail, fault records. One nz_rail per (rank, rail); each owns a
-// CUDA stream, which is the B200 form of the reference's "one collective
-// executor per rail".
+// copy-engine rail, launch status and fault records, loopback launches. One
+// nz_rail per (rank, rail); each owns a CUDA stream, which is the B200 form of
+// the reference's "one collective executor per rail".
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstring>
 
 #include "internal.h"
@@ -41,25 +42,39 @@ void shardOf(uint64_t lo, uint64_t hi, int rank, int world, uint64_t* s, uint64_
   *e = rank == world - 1 ? hi : A + 16 * (V * (rank + 1) / world);
 }
 
-// Device wait budget before a kernel gives up on a peer (watchdog).
-// NEZHA_WATCHDOG_MS overrides the 20 s default (tests use a short one).
+long long envLL(const char* name, long long def) {
+  const char* e = getenv(name);
+  return e ? atoll(e) : def;
+}
+
+// Device wait budget at the start of an op (ranks may legitimately arrive far
+// apart: the caller's stream decides when a launch starts). NEZHA_WATCHDOG_MS
+// overrides the 20 s default; past it a kernel gives up instead of hanging.
 uint64_t watchdogNs() {
   static const uint64_t ns = [] {
-    const char* e = getenv("NEZHA_WATCHDOG_MS");
-    const long long ms = e ? atoll(e) : 20000;
+    const long long ms = envLL("NEZHA_WATCHDOG_MS", 20000);
     return static_cast<uint64_t>(ms > 0 ? ms : 20000) * 1000000ull;
   }();
   return ns;
 }
 
-// NEZHA_BARRIER_POLL=relaxed: barrier waits poll with relaxed loads and fence
-// once (A/B knob; the default acquire-load poll is the validated one).
-bool barrierRelaxedPoll() {
-  static const bool on = [] {
-    const char* e = getenv("NEZHA_BARRIER_POLL");
-    return e && strcmp(e, "relaxed") == 0;
+// End-barrier budget: every rank passed the start barrier of the same op and
+// does the same work, so a peer missing for much longer than the op itself
+// takes has lost its link. max(floor, 2 x range / 100 GB/s),
+// floor NEZHA_DETECT_US (2000 us) or the rail's / engine's setting.
+uint64_t detectNs(const nz_rail* r, uint64_t range_bytes) {
+  static const double env_us = static_cast<double>(envLL("NEZHA_DETECT_US", 2000));
+  const double floor_us = r->detect_us > 0 ? r->detect_us : env_us;
+  const double scaled_us = 2.0 * static_cast<double>(range_bytes) / 100e9 * 1e6;
+  return static_cast<uint64_t>(std::max(floor_us, scaled_us) * 1000.0);
+}
+
+uint64_t waveBytes() {
+  static const uint64_t b = [] {
+    const long long v = envLL("NEZHA_WAVE_BYTES", 64ll << 20);
+    return static_cast<uint64_t>(v > 0 ? v : (64ll << 20));
   }();
-  return on;
+  return b;
 }
 
 BarrierArgs barrierArgs(nz_rail* r, uint32_t epoch) {
@@ -69,8 +84,8 @@ BarrierArgs barrierArgs(nz_rail* r, uint32_t epoch) {
   b.epoch = epoch;
   b.watchdog = r->wd_dev;
   b.timeout_ns = watchdogNs();
-  b.relaxed_poll = barrierRelaxedPoll() ? 1 : 0;
-  b.seq = r->seq_dev;
+  b.seq = r->graph_safe ? r->ctl_dev + kCtlSeq : nullptr;
+  b.abort = &r->status_dev->abort;
   return b;
 }
 
@@ -88,58 +103,55 @@ int gridFor(nz_rail* r, uint64_t range_bytes, int world, int unroll) {
   return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, std::min(budget, kMaxCtas))));
 }
 
+constexpr uint64_t kLLMaxBytes = 2048 * 1024;  // SM rail one-shot LL path up to this payload
+
+// LL pays 2 wire bytes per payload byte times N receivers; beyond ~4 MiB / N
+// the two-shot kernels win (measured crossover, profiles/README.md).
+uint64_t llMaxBytes(int world) {
+  // NEZHA_LL_MAX (bytes) lowers the ceiling for sweeps; it never raises it
+  // (the LL buffers are sized by this function at rail creation).
+  static const long long env = envLL("NEZHA_LL_MAX", -1);
+  const uint64_t def = std::min<uint64_t>(kLLMaxBytes, (uint64_t{4} << 20) / world);
+  return env >= 0 ? std::min<uint64_t>(def, static_cast<uint64_t>(env)) : def;
+}
+
+bool llPath(nz_rail* r, uint64_t lo, uint64_t hi) {
+  return r->comm->world > 1 && r->kind == NZ_RAIL_SM && r->ll && hi - lo <= r->ll_max && lo % 4 == 0;
+}
+
+int llGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
+  const uint64_t words = (hi - lo + 3) / 4;
+  const uint64_t threads = (words + 1) / 2 > words ? (words + 1) / 2 : words;
+  return static_cast<int>(
+      std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads, r->comm->sm_count)));
+}
+
+int copyGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
+  const uint64_t vec = (hi - lo) / 16 + 1;
+  return static_cast<int>(
+      std::max<uint64_t>(1, std::min<uint64_t>((vec + kThreads * 8 - 1) / (kThreads * 8), 2ull * r->comm->sm_count)));
+}
+
+int smGrid(nz_rail* r, uint64_t lo, uint64_t hi) { return gridFor(r, hi - lo, r->comm->world, 2); }
+
+// ------------------------------------------------------------ launches ----
 template <typename DT, int N, int NDST>
-void launchFold(const FoldArgs& a, int grid, cudaStream_t st) {
+void launchFoldT(const FoldArgs& a, int grid, cudaStream_t st) {
   fold_kernel<DT, N, NDST><<<grid, kThreads, 0, st>>>(a);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 template <int N, int NDST>
 void dispatchFoldDT(int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
   switch (dtype) {
-    case NZ_F32: return launchFold<F32, N, NDST>(a, grid, st);
-    case NZ_BF16: return launchFold<BF16, N, NDST>(a, grid, st);
-    case NZ_I32: return launchFold<I32, N, NDST>(a, grid, st);
-  }
-}
-
-// SM-rail TMA pipeline (K3t). Opt-in with NEZHA_SM_TMA=1 until its sweep is
-// committed; nz_emulate_fold_tma runs it on one GPU for the parity tests.
-bool smTmaEnabled() {
-  static const bool on = [] {
-    const char* e = getenv("NEZHA_SM_TMA");
-    return e && atoi(e) != 0;
-  }();
-  return on;
-}
-
-template <typename DT, int N>
-void launchTmaDT(const FoldArgs& a, int grid, cudaStream_t st) {
-  static bool configured = false;  // opt in to > 48 KiB of dynamic shared memory once
-  const size_t smem = tma_smem_bytes(N);
-  if (!configured) {
-    NZ_CUDA(cudaFuncSetAttribute(sm_tma_kernel<DT, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    configured = true;
-  }
-  sm_tma_kernel<DT, N><<<grid, 256, smem, st>>>(a);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
-void dispatchTma(int world, int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
-  switch (world) {
-#define NZ_CASE(n)                                                    \
-  case n:                                                             \
-    if (dtype == NZ_F32) return launchTmaDT<F32, n>(a, grid, st);     \
-    if (dtype == NZ_BF16) return launchTmaDT<BF16, n>(a, grid, st);   \
-    return launchTmaDT<I32, n>(a, grid, st);
-    NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
-#undef NZ_CASE
+    case NZ_F32: return launchFoldT<F32, N, NDST>(a, grid, st);
+    case NZ_BF16: return launchFoldT<BF16, N, NDST>(a, grid, st);
+    case NZ_I32: return launchFoldT<I32, N, NDST>(a, grid, st);
   }
 }
 
 template <int NDST_IS_N>
 void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (world) {
 #define NZ_CASE(n) \
   case n: return dispatchFoldDT<n, NDST_IS_N ? n : 1>(dtype, a, grid, st);
@@ -148,101 +160,146 @@ void dispatchFold(int world, int dtype, const FoldArgs& a, int grid, cudaStream_
   }
 }
 
-constexpr uint64_t kLLMaxBytes = 2048 * 1024;  // SM rail one-shot LL path up to this payload
-
-// LL pays 2 wire bytes per payload byte times N receivers; beyond ~4 MiB / N
-// the two-shot kernels win (measured crossover, profiles/README.md).
-// The multicast push (NVLS-LL) saturates earlier than the unicast one: at
-// N = 4 it is 9.1 us at 256 KiB but 24.8 us at 1 MiB vs 20 us two-shot.
-uint64_t llMaxBytes(int world, bool mc) {
-  const uint64_t cap = mc ? (uint64_t{512} << 10) : kLLMaxBytes;
-  // NEZHA_LL_MAX (bytes) lowers the ceiling for sweeps; it never raises it
-  // (the LL buffers are sized by this function at rail creation).
-  static const long long env = [] {
-    const char* e = getenv("NEZHA_LL_MAX");
-    return e ? atoll(e) : -1LL;
-  }();
-  const uint64_t def = std::min<uint64_t>(cap, (uint64_t{4} << 20) / world);
-  return env >= 0 ? std::min<uint64_t>(def, static_cast<uint64_t>(env)) : def;
-}
-
-template <int N, bool MC>
-void launchLL(int dtype, const LLArgs& a, int grid, cudaStream_t st) {
-  if (dtype == NZ_F32) return (void)(ll_kernel<F32, N, MC><<<grid, kThreads, 0, st>>>(a));
-  if (dtype == NZ_BF16) return (void)(ll_kernel<BF16, N, MC><<<grid, kThreads, 0, st>>>(a));
-  return (void)(ll_kernel<I32, N, MC><<<grid, kThreads, 0, st>>>(a));
-}
-
-void dispatchLL(int world, int dtype, bool mc, const LLArgs& a, int grid, cudaStream_t st) {
+void dispatchLL(int world, int dtype, const LLArgs& a, int grid, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (world) {
-#define NZ_CASE(n) \
-  case n:          \
-    return mc ? launchLL<n, true>(dtype, a, grid, st) : launchLL<n, false>(dtype, a, grid, st);
+#define NZ_CASE(n)                                                                             \
+  case n:                                                                                      \
+    if (dtype == NZ_F32) return (void)(ll_kernel<F32, n><<<grid, kThreads, 0, st>>>(a));      \
+    if (dtype == NZ_BF16) return (void)(ll_kernel<BF16, n><<<grid, kThreads, 0, st>>>(a));    \
+    return (void)(ll_kernel<I32, n><<<grid, kThreads, 0, st>>>(a));
     NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
 #undef NZ_CASE
-  }
-}
-
-// NVLS loop variant: unroll U and memory semantics. NEZHA_NVLS_VARIANT
-// (0: U4 relaxed.sys, 1: U4 weak, 2: U8 relaxed.sys, 3: U8 weak) is a tuning
-// knob for the sweeps recorded in profiles/; the default is variant 0.
-int nvlsVariant() {
-  static const int v = [] {
-    const char* e = getenv("NEZHA_NVLS_VARIANT");
-    const int x = e ? atoi(e) : 0;
-    return (x >= 0 && x <= 3) ? x : 0;
-  }();
-  return v;
-}
-
-template <typename DT, int N>
-void launchNvlsDT(const NvlsArgs& a, int grid, cudaStream_t st) {
-  switch (nvlsVariant()) {
-    case 1: nvls_kernel<DT, N, 4, true><<<grid, kThreads, 0, st>>>(a); return;
-    case 2: nvls_kernel<DT, N, 8, false><<<grid, kThreads, 0, st>>>(a); return;
-    case 3: nvls_kernel<DT, N, 8, true><<<grid, kThreads, 0, st>>>(a); return;
-    default: nvls_kernel<DT, N, 4, false><<<grid, kThreads, 0, st>>>(a); return;
   }
 }
 
 template <int N>
 void launchNvls(int dtype, const NvlsArgs& a, int grid, cudaStream_t st) {
-  if (dtype == NZ_F32) return launchNvlsDT<F32, N>(a, grid, st);
-  if (dtype == NZ_BF16) return launchNvlsDT<BF16, N>(a, grid, st);
-  return launchNvlsDT<I32, N>(a, grid, st);
+  if (dtype == NZ_F32) return (void)(nvls_kernel<F32, N><<<grid, kThreads, 0, st>>>(a));
+  if (dtype == NZ_BF16) return (void)(nvls_kernel<BF16, N><<<grid, kThreads, 0, st>>>(a));
+  return (void)(nvls_kernel<I32, N><<<grid, kThreads, 0, st>>>(a));
 }
 
 void dispatchNvls(int world, int dtype, const NvlsArgs& a, int grid, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (world) {
-#define NZ_CASE(n)                                                                          \
-  case n:                                                                                   \
-    return launchNvls<n>(dtype, a, grid, st);
+#define NZ_CASE(n) \
+  case n: return launchNvls<n>(dtype, a, grid, st);
     NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
 #undef NZ_CASE
   }
 }
 
-void launchBarrier(nz_rail* r, uint32_t epoch, FaultPost post, cudaStream_t st) {
-  const BarrierArgs b = barrierArgs(r, epoch);
+void dispatchBarrier(int world, const BarrierKArgs& k, cudaStream_t st) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  switch (r->comm->world) {
+  switch (world) {
 #define NZ_CASE(n) \
-  case n: barrier_kernel<n><<<1, 32, 0, st>>>(b, r->comm->rank, post); break;
+  case n: barrier_kernel<n><<<1, 32, 0, st>>>(k); break;
     NZ_CASE(1) NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
 #undef NZ_CASE
   }
 }
 
-void ensureStaging(nz_rail* r, size_t slot) {
+// Loopback: the last virtual rank to reach this launch runs one grid for all
+// of them (blockIdx.y = rank) on the pad's group stream, ordered after every
+// rank's stream and before each rank's next work. The grid is capped so that
+// every rail of the comm can have its grid resident at once: the cross-rank
+// waits inside are then between co-resident CTAs.
+template <typename A>
+void combine(nz_rail* r, int kind, int dtype, const A& a, int grid, cudaStream_t st) {
+  nz_comm* c = r->comm;
+  LoopRail& L = *r->lr;
+  const int me = c->rank, N = c->world;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  NZ_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) fail(NZ_ERR_UNSUPPORTED, "loopback ranks cannot be captured in a CUDA graph");
+  NZ_CUDA(cudaEventRecord(r->lr_ready, st));
+  std::unique_lock<std::mutex> lk(L.m);
+  const uint64_t gen = L.gen;
+  if (L.arrived == 0) {
+    L.kind = kind;
+    L.dtype = dtype;
+    L.grid = grid;
+    L.args.assign(sizeof(VPack<A>), 0);
+    L.error.clear();
+  } else if (L.kind != kind || L.dtype != dtype || L.grid != grid || L.args.size() != sizeof(VPack<A>)) {
+    L.error = "loopback ranks issued different launches on rail " + std::to_string(r->rail_id);
+  }
+  if (L.args.size() == sizeof(VPack<A>)) memcpy(L.args.data() + me * sizeof(A), &a, sizeof(A));
+  std::string err;
+  if (++L.arrived == N) {
+    err = L.error;
+    if (err.empty()) {
+      try {
+        for (int p = 0; p < N; ++p) NZ_CUDA(cudaStreamWaitEvent(L.stream, L.ready[p], 0));
+        const int occ = std::max(1, loopOccupancy(kind, N, dtype));
+        const int cap_ctas = std::max(1, occ * c->sm_count / (N * std::max(1, c->live_rails)));
+        launchLoopGrid(kind, N, dtype, L.args.data(), std::min(grid, cap_ctas), L.stream);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        NZ_CUDA(cudaGetLastError());
+        for (int p = 0; p < N; ++p) NZ_CUDA(cudaEventRecord(L.done[p], L.stream));
+      } catch (const std::exception& e) {
+        err = e.what();
+      }
+    }
+    L.arrived = 0;
+    L.error = err;
+    L.gen++;
+    L.cv.notify_all();
+  } else {
+    const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(c->timeout_ms);
+    while (L.gen == gen) {
+      if (L.cv.wait_until(lk, deadline) == std::cv_status::timeout && L.gen == gen) {
+        fail(NZ_ERR_TIMEOUT, "loopback launch: a virtual rank never reached rail " + std::to_string(r->rail_id));
+      }
+    }
+    err = L.error;
+  }
+  lk.unlock();
+  if (!err.empty()) fail(NZ_ERR_CUDA, err);
+  NZ_CUDA(cudaStreamWaitEvent(st, r->lr_done, 0));
+}
+
+// Cross-rank launches: direct on a real rank, combined across virtual ranks.
+void launchCrossFold(nz_rail* r, int dtype, const FoldArgs& a, int grid, cudaStream_t st) {
+  if (r->lr) return combine(r, kLoopFold, dtype, a, grid, st);
+  dispatchFold<1>(r->comm->world, dtype, a, grid, st);
+}
+
+void launchCrossLL(nz_rail* r, int dtype, const LLArgs& a, int grid, cudaStream_t st) {
+  if (r->lr) return combine(r, kLoopLL, dtype, a, grid, st);
+  dispatchLL(r->comm->world, dtype, a, grid, st);
+}
+
+void launchBarrier(nz_rail* r, uint32_t epoch, bool end, FaultPost post, const RailCtl& ctl, cudaStream_t st) {
+  BarrierKArgs k{};
+  k.bar = barrierArgs(r, epoch);
+  k.rank = r->comm->rank;
+  k.end = end ? 1 : 0;
+  k.post = post;
+  k.ctl = ctl;
+  if (r->lr) return combine(r, kLoopBarrier, NZ_F32, k, 1, st);
+  dispatchBarrier(r->comm->world, k, st);
+}
+
+void ensureStaging(nz_rail* r, size_t slot, std::vector<char*>* retired) {
   if (slot <= r->staging_slot) return;
-  if (r->staging) NZ_CUDA(cudaFree(r->staging));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  NZ_CUDA(cudaStreamIsCapturing(r->stream, &cap));
+  if (cap != cudaStreamCaptureStatusNone)
+    fail(NZ_ERR_INVALID, "CE staging must grow outside graph capture: run the largest op eagerly first");
+  // A captured graph may still reference the old buffer: keep it until the
+  // rail is destroyed instead of freeing it under the graph.
+  if (r->staging) retired->push_back(r->staging);
   r->staging = nullptr;
   const size_t want = (slot + (1u << 20)) & ~((size_t(1) << 20) - 1);
   NZ_CUDA(cudaMalloc(&r->staging, want * std::max(1, r->comm->world - 1)));
   r->staging_slot = want;
 }
+
+// Old staging buffers of every rail, freed at rail destruction.
+std::mutex g_retired_mu;
+std::map<nz_rail*, std::vector<char*>> g_retired;
 
 void gateEnter(ComputeGate* gate, cudaStream_t st) {
   if (!gate || gate->entered) return;
@@ -261,94 +318,18 @@ int gated(int grid, const ComputeGate* gate) {
   return gate && gate->max_ctas > 0 ? std::max(1, std::min(grid, gate->max_ctas)) : grid;
 }
 
-// NVLS-LL (one-shot multicast push) is opt-in: NEZHA_NVLS_LL=1. The only
-// NVLink error incident of this project came from a multicast store path
-// (profiles/README.md); until its fixed form has a clean hardware record the
-// NVLS rail runs small payloads two-shot, and the planner sends them to the
-// SM rail's unicast LL path, which is as fast.
-bool nvlsLLEnabled() {
-  static const bool on = [] {
-    const char* e = getenv("NEZHA_NVLS_LL");
-    return e && atoi(e) != 0;
-  }();
-  return on;
+// Pieces of a CE shard pipelined through gather / fold / scatter: the gather
+// of piece i+1 (inbound NVLink) overlaps the fold of piece i and the scatter
+// of piece i-1 (outbound), so both link directions work at once.
+int cePieces(uint64_t shard) {
+  const long long env = envLL("NEZHA_CE_PIECES", 0);
+  if (env > 0) return static_cast<int>(std::min<long long>(env, 8));
+  return static_cast<int>(std::clamp<uint64_t>(shard / (uint64_t{4} << 20), 1, 4));
 }
 
-// SM-rail one-shot (K7) for payloads between the LL ceiling and
-// min(4 MiB, 8 MiB / N): opt-in with NEZHA_SM_ONESHOT=1 until its sweep is in
-// profiles/. NEZHA_SM_ONESHOT_MAX overrides the ceiling (bytes).
-bool oneshotEnabled() {
-  static const bool on = [] {
-    const char* e = getenv("NEZHA_SM_ONESHOT");
-    return e && atoi(e) != 0;
-  }();
-  return on;
-}
-
-uint64_t oneshotMaxBytes(int world) {
-  static const long long env = [] {
-    const char* e = getenv("NEZHA_SM_ONESHOT_MAX");
-    return e ? atoll(e) : 0LL;
-  }();
-  const uint64_t def = std::min<uint64_t>(uint64_t{4} << 20, (uint64_t{8} << 20) / world);
-  return env > 0 ? std::min<uint64_t>(static_cast<uint64_t>(env), uint64_t{16} << 20) : def;
-}
-
-bool oneshotPath(nz_rail* r, uint64_t lo, uint64_t hi) {
-  return r->comm->world > 1 && r->kind == NZ_RAIL_SM && r->os && hi > lo && hi - lo <= r->os_max &&
-         hi - (lo & ~15ull) <= r->os_slot;
-}
-
-int oneshotGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
-  const int budget = std::min(r->sm_budget > 0 ? r->sm_budget : 64, r->comm->sm_count);
-  const uint64_t vec = (hi - lo) / 16 + 1;
-  const uint64_t g = (vec + 2 * kThreads - 1) / (2 * kThreads);
-  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, std::min(budget, kMaxCtas))));
-}
-
-template <typename DT>
-void launchOneshotDT(int world, const OneShotArgs& a, int grid, cudaStream_t st) {
-  switch (world) {
-#define NZ_CASE(n) \
-  case n: oneshot_kernel<DT, n><<<grid, kThreads, 0, st>>>(a); break;
-    NZ_CASE(2) NZ_CASE(3) NZ_CASE(4) NZ_CASE(5) NZ_CASE(6) NZ_CASE(7) NZ_CASE(8)
-#undef NZ_CASE
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-}
-
-bool llPath(nz_rail* r, uint64_t lo, uint64_t hi) {
-  const int N = r->comm->world;
-  const bool mc_ll = r->kind == NZ_RAIL_NVLS;
-  return N > 1 && (r->kind == NZ_RAIL_SM || mc_ll) && r->ll && hi - lo <= r->ll_max && lo % 4 == 0 &&
-         (!mc_ll || r->ll->mc_ptr);
-}
-
-int llGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
-  const uint64_t words = (hi - lo + 3) / 4;
-  const uint64_t threads = (words + 1) / 2 > words ? (words + 1) / 2 : words;
-  return static_cast<int>(
-      std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads, r->comm->sm_count)));
-}
-
-int copyGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
-  const uint64_t vec = (hi - lo) / 16 + 1;
-  return static_cast<int>(
-      std::max<uint64_t>(1, std::min<uint64_t>((vec + kThreads * 8 - 1) / (kThreads * 8), 2ull * r->comm->sm_count)));
-}
-
-int smGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
-  const int N = r->comm->world;
-  if (smTmaEnabled()) {
-    const uint64_t tiles = (hi - lo) / N / kTmaTile + 1;
-    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, gridFor(r, hi - lo, N, 2))));
-  }
-  return gridFor(r, hi - lo, N, 2);
-}
-
-// One rail op over [lo, hi) with order geometry g. `post` is posted after.
-void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const Geometry& g, int dtype, FaultPost post,
-            cudaStream_t st, ComputeGate* gate) {
+// One launch sequence of a rail over [lo, hi) with order geometry g.
+void railWave(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const Geometry& g, int dtype,
+              FaultPost post, const RailCtl& ctl, cudaStream_t st, ComputeGate* gate) {
   nz_comm* c = r->comm;
   const int N = c->world;
   const int me = c->rank;
@@ -357,20 +338,15 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
   const uint32_t epoch = r->epoch + 1;
   r->epoch += 2;  // start + end barrier; identical on every rank
 
-  const bool mc_ll = r->kind == NZ_RAIL_NVLS;
   if (llPath(r, lo, hi)) {
     LLArgs a{};
     a.in = in->ptrs[me];
     a.out = out->ptrs[me];
     for (int p = 0; p < N; ++p) a.peer[p] = reinterpret_cast<uint64_t*>(r->ll->ptrs[p]);
     a.local = reinterpret_cast<uint64_t*>(r->ll->ptrs[me]);
-    a.mc = reinterpret_cast<uint64_t*>(r->ll->mc_ptr);
-    // Every 16-byte push (unicast v4 or multimem.st) must be 16-byte aligned:
-    // a misaligned multimem store is not a clean trap on NVSwitch.
-    if ((r->ll_slot_words & 1u) != 0 || reinterpret_cast<uintptr_t>(r->ll->ptrs[me]) % 16 != 0 ||
-        (a.mc && reinterpret_cast<uintptr_t>(a.mc) % 16 != 0)) {
+    // Every 16-byte push must be 16-byte aligned.
+    if ((r->ll_slot_words & 1u) != 0 || reinterpret_cast<uintptr_t>(r->ll->ptrs[me]) % 16 != 0)
       fail(NZ_ERR_INVALID, "LL slots are not 16-byte aligned");
-    }
     a.lo = lo;
     a.hi = hi;
     a.words = (hi - lo + 3) / 4;
@@ -383,54 +359,20 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.watchdog = r->wd_dev;
     a.timeout_ns = watchdogNs();
     a.post = post;
-    a.seq = r->seq_dev;
+    a.seq = r->graph_safe ? r->ctl_dev + kCtlSeq : nullptr;
+    a.abort = &r->status_dev->abort;
+    a.ctl = ctl;
     gateEnter(gate, st);
-    dispatchLL(N, dtype, mc_ll, a, gated(llGrid(r, lo, hi), gate), st);
+    launchCrossLL(r, dtype, a, gated(llGrid(r, lo, hi), gate), st);
     NZ_CUDA(cudaGetLastError());
-    gateExit(gate, st);
-    return;
-  }
-
-  if (oneshotPath(r, lo, hi)) {
-    OneShotArgs a{};
-    a.in = in->ptrs[me];
-    for (int p = 0; p < N; ++p) a.stg_peer[p] = r->os->ptrs[p];
-    a.lo = lo;
-    a.hi = hi;
-    a.lo16 = lo & ~15ull;
-    a.slot_bytes = r->os_slot;
-    a.bar = barrierArgs(r, epoch);
-    a.rank = me;
-    a.post = post;
-    for (int par = 0; par < 2; ++par) {
-      FoldArgs& f = a.f[par];
-      for (int p = 0; p < N; ++p) {
-        f.src[p] = p == me ? in->ptrs[me]
-                           : r->os->ptrs[me] + (static_cast<uint64_t>(par) * N + p) * r->os_slot - a.lo16;
-      }
-      f.dst[0] = out->ptrs[me];
-      f.s = lo;
-      f.e = hi;
-      f.range_bytes = hi - lo;
-      f.g = g;
-      f.rank = me;
-    }
-    gateEnter(gate, st);
-    const int grid = gated(oneshotGrid(r, lo, hi), gate);
-    if (dtype == NZ_F32) launchOneshotDT<F32>(N, a, grid, st);
-    else if (dtype == NZ_BF16) launchOneshotDT<BF16>(N, a, grid, st);
-    else launchOneshotDT<I32>(N, a, grid, st);
-    NZ_CUDA(cudaGetLastError());
-    gateExit(gate, st);
     return;
   }
 
   if (N == 1) {  // identity allreduce: every rail is a local HBM copy
     gateEnter(gate, st);
-    copy_kernel<<<gated(copyGrid(r, lo, hi), gate), kThreads, 0, st>>>(in->ptrs[0], out->ptrs[0], lo, hi, post);
+    copy_kernel<<<gated(copyGrid(r, lo, hi), gate), kThreads, 0, st>>>(in->ptrs[0], out->ptrs[0], lo, hi, post, ctl);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     NZ_CUDA(cudaGetLastError());
-    gateExit(gate, st);
     return;
   }
 
@@ -440,32 +382,26 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
       a.src[p] = in->ptrs[p];
       a.dst[p] = out->ptrs[p];
     }
-    a.s = N == 1 ? lo : s;
-    a.e = N == 1 ? hi : e;
+    a.s = s;
+    a.e = e;
     a.range_bytes = hi - lo;
     a.g = g;
     a.bar = barrierArgs(r, epoch);
-    a.use_barrier = N > 1;
+    a.use_barrier = 1;
     a.rank = me;
     a.post = post;
+    a.ctl = ctl;
     gateEnter(gate, st);
-    const int grid = gated(smGrid(r, lo, hi), gate);
-    if (smTmaEnabled()) {
-      dispatchTma(N, dtype, a, grid, st);
-    } else {
-      dispatchFold<1>(N, dtype, a, grid, st);
-    }
+    launchCrossFold(r, dtype, a, gated(smGrid(r, lo, hi), gate), st);
     NZ_CUDA(cudaGetLastError());
-    gateExit(gate, st);
     return;
   }
 
   if (r->kind == NZ_RAIL_NVLS) {
     if (!in->mc_ptr || !out->mc_ptr) fail(NZ_ERR_UNSUPPORTED, "NVLS rail needs multicast-bound buffers");
-    NvlsArgs a{};
-    if (reinterpret_cast<uintptr_t>(in->mc_ptr) % 16 != 0 || reinterpret_cast<uintptr_t>(out->mc_ptr) % 16 != 0) {
+    if (reinterpret_cast<uintptr_t>(in->mc_ptr) % 16 != 0 || reinterpret_cast<uintptr_t>(out->mc_ptr) % 16 != 0)
       fail(NZ_ERR_INVALID, "multicast windows must be 16-byte aligned");
-    }
+    NvlsArgs a{};
     a.mc_in = in->mc_ptr;
     a.mc_out = out->mc_ptr;
     for (int p = 0; p < N; ++p) {
@@ -480,61 +416,98 @@ void railOp(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, const
     a.f.use_barrier = 1;
     a.f.rank = me;
     a.f.post = post;
+    a.f.ctl = ctl;
     gateEnter(gate, st);
     dispatchNvls(N, dtype, a, gated(gridFor(r, hi - lo, N, 4), gate), st);
     NZ_CUDA(cudaGetLastError());
-    gateExit(gate, st);
     return;
   }
 
-  // Copy-engine rail: barrier, DMA gather of my shard from every peer,
-  // local ring-order reduce, DMA scatter of the sum, barrier.
+  // Copy-engine rail: start barrier, then per piece of my shard a DMA gather
+  // from every peer, the local ring-order reduce and a DMA scatter of the sum
+  // to every peer, pipelined across pieces; end barrier.
+  RailCtl start_ctl = ctl;
+  start_ctl.final_wave = 0;
+  start_ctl.prog_chunk = ~0ull;
+  launchBarrier(r, epoch, false, FaultPost{}, start_ctl, st);
   const uint64_t len = e - s;
-  // Staged copies keep the 16-byte phase of the source so the reduce kernel's
-  // vector loads stay aligned: copy from s16 = align_down(s, 16).
-  const uint64_t s16 = s & ~15ull;
-  const uint64_t slen = e - s16;
-  ensureStaging(r, slen);
-  launchBarrier(r, epoch, FaultPost{}, st);
   if (len > 0) {
-    NZ_CUDA(cudaEventRecord(r->fork, st));
-    for (int j = 1; j < N; ++j) {
-      const int p = (me + j) % N;
-      cudaStream_t ss = r->side[j - 1];
-      NZ_CUDA(cudaStreamWaitEvent(ss, r->fork, 0));
-      NZ_CUDA(cudaMemcpyAsync(r->staging + (j - 1) * r->staging_slot, in->ptrs[p] + s16, slen, cudaMemcpyDeviceToDevice, ss));
-      NZ_CUDA(cudaEventRecord(r->join[j - 1], ss));
-      NZ_CUDA(cudaStreamWaitEvent(st, r->join[j - 1], 0));
+    // Staged copies keep the 16-byte phase of the source so the reduce
+    // kernel's vector loads stay aligned: copy from s16 = align_down(s, 16).
+    const uint64_t s16 = s & ~15ull;
+    {
+      std::lock_guard<std::mutex> lk(g_retired_mu);
+      ensureStaging(r, e - s16, &g_retired[r]);
     }
+    const int P = cePieces(len);
+    std::vector<uint64_t> cut(P + 1);
+    cut[0] = s;
+    cut[P] = e;
+    for (int i = 1; i < P; ++i) cut[i] = std::max<uint64_t>(s, (s16 + (e - s16) * i / P) & ~15ull);
+    const int peers = N - 1;  // side[0 .. peers) gather, side[peers .. 2 peers) scatter
+    NZ_CUDA(cudaEventRecord(r->fork, st));
+    for (int j = 0; j < 2 * peers; ++j) NZ_CUDA(cudaStreamWaitEvent(r->side[j], r->fork, 0));
     FoldArgs a{};
     for (int p = 0; p < N; ++p) {
       const int j = (p - me + N) % N;
       a.src[p] = j == 0 ? in->ptrs[me] : r->staging + (j - 1) * r->staging_slot - s16;
     }
     a.dst[0] = out->ptrs[me];
-    a.s = s;
-    a.e = e;
     a.range_bytes = hi - lo;
     a.g = g;
     a.use_barrier = 0;
     a.rank = me;
-    gateEnter(gate, st);  // computation phase: the local fold
-    dispatchFold<0>(N, dtype, a, gated(gridFor(r, hi - lo, N, 2), gate), st);
-    NZ_CUDA(cudaGetLastError());
-    gateExit(gate, st);
-    NZ_CUDA(cudaEventRecord(r->fork, st));
-    for (int j = 1; j < N; ++j) {
-      const int p = (me + j) % N;
-      cudaStream_t ss = r->side[j - 1];
-      NZ_CUDA(cudaStreamWaitEvent(ss, r->fork, 0));
-      NZ_CUDA(cudaMemcpyAsync(out->ptrs[p] + s, out->ptrs[me] + s, len, cudaMemcpyDeviceToDevice, ss));
-      NZ_CUDA(cudaEventRecord(r->join[j - 1], ss));
-      NZ_CUDA(cudaStreamWaitEvent(st, r->join[j - 1], 0));
+    for (int i = 0; i < P; ++i) {
+      const uint64_t ps = cut[i], pe = cut[i + 1];
+      if (pe <= ps) continue;
+      const uint64_t ps16 = ps & ~15ull;
+      for (int j = 1; j < N; ++j) {
+        const int p = (me + j) % N;
+        cudaStream_t gs = r->side[j - 1];
+        NZ_CUDA(cudaMemcpyAsync(r->staging + (j - 1) * r->staging_slot + (ps16 - s16), in->ptrs[p] + ps16, pe - ps16,
+                                cudaMemcpyDeviceToDevice, gs));
+        NZ_CUDA(cudaEventRecord(r->join[j - 1], gs));
+        NZ_CUDA(cudaStreamWaitEvent(st, r->join[j - 1], 0));
+      }
+      a.s = ps;
+      a.e = pe;
+      gateEnter(gate, st);  // computation phase: the local folds
+      dispatchFold<0>(N, dtype, a, gated(gridFor(r, (pe - ps) * N, N, 2), gate), st);
+      NZ_CUDA(cudaGetLastError());
+      NZ_CUDA(cudaEventRecord(r->fork, st));
+      for (int j = 1; j < N; ++j) {
+        const int p = (me + j) % N;
+        cudaStream_t ss = r->side[peers + j - 1];
+        NZ_CUDA(cudaStreamWaitEvent(ss, r->fork, 0));
+        NZ_CUDA(cudaMemcpyAsync(out->ptrs[p] + ps, out->ptrs[me] + ps, pe - ps, cudaMemcpyDeviceToDevice, ss));
+      }
+    }
+    for (int j = 0; j < peers; ++j) {
+      NZ_CUDA(cudaEventRecord(r->join[peers + j], r->side[peers + j]));
+      NZ_CUDA(cudaStreamWaitEvent(st, r->join[peers + j], 0));
     }
   }
-  launchBarrier(r, epoch + 1, post, st);
+  launchBarrier(r, epoch + 1, true, post, ctl, st);
   NZ_CUDA(cudaGetLastError());
-  gateExit(gate, st);  // empty shard: nothing was folded
+}
+
+// Orders a launch on `st` after the rail's previous launch on another stream.
+void orderOn(nz_rail* r, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  NZ_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    r->last_stream = nullptr;  // the capture's own edges order it; nothing to record across
+    return;
+  }
+  if (r->last_stream && r->last_stream != st) {
+    cudaStreamCaptureStatus pc = cudaStreamCaptureStatusNone;
+    NZ_CUDA(cudaStreamIsCapturing(r->last_stream, &pc));
+    if (pc == cudaStreamCaptureStatusNone) {
+      NZ_CUDA(cudaEventRecord(r->order_ev, r->last_stream));
+      NZ_CUDA(cudaStreamWaitEvent(st, r->order_ev, 0));
+    }
+  }
+  r->last_stream = st;
 }
 
 }  // namespace
@@ -552,47 +525,234 @@ void launchStamp(uint64_t* dst, cudaStream_t st) {
   NZ_CUDA(cudaGetLastError());
 }
 
-// Used by the engine (engine.cpp) without going through the C ABI.
-void railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes,
-                   uint64_t chunk_begin, uint64_t chunk_end, int dtype, uint32_t op_seq, int64_t fail_chunk,
-                   cudaStream_t st, ComputeGate* gate) {
-  const int es = elemSize(dtype);
-  if (chunk_bytes == 0 || chunk_bytes % es || seg_off % es || seg_len % es) {
+std::vector<std::pair<uint64_t, uint64_t>> railWaves(uint64_t seg_len, uint64_t chunk_bytes, uint64_t cb,
+                                                     uint64_t ce) {
+  std::vector<std::pair<uint64_t, uint64_t>> w;
+  if (ce <= cb || chunk_bytes == 0) return w;
+  const uint64_t per = std::max<uint64_t>(1, (waveBytes() + chunk_bytes - 1) / chunk_bytes);
+  (void)seg_len;
+  for (uint64_t c0 = cb; c0 < ce; c0 += per) w.emplace_back(c0, std::min(ce, c0 + per));
+  // A short last wave joins the previous one (no launch for a sliver).
+  if (w.size() > 1 && (w.back().second - w.back().first) * 2 < per) {
+    w[w.size() - 2].second = w.back().second;
+    w.pop_back();
+  }
+  return w;
+}
+
+uint32_t railRun(nz_rail* r, const RailOp& op) {
+  const int es = elemSize(op.dtype);
+  if (op.chunk_bytes == 0 || op.chunk_bytes % es || op.seg_off % es || op.seg_len % es) {
     fail(NZ_ERR_INVALID, "segment geometry not element aligned");
   }
-  if (in->comm != r->comm || out->comm != r->comm) fail(NZ_ERR_INVALID, "buffer from another comm");
-  if (seg_off + seg_len > in->size || seg_off + seg_len > out->size) fail(NZ_ERR_INVALID, "segment exceeds buffer");
-  const uint64_t nch = (seg_len + chunk_bytes - 1) / chunk_bytes;
-  chunk_end = std::min(chunk_end, nch);
-  if (chunk_begin > chunk_end) fail(NZ_ERR_INVALID, "chunk_begin > chunk_end");
+  if (op.in->comm != r->comm || op.out->comm != r->comm) fail(NZ_ERR_INVALID, "buffer from another comm");
+  if (op.seg_off + op.seg_len > op.in->size || op.seg_off + op.seg_len > op.out->size)
+    fail(NZ_ERR_INVALID, "segment exceeds buffer");
+  const uint64_t nch = (op.seg_len + op.chunk_bytes - 1) / op.chunk_bytes;
+  const uint64_t chunk_end = std::min(op.chunk_end, nch);
+  if (op.chunk_begin > chunk_end) fail(NZ_ERR_INVALID, "chunk_begin > chunk_end");
   uint64_t stop = chunk_end;
   FaultPost post{};
-  if (fail_chunk >= 0 && static_cast<uint64_t>(fail_chunk) >= chunk_begin && static_cast<uint64_t>(fail_chunk) < chunk_end) {
-    stop = static_cast<uint64_t>(fail_chunk);
+  if (op.fail_chunk >= 0 && static_cast<uint64_t>(op.fail_chunk) >= op.chunk_begin &&
+      static_cast<uint64_t>(op.fail_chunk) < chunk_end) {
+    stop = static_cast<uint64_t>(op.fail_chunk);
     post.rec = r->fault_dev;
-    post.op_seq = op_seq;
+    post.op_seq = op.op_seq;
     post.chunk = stop;
   }
-  const uint64_t lo = seg_off + std::min(seg_len, chunk_begin * chunk_bytes);
-  const uint64_t hi = seg_off + std::min(seg_len, stop * chunk_bytes);
-  if (!st) st = r->stream;
+  int64_t stall = op.stall_chunk >= 0 ? op.stall_chunk : r->stall_chunk;
+  r->stall_chunk = -1;
+  cudaStream_t st = op.st ? op.st : r->stream;
   NZ_CUDA(cudaSetDevice(r->comm->device));
-  if (hi > lo) {
-    railOp(r, in, out, lo, hi, Geometry{seg_off, seg_len, chunk_bytes}, dtype, post, st, gate);
-  } else if (post.rec) {
-    launchBarrier(r, r->epoch + 1, post, st);
+  orderOn(r, st);
+  if (++r->tag == 0) r->tag = 1;
+  const uint32_t tag = r->tag;
+  const Geometry g{op.seg_off, op.seg_len, op.chunk_bytes};
+  const uint64_t lo = op.seg_off + std::min(op.seg_len, op.chunk_begin * op.chunk_bytes);
+  const uint64_t hi = op.seg_off + std::min(op.seg_len, stop * op.chunk_bytes);
+  RailCtl ctl{};
+  ctl.dev = r->ctl_dev;
+  ctl.host = r->status_dev;
+  ctl.tag = tag;
+  if (hi <= lo) {
+    if (!post.rec) return 0;
+    // Nothing to reduce, but the trace-form failure is still posted.
+    ctl.final_wave = op.status ? 1 : 0;
+    ctl.prog_chunk = op.status ? stop : ~0ull;
+    ctl.end_timeout_ns = detectNs(r, 0);
+    launchBarrier(r, r->epoch + 1, true, post, ctl, st);
     r->epoch += 2;
+    gateExit(op.gate, st);
+    return op.status ? tag : 0;
   }
-  gateExit(gate, st);
+  std::vector<std::pair<uint64_t, uint64_t>> waves;
+  if (llPath(r, lo, hi))
+    waves.emplace_back(op.chunk_begin, stop);
+  else
+    waves = railWaves(op.seg_len, op.chunk_bytes, op.chunk_begin, stop);
+  for (size_t w = 0; w < waves.size(); ++w) {
+    const auto [c0, c1] = waves[w];
+    const bool last = w + 1 == waves.size();
+    const uint64_t wlo = op.seg_off + std::min(op.seg_len, c0 * op.chunk_bytes);
+    const uint64_t whi = op.seg_off + std::min(op.seg_len, c1 * op.chunk_bytes);
+    ctl.final_wave = last && op.status ? 1 : 0;
+    ctl.prog_chunk = op.status ? c1 : ~0ull;
+    ctl.stall = stall >= 0 && static_cast<uint64_t>(stall) >= c0 && static_cast<uint64_t>(stall) < c1 ? 1 : 0;
+    ctl.end_timeout_ns = detectNs(r, whi - wlo);
+    railWave(r, op.in, op.out, wlo, whi, g, op.dtype, last ? post : FaultPost{}, ctl, st, op.gate);
+  }
+  gateExit(op.gate, st);
+  return op.status ? tag : 0;
 }
 
 int railComputeCtas(nz_rail* r, uint64_t seg_len) {
   if (seg_len == 0) return 0;
   if (llPath(r, 0, seg_len)) return llGrid(r, 0, seg_len);
-  if (oneshotPath(r, 0, seg_len)) return oneshotGrid(r, 0, seg_len);
   if (r->comm->world == 1) return copyGrid(r, 0, seg_len);
   if (r->kind == NZ_RAIL_SM) return smGrid(r, 0, seg_len);
   return gridFor(r, seg_len, r->comm->world, r->kind == NZ_RAIL_NVLS ? 4 : 2);
+}
+
+CUdeviceptr railGateAddr(nz_rail* r) { return reinterpret_cast<CUdeviceptr>(r->ctl_dev + kCtlGate); }
+
+void railRevive(nz_rail* r, cudaStream_t st) {
+  NZ_CUDA(cudaSetDevice(r->comm->device));
+  if (!st) st = r->stream;
+  orderOn(r, st);
+  NZ_CUDA(cudaMemsetAsync(r->ctl_dev + kCtlRetired, 0, 2 * sizeof(uint32_t), st));
+  NZ_CUDA(cudaMemsetAsync(r->ctl_dev + kCtlSticky, 0, sizeof(uint32_t), st));
+  NZ_CUDA(cudaStreamSynchronize(st));
+  reinterpret_cast<volatile nz_rail_status_t*>(r->status_host)->abort = 0;
+  *reinterpret_cast<volatile int*>(r->wd_host) = 0;
+  r->stall_chunk = -1;
+}
+
+nz_rail* railCreate(nz_comm* comm, int kind, int rail_id, int sm_budget, bool graph_safe, bool recovery) {
+  if (kind < NZ_RAIL_NVLS || kind > NZ_RAIL_SM) fail(NZ_ERR_INVALID, "unknown rail kind");
+  if (kind == NZ_RAIL_NVLS && comm->world > 1 && !comm->multicast) {
+    fail(NZ_ERR_UNSUPPORTED, comm->loop ? "NVLS rail needs NVSwitch multicast: not available to loopback ranks"
+                                        : "NVLS rail requires NVSwitch multicast support");
+  }
+  NZ_CUDA(cudaSetDevice(comm->device));
+  int pad = -1;
+  bool reused = false;
+  if (!comm->free_pads.empty()) {
+    pad = comm->free_pads.front();
+    comm->free_pads.erase(comm->free_pads.begin());
+    reused = true;
+  } else {
+    if (comm->next_pad >= kMaxRails) fail(NZ_ERR_INVALID, "too many rails on one comm");
+    pad = comm->next_pad++;
+  }
+  auto* r = new nz_rail();
+  r->comm = comm;
+  r->kind = kind;
+  r->rail_id = rail_id;
+  r->sm_budget = sm_budget;
+  r->pad = pad;
+  r->graph_safe = graph_safe;
+  r->recovery = recovery;
+  try {
+    const size_t pad_off = kPadBytes * pad;
+    r->pad_local = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[comm->rank] + pad_off);
+    for (int p = 0; p < comm->world; ++p) r->pad_peer[p] = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[p] + pad_off);
+    if (reused) {  // a recycled pad starts from zero epochs on every rank
+      NZ_CUDA(cudaMemset(r->pad_local, 0, kPadBytes));
+      NZ_CUDA(cudaDeviceSynchronize());
+      exchange(comm, nullptr, 0, {});
+    }
+    NZ_CUDA(cudaMalloc(&r->ctl_dev, kCtlWords * sizeof(uint32_t)));
+    NZ_CUDA(cudaMemset(r->ctl_dev, 0, kCtlWords * sizeof(uint32_t)));
+    NZ_CUDA(cudaHostAlloc(&r->status_host, sizeof(nz_rail_status_t), cudaHostAllocMapped));
+    memset(r->status_host, 0, sizeof(nz_rail_status_t));
+    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->status_dev), r->status_host, 0));
+    NZ_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+    NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
+    NZ_CUDA(cudaEventCreateWithFlags(&r->order_ev, cudaEventDisableTiming));
+    if (kind == NZ_RAIL_SM && comm->world > 1 && !recovery) {
+      // LL slots: [parity 2][rank N][words] x 8 bytes, zeroed on every rank
+      // first. Even word count: every slot starts 16-byte aligned for the v4 pushes.
+      r->ll_slot_words = ((llMaxBytes(comm->world) + 7) / 4 + 1) & ~uint64_t{1};
+      r->ll = allocSymmetric(comm, 2 * comm->world * r->ll_slot_words * sizeof(uint64_t));
+      r->ll_cap = r->ll_max = llMaxBytes(comm->world);
+      NZ_CUDA(cudaMemset(r->ll->ptrs[comm->rank], 0, r->ll->mapped));
+      NZ_CUDA(cudaDeviceSynchronize());
+      exchange(comm, nullptr, 0, {});
+    }
+    if (kind == NZ_RAIL_CE) {
+      for (int j = 0; j < 2 * (comm->world - 1); ++j) {  // gather streams, then scatter streams
+        cudaStream_t s;
+        cudaEvent_t e;
+        NZ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        NZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        r->side.push_back(s);
+        r->join.push_back(e);
+      }
+    }
+    NZ_CUDA(cudaHostAlloc(&r->fault_host, sizeof(nz_fault_record_t), cudaHostAllocMapped));
+    memset(r->fault_host, 0, sizeof(nz_fault_record_t));
+    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->fault_dev), r->fault_host, 0));
+    NZ_CUDA(cudaHostAlloc(&r->wd_host, sizeof(int), cudaHostAllocMapped));
+    *r->wd_host = 0;
+    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->wd_dev), r->wd_host, 0));
+    if (comm->loop && comm->world > 1) {
+      NZ_CUDA(cudaEventCreateWithFlags(&r->lr_ready, cudaEventDisableTiming));
+      NZ_CUDA(cudaEventCreateWithFlags(&r->lr_done, cudaEventDisableTiming));
+      std::lock_guard<std::mutex> lk(comm->loop->m);
+      auto& slot = comm->loop->rails[pad];
+      if (!slot) {
+        slot = std::make_unique<LoopRail>();
+        NZ_CUDA(cudaStreamCreateWithFlags(&slot->stream, cudaStreamNonBlocking));
+      }
+      slot->ready[comm->rank] = r->lr_ready;
+      slot->done[comm->rank] = r->lr_done;
+      r->lr = slot.get();
+    }
+  } catch (...) {
+    comm->live_rails++;  // railDestroy returns the pad and the count
+    railDestroy(r);
+    throw;
+  }
+  comm->live_rails++;
+  return r;
+}
+
+void railDestroy(nz_rail* r) {
+  if (!r) return;
+  nz_comm* comm = r->comm;
+  cudaSetDevice(comm->device);
+  if (r->stream) cudaStreamSynchronize(r->stream);
+  for (auto s : r->side) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  for (auto e : r->join) cudaEventDestroy(e);
+  if (r->lr) {
+    // The group stream may still run this rank's last combined grid.
+    cudaStreamSynchronize(r->lr->stream);
+  }
+  if (r->fork) cudaEventDestroy(r->fork);
+  if (r->order_ev) cudaEventDestroy(r->order_ev);
+  if (r->lr_ready) cudaEventDestroy(r->lr_ready);
+  if (r->lr_done) cudaEventDestroy(r->lr_done);
+  if (r->stream) cudaStreamDestroy(r->stream);
+  if (r->staging) cudaFree(r->staging);
+  {
+    std::lock_guard<std::mutex> lk(g_retired_mu);
+    auto it = g_retired.find(r);
+    if (it != g_retired.end()) {
+      for (char* p : it->second) cudaFree(p);
+      g_retired.erase(it);
+    }
+  }
+  if (r->ll) freeSymmetric(r->ll);
+  if (r->fault_host) cudaFreeHost(r->fault_host);
+  if (r->wd_host) cudaFreeHost(r->wd_host);
+  if (r->status_host) cudaFreeHost(r->status_host);
+  if (r->ctl_dev) cudaFree(r->ctl_dev);
+  comm->free_pads.push_back(r->pad);
+  comm->live_rails = std::max(0, comm->live_rails - 1);
+  delete r;
 }
 
 }  // namespace nz
@@ -614,79 +774,14 @@ int nz_rail_create_ex(nz_comm_t* comm, int kind, int rail_id, int sm_budget, int
   return guarded([&] {
     if (!comm || !out) fail(NZ_ERR_INVALID, "null argument");
     if (flags & ~NZ_RAIL_FLAG_GRAPH_SAFE) fail(NZ_ERR_INVALID, "unknown rail flags");
-    if (kind < NZ_RAIL_NVLS || kind > NZ_RAIL_SM) fail(NZ_ERR_INVALID, "unknown rail kind");
-    if (kind == NZ_RAIL_NVLS && comm->world > 1 && !comm->multicast) {
-      fail(NZ_ERR_UNSUPPORTED, "NVLS rail requires NVSwitch multicast support");
-    }
-    if (comm->next_pad >= nz::kMaxRails) fail(NZ_ERR_INVALID, "too many rails on one comm");
-    NZ_CUDA(cudaSetDevice(comm->device));
-    auto* r = new nz_rail();
-    r->comm = comm;
-    r->kind = kind;
-    r->rail_id = rail_id;
-    if (flags & NZ_RAIL_FLAG_GRAPH_SAFE) {  // device op counter (kernels.cuh seq_retire), zero on every rank
-      NZ_CUDA(cudaMalloc(&r->seq_dev, 2 * sizeof(uint32_t)));
-      NZ_CUDA(cudaMemset(r->seq_dev, 0, 2 * sizeof(uint32_t)));
-    }
-    r->sm_budget = sm_budget;
-    const size_t pad_off = nz::kPadBytes * comm->next_pad++;
-    r->pad_local = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[comm->rank] + pad_off);
-    for (int p = 0; p < comm->world; ++p) r->pad_peer[p] = reinterpret_cast<uint32_t*>(comm->ctrl->ptrs[p] + pad_off);
-    NZ_CUDA(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
-    NZ_CUDA(cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming));
-    if ((kind == NZ_RAIL_SM || (kind == NZ_RAIL_NVLS && nz::nvlsLLEnabled())) && comm->world > 1) {
-      // LL slots: [parity 2][rank N][kLLMaxBytes / 4 words] x 8 bytes, zeroed on every rank first.
-      // Even word count: every slot starts 16-byte aligned for the v4 pushes.
-      r->ll_slot_words = ((nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS) + 7) / 4 + 1) & ~uint64_t{1};
-      r->ll = nz::allocSymmetric(comm, 2 * comm->world * r->ll_slot_words * sizeof(uint64_t));
-      r->ll_cap = r->ll_max = nz::llMaxBytes(comm->world, kind == NZ_RAIL_NVLS);
-      NZ_CUDA(cudaMemset(r->ll->ptrs[comm->rank], 0, r->ll->mapped));
-      NZ_CUDA(cudaDeviceSynchronize());
-      nz::exchange(comm, nullptr, 0, {});
-    }
-    if (kind == NZ_RAIL_SM && comm->world > 1 && nz::oneshotEnabled()) {
-      r->os_slot = (nz::oneshotMaxBytes(comm->world) + 16 + 255) & ~uint64_t{255};
-      r->os = nz::allocSymmetric(comm, 2 * comm->world * r->os_slot);
-      r->os_cap = r->os_max = nz::oneshotMaxBytes(comm->world);
-    }
-    if (kind == NZ_RAIL_CE) {
-      for (int j = 1; j < comm->world; ++j) {
-        cudaStream_t s;
-        cudaEvent_t e;
-        NZ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        NZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        r->side.push_back(s);
-        r->join.push_back(e);
-      }
-    }
-    NZ_CUDA(cudaHostAlloc(&r->fault_host, sizeof(nz_fault_record_t), cudaHostAllocMapped));
-    memset(r->fault_host, 0, sizeof(nz_fault_record_t));
-    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->fault_dev), r->fault_host, 0));
-    NZ_CUDA(cudaHostAlloc(&r->wd_host, sizeof(int), cudaHostAllocMapped));
-    *r->wd_host = 0;
-    NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r->wd_dev), r->wd_host, 0));
-    *out = r;
+    if ((flags & NZ_RAIL_FLAG_GRAPH_SAFE) && comm->loop && comm->world > 1)
+      fail(NZ_ERR_UNSUPPORTED, "graph-safe rails need one process per rank (loopback launches cannot be captured)");
+    *out = nz::railCreate(comm, kind, rail_id, sm_budget, (flags & NZ_RAIL_FLAG_GRAPH_SAFE) != 0, false);
   });
 }
 
 int nz_rail_destroy(nz_rail_t* r) {
-  return guarded([&] {
-    if (!r) return;
-    cudaSetDevice(r->comm->device);
-    cudaStreamSynchronize(r->stream);
-    for (auto s : r->side) cudaStreamDestroy(s);
-    for (auto e : r->join) cudaEventDestroy(e);
-    if (r->fork) cudaEventDestroy(r->fork);
-    if (r->stream) cudaStreamDestroy(r->stream);
-    if (r->staging) cudaFree(r->staging);
-    if (r->ll) nz::freeSymmetric(r->ll);
-    if (r->fault_host) cudaFreeHost(r->fault_host);
-    if (r->wd_host) cudaFreeHost(r->wd_host);
-    if (r->done) cudaEventDestroy(r->done);
-    if (r->seq_dev) cudaFree(r->seq_dev);
-    if (r->os) nz::freeSymmetric(r->os);
-    delete r;
-  });
+  return guarded([&] { nz::railDestroy(r); });
 }
 
 int nz_rail_kind(const nz_rail_t* r) { return r ? r->kind : NZ_ERR_INVALID; }
@@ -697,6 +792,7 @@ int nz_rail_synchronize(nz_rail_t* r) {
     NZ_CUDA(cudaSetDevice(r->comm->device));
     for (auto s : r->side) NZ_CUDA(cudaStreamSynchronize(s));
     NZ_CUDA(cudaStreamSynchronize(r->stream));
+    if (r->last_stream && r->last_stream != r->stream) NZ_CUDA(cudaStreamSynchronize(r->last_stream));
   });
 }
 void* nz_rail_stream(const nz_rail_t* r) { return r ? static_cast<void*>(r->stream) : nullptr; }
@@ -709,19 +805,31 @@ int nz_rail_allreduce(nz_rail_t* rail, nz_buf_t* in, nz_buf_t* out, uint64_t seg
     if (rail->aborted) fail(NZ_ERR_RAIL_DOWN, "rail " + std::to_string(rail->rail_id) + " was aborted");
     if (fail_chunk < 0 && rail->armed_fail >= 0) fail_chunk = rail->armed_fail;
     rail->armed_fail = -1;
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : rail->stream;
-    nz::railAllreduce(rail, in, out, seg_off, seg_len, chunk_bytes, chunk_begin, chunk_end, dtype, op_seq, fail_chunk,
-                      st);
+    nz::RailOp o;
+    o.in = in;
+    o.out = out;
+    o.seg_off = seg_off;
+    o.seg_len = seg_len;
+    o.chunk_bytes = chunk_bytes;
+    o.chunk_begin = chunk_begin;
+    o.chunk_end = chunk_end;
+    o.dtype = dtype;
+    o.op_seq = op_seq;
+    o.fail_chunk = fail_chunk;
+    o.st = stream ? static_cast<cudaStream_t>(stream) : rail->stream;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    NZ_CUDA(cudaStreamIsCapturing(o.st, &cap));
+    o.status = cap == cudaStreamCaptureStatusNone;
+    nz::railRun(rail, o);
     const uint64_t nch = chunk_bytes ? (seg_len + chunk_bytes - 1) / chunk_bytes : 0;
     const uint64_t end = std::min(chunk_end, nch);
+    rail->last_tag = rail->tag;
     rail->prog_begin = std::min(chunk_begin, end);
     rail->prog_stop = fail_chunk >= 0 && static_cast<uint64_t>(fail_chunk) >= rail->prog_begin &&
                               static_cast<uint64_t>(fail_chunk) < end
                           ? static_cast<uint64_t>(fail_chunk)
                           : end;
-    if (!rail->done) NZ_CUDA(cudaEventCreateWithFlags(&rail->done, cudaEventDisableTiming));
-    NZ_CUDA(cudaEventRecord(rail->done, st));
-    rail->prog_valid = true;
+    rail->prog_valid = o.status;
   });
 }
 
@@ -733,6 +841,45 @@ int nz_rail_inject_failure(nz_rail_t* rail, uint64_t chunk) {
   });
 }
 
+int nz_rail_inject_stall(nz_rail_t* rail, uint64_t chunk) {
+  return guarded([&] {
+    if (!rail) fail(NZ_ERR_INVALID, "null rail");
+    if (chunk > static_cast<uint64_t>(INT64_MAX)) fail(NZ_ERR_INVALID, "chunk out of range");
+    rail->stall_chunk = static_cast<int64_t>(chunk);
+  });
+}
+
+int nz_rail_revive(nz_rail_t* rail) {
+  return guarded([&] {
+    if (!rail) fail(NZ_ERR_INVALID, "null rail");
+    nz::railRevive(rail, nullptr);
+  });
+}
+
+int nz_rail_set_detect_us(nz_rail_t* rail, double us) {
+  return guarded([&] {
+    if (!rail || !(us >= 0)) fail(NZ_ERR_INVALID, "bad argument");
+    rail->detect_us = us;
+  });
+}
+
+int nz_rail_status(const nz_rail_t* rail, nz_rail_status_t* out) {
+  return guarded([&] {
+    if (!rail || !out) fail(NZ_ERR_INVALID, "null argument");
+    const volatile nz_rail_status_t* s = rail->status_host;
+    out->ok_tag = s->ok_tag;
+    out->prog_tag = s->prog_tag;
+    out->prog_chunk = s->prog_chunk;
+    out->start_tag = s->start_tag;
+    out->fail_tag = s->fail_tag;
+    out->t_start_ns = s->t_start_ns;
+    out->t_fail_ns = s->t_fail_ns;
+    out->det_tag = s->det_tag;
+    out->abort = s->abort;
+    out->t_det_ns = s->t_det_ns;
+  });
+}
+
 int nz_rail_progress(nz_rail_t* rail, uint64_t* chunks_done) {
   return guarded([&] {
     if (!rail || !chunks_done) fail(NZ_ERR_INVALID, "null argument");
@@ -740,14 +887,14 @@ int nz_rail_progress(nz_rail_t* rail, uint64_t* chunks_done) {
       *chunks_done = 0;
       return;
     }
-    NZ_CUDA(cudaSetDevice(rail->comm->device));
-    const cudaError_t q = cudaEventQuery(rail->done);
-    if (q == cudaErrorNotReady) {
+    const volatile nz_rail_status_t* s = rail->status_host;
+    if (s->ok_tag == rail->last_tag) {
+      *chunks_done = rail->prog_stop;
+    } else if (s->prog_tag == rail->last_tag) {
+      *chunks_done = std::min<uint64_t>(static_cast<uint64_t>(s->prog_chunk), rail->prog_stop);
+    } else {
       *chunks_done = rail->prog_begin;
-      return;
     }
-    NZ_CUDA(q);
-    *chunks_done = rail->prog_stop;
   });
 }
 
@@ -768,11 +915,10 @@ int nz_event_elapsed_us(void* start, void* end, double* us) {
   });
 }
 
-namespace {
-int emulateFold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst, uint64_t seg_off,
-                uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid, void* stream, bool tma) {
+int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
+                    uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
+                    void* stream) {
   return guarded([&] {
-    if (tma && (ndst != world || world < 2)) fail(NZ_ERR_INVALID, "TMA emulation needs ndst == world >= 2");
     if (world < 1 || world > nz::kMaxRanks || rank < 0 || rank >= world) fail(NZ_ERR_INVALID, "bad world/rank");
     if (!src || !dst || (ndst != 1 && ndst != world)) fail(NZ_ERR_INVALID, "bad src/dst");
     const int es = nz::elemSize(dtype);
@@ -796,27 +942,12 @@ int emulateFold(int world, int rank, int dtype, const void* const* src, void* co
       grid = static_cast<int>(std::min<uint64_t>(sms, (per_rank_vec + 2 * nz::kThreads - 1) / (2 * nz::kThreads)));
       grid = std::max(grid, 1);
     }
-    if (tma)
-      nz::dispatchTma(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
-    else if (ndst == 1)
+    if (ndst == 1)
       nz::dispatchFold<0>(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
     else
       nz::dispatchFold<1>(world, dtype, a, grid, static_cast<cudaStream_t>(stream));
     NZ_CUDA(cudaGetLastError());
   });
-}
-}  // namespace
-
-int nz_emulate_fold(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
-                    uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
-                    void* stream) {
-  return emulateFold(world, rank, dtype, src, dst, ndst, seg_off, seg_len, chunk_bytes, lo, hi, grid, stream, false);
-}
-
-int nz_emulate_fold_tma(int world, int rank, int dtype, const void* const* src, void* const* dst, int ndst,
-                        uint64_t seg_off, uint64_t seg_len, uint64_t chunk_bytes, uint64_t lo, uint64_t hi, int grid,
-                        void* stream) {
-  return emulateFold(world, rank, dtype, src, dst, ndst, seg_off, seg_len, chunk_bytes, lo, hi, grid, stream, true);
 }
 
 int nz_rail_poll_fault(nz_rail_t* r, nz_fault_record_t* rec, int consume) {

