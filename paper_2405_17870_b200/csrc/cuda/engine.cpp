@@ -122,11 +122,6 @@ void nz_engine::launchSegment(uint32_t seq, const nezha::Plan& plan, const nezha
     NZ_CUDA(cudaStreamWaitEvent(user, *end_out, 0));
   }
   if (!monitored || capturing || tag == 0) return;
-  // The caller's stream passes this segment only once its gate word holds
-  // the tag: written by the rail's last launch when it succeeded, or by the
-  // monitor's reroute when it did not (DESIGN.md §6b).
-  NZ_CU(NZ_DRV(cuStreamWaitValue32)(reinterpret_cast<CUstream>(user), nz::railGateAddr(r), tag,
-                                    CU_STREAM_WAIT_VALUE_GEQ));
   Entry e;
   e.op = seq;
   e.rail = ri;
@@ -147,7 +142,12 @@ void nz_engine::launchSegment(uint32_t seq, const nezha::Plan& plan, const nezha
     }
   }
   if (!e.end) NZ_CUDA(cudaEventCreateWithFlags(&e.end, cudaEventDisableTiming));
-  NZ_CUDA(cudaEventRecord(e.end, st));
+  NZ_CUDA(cudaEventRecord(e.end, st));  // before the gate: the monitor must see a failed launch retire
+  // The caller's stream passes this segment only once its gate word holds
+  // the tag: written by the rail's last launch when it succeeded, or by the
+  // monitor's reroute when it did not (DESIGN.md §6b).
+  NZ_CU(NZ_DRV(cuStreamWaitValue32)(reinterpret_cast<CUstream>(user), nz::railGateAddr(r), tag,
+                                    CU_STREAM_WAIT_VALUE_GEQ));
   if (p) p->tags.emplace_back(ri, tag);
   {
     std::lock_guard<std::mutex> lk(mu);

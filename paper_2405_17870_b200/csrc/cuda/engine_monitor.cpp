@@ -99,6 +99,7 @@ void nz_engine::monitorLoop() {
   cudaSetDevice(comm->device);
   const double hb = cfg.heartbeat_us;
   auto last_clock = std::chrono::steady_clock::now();
+  uint64_t beat_key = ~0ull;  // (rail, tag) of the entry whose start was fed to the heartbeat clock
   for (;;) {
     Entry front;
     {
@@ -138,7 +139,18 @@ void nz_engine::monitorLoop() {
         std::lock_guard<std::mutex> lk(mu);
         for (size_t i = 0; i < specs.size(); ++i) {
           if (agreed_failed.count(specs[i].rail_id)) continue;
-          if (static_cast<int>(i) == front.rail && started) continue;
+          if (static_cast<int>(i) == front.rail && started) {
+            // Its last sign of life is the start of the launch it is in:
+            // missed beats count from there, not from queueing time.
+            const uint64_t key = (static_cast<uint64_t>(front.rail) << 32) | front.tag;
+            if (key != beat_key) {
+              const double age_us =
+                  static_cast<double>(realtimeNs() - (static_cast<int64_t>(st->t_start_ns) - clock_offset_ns)) / 1000.0;
+              health->heartbeat(specs[i].rail_id, now - std::max(0.0, age_us));
+              beat_key = key;
+            }
+            continue;
+          }
           health->heartbeat(specs[i].rail_id, now);
         }
         for (int id : health->tick(now))
@@ -239,7 +251,8 @@ void nz_engine::failover(Entry e, int64_t seen_ns) {
   // Reroute (P9/P10): the orphan chunks on the target's twin with the failed
   // segment's geometry, so order-controlled rails reproduce the same bits.
   volatile uint64_t* stamps = rec_stamps_host;
-  stamps[0] = stamps[1] = 0;
+  stamps[0] = 0;
+  stamps[1] = 0;
   nz::launchStamp(rec_stamps_dev + 0, tw->stream);
   uint32_t tag2 = 0;
   if (orphan.length > 0) {

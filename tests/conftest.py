@@ -7,6 +7,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# Bounded device waits for the whole test session: a rail kernel whose peer
+# never arrives gives up after 5 s instead of the production 20 s (read once
+# by the library, so it is set before anything loads it).
+os.environ.setdefault("NEZHA_WATCHDOG_MS", "5000")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run on the GPU box via gpurun)")

@@ -1,5 +1,6 @@
-"""GPU: the multi-rail engine end to end (planner + rails + handoff) against
-the CPU oracle, one process per GPU, through the C ABI."""
+"""GPU: the multi-rail engine end to end (planner + rails + failure monitor)
+against the CPU oracle, one process per GPU, through the C ABI. The same
+checks with virtual ranks on one GPU are in test_gpu_loopback.py."""
 import json
 import os
 
@@ -140,7 +141,7 @@ def test_engine_failover_reroute(fail_rail):
     world = 4 if gpu_count() >= 4 else 2
     if gpu_count() < 2:
         pytest.skip("needs 2 GPUs")
-    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3,
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000,
             "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 3, "fail": [fail_rail, 3], "fail_rep": 1},
                       {"dtype": "i32", "nbytes": 64 << 20, "reps": 2},
                       {"dtype": "i32", "nbytes": 96 << 20, "reps": 1, "readmit": True}]}
@@ -149,7 +150,8 @@ def test_engine_failover_reroute(fail_rail):
         fo = [r for r in rk["results"] if "failover" in r][0]["failover"]
         assert fo is not None and fo["failed_rail"] == fail_rail
         assert fo["target_rail"] != fail_rail and fo["orphan_length"] > 0
-        assert fo["done_us"] > 0
+        assert fo["done_us"] > 0 and 0 < fo["resume_after_detect_us"] < 1000, fo
+        assert fo["stalled_here"] == (1 if rk["rank"] == world - 1 else 0), fo
         # After the failure the rail carries nothing until it is readmitted.
         later = [r for r in rk["results"] if r["case"] == 0 and r["rep"] == 2] + \
                 [r for r in rk["results"] if r["case"] in (1, 2)]
@@ -159,9 +161,9 @@ def test_engine_failover_reroute(fail_rail):
 
 @pytest.mark.multigpu
 def test_engine_failover_trials_acceptance5():
-    """SPEC acceptance 5 on B200: repeated single-rail failures at
-    random rails / chunks; every result bit-exact (int32), every reroute
-    completes far inside the 200 ms budget."""
+    """SPEC acceptance 5 on B200: repeated unplanned single-rail
+    link deaths at random rails / chunks / ranks; every result bit-exact
+    (int32), every reroute resumes within 1 ms of its detection."""
     import random
 
     world = 4 if gpu_count() >= 4 else 2
@@ -171,11 +173,12 @@ def test_engine_failover_trials_acceptance5():
     cases = [{"dtype": "i32", "nbytes": 256 << 20, "reps": 2}]  # settle the hot split
     for _ in range(16):
         cases.append({"dtype": "i32", "nbytes": 256 << 20, "reps": 1, "fail": [rng.randrange(3), rng.randrange(6)],
-                      "readmit": True})
-    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "cases": cases}, timeout=600)
-    done = [r["failover"]["done_us"] for rk in res for r in rk["results"] if r.get("failover")]
-    assert len(done) >= 8, done
-    assert sum(d < 200_000 for d in done) >= 0.99 * len(done), done
+                      "fail_rank": rng.randrange(world), "readmit": True})
+    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000,
+                       "cases": cases}, timeout=600)
+    fos = [r["failover"] for rk in res for r in rk["results"] if r.get("failover")]
+    assert len(fos) >= 8, fos
+    assert all(f["resume_after_detect_us"] < 1000 for f in fos), fos
 
 
 @pytest.mark.multigpu
@@ -187,7 +190,8 @@ def test_engine_failover_int32_every_rail_exact():
     cases = []
     for rail in (0, 1, 2):
         cases.append({"dtype": "i32", "nbytes": 256 << 20, "reps": 1, "fail": [rail, 2], "readmit": True})
-    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "cases": cases}, timeout=420)
+    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000, "cases": cases},
+               timeout=420)
     for rk in res:
         assert len([r for r in rk["results"] if r.get("failover")]) == 3
 

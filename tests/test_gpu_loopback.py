@@ -1,0 +1,334 @@
+"""GPU parity of the rails and the engine on ONE B200 with virtual ranks.
+
+nz_comm_init_loopback: every rank of an N-rank job is a host thread of this
+process driving cuda:0, and every cross-rank kernel runs all ranks in one
+co-resident grid (blockIdx.y = rank). The rails' own protocols therefore run
+end to end — the SM rail's two-shot fold with its cross-rank barriers, its LL
+one-shot with flag polling, the copy-engine rail's DMA gathers / scatters
+between ranks' buffers and its pipelined reduce, the engine's hot split,
+Timer, unplanned failure detection, agreed reroute and readmit — and are
+checked bit-exact against the CPU oracle (P1/P2, P9/P10;
+SPEC.md:189-205, :409). NVLS needs an NVSwitch multicast team of real GPUs:
+its parity is in test_gpu_rails.py (>= 2 GPUs).
+"""
+import hashlib
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from tests.conftest import gpu_count
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(autouse=True)
+def _one_gpu():
+    if gpu_count() < 1:
+        pytest.skip("no GPU")
+    import torch
+
+    torch.cuda.set_device(0)
+
+
+def _rails(world, cases, timeout=600):
+    from paper_2405_17870_b200 import run_ranks
+    from tests.workers import rail_worker
+
+    try:
+        return run_ranks(world, lambda comm: rail_worker.run(comm, cases), timeout=timeout)
+    finally:
+        rail_worker.clear_cache()
+
+
+def _engine(world, spec, timeout=900):
+    from paper_2405_17870_b200 import run_ranks
+    from tests.workers import engine_worker
+
+    try:
+        res = run_ranks(world, lambda comm: engine_worker.run(comm, spec), timeout=timeout)
+    finally:
+        engine_worker.clear_cache()
+    for rk in res:
+        for r in rk["results"]:
+            assert r["mismatch"] == 0, r
+    plans = [[r["segs"] for r in rk["results"]] for rk in res]
+    assert all(p == plans[0] for p in plans), "ranks ran different plans"
+    return res
+
+
+RAIL_CASES = [
+    {"kind": "sm", "dtype": "f32", "nbytes": 1 << 20},                     # LL one-shot
+    {"kind": "sm", "dtype": "f32", "nbytes": 24 << 20},                    # two-shot fold + barriers
+    {"kind": "sm", "dtype": "bf16", "nbytes": 3_000_002, "seg_off": 2, "seg_len": 2_999_998},
+    {"kind": "sm", "dtype": "i32", "nbytes": 65_540},
+    {"kind": "sm", "dtype": "f32", "nbytes": 8192},
+    {"kind": "sm", "dtype": "bf16", "nbytes": 200_002},                    # LL, odd bf16 tail word
+    {"kind": "sm", "dtype": "f32", "nbytes": 262_144, "seg_off": 1024, "seg_len": 200_000},
+    {"kind": "sm", "dtype": "f32", "nbytes": 12},                          # fewer elements than ranks
+    {"kind": "sm", "dtype": "i32", "nbytes": 262_144, "fail_chunk": 0},    # LL range empty -> fault only
+    {"kind": "sm", "dtype": "f32", "nbytes": 64 << 20, "fail_chunk": 2},
+    {"kind": "sm", "dtype": "bf16", "nbytes": 8 << 20, "chunk_begin": 1, "chunk_end": 3},
+    {"kind": "sm", "dtype": "f32", "nbytes": 32 << 20, "fail_chunk": 3, "armed": True},
+    {"kind": "sm", "dtype": "f32", "nbytes": 4096, "abort": True},
+    {"kind": "ce", "dtype": "f32", "nbytes": 8 << 20},
+    {"kind": "ce", "dtype": "f32", "nbytes": 40 << 20},                    # pipelined pieces
+    {"kind": "ce", "dtype": "bf16", "nbytes": 1_000_010, "seg_off": 6, "seg_len": 1_000_000},
+    {"kind": "ce", "dtype": "i32", "nbytes": 4096},
+    {"kind": "ce", "dtype": "bf16", "nbytes": 32 << 20, "fail_chunk": 1},
+    {"kind": "ce", "dtype": "f32", "nbytes": 16 << 20, "chunk_begin": 3},
+    {"kind": "ce", "dtype": "f32", "nbytes": 4 << 20, "fail_chunk": 1, "armed": True},
+]
+
+
+def _check_rails(res, cases):
+    for rank_res in res:
+        for r in rank_res["results"]:
+            case = cases[r["case"]]
+            assert r["watchdog"] == 0, r
+            assert r["outside_nonzero"] == 0, r
+            assert r["mismatch"] == 0, r
+            assert r["progress"] == r["stop"], r
+            if case.get("abort"):
+                assert r["abort_refused"], r
+            if case.get("fail_chunk", -1) >= 0:
+                assert r["fault"] is not None and r["fault"]["chunk"] == case["fail_chunk"], r
+            else:
+                assert r["fault"] is None, r
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_rails_bit_exact(world):
+    """SM (LL + two-shot) and CE rails, every dtype, ragged geometries, chunk
+    windows and trace-form failures: bit-exact to the oracle on every rank."""
+    _check_rails(_rails(world, RAIL_CASES), RAIL_CASES)
+
+
+def random_rail_cases(seed, n=16):
+    rng = random.Random(seed)
+    cases = []
+    for _ in range(n):
+        dtype = rng.choice(["f32", "bf16", "i32"])
+        es = 2 if dtype == "bf16" else 4
+        nbytes = es * rng.choice([rng.randint(1, 4096), rng.randint(4096, 600_000), rng.randint(600_000, 6_000_000)])
+        seg_off = es * rng.randint(0, min(64, nbytes // es - 1))
+        seg_len = es * rng.randint(1, nbytes // es - seg_off // es)
+        c = {"kind": rng.choice(["sm", "ce"]), "dtype": dtype, "nbytes": nbytes, "seg_off": seg_off,
+             "seg_len": seg_len}
+        r = rng.random()
+        if r < 0.2:
+            c["fail_chunk"] = rng.randint(0, 3)
+        elif r < 0.35:
+            c["chunk_begin"] = rng.randint(0, 2)
+        cases.append(c)
+    return cases
+
+
+@pytest.mark.parametrize("world", [3, 5, 6, 7])
+def test_loopback_rails_randomized(world):
+    cases = random_rail_cases(200 + world)
+    res = _rails(world, cases)
+    for rank_res in res:
+        for r in rank_res["results"]:
+            assert r["watchdog"] == 0 and r["mismatch"] == 0 and r["outside_nonzero"] == 0, (r, cases[r["case"]])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("kind", ["sm", "ce"])
+def test_loopback_unplanned_link_death_detected(world, kind):
+    """One rank's link dies mid-op (nz_rail_inject_stall, the others are not
+    told): every rank's launch fails within the detection budget — the dead
+    rank stops, the peers' end-barrier waits give up — the waves completed
+    before the death are exact, and after nz_rail_revive the op is exact."""
+    big = 160 << 20  # several 64 MiB waves: progress is published between them
+    cases = [
+        {"kind": kind, "dtype": "f32", "nbytes": big, "stall": [world - 1, 7 if world >= 4 else 3], "detect_us": 2000},
+        {"kind": kind, "dtype": "i32", "nbytes": 24 << 20, "stall": [0, 0], "detect_us": 2000},
+    ]
+    if kind == "sm":
+        cases.append({"kind": "sm", "dtype": "bf16", "nbytes": 65536, "stall": [world // 2, 0], "detect_us": 2000})
+    res = _rails(world, cases)
+    for rank_res in res:
+        rank = rank_res["rank"]
+        for r in rank_res["results"]:
+            case = cases[r["case"]]
+            dead = case["stall"][0]
+            assert r["failed"], r
+            assert r["mismatch"] == 0, r  # completed waves
+            assert r["after_revive_mismatch"] == 0 and r["after_revive_watchdog"] == 0, r
+            if rank == dead:
+                assert r["stalled_here"], r
+            elif r["nbytes"] > 65536:
+                assert r["detected_here"] and r["watchdog"] == 1, r
+                assert r["seconds"] < 5.0, r
+    big_res = [rr for rk in res for rr in rk["results"] if rr["case"] == 0]
+    assert len({rr["progress"] for rr in big_res}) == 1  # every rank published the same completed waves
+    assert big_res[0]["progress"] > 0
+
+
+# Rails with fixed profiles so the hot split is exercised deterministically.
+TOML_LOOP = """
+[[rail]]
+protocol = "ce"
+t_setup_us = 40.0
+bandwidth_bps = 5.0e11
+[[rail]]
+protocol = "sm"
+t_setup_us = 14.0
+bandwidth_bps = 5.0e11
+[[rail]]
+protocol = "sm"
+t_setup_us = 12.0
+bandwidth_bps = 6.0e11
+"""
+KINDS3 = ["ce", "sm", "sm"]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_engine_multirail_parity(world):
+    spec = {"rails": KINDS3, "rails_toml": TOML_LOOP, "sync_overhead_us": 0.0, "window": 4,
+            "cases": [
+                {"dtype": "f32", "nbytes": 48 << 20, "reps": 10},
+                {"dtype": "bf16", "nbytes": 24 << 20, "reps": 2},
+                {"dtype": "i32", "nbytes": (16 << 20) + 12, "reps": 2},
+                {"dtype": "f32", "nbytes": 8192, "reps": 3},
+                {"dtype": "f32", "nbytes": 1 << 20, "reps": 2, "host": True},
+                {"dtype": "bf16", "nbytes": (12 << 20) + 2, "reps": 1, "host": True},
+                {"dtype": "f32", "nbytes": 4, "reps": 2},
+                {"dtype": "bf16", "nbytes": 2, "reps": 2},
+                {"dtype": "i32", "nbytes": 12, "reps": 1, "host": True},
+                {"dtype": "f32", "nbytes": (20 << 20) + 4, "reps": 2, "device": True},
+            ]}
+    res = _engine(world, spec)
+    hot = [r for r in res[0]["results"] if len(r["segs"]) > 1]
+    assert hot, "no op ran a multi-rail split"
+
+
+def test_loopback_engine_calibrated():
+    """No profiles given: the engine calibrates every rail alone and together
+    at startup (P13) and tunes the LL crossover; the
+    ops it then plans are exact."""
+    spec = {"rails": ["ce", "sm"], "calibrate_max_bytes": 16 << 20, "calibrate_iters": 4, "tune_budgets": 1,
+            "cases": [{"dtype": "f32", "nbytes": 16 << 20, "reps": 3}, {"dtype": "bf16", "nbytes": 65536, "reps": 2}]}
+    res = _engine(4, spec)
+    st = res[0]["state"]
+    assert all(r["calibration"] for r in st["rails"]), st
+    assert [r["ll_max"] for r in st["rails"]] == [r["ll_max"] for r in res[1]["state"]["rails"]]
+
+
+def test_loopback_config1_hash():
+    """BASELINE config 1 on the product path: 8 ranks, 2 rails with identical
+    profiles -> static 50/50 split, Ring, 64 MiB fp32, through the engine
+    (nz_engine_allreduce): the output hash equals the golden generated from
+    the reference's InMemoryFabric ring (tests/golden/config1_hash.json)."""
+    from paper_2405_17870_b200 import Engine, SymmetricBuffer, run_ranks
+
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "config1_hash.json")))
+    world, n = g["world"], g["bytes"]
+    toml = "".join(f'[[rail]]\nprotocol = "{k}"\nt_setup_us = 20.0\nbandwidth_bps = 5.0e11\n' for k in ("sm", "ce"))
+    inputs = [oracle.synthetic_input(oracle.F32, r, n) for r in range(world)]
+
+    def body(comm):
+        eng = Engine(comm, kinds=["sm", "ce"], rails_toml=toml, algorithm=0, window=1 << 30, sync_overhead_us=0.0)
+        bi, bo = SymmetricBuffer(comm, n), SymmetricBuffer(comm, n)
+        bi.write(inputs[comm.rank], n)
+        comm.barrier()
+        eng.allreduce(bi, bo, n, oracle.F32)
+        eng.synchronize()
+        got = np.zeros(n // 4, dtype=np.float32)
+        bo.read(got, n)
+        plan = eng.last_plans()[0]["segs"]
+        eng.close()
+        bi.free()
+        bo.free()
+        return hashlib.sha256(got.tobytes()).hexdigest(), plan
+
+    res = run_ranks(world, body)
+    for digest, plan in res:
+        assert [[s[0], s[1], s[2]] for s in plan] == g["segments"], plan
+        assert digest == g["sha256"]
+
+
+@pytest.mark.parametrize("fail_rail", [0, 1, 2])
+def test_loopback_engine_unplanned_failover(fail_rail):
+    """Config 4 shape (bf16, largest rail killed mid-op) with an UNPLANNED
+    failure: one rank's link of the rail dies at a chunk; every rank detects
+    it, the ranks agree on the orphan (min over ranks of completed chunks)
+    and reroute it to the P9 target; the result is bit-exact and the rail
+    carries nothing until it is readmitted (after the hold)."""
+    world = 4
+    spec = {"rails": KINDS3, "rails_toml": TOML_LOOP, "sync_overhead_us": 0.0, "readmit_hold_us": 100000, "heartbeat_us": 50000,
+            "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 3, "fail": [fail_rail, 5], "fail_rep": 1},
+                      {"dtype": "i32", "nbytes": 64 << 20, "reps": 2},
+                      {"dtype": "i32", "nbytes": 96 << 20, "reps": 1, "readmit": True}]}
+    res = _engine(world, spec)
+    for rk in res:
+        rec = [r for r in rk["results"] if "failover" in r][0]
+        fo = rec["failover"]
+        assert fo is not None and fo["failed_rail"] == fail_rail, rec
+        assert fo["target_rail"] != fail_rail and fo["orphan_length"] > 0
+        assert fo["stalled_here"] == (1 if rk["rank"] == world - 1 else 0), fo
+        assert 0 < fo["resume_after_detect_us"] < 1000, fo
+        assert fo["done_us"] > fo["resume_us"] > 0, fo
+        later = [r for r in rk["results"] if r["case"] == 0 and r["rep"] == 2] + \
+                [r for r in rk["results"] if r["case"] == 1]
+        for r in later:
+            assert all(s[0] != fail_rail for s in r["segs"]), r
+    # Identical reports on every rank (the agreement), timings aside.
+    keys = ("op_seq", "failed_rail", "target_rail", "orphan_offset", "orphan_length", "orphan_chunk")
+    reps = [tuple(rk["results"][1]["failover"][k] for k in keys) for rk in res]
+    assert len(set(reps)) == 1, reps
+
+
+def test_loopback_failover_trials_acceptance5():
+    """SPEC acceptance 5 with unplanned failures: repeated
+    single-rail link deaths at random rails / chunks / ranks, int32 (exact on
+    every rail), readmitted after each; every result bit-exact, every reroute
+    resumes within 1 ms of detection."""
+    rng = random.Random(539)
+    world = 4
+    cases = [{"dtype": "i32", "nbytes": 128 << 20, "reps": 2}]
+    for _ in range(8):
+        cases.append({"dtype": "i32", "nbytes": 128 << 20, "reps": 1, "fail": [rng.randrange(3), rng.randrange(6)],
+                      "fail_rank": rng.randrange(world), "readmit": True})
+    res = _engine(world, {"rails": KINDS3, "rails_toml": TOML_LOOP, "sync_overhead_us": 0.0, "readmit_hold_us": 50000, "cases": cases},
+                  timeout=1200)
+    fos = [r["failover"] for rk in res for r in rk["results"] if r.get("failover")]
+    assert len(fos) >= 4 * world, fos
+    assert all(f["resume_after_detect_us"] < 1000 for f in fos), fos
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_loopback_engine_compute_pool_parity(mode):
+    """SM arbitration of concurrent rails (ComputePool, P14): the
+    result is unchanged and every op's grants are the oracle's for its demands."""
+    from oracle.compute_pool import plan_grants
+
+    tokens = 100
+    spec = {"rails": KINDS3, "rails_toml": TOML_LOOP, "sync_overhead_us": 0.0, "window": 4, "compute_pool": mode, "pool_tokens": tokens,
+            "cases": [{"dtype": "f32", "nbytes": 48 << 20, "reps": 6},
+                      {"dtype": "bf16", "nbytes": 24 << 20, "reps": 2}]}
+    res = _engine(2, spec)
+    arbitrated = 0
+    for rk in res:
+        assert rk["state"]["compute_pool"]["mode"] == mode
+        for r in rk["results"]:
+            for g in r["grants"]:
+                want = plan_grants(tokens, mode, [(x[0], x[1]) for x in g])
+                assert [[w["rail"], w["demand"], w["grant"], w["waits"]] for w in want] == g, r
+                arbitrated += 1
+    assert arbitrated > 0
+
+
+def test_loopback_engine_oversized_split():
+    """Payloads above 1 GiB run as 256 MiB pieces."""
+    n = (1 << 30) + (64 << 20)
+    spec = {"rails": KINDS3, "rails_toml": TOML_LOOP, "sync_overhead_us": 0.0, "cases": [{"dtype": "f32", "nbytes": n}]}
+    res = _engine(2, spec)
+    r = res[0]["results"][0]
+    assert max(s[1] + s[2] for s in r["segs"]) == n
+    assert len({(s[1] // (256 << 20)) for s in r["segs"]}) == 5

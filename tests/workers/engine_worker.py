@@ -1,15 +1,25 @@
-"""One rank of a multi-GPU engine run (spawned by tests/mp_util.spawn).
+"""One rank of an engine run: a process per GPU (tests/mp_util.spawn, argv[1]
+= JSON spec, prints one JSON line) or a thread per virtual rank on one GPU
+(``run`` through paper_2405_17870_b200.run_ranks).
 
-argv[1] = JSON {"rails": [...kinds], "cases": [...]} where each case is
-{"dtype", "nbytes", "reps", "fail": [rail, chunk] | null, "host": bool}.
+spec = {"rails": [...kinds], "cases": [...]} where each case is
+{"dtype", "nbytes", "reps", "fail": [rail, chunk] | null, "fail_rank": r,
+ "fail_rep": i, "host": bool, "device": bool, "graph": n, "readmit": bool}.
 Every op's output is compared with the CPU oracle evaluated on the plan the
 engine reports it ran (nz_engine_last_plan_json): bit-exact on CE/SM
 segments and int32, NVLS fp32 within 1e-6 of sum|x|, NVLS bf16 within 1 ulp.
-A failure case also checks the rerouted result and reports the failover times.
+
+A failure case kills ONE rank's link of the rail (``fail_rank``, default the
+last rank) at the chunk, unplanned (nz_engine_inject_failure on that rank
+only): every rank's monitor must detect it, agree on the orphan and reroute
+it, so the result is still the oracle's — the orphan reduced by the target
+rail with the failed segment's geometry (P9/P10) — and the report carries
+the failover times.
 """
 import json
 import os
 import sys
+import threading
 
 import numpy as np
 
@@ -18,22 +28,54 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402  (checker only)
 from paper_2405_17870_b200 import Comm, Engine, SymmetricBuffer  # noqa: E402
-from paper_2405_17870_b200._lib import DTYPES, RAIL_KINDS  # noqa: E402
+from paper_2405_17870_b200._lib import DTYPES  # noqa: E402
 
 ES = {oracle.F32: 4, oracle.BF16: 2, oracle.I32: 4}
+_cache: dict = {}
+_cache_lock = threading.Lock()
+
+
+def clear_cache() -> None:
+    with _cache_lock:
+        _cache.clear()
+
+
+def cached(key, fn):
+    with _cache_lock:
+        ev = _cache.get(key)
+        if ev is None:
+            ev = _cache[key] = [threading.Event(), None]
+            owner = True
+        else:
+            owner = False
+    if owner:
+        try:
+            ev[1] = fn()
+        finally:
+            ev[0].set()
+    else:
+        ev[0].wait()
+    return ev[1]
 
 
 def check_segment(kind, dt, got, inputs, off, length, chunk):
     return check_segment_range(kind, dt, got, inputs, off, length, chunk, off, off + length)
 
 
-def check_segment_range(kind, dt, got, inputs, off, length, chunk, lo, hi):
+def _want(dt, inputs, n, off, length, chunk, lo, hi, key):
+    def make():
+        want = np.zeros(n // ES[dt], dtype=oracle.NP_DTYPE[dt])
+        oracle.reduce_range(inputs, dt, off, length, chunk, lo, hi, want)
+        return want
+    return cached(("want", key, off, length, chunk, lo, hi), make) if key is not None else make()
+
+
+def check_segment_range(kind, dt, got, inputs, off, length, chunk, lo, hi, key=None):
     """Mismatches of bytes [lo, hi) of a segment with geometry (off, length, chunk)."""
     es = ES[dt]
     if hi <= lo:
         return 0
-    want = np.zeros_like(got)
-    oracle.reduce_range(inputs, dt, off, length, chunk, lo, hi, want)
+    want = _want(dt, inputs, got.size * es, off, length, chunk, lo, hi, key)
     a, b = lo // es, hi // es
     g, w = got[a:b], want[a:b]
     if kind != "nvls" or dt == oracle.I32:
@@ -49,14 +91,13 @@ def check_segment_range(kind, dt, got, inputs, off, length, chunk, lo, hi):
     return int(np.count_nonzero(ulp > 1))
 
 
-def main():
-    spec = json.loads(sys.argv[1])
-    comm = Comm.from_env(session=os.environ["NZ_SESSION"])
+def run(comm, spec) -> dict:
     rank, world = comm.rank, comm.world
     kinds = spec["rails"]
     over = {"kinds": kinds}
     for k in ("window", "eta", "demote_after", "calibrate_max_bytes", "calibrate_iters", "compute_pool", "pool_tokens",
-              "graph_safe", "tune_budgets"):
+              "graph_safe", "tune_budgets", "monitor", "detect_us", "heartbeat_us", "readmit_hold_us", "algorithm",
+              "sync_overhead_us"):
         if k in spec:
             over[k] = spec[k]
     if "rails_toml" in spec:
@@ -68,11 +109,14 @@ def main():
     for ci, c in enumerate(spec["cases"]):
         dt = DTYPES[c["dtype"]]
         n = c["nbytes"]
-        inputs = [oracle.synthetic_input(dt, r, n, seed_base=oracle.SEED_BASE + 131 * ci) for r in range(world)]
+        inputs = cached(("in", ci, dt, n, world),
+                        lambda: [oracle.synthetic_input(dt, r, n, seed_base=oracle.SEED_BASE + 131 * ci)
+                                 for r in range(world)])
         for rep in range(c.get("reps", 1)):
-            if c.get("fail") and rep == c.get("fail_rep", 0):
-                inj_seq = eng.op_seq
-                eng.inject_failure(inj_seq, c["fail"][0], c["fail"][1])
+            failing = bool(c.get("fail")) and rep == c.get("fail_rep", 0)
+            n_fo = len(eng.failovers())
+            if failing and rank == c.get("fail_rank", world - 1):
+                eng.inject_failure(eng.op_seq, c["fail"][0], c["fail"][1])
             got = np.zeros(n // ES[dt], dtype=oracle.NP_DTYPE[dt])
             if c.get("host"):
                 eng.allreduce_host(inputs[rank], got, n, dt)
@@ -111,41 +155,49 @@ def main():
                 eng.synchronize()
                 bout.read(got, n)
             plans = eng.last_plans()
-            failing = c.get("fail") and rep == c.get("fail_rep", 0)
-            fo = eng.last_failover() if failing else None
-            if fo is not None and fo["op_seq"] != inj_seq:
-                fo = None  # the failed rail carried nothing of this op (idle failure): no reroute
+            fos = eng.failovers()[n_fo:]
             bad = 0
             segs = []
             for p in plans:
                 for rail_id, off, length, chunk in p["segs"]:
                     kind = kinds[rail_id]
-                    if fo and rail_id == fo["failed_rail"] and fo["orphan_length"] and \
-                            off <= fo["orphan_offset"] < off + length:
-                        # Chunks before the failure: the failed rail's result; the
+                    fo = next((f for f in fos if f["op_seq"] == p["op"] and f["failed_rail"] == rail_id), None)
+                    if fo and fo["orphan_length"]:
+                        # Chunks before the orphan: the failed rail's result; the
                         # orphan: the target rail's result, same geometry (P10).
                         k = fo["orphan_offset"]
-                        bad += check_segment_range(kind, dt, got, inputs, off, length, chunk, off, k)
+                        bad += check_segment_range(kind, dt, got, inputs, off, length, chunk, off, k, key=ci)
                         bad += check_segment_range(kinds[fo["target_rail"]], dt, got, inputs, off, length, chunk, k,
-                                                   off + length)
+                                                   off + length, key=ci)
                     else:
-                        bad += check_segment(kind, dt, got, inputs, off, length, chunk)
+                        bad += check_segment_range(kind, dt, got, inputs, off, length, chunk, off, off + length,
+                                                   key=ci)
                     segs.append([rail_id, off, length, chunk])
             rec = {"case": ci, "rep": rep, "dtype": c["dtype"], "nbytes": n, "mismatch": bad, "segs": segs,
                    "grants": [p["grants"] for p in plans if "grants" in p]}
             if failing:
-                rec["failover"] = fo
+                rec["failover"] = fos[0] if fos else None
+                rec["failovers"] = fos
             out.append(rec)
         if c.get("readmit") and c.get("fail"):
-            eng.readmit(c["fail"][0])
+            st = eng.state()
+            if c["fail"][0] in st["monitor"]["failed"]:
+                eng.readmit(c["fail"][0])
     state = eng.state()
     eng.close()
     bin_.free()
     bout.free()
+    return {"rank": rank, "results": out, "state": {"sync": state["sync_overhead_us"], "rails": state["rails"],
+                                                     "compute_pool": state.get("compute_pool"),
+                                                     "monitor": state.get("monitor")}}
+
+
+def main():
+    spec = json.loads(sys.argv[1])
+    comm = Comm.from_env(session=os.environ["NZ_SESSION"])
+    out = run(comm, spec)
     comm.close()
-    print(json.dumps({"rank": rank, "results": out, "state": {"sync": state["sync_overhead_us"],
-                                                               "rails": state["rails"],
-                                                               "compute_pool": state.get("compute_pool")}}))
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":

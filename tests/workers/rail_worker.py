@@ -1,14 +1,27 @@
-"""One rank of a multi-GPU rail parity run (spawned by tests/mp_util.spawn).
+"""One rank of a rail parity run.
 
-argv[1] = JSON list of cases. Each case reduces one segment geometry on one
-rail and compares this rank's output buffer with the CPU oracle:
-bit-exact for the CE and SM rails (P1/P2) and for int32 on every
-rail; NVLS fp32 within 1e-6 of sum(|x|) per element, NVLS bf16 within one
-bf16 ulp of the oracle (P2). Prints one JSON line.
+Two launch forms, the same checks:
+  * a process per GPU (spawned by tests/mp_util.spawn): argv[1] = JSON cases,
+    prints one JSON line;
+  * a thread per virtual rank on one GPU (tests call ``run`` through
+    paper_2405_17870_b200.run_ranks, nz_comm_init_loopback).
+
+Each case reduces one segment geometry on one rail and compares this rank's
+output buffer with the CPU oracle: bit-exact for the CE and SM rails
+(P1/P2) and for int32 on every rail; NVLS fp32 within 1e-6 of
+sum(|x|) per element, NVLS bf16 within one bf16 ulp of the oracle (P2).
+
+A case with ``"stall": [rank, chunk]`` kills that rank's link of the rail at
+that chunk (nz_rail_inject_stall, unplanned: the other ranks are not told)
+and checks the device-side detection: every rank's launch fails, the peers'
+end-barrier waits give up within the detection budget, the chunks of the
+waves completed before the failure are exact, and after nz_rail_revive on
+every rank the same op is exact again.
 """
 import json
 import os
 import sys
+import threading
 import time
 
 import numpy as np
@@ -19,6 +32,33 @@ sys.path.insert(0, ROOT)
 import oracle  # noqa: E402  (checker only)
 from paper_2405_17870_b200 import Comm, Rail, SymmetricBuffer  # noqa: E402
 from paper_2405_17870_b200._lib import DTYPES, RAIL_KINDS  # noqa: E402
+
+# Virtual ranks share one process: inputs and oracle results are computed once.
+_cache: dict = {}
+_cache_lock = threading.Lock()
+
+
+def clear_cache() -> None:
+    with _cache_lock:
+        _cache.clear()
+
+
+def cached(key, fn):
+    with _cache_lock:
+        ev = _cache.get(key)
+        if ev is None:
+            ev = _cache[key] = [threading.Event(), None]
+            owner = True
+        else:
+            owner = False
+    if owner:
+        try:
+            ev[1] = fn()
+        finally:
+            ev[0].set()
+    else:
+        ev[0].wait()
+    return ev[1]
 
 
 def compare(kind, dtype, got, want, inputs, lo, hi, es):
@@ -42,9 +82,23 @@ def compare(kind, dtype, got, want, inputs, lo, hi, es):
             "bitexact_frac": float(np.mean(g == w)) if g.size else 1.0}
 
 
-def main():
-    cases = json.loads(sys.argv[1])
-    comm = Comm.from_env(session=os.environ["NZ_SESSION"])
+def _inputs(ci, dt, nbytes, world):
+    return cached(("in", ci, dt, nbytes, world),
+                  lambda: [oracle.synthetic_input(dt, r, nbytes, seed_base=oracle.SEED_BASE + 97 * ci)
+                           for r in range(world)])
+
+
+def _want(ci, dt, nbytes, world, seg_off, seg_len, chunk, lo, hi):
+    def make():
+        inputs = _inputs(ci, dt, nbytes, world)
+        want = np.zeros(nbytes // (2 if dt == oracle.BF16 else 4), dtype=oracle.NP_DTYPE[dt])
+        if hi > lo:
+            oracle.reduce_range(inputs, dt, seg_off, seg_len, chunk, lo, hi, want)
+        return want
+    return cached(("want", ci, dt, nbytes, world, seg_off, seg_len, chunk, lo, hi), make)
+
+
+def run(comm, cases) -> dict:
     rank, world = comm.rank, comm.world
     cap = max(c["nbytes"] for c in cases)
     bin_, bout = SymmetricBuffer(comm, cap), SymmetricBuffer(comm, cap)
@@ -61,18 +115,26 @@ def main():
         nbytes = c["nbytes"]
         check = c.get("check", True)
         if check:
-            inputs = [oracle.synthetic_input(dt, r, nbytes, seed_base=oracle.SEED_BASE + 97 * ci) for r in range(world)]
+            inputs = _inputs(ci, dt, nbytes, world)
+            mine = inputs[rank]
         else:  # timing-only case: this rank's synthetic input, no oracle comparison
-            inputs = [oracle.synthetic_input(dt, rank, nbytes, seed_base=oracle.SEED_BASE + 97 * ci)]
+            inputs = None
+            mine = oracle.synthetic_input(dt, rank, nbytes, seed_base=oracle.SEED_BASE + 97 * ci)
         bin_.zero()
         bout.zero()
-        bin_.write(inputs[rank if check else 0], nbytes)
+        bin_.write(mine, nbytes)
         seg_off, seg_len = c.get("seg_off", 0), c.get("seg_len", nbytes)
         chunk = c.get("chunk") or oracle.default_chunk_bytes(seg_len, world, c.get("chunked", True))
         nch = (seg_len + chunk - 1) // chunk
         cb, ce = c.get("chunk_begin", 0), min(c.get("chunk_end", nch), nch)
         fail = c.get("fail_chunk", -1)
+        stall = c.get("stall")
+        if stall:
+            rail.set_detect_us(c.get("detect_us", 2000))
         comm.barrier()
+        t0 = time.time()
+        if stall and stall[0] == rank:
+            rail.inject_stall(stall[1])
         if c.get("armed") and fail >= 0:  # nz_rail_inject_failure instead of the fail_chunk argument
             rail.inject_failure(fail)
             rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce)
@@ -80,29 +142,57 @@ def main():
             rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce,
                            fail_chunk=fail)
         rail.synchronize()
+        seconds = time.time() - t0
         wd = rail.watchdog()
         progress = rail.progress()
         stop = fail if 0 <= fail < ce and fail >= cb else ce
         lo, hi = seg_off + min(seg_len, cb * chunk), seg_off + min(seg_len, stop * chunk)
         res = {"case": ci, "kind": kind, "dtype": c["dtype"], "nbytes": nbytes, "lo": lo, "hi": hi, "watchdog": wd,
-               "progress": progress, "stop": min(stop, nch)}
+               "progress": progress, "stop": min(stop, nch), "seconds": round(seconds, 4)}
+        if stall:
+            st = rail.status()
+            res["status"] = {k: int(v) for k, v in st.items()}
+            res["failed"] = st["ok_tag"] != st["start_tag"]  # the call's launches did not all succeed
+            res["stalled_here"] = st["fail_tag"] == st["start_tag"] and st["t_fail_ns"] > 0
+            res["detected_here"] = st["det_tag"] == st["start_tag"] and st["t_det_ns"] > 0
+            # Chunks of the waves that completed everywhere before the death.
+            hi = seg_off + min(seg_len, progress * chunk)
+            res["hi"] = hi
         if check:
             got = np.zeros(nbytes // es, dtype=oracle.NP_DTYPE[dt])
             bout.read(got, nbytes)
-            want = np.zeros_like(got)
-            if hi > lo:
-                oracle.reduce_range(inputs, dt, seg_off, seg_len, chunk, lo, hi, want)
+            want = _want(ci, dt, nbytes, world, seg_off, seg_len, chunk, lo, hi)
             res.update(compare(kind, dt, got, want, inputs, lo, hi, es))
-            outside = np.concatenate([got[: lo // es], got[hi // es:]])
-            res["outside_nonzero"] = int(np.count_nonzero(outside))
+            if not stall:
+                outside = np.concatenate([got[: lo // es], got[hi // es:]])
+                res["outside_nonzero"] = int(np.count_nonzero(outside))
+            else:
+                res["outside_nonzero"] = 0
         rec = rail.poll_fault()
         res["fault"] = None if rec is None else {"op_seq": rec.op_seq, "chunk": rec.chunk}
+        if stall:
+            # Every rank revives the rail; the same op is then exact again.
+            comm.barrier()
+            rail.revive()
+            rail.set_detect_us(0)
+            comm.barrier()
+            bout.zero()
+            comm.barrier()
+            rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce)
+            rail.synchronize()
+            got = np.zeros(nbytes // es, dtype=oracle.NP_DTYPE[dt])
+            bout.read(got, nbytes)
+            lo2, hi2 = seg_off + min(seg_len, cb * chunk), seg_off + min(seg_len, ce * chunk)
+            want = _want(ci, dt, nbytes, world, seg_off, seg_len, chunk, lo2, hi2)
+            res["after_revive_mismatch"] = compare(kind, dt, got, want, inputs, lo2, hi2, es)["mismatch"]
+            res["after_revive_watchdog"] = rail.watchdog()
         if c.get("graph") and check:
             # Graph-safe rail: capture `graph` ops (the eager op above was the
             # warm-up), replay three times, then one more eager op; every
             # result must equal the oracle.
             import torch
             torch.cuda.set_device(comm.device)
+            want = _want(ci, dt, nbytes, world, seg_off, seg_len, chunk, lo, hi)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=torch.cuda.Stream()):
                 for _ in range(c["graph"]):
@@ -152,15 +242,21 @@ def main():
             except NezhaError:
                 res["abort_refused"] = True
             rails[key] = Rail(comm, RAIL_KINDS[kind], len(rails) + 10, c.get("sm_budget", 0))
-            r_old = rail
-            r_old.close()
+            rail.close()
         results.append(res)
     for r in rails.values():
         r.close()
     bin_.free()
     bout.free()
+    return {"rank": rank, "results": results}
+
+
+def main():
+    cases = json.loads(sys.argv[1])
+    comm = Comm.from_env(session=os.environ["NZ_SESSION"])
+    out = run(comm, cases)
     comm.close()
-    print(json.dumps({"rank": rank, "results": results}))
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":
