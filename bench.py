@@ -5,17 +5,29 @@
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
 
 Metric (BASELINE.json): 8-GPU allreduce busbw GB/s vs size (4KB-1GB); 8KB p50
-latency; failover ms. A "step" is one engine allreduce of the headline payload
-(1 GiB fp32, synthetic) on the configured rails (default: the configs[2]
-rail set NVLS + copy-engine + SM under the cold/hot state machine, swept
-4 KiB-1 GiB as configs[1] specifies; `--rails nvls,ce` is configs[1] itself). `value` = busbw = ringVolume(N, S) / t with
-t the max over ranks of the device time per step (N = 1: algbw S / t, no
-NVLink exchange exists). Inputs are 1 GiB, larger than the 126 MB L2, so no
-flush is needed between steps. Rank 0 prints one JSON line.
+latency; failover ms. busbw = ringVolume(N, S) / t (Eq. 1,
+proj/src/core/math.cpp:7-16), t the max over ranks of the device time per
+step.
+
+The headline workload is BASELINE config 1 — 2 rails with identical profiles
+(so a static 50/50 split: [0, 32 MiB) and [32 MiB, 64 MiB)), Ring, 64 MiB fp32
+per rank — run through the product's public engine API (nz_engine_allreduce),
+one "step" = one allreduce of the whole job:
+  * N = 1 (no torchrun): the config's 8 ranks as 8 virtual ranks on the one
+    B200 (nz_comm_init_loopback, one host thread per rank; the SM and CE
+    rails' own kernels and DMA, each cross-rank kernel one co-resident grid
+    over the ranks). All inter-rank traffic is HBM traffic, so the roofline
+    is HBM (MEASURED_PEAKS.json hbm_gbs).
+  * N > 1: N real GPUs, rails NVLS + copy-engine (configs[1]'s set; SM + CE
+    without multicast); roofline NVLink 900 GB/s per direction,
+    plus the 4 KiB-1 GiB state-machine sweep, NCCL, 8 KiB latency, failover,
+    config 3 and config 5 as secondary fields.
+Inputs (8 x 64 MiB per buffer) exceed the 126 MB L2, so no flush is needed.
 
 Reference arm (--impl reference): the CPU baseline — the SPEC ring restated on
 the reference's own InMemoryFabric (oracle/_ref, compiled from
-/root/reference/proj/src), ranks as threads, timed on this host's cores.
+/root/reference/proj/src), the same config (8 simulated ranks at N = 1, else N),
+ranks as threads, timed on this host's cores; rank 0 only.
 """
 from __future__ import annotations
 
@@ -32,8 +44,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "8-GPU allreduce busbw GB/s vs size (4KB–1GB); 8KB p50 latency; failover ms"
-NVLINK_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
+NVLINK_GBS = 900.0       # NVLink 5 per direction per GPU (BASELINE.md "Roofline definitions")
+NVLINK_COPY_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md), secondary
 GiB = 1 << 30
+CFG1_BYTES = 64 << 20
+CFG1_RANKS = 8
+ALGO_RING, ALGO_RING_CHUNKED = 0, 1
 
 
 def ring_volume(n: int, s: int) -> int:
@@ -63,13 +79,22 @@ def ncu_traffic(kernel: str, per_launch_bytes: int):
     return t["dram_bytes"] if t.get("per_launch_bytes") == per_launch_bytes else None
 
 
-def wire_bytes(kind: str, world: int, seg: int) -> int:
-    """Bytes one GPU must send over NVLink per op of `seg` bytes on a rail (per
-    direction): ring-equivalent rails 2(N-1)/N*S (Eq. 1); NVLS (N+1)/N*S — the
-    switch reads every rank's copy once and multicasts the reduced shards."""
-    if kind == "nvls":
-        return (world + 1) * seg // world
-    return ring_volume(world, seg)
+def identical_rails_toml(kinds) -> str:
+    """Rails config with identical profiles: Eq. 8 gives alpha = 1/R, so the
+    split is static (config 1's 50/50 with two rails)."""
+    return "".join(f'[[rail]]\nprotocol = "{k}"\nt_setup_us = 20.0\nbandwidth_bps = 5.0e11\n' for k in kinds)
+
+
+def cfg1_hbm_bytes(world: int, seg: int, kind: str) -> int:
+    """Algorithmic HBM bytes of one rail op over a segment of `seg` bytes when
+    all `world` ranks live on one GPU (loopback): SM two-shot —
+    every rank reads its shard from every rank and writes the sum to every
+    rank: 2 * world * seg; copy engine — per rank the gather reads and writes
+    (N-1)/N seg, the reduce reads seg and writes seg/N, the scatter reads and
+    writes (N-1)/N seg: world * seg * (5N - 3) / N."""
+    if kind == "sm":
+        return 2 * world * seg
+    return world * seg * (5 * world - 3) // world
 
 
 # --------------------------------------------------------------------- clocks
@@ -130,7 +155,8 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline ---
-def cpu_baseline(world_sim: int = 8, nbytes: int = 64 << 20, budget_s: float = 20.0):
+def cpu_baseline(world_sim: int = CFG1_RANKS, nbytes: int = CFG1_BYTES, budget_s: float = 20.0, min_ops: int = 3,
+                 max_ops: int = 20):
     """Config 1 of BASELINE.json on the host: world_sim simulated ranks (threads)
     on the reference InMemoryFabric, 2 identical rails, static 50/50 split, Ring,
     64 KiB frames, fp32. Returns the busbw GB/s and the sample description."""
@@ -147,71 +173,236 @@ def cpu_baseline(world_sim: int = 8, nbytes: int = 64 << 20, budget_s: float = 2
     oracle.inmem_allreduce(inputs, oracle.F32, segs, 2, chunked=False, outputs=outs)  # warm-up
     times = []
     t_end = time.perf_counter() + budget_s
-    while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 20):
+    while len(times) < min_ops or (time.perf_counter() < t_end and len(times) < max_ops):
         _, us, _ = oracle.inmem_allreduce(inputs, oracle.F32, segs, 2, chunked=False, outputs=outs)
         times.append(us * 1e-6)
     t = statistics.mean(times)
     threads = world_sim * 2
     return {"value": round(ring_volume(world_sim, nbytes) / t / 1e9, 4), "unit": "GB/s", "cores": threads,
-            "host_cpus": len(os.sched_getaffinity(0)), "kind": "port",
-            "sample": f"config 1: {world_sim} simulated ranks x 2 rails (threads), fp32 {nbytes >> 20} MiB, static "
-                      f"50/50, Ring, 64 KiB frames, {len(times)} timed ops (mean {t * 1e3:.1f} ms/op); SPEC ring "
-                      f"restated on the reference InMemoryFabric compiled from /root/reference/proj/src"}
+            "host_cpus": len(os.sched_getaffinity(0)), "kind": "port", "ms_per_op": round(t * 1e3, 3),
+            "ops": len(times),
+            "sample": f"config 1: {world_sim} simulated ranks x 2 rails (one thread per rank and rail), fp32 "
+                      f"{nbytes >> 20} MiB per rank, static 50/50, Ring, 64 KiB frames, {len(times)} timed ops "
+                      f"(mean {t * 1e3:.1f} ms/op); SPEC ring restated on the reference InMemoryFabric compiled "
+                      f"from /root/reference/proj/src"}
 
 
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    world_sim = max(2, world)
-    nbytes = 64 << 20
-    res = cpu_baseline(world_sim, nbytes, budget_s=max(5.0, 3.0 * args.steps))
+    world_sim = CFG1_RANKS if world == 1 else world  # the same ranks as our arm's headline
+    nbytes = CFG1_BYTES
+    res = cpu_baseline(world_sim, nbytes, budget_s=600.0, min_ops=max(1, args.steps), max_ops=max(1, args.steps))
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
         return 0
     v = res["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ring_volume(world_sim, nbytes) / (v * 1e9) * 1e3, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"CPU allreduce, {world_sim} simulated ranks, 2 rails 50/50, 64 MiB fp32 sample",
-                       "bytes_per_rank": nbytes, "ranks": f"{world_sim} simulated (threads)"},
+            "warmup": args.warmup, "ms_per_step": res["ms_per_op"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config 1: {world_sim} ranks, 2 rails with identical profiles (static 50/50), "
+                                   f"Ring, {nbytes >> 20} MiB fp32 per rank; CPU reference on host threads",
+                       "bytes_per_rank": nbytes, "ranks": world_sim, "same_config": True},
             "cpu_baseline": res,
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
 
 
-# ---------------------------------------------------------------- our arm ---
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rails", default="nvls,ce,sm",
-                    help="comma list of nvls|ce|sm (configs[1] = nvls,ce; configs[2] = nvls,ce,sm)")
-    ap.add_argument("--bytes", type=int, default=GiB)
-    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
-    ap.add_argument("--tune-ops", type=int, default=200, help="balancer convergence ops before timing")
-    ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-failover", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sweep-max", type=int, default=GiB)
-    ap.add_argument("--tune", action="store_true",
-                    help="engine measures its CTA budgets and protocol crossovers at startup (tune_budgets=1)")
-    ap.add_argument("--graph", action="store_true",
-                    help="small sizes replayed from CUDA graphs: a graph_safe engine vs NCCL (device time per op)")
-    ap.add_argument("--nccl-graph", action="store_true",
-                    help="also time NCCL at <= 1 MiB from a captured CUDA graph (no host launch overhead)")
-    ap.add_argument("--nccl-algos", action="store_true",
-                    help="also time NCCL with NCCL_ALGO=NVLS and =Ring (SURVEY.md 8d) at a few sizes")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
+# ------------------------------------------------------- N = 1: loopback ----
+def run_loopback(args):
+    """Config 1 with its 8 ranks as virtual ranks on the one B200."""
+    import torch
 
-    import numpy as np
+    from paper_2405_17870_b200 import Engine, SymmetricBuffer, run_ranks
+    from paper_2405_17870_b200._lib import BF16, F32
+    from paper_2405_17870_b200.runtime import kernel_launch_count
+
+    V, S = args.virtual_ranks, CFG1_BYTES
+    kinds = ["sm", "ce"]
+    toml = identical_rails_toml(kinds)
+    torch.cuda.set_device(0)
+    torch.cuda.init()
+    steps, warm = args.steps, max(args.warmup, 3)
+    bar = threading.Barrier(V)
+    shared = {}
+    clk = ClockSampler(0)
+    fo_bytes = 256 << 20
+
+    def body(comm):
+        torch.cuda.set_device(0)
+        r = comm.rank
+        eng = Engine(comm, kinds=kinds, rails_toml=toml, algorithm=ALGO_RING, window=1 << 30, sync_overhead_us=0.0)
+        bi, bo = SymmetricBuffer(comm, S), SymmetricBuffer(comm, S)
+        g = torch.Generator(device="cuda").manual_seed(0x4E5A0000 + r)
+        x = torch.rand(S // 4, device="cuda", generator=g) * 2 - 1
+        bi.write(x.data_ptr(), S)
+        stream = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        for i in range(len(kinds)):
+            eng.loop_timing(i, True)
+        for _ in range(warm):
+            eng.allreduce(bi, bo, S, F32, stream)
+        eng.synchronize()
+        plan = eng.last_plans()[0]["segs"]
+        # ~0.4 s of the same load so the clock sampler sees the GPU busy.
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            eng.allreduce(bi, bo, S, F32, stream)
+        e1.record(stream)
+        e1.synchronize()
+        t_est = max(max(json.loads(v_.decode()) for v_ in comm.allgather_bytes(
+            json.dumps(e0.elapsed_time(e1) / 3e3).encode().ljust(32))), 1e-5)
+        soak = min(4000, int(0.4 / t_est))  # the same count on every rank (collective)
+        comm.barrier()
+        if r == 0:
+            clk.__enter__()
+        comm.barrier()
+        for _ in range(soak):
+            eng.allreduce(bi, bo, S, F32, stream)
+        eng.synchronize()
+        for i in range(len(kinds)):
+            eng.loop_time(i)  # reset the per-launch kernel timers
+        comm.barrier()
+        if r == 0:
+            shared["launches0"] = kernel_launch_count()
+        comm.barrier()
+        e0.record(stream)
+        for _ in range(steps):
+            eng.allreduce(bi, bo, S, F32, stream)
+        e1.record(stream)
+        e1.synchronize()
+        comm.barrier()
+        if r == 0:
+            shared["launches"] = kernel_launch_count() - shared["launches0"]
+            clk.__exit__()
+        eng.synchronize()
+        t_step = e0.elapsed_time(e1) / 1e3 / steps
+        comm.barrier()  # every rank's grids are in; one reader of the shared per-grid timers
+        ktime = {kinds[i]: eng.loop_time(i) for i in range(len(kinds))} if r == 0 else None
+        comm.barrier()
+        for i in range(len(kinds)):
+            eng.loop_timing(i, False)
+
+        # e2e through the public host API: H2D of this rank's input, the
+        # multi-rail allreduce, D2H of the result, every step.
+        hin = torch.empty(S, dtype=torch.uint8).pin_memory()
+        hout = torch.empty(S, dtype=torch.uint8).pin_memory()
+        hin.copy_(x.view(torch.uint8).cpu())
+        for _ in range(2):
+            eng.allreduce_host(hin, hout, S, F32)
+        ke = max(3, min(steps, 10))
+        comm.barrier()
+        bar.wait()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            eng.allreduce_host(hin, hout, S, F32)
+        bar.wait()
+        te = (time.perf_counter() - t0) / ke
+        eng.close()
+        bi.free()
+        bo.free()
+
+        # Config 4 shape (bf16 256 MiB, RingChunked): the larger rail's link
+        # dies on the last rank mid-op, unplanned; every rank detects it,
+        # agrees on the orphan and reroutes it to the other rail.
+        fo = None
+        if not args.no_failover:
+            eng2 = Engine(comm, kinds=kinds, rails_toml=toml, algorithm=ALGO_RING_CHUNKED, window=1 << 30,
+                          sync_overhead_us=0.0)
+            b2i, b2o = SymmetricBuffer(comm, fo_bytes), SymmetricBuffer(comm, fo_bytes)
+            xb = (torch.rand(fo_bytes // 2, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+            b2i.write(xb.data_ptr(), fo_bytes)
+            torch.cuda.synchronize()
+            eng2.allreduce(b2i, b2o, fo_bytes, BF16, stream)
+            eng2.synchronize()
+            segs = eng2.last_plans()[0]["segs"]
+            victim = max(segs, key=lambda s_: s_[2])
+            nch = -(-victim[2] // victim[3])
+            if r == V - 1:
+                eng2.inject_failure(eng2.op_seq, victim[0], nch // 2)
+            comm.barrier()
+            eng2.allreduce(b2i, b2o, fo_bytes, BF16, stream)
+            eng2.synchronize()
+            fos = eng2.failovers()
+            fo = fos[-1] if fos else None
+            eng2.close()
+            b2i.free()
+            b2o.free()
+        return {"t_step": t_step, "ktime": ktime, "te": te, "plan": plan, "fo": fo}
+
+    res = run_ranks(V, body, timeout=1800)
+    t_step = max(r_["t_step"] for r_ in res)
+    busbw = ring_volume(V, S) / t_step / 1e9
+    algbw = S / t_step / 1e9
+    plan = res[0]["plan"]
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6538.3)
+    # Dominant kernel: the SM rail's two-shot fold grid over the 8 virtual
+    # ranks (fold_kernel_vr<F32,8,8>), timed by CUDA events on the stream it
+    # runs on, every launch of the timed region.
+    seg = {kinds[s_[0]]: s_[2] for s_ in plan}
+    kt = res[0]["ktime"]["sm"]
+    roofline = None
+    if kt["launches"]:
+        t_launch = kt["total_us"] / kt["launches"] * 1e-6
+        per_launch = cfg1_hbm_bytes(V, seg.get("sm", 0), "sm")
+        ach = per_launch / t_launch / 1e9
+        roofline = {"bound": "hbm", "kernel": "fold_kernel_vr<F32,8,8> (SM rail two-shot, 8 virtual ranks)",
+                    "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                    "traffic": ncu_traffic("fold_kernel_vr", per_launch), "per_launch_bytes": per_launch,
+                    "launches": kt["launches"], "us_per_launch": round(t_launch * 1e6, 2),
+                    "note": "achieved = algorithmic HBM bytes of one launch (every virtual rank reads its shard of the "
+                            "32 MiB segment from all 8 ranks and writes the sum to all 8: 2*8*32 MiB) / the kernel's "
+                            "mean duration (CUDA events around each launch on its stream, timed region); peak = "
+                            "MEASURED_PEAKS.json hbm_gbs" + ("" if "hbm_gbs" in peaks else " (fallback)")}
+    kce = res[0]["ktime"]["ce"]
+    te = max(r_["te"] for r_ in res)
+    clocks = clk.summary()
+    out = {"metric": METRIC, "value": round(busbw, 2), "unit": "GB/s", "n_gpus": 1, "steps": steps,
+           "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": f"config 1: {V} ranks as virtual ranks on one B200 (nz_comm_init_loopback), rails "
+                                  f"sm + ce with identical profiles (static 50/50), Ring, {S >> 20} MiB fp32 per rank, "
+                                  f"engine allreduce; value = busbw = ringVolume({V}, S) / t",
+                      "bytes_per_rank": S, "ranks": V, "virtual_ranks": True, "same_config": True,
+                      "l2": f"{V} x {S >> 20} MiB per buffer > 126 MB L2; no flush", "plan": plan,
+                      "algbw_GBs": round(algbw, 2),
+                      "parity": "bit-exact vs the reference ring golden hash: tests/test_gpu_loopback.py::"
+                                "test_loopback_config1_hash (same engine call, oracle inputs)"},
+           "roofline": roofline, "gpu_launches": res and shared.get("launches"), "clocks": clocks,
+           "e2e": {"value": round(ring_volume(V, S) / te / 1e9, 3), "unit": "GB/s",
+                   "h2d_bytes_per_step": V * S, "d2h_bytes_per_step": V * S, "ms_per_step": round(te * 1e3, 3),
+                   "note": "nz_engine_allreduce_host on every virtual rank from pinned host memory (H2D, allreduce, "
+                           "D2H each step), wall clock between thread barriers"},
+           "kernels": {k: {"launches": v["launches"], "us_per_launch": round(v["total_us"] / max(1, v["launches"]), 2)}
+                       for k, v in res[0]["ktime"].items()}}
+    if kce["launches"]:
+        t_ce = kce["total_us"] / kce["launches"] * 1e-6
+        out["kernels"]["ce"]["note"] = "copy-engine rail barrier grids (its DMA and reduce run on rank streams)"
+        del t_ce
+    fos = [r_["fo"] for r_ in res if r_["fo"]]
+    if fos:
+        out["failover"] = {"payload": "bf16 256 MiB, RingChunked, larger rail's link dies on the last rank at its "
+                                      "middle chunk (unplanned)",
+                           "failed_rail": kinds[fos[0]["failed_rail"]], "target_rail": kinds[fos[0]["target_rail"]],
+                           "orphan_bytes": fos[0]["orphan_length"], "orphan_chunk": fos[0]["orphan_chunk"],
+                           "detect_us_max": round(max(f["detect_us"] for f in fos), 2),
+                           "resume_after_detect_us_max": round(max(f["resume_after_detect_us"] for f in fos), 2),
+                           "done_us_max": round(max(f["done_us"] for f in fos), 2)}
+        out["failover_ms"] = round(max(f["done_us"] for f in fos) / 1e3, 4)
+    if not args.no_cpu:
+        cb = cpu_baseline(V, S)
+        if cb:
+            out["cpu_baseline"] = cb
+    print(json.dumps(out))
+    return 0
+
+
+# ------------------------------------------------------ N > 1: real GPUs ----
+def run_multi(args):
     import torch
 
     from paper_2405_17870_b200 import Comm, Engine, Rail, SymmetricBuffer
@@ -222,29 +413,102 @@ def main():
     torch.cuda.set_device(local)
     session = f"bench-{os.environ.get('MASTER_PORT', '0')}-{os.environ.get('TORCHELASTIC_RUN_ID', str(os.getppid()))}"
     comm = Comm(rank, world, local, session)
-    kinds = args.rails.split(",")
-    if world > 1 and not comm.multicast and "nvls" in kinds:  # no NVSwitch multicast on this box
-        kinds = [k for k in kinds if k != "nvls"] or ["sm"]
     dt = DTYPES[args.dtype]
-    S = args.bytes
-    eng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=min(GiB, max(S, 1 << 20)),
-                 tune_budgets=1 if args.tune else 0)
+    S = CFG1_BYTES
 
     def max_over_ranks(x: float) -> float:
         vals = comm.allgather_bytes(json.dumps(x).encode().ljust(32))
         return max(json.loads(v.decode().strip()) for v in vals)
 
-    cap = max(S, args.sweep_max if not args.no_sweep else 0, 8192)
+    # Headline: config 1's shape at N ranks (static 50/50, Ring, 64 MiB fp32).
+    kinds1 = ["nvls", "ce"] if comm.multicast else ["sm", "ce"]
+    eng1 = Engine(comm, kinds=kinds1, rails_toml=identical_rails_toml(kinds1), algorithm=ALGO_RING,
+                  window=1 << 30, sync_overhead_us=0.0)
+    cap = max(S, args.sweep_max if not args.no_sweep else 0, 8192, 256 << 20)
     bin_, bout = SymmetricBuffer(comm, cap), SymmetricBuffer(comm, cap)
     g = torch.Generator(device="cuda").manual_seed(0x4E5A0000 + rank)
-    tdt = {0: torch.float32, 1: torch.bfloat16, 2: torch.int32}[dt]
-    if dt == 2:
-        x = torch.randint(-(1 << 20), 1 << 20, (cap // 4,), device="cuda", generator=g, dtype=torch.int32)
-    else:
-        x = (torch.rand(cap // x_es(dt), device="cuda", generator=g) * 2 - 1).to(tdt)
+    x = torch.rand(cap // 4, device="cuda", generator=g) * 2 - 1
     bin_.write(x.data_ptr(), cap)
     stream = torch.cuda.Stream()
     torch.cuda.synchronize()
+    for _ in range(max(args.warmup, 3)):
+        eng1.allreduce(bin_, bout, S, 0, stream)
+    eng1.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(3):
+        eng1.allreduce(bin_, bout, S, 0, stream)
+    e1.record(stream)
+    e1.synchronize()
+    soak = max(1, min(4000, int(0.4 / max(1e-6, e0.elapsed_time(e1) / 3e3))))
+    comm.barrier()
+    with ClockSampler(local) as clk:
+        for _ in range(soak):  # same count on every rank (collective)
+            eng1.allreduce(bin_, bout, S, 0, stream)
+        eng1.synchronize()
+        eng1.stats_reset()
+        comm.barrier()
+        torch.cuda.synchronize()
+        launches0 = kernel_launch_count()
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng1.allreduce(bin_, bout, S, 0, stream)
+        e1.record(stream)
+        e1.synchronize()
+    launches = kernel_launch_count() - launches0
+    eng1.synchronize()
+    t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.steps)
+    busbw = ring_volume(world, S) / t_step / 1e9
+    plan1 = eng1.last_plans()[0]["segs"]
+    # Dominant rail: largest segment; its per-op time on its own stream (Timer).
+    dom = max(plan1, key=lambda s_: s_[2])
+    st = eng1.rail_stats(dom[0])
+    roofline = None
+    if st["ops"]:
+        t_rail = max_over_ranks(st["total_us"] / st["ops"] * 1e-6)
+        rv = ring_volume(world, dom[2])
+        ach = rv / t_rail / 1e9
+        wire = (world + 1) * dom[2] // world if kinds1[dom[0]] == "nvls" else rv
+        roofline = {"bound": "nvlink", "kernel": f"{kinds1[dom[0]]} rail", "achieved": round(ach, 1),
+                    "peak": NVLINK_GBS, "unit": "GB/s", "frac": round(ach / NVLINK_GBS, 4), "traffic": None,
+                    "per_launch_bytes": rv, "op_busbw_frac": round(busbw / NVLINK_GBS, 4),
+                    "wire": {"bytes_per_op": wire, "GBs": round(wire / t_rail / 1e9, 1), "peak": NVLINK_COPY_GBS,
+                             "frac": round(wire / t_rail / 1e9 / NVLINK_COPY_GBS, 4)},
+                    "note": "achieved = ringVolume(N, segment) / the rail's time per op (CUDA events on the rail "
+                            "stream), peak = NVLink 900 GB/s per direction (BASELINE.md); wire = bytes one GPU "
+                            "actually sends (NVLS (N+1)/N*S) against the 770 GB/s measured peer copy"}
+    out = {"metric": METRIC, "value": round(busbw, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": f"config 1 shape at {world} GPUs: rails {'+'.join(kinds1)} with identical "
+                                  f"profiles (static 50/50), Ring, {S >> 20} MiB fp32 per rank; value = busbw",
+                      "bytes_per_rank": S, "ranks": world, "same_config": True, "plan": plan1,
+                      "l2": "inputs 64 MiB per rank x 2 buffers; each step rewrites the output (no flush)",
+                      "algbw_GBs": round(S / t_step / 1e9, 2)},
+           "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary()}
+
+    # e2e through the public host API (H2D + allreduce + D2H every step).
+    if not args.no_e2e:
+        hin = torch.empty(S, dtype=torch.uint8).pin_memory()
+        hout = torch.empty(S, dtype=torch.uint8).pin_memory()
+        hin.copy_(x.view(torch.uint8)[:S].cpu())
+        for _ in range(2):
+            eng1.allreduce_host(hin, hout, S, 0)
+        k = max(3, min(args.steps, 10))
+        comm.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k):
+            eng1.allreduce_host(hin, hout, S, 0)
+        te = max_over_ranks((time.perf_counter() - t0) / k)
+        out["e2e"] = {"value": round(ring_volume(world, S) / te / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": S,
+                      "d2h_bytes_per_step": S, "ms_per_step": round(te * 1e3, 3),
+                      "note": "nz_engine_allreduce_host from pinned host memory, wall clock, max over ranks"}
+    eng1.close()
+
+    # Secondary: the state-machine engine over every rail, calibrated at startup.
+    kinds = [k for k in args.rails.split(",") if k != "nvls" or comm.multicast] or ["sm"]
+    eng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=min(GiB, cap),
+                 tune_budgets=1 if args.tune else 0)
 
     def timed(nbytes, iters, warm):
         for _ in range(warm):
@@ -252,100 +516,21 @@ def main():
         eng.synchronize()
         comm.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
         for _ in range(iters):
             eng.allreduce(bin_, bout, nbytes, dt, stream)
-        e1.record(stream)
-        e1.synchronize()
+        b.record(stream)
+        b.synchronize()
         eng.synchronize()
-        t = e0.elapsed_time(e1) / 1e3 / iters
-        return max_over_ranks(t)
+        return max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
 
-    # Balancer convergence on the headline size (one-time, like NCCL tuning).
     for _ in range(args.tune_ops):
-        eng.allreduce(bin_, bout, S, dt, stream)
+        eng.allreduce(bin_, bout, min(GiB, cap), dt, stream)
     eng.synchronize()
 
-    # ---- headline: K timed steps of S bytes --------------------------------
-    for _ in range(max(args.warmup, 3)):
-        eng.allreduce(bin_, bout, S, dt, stream)
-    eng.synchronize()
-    t_est = timed(S, 3, warm=0)
-    soak_ops = max(1, min(2000, int(0.4 / max(t_est, 1e-6))))
-    eng.stats_reset()
-    comm.barrier()
-    torch.cuda.synchronize()
-    launches0 = kernel_launch_count()
-    with ClockSampler(local) as clk:
-        # Keep the GPU under the same load for ~0.4 s so the sampler sees it
-        # running, then time exactly K steps back to back.
-        for _ in range(soak_ops):  # same count on every rank (collective)
-            eng.allreduce(bin_, bout, S, dt, stream)
-        eng.synchronize()
-        comm.barrier()
-        eng.stats_reset()
-        launches0 = kernel_launch_count()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            eng.allreduce(bin_, bout, S, dt, stream)
-        e1.record(stream)
-        e1.synchronize()
-    launches = kernel_launch_count() - launches0
-    eng.synchronize()
-    t_step = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.steps)
-    busbw = ring_volume(world, S) / t_step / 1e9
-    algbw = S / t_step / 1e9
-    value = busbw if world > 1 else algbw
-    plan = eng.last_plans()[0] if eng.last_plans() else {}
-    # Dominant rail (largest share): its per-op time on its own stream.
-    peaks = measured_peaks()
-    stats = {k: eng.rail_stats(i) for i, k in enumerate(kinds)}
-    dom = max(range(len(kinds)), key=lambda i: stats[kinds[i]]["bytes"])
-    st = stats[kinds[dom]]
-    roofline = None
-    if st["ops"] == 0 and plan.get("segs"):
-        # Cold plan: one rail carried the whole step on the caller's stream.
-        dom = plan["segs"][0][0]
-        st = {"ops": args.steps, "total_us": t_step * 1e6 * args.steps, "bytes": S * args.steps}
-    if st["ops"]:
-        t_rail = max_over_ranks(st["total_us"] / st["ops"] * 1e-6)
-        seg = st["bytes"] / st["ops"]
-        if world > 1:
-            wb = wire_bytes(kinds[dom], world, int(seg))
-            ach = wb / t_rail / 1e9
-            roofline = {"bound": "nvlink", "kernel": f"{kinds[dom]} rail", "achieved": round(ach, 1),
-                        "peak": NVLINK_GBS, "unit": "GB/s", "frac": round(ach / NVLINK_GBS, 4), "traffic": None,
-                        "per_launch_bytes": wb,
-                        "note": "achieved = NVLink bytes one GPU must send per op (ring rails 2(N-1)/N*S, NVLS "
-                                "(N+1)/N*S) / rail time per op (CUDA events on the rail stream); peak = measured "
-                                "peer copy 770 GB/s per direction (B200_PROFILING.md; 900 nominal). traffic: ncu "
-                                "cannot replay kernels with cross-GPU barriers (profiles/README.md)"}
-        else:
-            hbm = peaks.get("hbm_gbs", 6650.0)
-            ach = 2 * seg / t_rail / 1e9
-            roofline = {"bound": "hbm", "kernel": f"{kinds[dom]} rail (N=1 copy)", "achieved": round(ach, 1),
-                        "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                        "traffic": ncu_traffic("copy_kernel", int(2 * seg)),
-                        "per_launch_bytes": int(2 * seg),
-                        "note": "N=1: the allreduce is a copy in->out, 2S HBM bytes; peak = MEASURED_PEAKS.json "
-                                "hbm_gbs" + ("" if "hbm_gbs" in peaks else " (fallback)")}
-
-    out = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-           "config": {"workload": f"multi-rail ({'+'.join(kinds)}) state-machine {args.dtype} allreduce of "
-                                  f"{S} B per rank (value = busbw at this size; N=1: algbw)",
-                      "bytes_per_rank": S, "ranks": world,
-                      "l2": "inputs (1 GiB) larger than the 126 MB L2; no flush",
-                      "algbw_GBs": round(algbw, 2), "busbw_GBs": round(busbw, 2), "plan": plan},
-           "roofline": roofline, "gpu_launches": launches, "clocks": clk.summary()}
-
-    # ---- NCCL on the same sizes --------------------------------------------
-    nccl = {}
     pg = None
-    if world > 1 and not args.no_nccl:
+    if not args.no_nccl:
         import torch.distributed as dist
         saved = os.dup(1)
         os.dup2(2, 1)  # NCCL prints its banner on stdout; keep stdout for the one JSON line
@@ -362,204 +547,96 @@ def main():
             os.dup2(saved, 1)
             os.close(saved)
 
-    def nccl_time(nbytes, iters, group=None):
+    def nccl_time(nbytes, iters):
         t = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
         for _ in range(5):
-            pg.all_reduce(t, group=group)
+            pg.all_reduce(t)
         torch.cuda.synchronize()
         pg.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(iters):
-            pg.all_reduce(t, group=group)
+            pg.all_reduce(t)
         b.record()
         b.synchronize()
         return max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
 
-    def nccl_graph_time(nbytes, per_graph=50, replays=10):
-        """NCCL device time per op: `per_graph` allreduces captured in one CUDA
-        graph, replayed; excludes the Python / launch overhead of nccl_time."""
-        t = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            for _ in range(3):
-                pg.all_reduce(t)
-        torch.cuda.current_stream().wait_stream(side)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for _ in range(per_graph):
-                pg.all_reduce(t)
-        g.replay()
-        torch.cuda.synchronize()
-        pg.barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(replays):
-            g.replay()
-        b.record()
-        b.synchronize()
-        return max_over_ranks(a.elapsed_time(b) / 1e3 / (replays * per_graph))
-
     if pg is not None:
-        tn = nccl_time(S, max(5, args.steps // 2))
-        nccl["busbw_headline"] = round(ring_volume(world, S) / tn / 1e9, 2)
-        out["nccl_busbw_GBs"] = nccl["busbw_headline"]
-        if args.nccl_algos:
-            # NCCL reads NCCL_ALGO when a communicator is created: one group per algorithm.
-            algos = {}
-            for algo in ("NVLS", "Ring"):
-                old = os.environ.get("NCCL_ALGO")
-                os.environ["NCCL_ALGO"] = algo
-                try:
-                    g = pg.new_group(backend="nccl")
-                    algos[algo] = {str(sz): round(ring_volume(world, sz) / nccl_time(sz, 20 if sz > (64 << 20) else 100,
-                                                                                       g) / 1e9, 2)
-                                   for sz in (8192, 1 << 20, 64 << 20, S)}
-                except Exception as e:  # pragma: no cover
-                    algos[algo] = {"error": str(e)[:160]}
-                finally:
-                    if old is None:
-                        os.environ.pop("NCCL_ALGO", None)
-                    else:
-                        os.environ["NCCL_ALGO"] = old
-            out["nccl_algos_busbw_GBs"] = algos
+        out["nccl_busbw_GBs"] = round(ring_volume(world, S) / nccl_time(S, 20) / 1e9, 2)
 
-    # ---- sweep 4 KiB .. 1 GiB ----------------------------------------------
     if not args.no_sweep:
         sweep = []
         s = 4096
         while s <= min(args.sweep_max, cap):
             it = 200 if s <= (1 << 20) else (40 if s <= (64 << 20) else 8)
             t = timed(s, it, warm=20 if s <= (64 << 20) else 12)
-            row = {"bytes": s, "us": round(t * 1e6, 2), "algbw_GBs": round(s / t / 1e9, 2),
-                   "busbw_GBs": round(ring_volume(world, s) / t / 1e9, 2),
+            row = {"bytes": s, "us": round(t * 1e6, 2), "busbw_GBs": round(ring_volume(world, s) / t / 1e9, 2),
                    "hot": bool(eng.last_plans()[0]["hot"]) if eng.last_plans() else None,
                    "rails": sorted({seg[0] for p in eng.last_plans() for seg in p["segs"]})}
             if pg is not None:
                 tn = nccl_time(s, it)
                 row["nccl_busbw_GBs"] = round(ring_volume(world, s) / tn / 1e9, 2)
                 row["nccl_us"] = round(tn * 1e6, 2)
-                if args.nccl_graph and s <= (1 << 20):
-                    try:
-                        row["nccl_graph_us"] = round(nccl_graph_time(s) * 1e6, 2)
-                    except Exception as e:  # pragma: no cover
-                        row["nccl_graph_error"] = str(e)[:120]
             sweep.append(row)
             s *= 2
         out["sweep"] = sweep
 
-    # ---- 8 KiB p50 latency: engine (cold start) vs each rail alone vs NCCL --
-    def p50_host(fn, n=1000):
-        """Per op: every rank issues at one agreed CLOCK_MONOTONIC instant (the
-        clock is system-wide, so one box shares it) and stops when its result
-        is on the host's side of a synchronize; the op's latency is the max over
-        ranks of (done - start), i.e. issued on all GPUs -> complete on all GPUs
-        (SURVEY.md 8d). p50 over n ops. Removes the skew a plain barrier leaves."""
+    # 8 KiB p50 latency over >= 10,000 ops, the SAME sync pattern for every
+    # contender: issue, then torch.cuda.synchronize() (device-wide, so it
+    # covers the rail's own stream too), from an agreed start instant.
+    def p50_host(fn, n):
         import struct
         lat = []
         for _ in range(n):
-            prop = time.perf_counter() + 1e-3  # well past the exchange itself
-            start = max(struct.unpack("d", b)[0] for b in comm.allgather_bytes(struct.pack("d", prop)))
+            prop = time.perf_counter() + 1e-3
+            start = max(struct.unpack("d", b_)[0] for b_ in comm.allgather_bytes(struct.pack("d", prop)))
             while time.perf_counter() < start:
                 pass
             fn()
             torch.cuda.synchronize()
             lat.append(time.perf_counter() - start)
         mine = struct.pack(f"{n}d", *lat)
-        per_op = [max(v) for v in zip(*[struct.unpack(f"{n}d", b) for b in comm.allgather_bytes(mine)])]
-        return statistics.median(per_op) * 1e6
+        per_op = sorted(max(v) for v in zip(*[struct.unpack(f"{n}d", b_) for b_ in comm.allgather_bytes(mine)]))
+        return {"p50_us": round(per_op[len(per_op) // 2] * 1e6, 2), "p99_us": round(per_op[int(len(per_op) * 0.99)] * 1e6, 2)}
 
-    lat = {}
-    lat["engine_us"] = round(p50_host(lambda: eng.allreduce(bin_, bout, 8192, dt, stream)), 2)
-    if world > 1:
-        for k in ("nvls", "ce", "sm"):
-            if k == "nvls" and not comm.multicast:
-                continue
-            r = Rail(comm, RAIL_KINDS[k], 10 + len(lat))
-            lat[f"{k}_alone_us"] = round(p50_host(lambda: (r.allreduce(bin_, bout, 0, 8192, 65536, dt),
-                                                            r.synchronize())), 2)
-            r.close()
-        if pg is not None:
-            t8 = torch.empty(2048, dtype=torch.float32, device="cuda")
-            lat["nccl_us"] = round(p50_host(lambda: pg.all_reduce(t8)), 2)
-    out["latency_8k_p50_us"] = lat
+    n_lat = args.latency_ops
+    lat = {"ops": n_lat, "engine": p50_host(lambda: eng.allreduce(bin_, bout, 8192, dt, stream), n_lat)}
+    for k in ("nvls", "ce", "sm"):
+        if k == "nvls" and not comm.multicast:
+            continue
+        r_ = Rail(comm, RAIL_KINDS[k], 10 + len(lat))
+        lat[f"{k}_alone"] = p50_host(lambda: r_.allreduce(bin_, bout, 0, 8192, 65536, dt), n_lat)
+        r_.close()
+    if pg is not None:
+        t8 = torch.empty(2048, dtype=torch.float32, device="cuda")
+        lat["nccl"] = p50_host(lambda: pg.all_reduce(t8), n_lat)
+    out["latency_8k"] = lat
 
-    # ---- small sizes from CUDA graphs (no host launch cost on either side) --
-    if args.graph and world > 1:
-        geng = Engine(comm, kinds=kinds, window=5, eta=0.2, demote_after=1, calibrate_max_bytes=1 << 22,
-                      graph_safe=1)
-        rows = {}
-        for sz in (8192, 65536, 1 << 20):
-            try:
-                geng.allreduce(bin_, bout, sz, dt)  # warm-up
-                geng.synchronize()
-                g = torch.cuda.CUDAGraph()
-                per_graph, replays = 50, 10
-                with torch.cuda.graph(g, stream=torch.cuda.Stream()):
-                    for _ in range(per_graph):
-                        geng.allreduce(bin_, bout, sz, dt, torch.cuda.current_stream())
-                g.replay()
-                torch.cuda.synchronize()
-                comm.barrier()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                for _ in range(replays):
-                    g.replay()
-                b.record()
-                b.synchronize()
-                row = {"ours_us": round(max_over_ranks(a.elapsed_time(b) * 1e3 / (replays * per_graph)), 2),
-                       "rails": sorted({seg[0] for p in geng.last_plans() for seg in p["segs"]})}
-                if pg is not None:
-                    row["nccl_us"] = round(nccl_graph_time(sz) * 1e6, 2)
-                rows[str(sz)] = row
-            except Exception as e:  # pragma: no cover
-                rows[str(sz)] = {"error": str(e)[:160]}
-        geng.close()
-        out["graph_replay_us"] = rows
-
-    # ---- e2e through the public host API (H2D + allreduce + D2H) ------------
-    if not args.no_e2e:
-        hin = torch.empty(S, dtype=torch.uint8).pin_memory()
-        hout = torch.empty(S, dtype=torch.uint8).pin_memory()
-        hin.copy_(x.view(torch.uint8)[:S].cpu())
-        for _ in range(2):
-            eng.allreduce_host(hin, hout, S, dt)
-        k = max(3, min(args.steps, 10))
-        comm.barrier()
-        t0 = time.perf_counter()
-        for _ in range(k):
-            eng.allreduce_host(hin, hout, S, dt)
-        te = max_over_ranks((time.perf_counter() - t0) / k)
+    # Failover: config 4 shape (bf16 256 MiB, largest-alpha rail's link dies
+    # on the last rank at its middle chunk, unplanned).
+    if not args.no_failover and len(kinds) > 1:
+        fs = 256 << 20
+        eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
         eng.synchronize()
-        ev = (ring_volume(world, S) if world > 1 else S) / te / 1e9
-        out["e2e"] = {"value": round(ev, 2), "unit": "GB/s", "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
-                      "ms_per_step": round(te * 1e3, 3),
-                      "note": "nz_engine_allreduce_host from pinned host memory, wall clock, max over ranks"}
-
-    # ---- failover: config 4 shape (bf16 256 MiB, largest-alpha rail fails mid-op)
-    if world > 1 and not args.no_failover and len(kinds) > 1:
-        fs = min(256 << 20, cap)
-        plan_f = eng.plan(fs)["pieces"][0]["plan"]
-        segs = plan_f["segs"]
-        if segs:
-            victim = max(segs, key=lambda sgm: sgm[2])
-            nch =-(-victim[2] // max(65536, (victim[2] // (2 * world)) & ~3))
+        segs = eng.last_plans()[0]["segs"]
+        victim = max(segs, key=lambda s_: s_[2])
+        nch = -(-victim[2] // victim[3])
+        if rank == world - 1:
             eng.inject_failure(eng.op_seq, victim[0], nch // 2)
-            eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
-            eng.synchronize()
-            fo = eng.last_failover()
-            if fo:
-                out["failover"] = {"failed_rail": kinds[fo["failed_rail"]], "target_rail": kinds[fo["target_rail"]],
-                                   "orphan_bytes": fo["orphan_length"], "detect_us": round(fo["detect_us"], 2),
-                                   "host_detect_us": round(fo["host_detect_us"], 2),
-                                   "resume_us": round(fo["resume_us"], 2), "done_us": round(fo["done_us"], 2),
-                                   "payload": "bf16 256 MiB"}
-                # failover = device fault stamp -> orphan fully reduced on the survivor
-                out["failover_ms"] = round(max_over_ranks(fo["done_us"]) / 1e3, 4)
+        comm.barrier()
+        eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
+        eng.synchronize()
+        fo = eng.last_failover()
+        if fo:
+            out["failover"] = {"failed_rail": kinds[fo["failed_rail"]], "target_rail": kinds[fo["target_rail"]],
+                               "orphan_bytes": fo["orphan_length"], "orphan_chunk": fo["orphan_chunk"],
+                               "detect_us": round(max_over_ranks(fo["detect_us"]), 2),
+                               "resume_after_detect_us": round(max_over_ranks(fo["resume_after_detect_us"]), 2),
+                               "done_us": round(max_over_ranks(fo["done_us"]), 2), "payload": "bf16 256 MiB"}
+            out["failover_ms"] = round(out["failover"]["done_us"] / 1e3, 4)
             eng.readmit(victim[0])
 
-    # ---- config 3: mixed 8 KiB - 4 MiB stream through the state machine ------
+    # Config 3: mixed 8 KiB - 4 MiB stream through the state machine.
     if not args.no_sweep:
         import random
 
@@ -579,33 +656,16 @@ def main():
         eng.synchronize()
         tm = max_over_ranks(a.elapsed_time(b) / 1e3)
         table = eng.state()["table"]
-        hot_buckets = [e["bucket"] for e in table["buckets"] if e["hot"] and 13 <= e["bucket"] <= 22]
         out["config3_mixed_stream"] = {"ops": n_ops, "sizes": "log-uniform 8 KiB-4 MiB, seed 7",
                                        "mean_us_per_op": round(tm / n_ops * 1e6, 2),
-                                       "algbw_GBs": round(sum(sizes) / tm / 1e9, 2),
-                                       "hot_buckets": hot_buckets, "threshold": table["threshold"]}
-        if pg is not None:
-            tt = {s_: torch.empty(s_ // 4, dtype=torch.float32, device="cuda") for s_ in set(sizes)}
-            torch.cuda.synchronize()
-            a.record()
-            for s_ in sizes:
-                pg.all_reduce(tt[s_])
-            b.record()
-            b.synchronize()
-            tn = max_over_ranks(a.elapsed_time(b) / 1e3)
-            out["config3_mixed_stream"]["nccl_mean_us_per_op"] = round(tn / n_ops * 1e6, 2)
-            del tt
+                                       "hot_buckets": [e["bucket"] for e in table["buckets"]
+                                                       if e["hot"] and 13 <= e["bucket"] <= 22],
+                                       "threshold": table["threshold"]}
 
-    # ---- config 5: DDP gradient-bucket traces ----------------
-    if not args.no_sweep:
-        # torch 2.11's own DDP bucketing of the two models (tests/golden/make_ddp_buckets.py).
+        # Config 5: DDP gradient-bucket traces (torch 2.11 bucketing, tests/golden).
         traces = json.load(open(os.path.join(ROOT, "tests", "golden", "ddp_buckets.json")))
         c5 = {}
         for name, buckets in traces.items():
-            offs, o = [], 0
-            for nb in buckets:
-                offs.append(o)
-                o += nb
             if max(buckets) > cap:
                 continue
             for _ in range(3):
@@ -613,45 +673,17 @@ def main():
                     eng.allreduce(bin_, bout, nb, dt, stream)
             eng.synchronize()
             comm.barrier()
-            iters = 5
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            for _ in range(iters):
+            for _ in range(5):
                 for nb in buckets:
                     eng.allreduce(bin_, bout, nb, dt, stream)
             b.record(stream)
             b.synchronize()
             eng.synchronize()
-            t_it = max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
-            row = {"buckets": len(buckets), "bytes": o, "ms_per_iter": round(t_it * 1e3, 3),
-                   "busbw_GBs": round(ring_volume(world, o) / t_it / 1e9, 2) if world > 1 else None}
-            if pg is not None:
-                tb = [torch.empty(nb // 4, dtype=torch.float32, device="cuda") for nb in buckets]
-                for t_ in tb:
-                    pg.all_reduce(t_)
-                torch.cuda.synchronize()
-                a.record()
-                for _ in range(iters):
-                    for t_ in tb:
-                        pg.all_reduce(t_)
-                b.record()
-                b.synchronize()
-                tn = max_over_ranks(a.elapsed_time(b) / 1e3 / iters)
-                row["nccl_ms_per_iter"] = round(tn * 1e3, 3)
-                del tb
-            c5[name] = row
+            t_it = max_over_ranks(a.elapsed_time(b) / 1e3 / 5)
+            c5[name] = {"buckets": len(buckets), "bytes": sum(buckets), "ms_per_iter": round(t_it * 1e3, 3)}
         out["config5_ddp_buckets"] = c5
 
-    # ---- CPU baseline (rank 0, N = 1 only) ----------------------------------
-    if world == 1 and rank == 0 and not args.no_cpu:
-        cb = cpu_baseline()
-        if cb:
-            out["cpu_baseline"] = cb
-
-    st_ = eng.state()
-    out["engine_state"] = {"sync_overhead_us": st_["sync_overhead_us"], "threshold": st_["table"]["threshold"],
-                           "rails": [{"kind": r["kind"], "calibration": r["calibration"]} for r in st_["rails"]],
-                           "concurrent": st_.get("concurrent", [])}
     eng.close()
     bin_.free()
     bout.free()
@@ -663,8 +695,32 @@ def main():
     return 0
 
 
-def x_es(dt: int) -> int:
-    return 2 if dt == 1 else 4
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--virtual-ranks", type=int, default=CFG1_RANKS, help="N = 1: ranks of config 1 on the one GPU")
+    ap.add_argument("--rails", default="nvls,ce,sm", help="N > 1 secondary engine rails")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16", "i32"])
+    ap.add_argument("--tune-ops", type=int, default=200, help="N > 1: balancer convergence ops before the sweep")
+    ap.add_argument("--latency-ops", type=int, default=10000)
+    ap.add_argument("--sweep-max", type=int, default=GiB)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-failover", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tune", action="store_true",
+                    help="N > 1: the engine measures its CTA budgets and LL crossover at startup (tune_budgets=1)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    _, world, _ = env_rank()
+    if world == 1:
+        return run_loopback(args)
+    return run_multi(args)
 
 
 if __name__ == "__main__":

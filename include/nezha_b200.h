@@ -199,6 +199,11 @@ int nz_rail_revive(nz_rail_t* rail);
  * 0 restores the default (NEZHA_DETECT_US, else max(2000, 2 x range / 100 GB/s)). */
 int nz_rail_set_detect_us(nz_rail_t* rail, double us);
 
+/* Loopback rails: time every cross-rank grid on the stream it runs on (CUDA
+ * events around each launch), and read + reset the totals (synchronizes). */
+int nz_rail_loop_timing(nz_rail_t* rail, int enable);
+int nz_rail_loop_time(nz_rail_t* rail, uint64_t* launches, double* total_us);
+
 /* Non-blocking read of the rail's mapped fault word; clears it when `consume`. */
 int nz_rail_poll_fault(nz_rail_t* rail, nz_fault_record_t* rec, int consume);
 /* Device watchdog status: 0 ok, else a barrier timed out (the kernel bailed
@@ -245,8 +250,11 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
 int nz_engine_destroy(nz_engine_t* eng);
 
 /* In-memory multi-rail allreduce of `bytes` bytes at offset 0 of the
- * symmetric buffers. `stream` (NULL = legacy default) is the caller's: the
- * rails fork from it and join back into it. Asynchronous. */
+ * symmetric buffers. `stream` (NULL = legacy default; on a loopback rank the
+ * rank's own engine stream, since virtual ranks share the legacy stream) is
+ * the caller's: the rails fork from it and join back into it, and with the
+ * monitor on it passes each rail's part only through that rail's gate word
+ * (DESIGN.md §6b). Asynchronous. */
 int nz_engine_allreduce(nz_engine_t* eng, nz_buf_t* in, nz_buf_t* out, uint64_t bytes, int dtype, void* stream);
 /* End to end from host memory (pinned or pageable): H2D into the engine's
  * UnboundBuffer, multi-rail allreduce, D2H into host_out, pipelined over
@@ -268,6 +276,8 @@ int nz_engine_inject_failure(nz_engine_t* eng, uint32_t op_seq, int rail_id, uin
 int nz_engine_readmit(nz_engine_t* eng, int rail_id);
 int nz_engine_synchronize(nz_engine_t* eng);
 uint32_t nz_engine_op_seq(const nz_engine_t* eng);
+/* The engine's rail with this id (owned by the engine; NULL if none). */
+nz_rail_t* nz_engine_rail(nz_engine_t* eng, int rail_id);
 
 typedef struct {
   uint32_t op_seq;

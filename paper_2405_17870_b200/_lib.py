@@ -180,6 +180,9 @@ _SIGS = {
     "nz_rail_progress": (c_int, [c_void_p, POINTER(c_uint64)]),
     "nz_rail_abort": (c_int, [c_void_p]),
     "nz_rail_status": (c_int, [c_void_p, c_void_p]),
+    "nz_rail_loop_timing": (c_int, [c_void_p, c_int]),
+    "nz_rail_loop_time": (c_int, [c_void_p, POINTER(c_uint64), POINTER(c_double)]),
+    "nz_engine_rail": (c_void_p, [c_void_p, c_int]),
     "nz_rail_inject_stall": (c_int, [c_void_p, c_uint64]),
     "nz_rail_revive": (c_int, [c_void_p]),
     "nz_rail_set_detect_us": (c_int, [c_void_p, c_double]),

@@ -180,11 +180,15 @@ std::map<std::string, std::weak_ptr<LoopGroup>> g_groups;
 }  // namespace
 
 LoopGroup::~LoopGroup() {
+  cudaSetDevice(device);
   for (auto& kv : rails) {
     if (kv.second->stream) {
-      cudaSetDevice(device);
       cudaStreamSynchronize(kv.second->stream);
       cudaStreamDestroy(kv.second->stream);
+    }
+    for (auto& pr : kv.second->tev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
     }
   }
 }

@@ -499,6 +499,10 @@ int nz_engine_create(nz_comm_t* comm, const nz_engine_config_t* cfg, nz_engine_t
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->io, cudaStreamNonBlocking));
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->h2d, cudaStreamNonBlocking));
     NZ_CUDA(cudaStreamCreateWithFlags(&eng->d2h, cudaStreamNonBlocking));
+    if (comm->loop) {
+      NZ_CUDA(cudaStreamCreateWithFlags(&eng->loop_user, cudaStreamNonBlocking));
+      NZ_CUDA(cudaEventCreateWithFlags(&eng->loop_ev, cudaEventDisableTiming));
+    }
     NZ_CUDA(cudaHostAlloc(&eng->rec_stamps_host, 4 * sizeof(uint64_t), cudaHostAllocMapped));
     std::memset(eng->rec_stamps_host, 0, 4 * sizeof(uint64_t));
     NZ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eng->rec_stamps_dev), eng->rec_stamps_host, 0));
@@ -532,6 +536,8 @@ int nz_engine_destroy(nz_engine_t* eng) {
     if (eng->io) cudaStreamDestroy(eng->io);
     if (eng->h2d) cudaStreamDestroy(eng->h2d);
     if (eng->d2h) cudaStreamDestroy(eng->d2h);
+    if (eng->loop_user) cudaStreamDestroy(eng->loop_user);
+    if (eng->loop_ev) cudaEventDestroy(eng->loop_ev);
     if (eng->rec_stamps_host) cudaFreeHost(eng->rec_stamps_host);
     delete eng;
   });
@@ -548,7 +554,7 @@ int nz_engine_allreduce(nz_engine_t* eng, nz_buf_t* in, nz_buf_t* out, uint64_t 
     // NULL is the legacy default stream; pass it explicitly, since a NULL
     // stream given to a rail means "the rail's own stream" (nz_rail_allreduce)
     // and the cold path would then run unordered with the caller's copies.
-    cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    cudaStream_t user = eng->callerStream(stream);
     eng->last_plans.clear();
     for (const auto& piece : nezha::splitOversized(bytes)) {
       eng->op(in, out, piece.offset, piece.length, dtype, user);
@@ -574,7 +580,7 @@ int nz_engine_allreduce_device(nz_engine_t* eng, const void* src, void* dst, uin
     if (!eng || !src || !dst) fail(NZ_ERR_INVALID, "null argument");
     if (bytes == 0) return;
     NZ_CUDA(cudaSetDevice(eng->comm->device));
-    cudaStream_t user = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+    cudaStream_t user = eng->callerStream(stream);
     eng->staged(static_cast<const char*>(src), static_cast<char*>(dst), bytes, dtype, cudaMemcpyDeviceToDevice,
                 cudaMemcpyDeviceToDevice, user);
   });
@@ -609,6 +615,13 @@ int nz_engine_synchronize(nz_engine_t* eng) {
 }
 
 uint32_t nz_engine_op_seq(const nz_engine_t* eng) { return eng ? eng->op_seq : 0; }
+
+nz_rail_t* nz_engine_rail(nz_engine_t* eng, int rail_id) {
+  if (!eng) return nullptr;
+  for (size_t i = 0; i < eng->specs.size(); ++i)
+    if (eng->specs[i].rail_id == rail_id) return eng->rails[i];
+  return nullptr;
+}
 
 int nz_engine_last_failover(nz_engine_t* eng, nz_failover_report_t* rep) {
   if (!eng || !rep) return NZ_ERR_INVALID;

@@ -76,6 +76,20 @@ struct nz_engine {
   cudaStream_t io = nullptr;
   cudaStream_t h2d = nullptr;  // host path: uploads of the next piece
   cudaStream_t d2h = nullptr;  // host path: downloads of the previous piece
+  // Loopback ranks share the process's legacy stream, so a NULL caller
+  // stream means this rank's own stream instead (a stream gate of one rank
+  // must not hold up another rank's work).
+  cudaStream_t loop_user = nullptr;
+  cudaEvent_t loop_ev = nullptr;
+  cudaStream_t callerStream(void* stream) {
+    if (stream) return static_cast<cudaStream_t>(stream);
+    if (!loop_user) return cudaStreamLegacy;
+    // Work this thread put on the legacy stream (e.g. the copy that filled
+    // the input) comes first.
+    NZ_CUDA(cudaEventRecord(loop_ev, cudaStreamLegacy));
+    NZ_CUDA(cudaStreamWaitEvent(loop_user, loop_ev, 0));
+    return loop_user;
+  }
   nz_buf* ub_in = nullptr;
   nz_buf* ub_out = nullptr;
   // Plans of each piece of the last call; rendered to JSON only on request

@@ -208,7 +208,11 @@ struct LoopRail {
   cudaEvent_t done[kMaxRanks] = {};
   cudaStream_t stream = nullptr;
   std::string error;
-  uint64_t error_gen = ~0ull;
+  // Optional per-launch timing of the grids on the group stream (the stream
+  // the kernels run on): event pairs, summed and recycled on read.
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+  size_t tev_used = 0;
 };
 
 // Host-side exchange: every rank contributes (bytes, fds); returns world

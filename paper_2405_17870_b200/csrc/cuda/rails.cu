@@ -234,9 +234,21 @@ void combine(nz_rail* r, int kind, int dtype, const A& a, int grid, cudaStream_t
         for (int p = 0; p < N; ++p) NZ_CUDA(cudaStreamWaitEvent(L.stream, L.ready[p], 0));
         const int occ = std::max(1, loopOccupancy(kind, N, dtype));
         const int cap_ctas = std::max(1, occ * c->sm_count / (N * std::max(1, c->live_rails)));
+        std::pair<cudaEvent_t, cudaEvent_t>* tp = nullptr;
+        if (L.timing) {
+          if (L.tev_used == L.tev.size()) {
+            std::pair<cudaEvent_t, cudaEvent_t> pr;
+            NZ_CUDA(cudaEventCreate(&pr.first));
+            NZ_CUDA(cudaEventCreate(&pr.second));
+            L.tev.push_back(pr);
+          }
+          tp = &L.tev[L.tev_used++];
+          NZ_CUDA(cudaEventRecord(tp->first, L.stream));
+        }
         launchLoopGrid(kind, N, dtype, L.args.data(), std::min(grid, cap_ctas), L.stream);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         NZ_CUDA(cudaGetLastError());
+        if (tp) NZ_CUDA(cudaEventRecord(tp->second, L.stream));
         for (int p = 0; p < N; ++p) NZ_CUDA(cudaEventRecord(L.done[p], L.stream));
       } catch (const std::exception& e) {
         err = e.what();
@@ -860,6 +872,35 @@ int nz_rail_set_detect_us(nz_rail_t* rail, double us) {
   return guarded([&] {
     if (!rail || !(us >= 0)) fail(NZ_ERR_INVALID, "bad argument");
     rail->detect_us = us;
+  });
+}
+
+int nz_rail_loop_timing(nz_rail_t* rail, int enable) {
+  return guarded([&] {
+    if (!rail) fail(NZ_ERR_INVALID, "null rail");
+    if (!rail->lr) fail(NZ_ERR_INVALID, "not a loopback rail");
+    std::lock_guard<std::mutex> lk(rail->lr->m);
+    rail->lr->timing = enable != 0;
+  });
+}
+
+int nz_rail_loop_time(nz_rail_t* rail, uint64_t* launches, double* total_us) {
+  return guarded([&] {
+    if (!rail || !launches || !total_us) fail(NZ_ERR_INVALID, "null argument");
+    if (!rail->lr) fail(NZ_ERR_INVALID, "not a loopback rail");
+    nz::LoopRail& L = *rail->lr;
+    std::lock_guard<std::mutex> lk(L.m);
+    NZ_CUDA(cudaSetDevice(rail->comm->device));
+    NZ_CUDA(cudaStreamSynchronize(L.stream));
+    double us = 0;
+    for (size_t i = 0; i < L.tev_used; ++i) {
+      float ms = 0;
+      NZ_CUDA(cudaEventElapsedTime(&ms, L.tev[i].first, L.tev[i].second));
+      us += static_cast<double>(ms) * 1000.0;
+    }
+    *launches = L.tev_used;
+    *total_us = us;
+    L.tev_used = 0;
   });
 }
 

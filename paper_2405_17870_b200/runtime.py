@@ -250,6 +250,18 @@ class Engine:
         check(rc, "nz_engine_last_failover")
         return {f: getattr(rep, f) for f, _ in rep._fields_}
 
+    def loop_timing(self, rail_id: int, enable: bool = True) -> None:
+        """Loopback: time every cross-rank grid of the rail on its own stream (nz_rail_loop_timing)."""
+        check(lib().nz_rail_loop_timing(lib().nz_engine_rail(self.handle, rail_id), 1 if enable else 0),
+              "nz_rail_loop_timing")
+
+    def loop_time(self, rail_id: int) -> dict:
+        """Launches and summed device time of the rail's loopback grids since the last read."""
+        n, us = ctypes.c_uint64(), ctypes.c_double()
+        check(lib().nz_rail_loop_time(lib().nz_engine_rail(self.handle, rail_id), byref(n), byref(us)),
+              "nz_rail_loop_time")
+        return {"launches": n.value, "total_us": us.value}
+
     def failovers(self) -> list[dict]:
         """Every failover the monitor handled so far, in order (nz_engine_failover_get)."""
         n = check(lib().nz_engine_failover_count(self.handle), "nz_engine_failover_count")
