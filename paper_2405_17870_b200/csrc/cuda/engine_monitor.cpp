@@ -312,7 +312,7 @@ void nz_engine::readmit(int rail_id) {
   // succeeded on every rank.
   ensureUnbound(1 << 16);
   const double hold = cfg.readmit_hold_us;
-  const double t0 = nowUs();
+  double t_first = -1;  // first successful probe: the start of the healthy streak
   for (;;) {
     nz::RailOp o;
     o.in = ub_in;
@@ -331,18 +331,19 @@ void nz_engine::readmit(int rail_id) {
     }
     if (!ok) fail(NZ_ERR_RAIL_DOWN, "readmit: probe allreduce on rail " + std::to_string(rail_id) + " failed");
     const double now = nowUs();
+    if (t_first < 0) t_first = now;
     {
       std::lock_guard<std::mutex> lk(mu);
       health->heartbeat(rail_id, now);
     }
     // Every rank leaves the loop after the same number of probes.
-    int32_t done = now - t0 >= hold ? 1 : 0;
+    int32_t done = now - t_first >= hold ? 1 : 0;
     if (comm->world > 1) {
       const auto msgs = nz::exchange(comm, &done, sizeof(done), {});
       for (const auto& m : msgs) done &= *reinterpret_cast<const int32_t*>(m.data.data());
     }
     if (done) break;
-    const double left = hold - (now - t0);
+    const double left = hold - (now - t_first);
     std::this_thread::sleep_for(
         std::chrono::microseconds(static_cast<int64_t>(std::clamp(left, 0.0, cfg.heartbeat_us / 2))));
   }
@@ -350,7 +351,8 @@ void nz_engine::readmit(int rail_id) {
     std::lock_guard<std::mutex> lk(mu);
     if (health->state(rail_id).status == nezha::HealthStatus::Failed) {
       // The streak started at the first successful probe (after channelDown).
-      health->readmit(rail_id, nowUs(), std::min(hold, nowUs() - t0));
+      const double now = nowUs();
+      health->readmit(rail_id, now, std::min(hold, now - t_first));
     }
     agreed_failed.erase(rail_id);
     for (auto it = table_events.begin(); it != table_events.end();)

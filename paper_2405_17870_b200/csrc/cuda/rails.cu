@@ -294,10 +294,10 @@ void launchBarrier(nz_rail* r, uint32_t epoch, bool end, FaultPost post, const R
   dispatchBarrier(r->comm->world, k, st);
 }
 
-void ensureStaging(nz_rail* r, size_t slot, std::vector<char*>* retired) {
+void ensureStaging(nz_rail* r, size_t slot, cudaStream_t st, std::vector<char*>* retired) {
   if (slot <= r->staging_slot) return;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  NZ_CUDA(cudaStreamIsCapturing(r->stream, &cap));
+  NZ_CUDA(cudaStreamIsCapturing(st, &cap));
   if (cap != cudaStreamCaptureStatusNone)
     fail(NZ_ERR_INVALID, "CE staging must grow outside graph capture: run the largest op eagerly first");
   // A captured graph may still reference the old buffer: keep it until the
@@ -449,7 +449,7 @@ void railWave(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, con
     const uint64_t s16 = s & ~15ull;
     {
       std::lock_guard<std::mutex> lk(g_retired_mu);
-      ensureStaging(r, e - s16, &g_retired[r]);
+      ensureStaging(r, e - s16, st, &g_retired[r]);
     }
     const int P = cePieces(len);
     std::vector<uint64_t> cut(P + 1);

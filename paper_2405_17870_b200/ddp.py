@@ -24,7 +24,11 @@ import torch
 from ._lib import BF16, F32, I32
 from .runtime import Comm, Engine
 
-_DTYPES = {torch.float32: F32, torch.bfloat16: BF16, torch.int32: I32}
+# Gradient dtypes the hook averages. int32 is an engine dtype (sum with
+# wraparound) but a mean of integers is not a gradient: it is refused up front,
+# before anything is reduced.
+_DTYPES = {torch.float32: F32, torch.bfloat16: BF16}
+_ENGINE_ONLY = {torch.int32: I32}
 
 
 @dataclass
@@ -64,7 +68,8 @@ def nezha_allreduce_hook(state: NezhaHookState, bucket) -> torch.futures.Future[
     t = bucket.buffer()
     dtype = _DTYPES.get(t.dtype)
     if dtype is None:
-        raise TypeError(f"nezha hook: unsupported gradient dtype {t.dtype}")
+        why = " (integer buckets have no mean; use Engine.allreduce_device for a sum)" if t.dtype in _ENGINE_ONLY else ""
+        raise TypeError(f"nezha hook: unsupported gradient dtype {t.dtype}{why}")
     nbytes = t.numel() * t.element_size()
     stream = state.stream or torch.cuda.current_stream()
     stream.wait_stream(torch.cuda.current_stream())  # the gradients of this bucket are written

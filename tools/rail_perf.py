@@ -23,4 +23,3 @@ for rr in res:
 for (k, s), us in sorted(rows.items()):
     bus = 2 * (world - 1) / world * s / (us * 1e-6) / 1e9
     print(json.dumps({"world": world, "rail": k, "bytes": s, "us_max_over_ranks": round(us, 2), "busbw_GBs": round(bus, 1)}))
-# Tip: NEZHA_SM_TMA=1 python tools/rail_perf.py 4 sm ... measures the TMA-pipelined SM rail.

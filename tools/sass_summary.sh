@@ -1,18 +1,21 @@
 #!/bin/bash
 # Static kernel evidence, no GPU needed: per-kernel ptxas resources and the
 # SASS instructions that prove each rail's data path compiled as designed.
-#   bash tools/sass_summary.sh > profiles/r01/sass_summary.txt
-# Run after `make -C paper_2405_17870_b200/csrc` (reads its ptxas log and .o).
+#   bash tools/sass_summary.sh > profiles/r02/sass_summary.txt
+# Run after `make -C paper_2405_17870_b200/csrc` (reads its ptxas logs and .o).
 set -eu
 cd "$(dirname "$0")/.."
-OBJ=build/csrc/cuda/rails.cu.o
-LOG=$OBJ.ptxas.log
-[ -f "$OBJ" ] && [ -f "$LOG" ] || { echo "build first: make -C paper_2405_17870_b200/csrc" >&2; exit 1; }
+OBJS="build/csrc/cuda/rails.cu.o build/csrc/cuda/rails_vr.cu.o"
+LOG=$(mktemp)
 SASS=$(mktemp)
-trap 'rm -f "$SASS"' EXIT
-cuobjdump -sass "$OBJ" > "$SASS"
+trap 'rm -f "$SASS" "$LOG"' EXIT
+for OBJ in $OBJS; do
+  [ -f "$OBJ" ] && [ -f "$OBJ.ptxas.log" ] || { echo "build first: make -C paper_2405_17870_b200/csrc" >&2; exit 1; }
+  cat "$OBJ.ptxas.log" >> "$LOG"
+  cuobjdump -sass "$OBJ" >> "$SASS"
+done
 
-echo "# sm_100a static summary of $OBJ ($(git rev-parse --short HEAD 2>/dev/null || echo '?'))"
+echo "# sm_100a static summary of $OBJS ($(git rev-parse --short HEAD 2>/dev/null || echo '?'))"
 echo "# nvcc: $(nvcc --version | tail -1)"
 echo
 echo "## ptxas resources per kernel (registers | stack | spills)"
@@ -26,7 +29,7 @@ awk '/Function properties for/{f=$NF} /spill stores/ && !/ 0 bytes spill stores,
 echo
 echo "## data-path SASS per kernel family (instruction counts over all instances)"
 echo "# LDGMC.* = multimem.ld_reduce (NVSwitch reduce, NVLS rail)"
-echo "# UBLKCP.* / SYNCS.* = cp.async.bulk + mbarrier (TMA SM-rail variant)"
+echo "# LDL / STL = local memory (spills); the loopback *_vr grids select their rank's arguments by blockIdx.y"
 echo "# LDG.E.NA.128 / STG.E.128* = 128-bit vectorised loads / peer stores"
 awk '
   /Function :/ { fn = $3; next }

@@ -19,7 +19,7 @@ step() {
 }
 step smoke 300 "python -c 'import __graft_entry__ as g; g.smoke()'"
 step single_gpu 900 "python -m pytest tests/test_gpu_rails.py tests/test_gpu_engine.py -m gpu -q -p no:cacheprovider --timeout 600 -rfE -k 'emulated or golden or config1 or single_gpu'"
-step rails 600 "python tools/run_spawn.py 2 tests/workers/rail_worker.py \"\$(python -c 'import json,sys; sys.path.insert(0,\".\"); from tests.test_gpu_rails import MULTI, ONESHOT, random_rail_cases; print(json.dumps([c for c in MULTI + random_rail_cases(102) if c[\"kind\"] != \"nvls\"]))')\""
+step rails 600 "python tools/run_spawn.py 2 tests/workers/rail_worker.py \"\$(python -c 'import json,sys; sys.path.insert(0,\".\"); from tests.test_gpu_rails import MULTI, random_rail_cases; print(json.dumps([c for c in MULTI + random_rail_cases(102) if c[\"kind\"] != \"nvls\"]))')\""
 step engine 600 "python tools/run_spawn.py 2 tests/workers/engine_worker.py '{\"rails\": [\"ce\", \"sm\"], \"calibrate_max_bytes\": 67108864, \"cases\": [{\"dtype\": \"f32\", \"nbytes\": 67108864, \"reps\": 3}, {\"dtype\": \"bf16\", \"nbytes\": 3000002, \"reps\": 2}, {\"dtype\": \"i32\", \"nbytes\": 8192, \"reps\": 2, \"host\": true}, {\"dtype\": \"f32\", \"nbytes\": 41943044, \"reps\": 1, \"device\": true}, {\"dtype\": \"bf16\", \"nbytes\": 268435456, \"reps\": 2, \"fail\": [1, 3], \"fail_rep\": 1}]}'"
 step bench2 900 "python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --steps 5 --warmup 3 --rails ce,sm"
 cat $S
