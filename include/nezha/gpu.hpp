@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "nezha/core/error.hpp"
 #include "nezha/core/types.hpp"
@@ -41,6 +42,12 @@ class Comm {
  public:
   Comm(int rank, int world, int device, const std::string& session, int timeout_ms = 120000) {
     check(nz_comm_init(rank, world, device, session.c_str(), timeout_ms, &h_));
+  }
+  // One virtual rank of a job whose ranks are threads on one GPU
+  // (nz_comm_init_loopback; the reference's ranks-as-threads fabric).
+  struct Loopback {};
+  Comm(Loopback, int rank, int world, int device, const std::string& session, int timeout_ms = 120000) {
+    check(nz_comm_init_loopback(rank, world, device, session.c_str(), timeout_ms, &h_));
   }
   ~Comm() { nz_comm_destroy(h_); }
   Comm(const Comm&) = delete;
@@ -99,9 +106,16 @@ class Engine {
   void allreduceDevice(const void* src, void* dst, Bytes bytes, nz_dtype_t dtype, void* stream = nullptr) {
     check(nz_engine_allreduce_device(h_, src, dst, bytes, dtype, stream));
   }
-  // InMemoryFabric::failRailAtFrame (inmem.hpp:22-24) in trace form.
+  // This rank's link of `rail` dies at `chunk` of op `op_seq` (unplanned:
+  // the other ranks' monitors detect it, agree and reroute).
   void failRailAt(std::uint32_t op_seq, int rail, std::uint64_t chunk) {
     check(nz_engine_inject_failure(h_, op_seq, rail, chunk));
+  }
+  // Every handoff so far (HandoffTicket, with timings).
+  std::vector<nz_failover_report_t> failovers() {
+    std::vector<nz_failover_report_t> v(static_cast<size_t>(nz_engine_failover_count(h_)));
+    for (size_t i = 0; i < v.size(); ++i) check(nz_engine_failover_get(h_, static_cast<int>(i), &v[i]));
+    return v;
   }
   void readmit(int rail) { check(nz_engine_readmit(h_, rail)); }
   void synchronize() { check(nz_engine_synchronize(h_)); }
