@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "nezha/core/types.hpp"
@@ -65,6 +66,20 @@ inline int ringBlockOf(std::uint64_t elem, std::uint64_t chunk_elems, int world)
 // payloads above 2^30 bytes become ceil(S / 256 MiB)
 // contiguous pieces of at most 256 MiB; everything else is one piece.
 std::vector<Segment> splitOversized(Bytes payload);
+
+// Waves of one rail call over chunks [cb, ce): consecutive
+// groups of ceil(wave_bytes / chunk_bytes) chunks, a last group shorter than
+// half a group joined to the one before; one launch sequence per wave, whose
+// success publishes its end chunk (the failure monitor's progress unit).
+inline constexpr Bytes kDefaultWaveBytes = Bytes{64} << 20;
+std::vector<std::pair<std::uint64_t, std::uint64_t>> waveRanges(Bytes chunk_bytes, std::uint64_t cb, std::uint64_t ce,
+                                                                 Bytes wave_bytes = kDefaultWaveBytes);
+// Chunks complete on every rank when one rank's link dies at chunk `stall`
+// of a call over [cb, ce): the start of the wave holding it (SPEC.md:414's
+// "min over ranks of completed chunks" for the engine's wave-granular
+// progress); ce when no wave holds it (the link death is never hit).
+std::uint64_t completedBeforeStall(Bytes chunk_bytes, std::uint64_t cb, std::uint64_t ce, std::uint64_t stall,
+                                   Bytes wave_bytes = kDefaultWaveBytes);
 
 // Pieces of the host-memory allreduce pipeline (nz_engine_allreduce_host,
 // DESIGN.md §4c): below 8 MiB one piece; else pieces of

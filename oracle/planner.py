@@ -462,7 +462,7 @@ def unit(x):
 
 def parse(text):
     sc = {"world": 8, "chunked": True, "rails": [], "truth": {}, "truth_sync": 0.0, "seed": 0, "sizes": [],
-          "faults": [], "readmits": [], "concurrent": [],
+          "faults": [], "readmits": [], "concurrent": [], "stalls": [], "wave_bytes": 64 << 20,
           "cfg": {"tau": 5.0, "eta": 0.05, "eps": 0.01, "sync_us": 0.0, "window": 100, "max_iters": 100,
                   "demote_after": 0, "probe_lo": 4096, "probe_hi": 1 << 30}}
     keys = {"tau": "tau", "eta": "eta", "eps": "eps", "sync_us": "sync_us", "window": "window",
@@ -511,6 +511,12 @@ def parse(text):
             sc["faults"].append((int(a[0]), int(a[1]), int(a[2])))
         elif k == "readmit":
             sc["readmits"].append((int(a[0]), int(a[1])))
+        elif k == "stall":
+            sc["stalls"].append((int(a[0]), int(a[1]), int(a[2]), int(a[3])))
+        elif k == "wave_bytes":
+            sc["wave_bytes"] = int(a[0])
+            if sc["wave_bytes"] <= 0:
+                raise ValueError("wave_bytes")
         else:
             raise ValueError(k)
     return sc
@@ -528,20 +534,75 @@ def truth(sc, op, rail_id, n, multi):
     return us
 
 
+def wave_ranges(C, cb, ce, wave_bytes):
+    """Waves of a rail call over chunks [cb, ce): groups of
+    ceil(wave_bytes / C) chunks; a last group shorter than half a group joins
+    the one before."""
+    if ce <= cb or C == 0:
+        return []
+    per = max(1, -(-max(wave_bytes, 1) // C))
+    w = [[c0, min(ce, c0 + per)] for c0 in range(cb, ce, per)]
+    if len(w) > 1 and (w[-1][1] - w[-1][0]) * 2 < per:
+        w[-2][1] = w[-1][1]
+        w.pop()
+    return w
+
+
+def completed_before_stall(C, cb, ce, stall, wave_bytes):
+    """Chunks complete on every rank when one rank's link dies at `stall`:
+    the start of the wave that holds it (ce when none does) — SPEC.md:414's
+    minimum over ranks of the chunks each completed, at wave granularity."""
+    for c0, c1 in wave_ranges(C, cb, ce, wave_bytes):
+        if c0 <= stall < c1:
+            return c0
+    return ce
+
+
+def _ticket(plan, op, rid, off, n, C, k, healthy):
+    """P9 / P10 ticket JSON (or "null") and whether no survivor existed."""
+    if k * C >= n:
+        return "null", False
+    cands = sorted(r for r in healthy if r != rid)
+    if not cands:
+        return "null", True
+    lens = {r: sum(s[2] for s in plan["segs"] if s[0] == r) for r in cands}
+    tgt = cands[0]
+    for r in cands:
+        if lens[r] > lens[tgt]:
+            tgt = r
+    return '{"op_seq":%d,"offset":%d,"length":%d,"source":%d,"target":%d}' % (op, off + k * C, n - k * C, rid, tgt), False
+
+
 def run(text: str) -> str:
     """Decision log for a scenario; must equal nz_planner_run_trace byte for byte."""
     sc = parse(text)
     t = Table(sc["rails"], sc["cfg"])
     if sc["concurrent"]:
         t.set_concurrent(sc["concurrent"])
-    healthy = sorted(r.rail_id for r in t.rails)
+    healthy = sorted(r.rail_id for r in t.rails)  # not failed by agreement (P9's survivors)
+    activations = []  # [op, rail]: the planner drops the rail before planning op
+    dead = []  # links dead on some rank: launches on them fail at entry
     out = []
     for op, S in enumerate(sc["sizes"]):
         for (rop, rid) in sc["readmits"]:
             if rop == op:
-                t.readmit(rid)
-                healthy = sorted(healthy + [rid])
+                if not any(a[1] == rid for a in activations):
+                    t.readmit(rid)
+                activations = [a for a in activations if a[1] != rid]
+                if rid not in healthy:
+                    healthy.append(rid)
+                healthy = sorted(healthy)
+                dead = [r for r in dead if r != rid]
                 out.append('{"readmit":%d,"op":%d}' % (rid, op))
+        keep = []
+        for a in activations:
+            if a[0] > op:
+                keep.append(a)
+                continue
+            if t.ok[t.idx(a[1])]:
+                t.fail(a[1])
+            out.append('{"dropped":%d,"op":%d}' % (a[1], op))
+        activations = keep
         plan = t.allocate(S)
         if plan is None:
             out.append('{"op":%d,"S":%d,"unrecoverable":true}' % (op, S))
@@ -559,22 +620,41 @@ def run(text: str) -> str:
             if seg:
                 _, off, n = seg[-1]
                 C = chunk_bytes(n, sc["world"], sc["chunked"])
-                if k * C < n:
-                    cands = sorted(r for r in healthy if r != rid)
-                    if cands:
-                        lens = {r: sum(s[2] for s in plan["segs"] if s[0] == r) for r in cands}
-                        tgt = cands[0]
-                        for r in cands:
-                            if lens[r] > lens[tgt]:
-                                tgt = r
-                        ticket = '{"op_seq":%d,"offset":%d,"length":%d,"source":%d,"target":%d}' % (
-                            op, off + k * C, n - k * C, rid, tgt)
-                    else:
-                        unrec = True
+                ticket, unrec = _ticket(plan, op, rid, off, n, C, k, healthy)
             out.append('{"fail":{"op":%d,"rail":%d,"chunk":%d},"ticket":%s%s}' % (
                 op, rid, k, ticket, ',"unrecoverable":true' if unrec else ""))
             healthy = [r for r in healthy if r != rid]
             t.fail(rid)
+        for (rid, off, n) in plan["segs"]:
+            if rid not in dead:
+                continue
+            failed = True
+            C = chunk_bytes(n, sc["world"], sc["chunked"])
+            ticket, unrec = _ticket(plan, op, rid, off, n, C, 0, healthy)
+            out.append('{"lost":{"op":%d,"rail":%d},"ticket":%s%s}' % (
+                op, rid, ticket, ',"unrecoverable":true' if unrec else ""))
+        for (sop, rid, k, lag) in sc["stalls"]:
+            if sop != op:
+                continue
+            seg = [s for s in plan["segs"] if s[0] == rid]
+            head = '{"stall":{"op":%d,"rail":%d,"chunk":%d}' % (op, rid, k)
+            if not seg or rid in dead:
+                out.append(head + ',"fired":false}')
+                continue
+            _, off, n = seg[-1]
+            C = chunk_bytes(n, sc["world"], sc["chunked"])
+            nch = -(-n // C)
+            kk = completed_before_stall(C, 0, nch, k, sc["wave_bytes"])
+            if kk >= nch:
+                out.append(head + ',"fired":false}')
+                continue
+            failed = True
+            healthy = [r for r in healthy if r != rid]
+            dead.append(rid)
+            activations.append([op + 1 + lag, rid])
+            ticket, unrec = _ticket(plan, op, rid, off, n, C, kk, healthy)
+            out.append(head + ',"fired":true,"orphan_chunk":%d,"activation":%d,"ticket":%s%s}' % (
+                kk, op + 1 + lag, ticket, ',"unrecoverable":true' if unrec else ""))
         if failed:
             continue
         multi = len(plan["segs"]) > 1

@@ -275,8 +275,7 @@ inline uint32_t railAllreduce(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t seg_
 }
 // Waves of a call: consecutive chunk groups of >= NEZHA_WAVE_BYTES (64 MiB)
 // each, one launch sequence apiece, so progress is published between them.
-std::vector<std::pair<uint64_t, uint64_t>> railWaves(uint64_t seg_len, uint64_t chunk_bytes, uint64_t cb,
-                                                     uint64_t ce);
+std::vector<std::pair<uint64_t, uint64_t>> railWaves(uint64_t chunk_bytes, uint64_t cb, uint64_t ce);
 // CTAs of the rail's computation-phase kernel for a whole segment of
 // `seg_len` bytes (the ComputePool demand); 0 when it launches none.
 int railComputeCtas(nz_rail* r, uint64_t seg_len);

@@ -9,6 +9,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "nezha/collective.hpp"
 
 namespace nz {
 
@@ -537,19 +538,8 @@ void launchStamp(uint64_t* dst, cudaStream_t st) {
   NZ_CUDA(cudaGetLastError());
 }
 
-std::vector<std::pair<uint64_t, uint64_t>> railWaves(uint64_t seg_len, uint64_t chunk_bytes, uint64_t cb,
-                                                     uint64_t ce) {
-  std::vector<std::pair<uint64_t, uint64_t>> w;
-  if (ce <= cb || chunk_bytes == 0) return w;
-  const uint64_t per = std::max<uint64_t>(1, (waveBytes() + chunk_bytes - 1) / chunk_bytes);
-  (void)seg_len;
-  for (uint64_t c0 = cb; c0 < ce; c0 += per) w.emplace_back(c0, std::min(ce, c0 + per));
-  // A short last wave joins the previous one (no launch for a sliver).
-  if (w.size() > 1 && (w.back().second - w.back().first) * 2 < per) {
-    w[w.size() - 2].second = w.back().second;
-    w.pop_back();
-  }
-  return w;
+std::vector<std::pair<uint64_t, uint64_t>> railWaves(uint64_t chunk_bytes, uint64_t cb, uint64_t ce) {
+  return nezha::waveRanges(chunk_bytes, cb, ce, waveBytes());
 }
 
 uint32_t railRun(nz_rail* r, const RailOp& op) {
@@ -601,7 +591,7 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
   if (llPath(r, lo, hi))
     waves.emplace_back(op.chunk_begin, stop);
   else
-    waves = railWaves(op.seg_len, op.chunk_bytes, op.chunk_begin, stop);
+    waves = railWaves(op.chunk_bytes, op.chunk_begin, stop);
   for (size_t w = 0; w < waves.size(); ++w) {
     const auto [c0, c1] = waves[w];
     const bool last = w + 1 == waves.size();

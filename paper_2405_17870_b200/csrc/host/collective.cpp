@@ -50,4 +50,24 @@ std::vector<Segment> hostPipelinePieces(Bytes payload, int elem_size) {
   return out;
 }
 
+std::vector<std::pair<std::uint64_t, std::uint64_t>> waveRanges(Bytes chunk_bytes, std::uint64_t cb, std::uint64_t ce,
+                                                                 Bytes wave_bytes) {
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> w;
+  if (ce <= cb || chunk_bytes == 0) return w;
+  const std::uint64_t per = std::max<std::uint64_t>(1, (std::max<Bytes>(wave_bytes, 1) + chunk_bytes - 1) / chunk_bytes);
+  for (std::uint64_t c0 = cb; c0 < ce; c0 += per) w.emplace_back(c0, std::min(ce, c0 + per));
+  if (w.size() > 1 && (w.back().second - w.back().first) * 2 < per) {
+    w[w.size() - 2].second = w.back().second;
+    w.pop_back();
+  }
+  return w;
+}
+
+std::uint64_t completedBeforeStall(Bytes chunk_bytes, std::uint64_t cb, std::uint64_t ce, std::uint64_t stall,
+                                   Bytes wave_bytes) {
+  for (const auto& [c0, c1] : waveRanges(chunk_bytes, cb, ce, wave_bytes))
+    if (stall >= c0 && stall < c1) return c0;
+  return ce;
+}
+
 }  // namespace nezha

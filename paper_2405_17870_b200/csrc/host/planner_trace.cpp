@@ -114,6 +114,12 @@ Scenario parseScenario(const std::string& text) {
       FaultLine f;
       if (!(ls >> f.op >> f.rail >> f.chunk)) bad("fail");
       sc.faults.push_back(f);
+    } else if (key == "stall") {
+      StallLine t;
+      if (!(ls >> t.op >> t.rail >> t.chunk >> t.lag)) bad("stall");
+      sc.stalls.push_back(t);
+    } else if (key == "wave_bytes") {
+      if (!(ls >> sc.wave_bytes) || sc.wave_bytes == 0) bad("wave_bytes");
     } else if (key == "readmit") {
       ReadmitLine r;
       if (!(ls >> r.op >> r.rail)) bad("readmit");
@@ -152,20 +158,70 @@ std::string planJson(std::uint32_t op, Bytes S, const Plan& p) {
   return o.str();
 }
 
+namespace {
+
+void ticketJson(std::ostringstream& log, const std::optional<HandoffTicket>& ticket, bool unrecoverable) {
+  if (ticket) {
+    log << "{\"op_seq\":" << ticket->op_seq << ",\"offset\":" << ticket->orphan.offset
+        << ",\"length\":" << ticket->orphan.length << ",\"source\":" << ticket->source_rail
+        << ",\"target\":" << ticket->target_rail << "}";
+  } else {
+    log << "null";
+  }
+  if (unrecoverable) log << ",\"unrecoverable\":true";
+}
+
+// P9 over `healthy` for the orphan of `seg` from chunk k: nullopt ticket and
+// unrecoverable = true when no survivor exists; nullopt, false when empty.
+std::optional<HandoffTicket> handoff(const Plan& plan, std::uint32_t op, int rail, const Segment& seg, Bytes C,
+                                     std::uint64_t k, const std::vector<int>& healthy, bool* unrecoverable) {
+  *unrecoverable = false;
+  const Segment orphan = orphanOf(seg, C, k);
+  if (orphan.length == 0) return std::nullopt;
+  const auto target = chooseHandoffTarget(plan, rail, healthy);
+  if (!target) {
+    *unrecoverable = true;
+    return std::nullopt;
+  }
+  return HandoffTicket{op, orphan, rail, *target, 0};
+}
+
+}  // namespace
+
 std::string runTrace(const std::string& text) {
   Scenario sc = parseScenario(text);
   Balancer bal(sc.rails, sc.cfg);
   if (!sc.concurrent.empty()) bal.setConcurrentProfiles(sc.concurrent);
   std::ostringstream log;
-  std::vector<int> healthy;
+  std::vector<int> healthy;  // not failed by agreement (P9's survivors)
   for (const auto& r : bal.rails()) healthy.push_back(r.rail_id);
+  std::vector<std::pair<std::uint32_t, int>> activations;  // (op, rail): the planner drops the rail there
+  std::vector<int> dead;  // links dead on some rank: every launch on them fails at entry
+  auto erase = [](std::vector<int>& v, int x) { v.erase(std::remove(v.begin(), v.end(), x), v.end()); };
   for (std::uint32_t op = 0; op < sc.sizes.size(); ++op) {
     for (const auto& r : sc.readmits) {
       if (r.op != op) continue;
-      bal.readmit(r.rail);
-      healthy.push_back(r.rail);
+      // A rail whose agreed drop has not reached the planner yet is still
+      // planned: readmitting it only cancels the drop (as the engine does).
+      const auto pending = std::find_if(activations.begin(), activations.end(),
+                                        [&](const auto& a) { return a.second == r.rail; });
+      if (pending == activations.end()) bal.readmit(r.rail);
+      activations.erase(std::remove_if(activations.begin(), activations.end(),
+                                       [&](const auto& a) { return a.second == r.rail; }),
+                        activations.end());
+      if (std::find(healthy.begin(), healthy.end(), r.rail) == healthy.end()) healthy.push_back(r.rail);
       std::sort(healthy.begin(), healthy.end());
+      erase(dead, r.rail);
       log << "{\"readmit\":" << r.rail << ",\"op\":" << op << "}\n";
+    }
+    for (auto it = activations.begin(); it != activations.end();) {
+      if (it->first > op) {
+        ++it;
+        continue;
+      }
+      if (bal.healthy(it->second)) bal.markFailed(it->second);
+      log << "{\"dropped\":" << it->second << ",\"op\":" << op << "}\n";
+      it = activations.erase(it);
     }
     const Bytes S = sc.sizes[op];
     Plan plan;
@@ -188,27 +244,53 @@ std::string runTrace(const std::string& text) {
       bool unrecoverable = false;
       if (seg) {
         const Bytes C = defaultChunkBytes(seg->length, sc.world, sc.algorithm);
-        const Segment orphan = orphanOf(*seg, C, f.chunk);
-        if (orphan.length > 0) {
-          auto target = chooseHandoffTarget(plan, f.rail, healthy);
-          if (target) {
-            ticket = HandoffTicket{op, orphan, f.rail, *target, 0};
-          } else {
-            unrecoverable = true;
-          }
-        }
+        ticket = handoff(plan, op, f.rail, *seg, C, f.chunk, healthy, &unrecoverable);
       }
-      if (ticket) {
-        log << "{\"op_seq\":" << ticket->op_seq << ",\"offset\":" << ticket->orphan.offset
-            << ",\"length\":" << ticket->orphan.length << ",\"source\":" << ticket->source_rail
-            << ",\"target\":" << ticket->target_rail << "}";
-      } else {
-        log << "null";
-      }
-      if (unrecoverable) log << ",\"unrecoverable\":true";
+      ticketJson(log, ticket, unrecoverable);
       log << "}\n";
-      healthy.erase(std::remove(healthy.begin(), healthy.end(), f.rail), healthy.end());
+      erase(healthy, f.rail);
       bal.markFailed(f.rail);
+    }
+    // Launches on a dead link fail at entry on every rank: the monitor
+    // reroutes the whole segment (no chunk completed).
+    for (const auto& rs : plan.segments) {
+      if (std::find(dead.begin(), dead.end(), rs.rail_id) == dead.end()) continue;
+      failed_this_op = true;
+      const Bytes C = defaultChunkBytes(rs.segment.length, sc.world, sc.algorithm);
+      bool unrecoverable = false;
+      const auto ticket = handoff(plan, op, rs.rail_id, rs.segment, C, 0, healthy, &unrecoverable);
+      log << "{\"lost\":{\"op\":" << op << ",\"rail\":" << rs.rail_id << "},\"ticket\":";
+      ticketJson(log, ticket, unrecoverable);
+      log << "}\n";
+    }
+    for (const auto& t : sc.stalls) {
+      if (t.op != op) continue;
+      const Segment* seg = nullptr;
+      for (const auto& rs : plan.segments)
+        if (rs.rail_id == t.rail) seg = &rs.segment;
+      const bool already = std::find(dead.begin(), dead.end(), t.rail) != dead.end();
+      log << "{\"stall\":{\"op\":" << op << ",\"rail\":" << t.rail << ",\"chunk\":" << t.chunk << "}";
+      if (!seg || already) {  // the link died where this op never touched it
+        log << ",\"fired\":false}\n";
+        continue;
+      }
+      const Bytes C = defaultChunkBytes(seg->length, sc.world, sc.algorithm);
+      const std::uint64_t nch = (seg->length + C - 1) / C;
+      const std::uint64_t k = completedBeforeStall(C, 0, nch, t.chunk, sc.wave_bytes);
+      if (k >= nch) {
+        log << ",\"fired\":false}\n";
+        continue;
+      }
+      failed_this_op = true;
+      erase(healthy, t.rail);
+      dead.push_back(t.rail);
+      const std::uint32_t activation = op + 1 + t.lag;
+      activations.emplace_back(activation, t.rail);
+      bool unrecoverable = false;
+      const auto ticket = handoff(plan, op, t.rail, *seg, C, k, healthy, &unrecoverable);
+      log << ",\"fired\":true,\"orphan_chunk\":" << k << ",\"activation\":" << activation << ",\"ticket\":";
+      ticketJson(log, ticket, unrecoverable);
+      log << "}\n";
     }
     if (failed_this_op) continue;  // an op that lost a rail is not a Timer sample
     std::vector<std::pair<int, Micros>> lat;

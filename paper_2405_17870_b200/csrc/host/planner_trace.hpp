@@ -27,6 +27,16 @@ struct FaultLine {
   std::uint64_t chunk = 0;
 };
 
+// Unplanned failure: one rank's link of `rail` dies at
+// `chunk` of op `op`; the monitors agree and the planner stops using the rail
+// from op `op + 1 + lag` (lag = ops issued before the agreement landed).
+struct StallLine {
+  std::uint32_t op = 0;
+  int rail = 0;
+  std::uint64_t chunk = 0;
+  std::uint32_t lag = 0;
+};
+
 struct ReadmitLine {
   std::uint32_t op = 0;
   int rail = 0;
@@ -43,7 +53,9 @@ struct Scenario {
   std::uint64_t seed = 0;
   std::vector<std::uint64_t> sizes;
   std::vector<FaultLine> faults;
+  std::vector<StallLine> stalls;
   std::vector<ReadmitLine> readmits;
+  Bytes wave_bytes = kDefaultWaveBytes;
 };
 
 Scenario parseScenario(const std::string& text);

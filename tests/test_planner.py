@@ -228,10 +228,37 @@ ops 4 1048576
 """
 
 
+# Unplanned failures: one rank's link dies mid-op; the
+# orphan starts at the last wave boundary every rank completed, the ops the
+# issuing thread planned before the agreement landed (lag) lose the rail at
+# entry and are rerouted whole, the planner drops the rail at the agreed op.
+UNPLANNED = """
+world 8
+config sync_us 6 window 10
+rail 0 nvls 12 7.0e11
+rail 1 ce 45 5.0e11
+rail 2 sm 15 4.5e11
+truth 0 14 6.2e11 0.02
+truth 1 40 3.8e11 0.02
+truth 2 16 3.0e11 0.02
+seed 11
+wave_bytes 33554432
+ops 40 1073741824
+stall 20 0 11 3
+ops 30 268435456
+readmit 60 0
+ops 20 268435456
+stall 80 2 0 0
+stall 85 2 3 1
+ops 10 4096
+"""
+
+
 @needs_lib
 @pytest.mark.parametrize("name,scenario", [("two_homog", TWO_HOMOG), ("three_hetero", THREE_HETERO),
                                            ("failover", FAILOVER), ("gated", GATED), ("ring", RING_ALGO),
-                                           ("shared_links", SHARED_LINKS), ("cascade", CASCADE)])
+                                           ("shared_links", SHARED_LINKS), ("cascade", CASCADE),
+                                           ("unplanned", UNPLANNED)])
 def test_trace_parity_byte_exact(name, scenario):
     got = run_trace(scenario)
     want = P.run(scenario)
@@ -253,6 +280,32 @@ def test_trace_behaviour_three_rails():
     assert all(len(o["segs"]) == 1 for o in small)
     assert all(len(o["segs"]) == 3 for o in big)
     assert any("flush" in l for l in lines)
+
+
+@needs_lib
+def test_trace_unplanned_failure():
+    """Orphan = last wave boundary at or before the dead chunk; lagged ops lose
+    the rail whole; the planner drops it at op + 1 + lag; P9 target."""
+    import json
+
+    lines = [json.loads(l) for l in run_trace(UNPLANNED).splitlines()]
+    st = [l for l in lines if l.get("stall", {}).get("op") == 20][0]
+    assert st["fired"] and st["activation"] == 24
+    op20 = [l for l in lines if l.get("op") == 20 and "segs" in l][0]
+    seg0 = [s_ for s_ in op20["segs"] if s_[0] == 0][0]
+    C = P.chunk_bytes(seg0[2], 8)
+    waves = P.wave_ranges(C, 0, -(-seg0[2] // C), 32 << 20)
+    k = [w[0] for w in waves if w[0] <= 11 < w[1]][0]
+    assert st["orphan_chunk"] == k and st["ticket"]["offset"] == seg0[1] + k * C
+    lost = [l for l in lines if "lost" in l]
+    assert [l["lost"]["op"] for l in lost if l["lost"]["rail"] == 0] == [21, 22, 23]
+    assert all(l["ticket"]["offset"] == [s_ for s_ in p["segs"] if s_[0] == 0][0][1]
+               for l in lost if l["lost"]["rail"] == 0
+               for p in [x for x in lines if x.get("op") == l["lost"]["op"] and "segs" in x])
+    assert any(l.get("dropped") == 0 and l["op"] == 24 for l in lines)
+    for l in lines:
+        if "segs" in l and 24 <= l["op"] < 60:
+            assert all(s_[0] != 0 for s_ in l["segs"])
 
 
 @needs_lib
@@ -407,6 +460,13 @@ def _gen(R):
         fails.append((op, rail))
         lines.append(f"fail {op} {rail} {R.randint(0, 7)}")
     for op, rail in fails:
+        if R.random() < 0.5 and op + 2 < total:
+            lines.append(f"readmit {R.randint(op + 1, total - 1)} {rail}")
+    if R.random() < 0.4:
+        lines.append(f"wave_bytes {R.choice([1 << 20, 8 << 20, 64 << 20])}")
+    for _ in range(R.randint(0, 2)):
+        op = R.randint(0, max(0, total - 1)); rail = R.randrange(nr)
+        lines.append(f"stall {op} {rail} {R.randint(0, 9)} {R.randint(0, 4)}")
         if R.random() < 0.5 and op + 2 < total:
             lines.append(f"readmit {R.randint(op + 1, total - 1)} {rail}")
     return "\n".join(lines) + "\n"
