@@ -366,7 +366,8 @@ std::string nz_engine::stateJson() {
   o << "],\"compute_pool\":{\"mode\":" << static_cast<int>(pool_mode) << ",\"tokens\":"
     << (cpool ? cpool->totalTokens() : 0) << ",\"ops\":" << pool_stats.ops << ",\"waits\":" << pool_stats.waits
     << ",\"shrunk\":" << pool_stats.shrunk << "}";
-  o << ",\"monitor\":{\"on\":" << (monitored ? "true" : "false") << ",\"failovers\":" << reports.size()
+  o << ",\"monitor\":{\"on\":" << (monitored ? "true" : "false") << ",\"off_reason\":\"" << mon_off_reason
+    << "\",\"failovers\":" << reports.size()
     << ",\"inflight\":" << inflight.size() << ",\"failed\":[";
   bool first = true;
   for (int id : agreed_failed) {

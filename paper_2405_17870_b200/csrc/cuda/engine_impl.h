@@ -119,6 +119,7 @@ struct nz_engine {
 
   // ---- failure monitor (engine_monitor.cpp) ----
   bool monitored = false;  // cfg.monitor and world > 1
+  std::string mon_off_reason;
   std::mutex mu;           // everything below, shared by the two threads
   std::condition_variable cv;
   std::deque<Entry> inflight;                 // issue order

@@ -64,6 +64,29 @@ void nz_engine::calibrateClock() {
 void nz_engine::startMonitor() {
   monitored = cfg.monitor != 0 && comm->world > 1;
   if (!monitored) return;
+  // The stream gates are CUDA stream memory operations: check once that the
+  // driver takes them (a wait that is already satisfied, then a write) on
+  // every rank; without them the engine runs unmonitored (round-1 behaviour:
+  // a failed rail raises ChannelDownError at nz_engine_synchronize).
+  int32_t ok = 1;
+  {
+    nz_rail* r = rails.front();
+    const CUstream st = reinterpret_cast<CUstream>(ctrl);
+    if (!NZ_DRV(cuStreamWaitValue32) || !NZ_DRV(cuStreamWriteValue32) ||
+        NZ_DRV(cuStreamWaitValue32)(st, nz::railGateAddr(r), 0, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
+        NZ_DRV(cuStreamWriteValue32)(st, nz::railGateAddr(r), 0, 0) != CUDA_SUCCESS ||
+        cudaStreamSynchronize(ctrl) != cudaSuccess) {
+      ok = 0;
+      cudaGetLastError();
+    }
+  }
+  const auto all = nz::exchange(comm, &ok, sizeof(ok), {});
+  for (const auto& m : all) ok &= *reinterpret_cast<const int32_t*>(m.data.data());
+  if (!ok) {
+    monitored = false;
+    mon_off_reason = "CUDA stream memory operations unavailable";
+    return;
+  }
   for (auto& s : specs) twins.push_back(nz::railCreate(comm, s.kind, s.rail_id, s.sm_budget, false, true));
   for (size_t i = 0; i < twins.size(); ++i) twins[i]->detect_us = cfg.detect_us;
   mon = std::thread([this] { monitorLoop(); });
