@@ -121,7 +121,11 @@ struct nz_comm {
   nz_buf* ctrl = nullptr;  // barrier pads, one kPadBytes region per rail
   int next_pad = 0;
   std::vector<int> free_pads;  // returned by destroyed rails (same order on every rank)
-  int live_rails = 0;          // rails alive on this rank (loopback co-residency divisor)
+  // Rails alive on this rank: the loopback co-residency divisor is
+  // live_rails + (live_twins ? 1 : 0), since the engine's monitor runs one
+  // recovery (one twin grid) at a time.
+  int live_rails = 0;
+  int live_twins = 0;
 };
 
 struct nz_rail {

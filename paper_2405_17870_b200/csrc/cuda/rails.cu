@@ -204,8 +204,9 @@ void dispatchBarrier(int world, const BarrierKArgs& k, cudaStream_t st) {
 // Loopback: the last virtual rank to reach this launch runs one grid for all
 // of them (blockIdx.y = rank) on the pad's group stream, ordered after every
 // rank's stream and before each rank's next work. The grid is capped so that
-// every rail of the comm can have its grid resident at once: the cross-rank
-// waits inside are then between co-resident CTAs.
+// every rail of the comm (plus the one recovery twin that can be running)
+// can have its grid resident at once: the cross-rank waits inside are then
+// between co-resident CTAs, and no grid waits on another launch.
 template <typename A>
 void combine(nz_rail* r, int kind, int dtype, const A& a, int grid, cudaStream_t st) {
   nz_comm* c = r->comm;
@@ -234,7 +235,8 @@ void combine(nz_rail* r, int kind, int dtype, const A& a, int grid, cudaStream_t
       try {
         for (int p = 0; p < N; ++p) NZ_CUDA(cudaStreamWaitEvent(L.stream, L.ready[p], 0));
         const int occ = std::max(1, loopOccupancy(kind, N, dtype));
-        const int cap_ctas = std::max(1, occ * c->sm_count / (N * std::max(1, c->live_rails)));
+        const int slots = std::max(1, c->live_rails + (c->live_twins ? 1 : 0));
+        const int cap_ctas = std::max(1, occ * c->sm_count / (N * slots));
         std::pair<cudaEvent_t, cudaEvent_t>* tp = nullptr;
         if (L.timing) {
           if (L.tev_used == L.tev.size()) {
@@ -711,11 +713,11 @@ nz_rail* railCreate(nz_comm* comm, int kind, int rail_id, int sm_budget, bool gr
       r->lr = slot.get();
     }
   } catch (...) {
-    comm->live_rails++;  // railDestroy returns the pad and the count
+    (recovery ? comm->live_twins : comm->live_rails)++;  // railDestroy returns the pad and the count
     railDestroy(r);
     throw;
   }
-  comm->live_rails++;
+  (recovery ? comm->live_twins : comm->live_rails)++;
   return r;
 }
 
@@ -753,7 +755,8 @@ void railDestroy(nz_rail* r) {
   if (r->status_host) cudaFreeHost(r->status_host);
   if (r->ctl_dev) cudaFree(r->ctl_dev);
   comm->free_pads.push_back(r->pad);
-  comm->live_rails = std::max(0, comm->live_rails - 1);
+  int& live = r->recovery ? comm->live_twins : comm->live_rails;
+  live = std::max(0, live - 1);
   delete r;
 }
 
