@@ -74,7 +74,7 @@ void nz_engine::startMonitor() {
     const CUstream st = reinterpret_cast<CUstream>(ctrl);
     if (!NZ_DRV(cuStreamWaitValue32) || !NZ_DRV(cuStreamWriteValue32) ||
         NZ_DRV(cuStreamWaitValue32)(st, nz::railGateAddr(r), 0, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS ||
-        NZ_DRV(cuStreamWriteValue32)(st, nz::railGateAddr(r), 0, 0) != CUDA_SUCCESS ||
+        NZ_DRV(cuStreamWriteValue32)(st, nz::railGateAddr(r), r->tag, 0) != CUDA_SUCCESS ||
         cudaStreamSynchronize(ctrl) != cudaSuccess) {
       ok = 0;
       cudaGetLastError();

@@ -222,6 +222,7 @@ __device__ __forceinline__ void rail_exit(const RailCtl& c, bool ok) {
       st_release_sys(c.dev + kCtlGate, c.tag);
       if (h) h->ok_tag = c.tag;
     }
+    __threadfence_system();  // the mapped record is out before the launch counts as complete
   }
   atomicAdd(c.dev + kCtlSeq, 1u);
 }
