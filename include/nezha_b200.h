@@ -67,6 +67,10 @@ typedef struct nz_engine nz_engine_t;
 
 const char* nz_last_error(void);
 int nz_abi_version(void);
+/* sizeof of the ABI's structs for FFI bindings that lay them out themselves:
+ * "engine_config", "failover_report", "rail_status", "fault_record";
+ * NZ_ERR_INVALID for another name. */
+int nz_abi_sizeof(const char* type_name);
 /* 1 when this build contains the sm_100a kernels (always, for the product). */
 int nz_has_cuda_kernels(void);
 

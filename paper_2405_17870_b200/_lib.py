@@ -145,6 +145,7 @@ AGREE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, c_int, c_int, POINTER(c_int), POINT
 _SIGS = {
     "nz_last_error": (c_char_p, []),
     "nz_abi_version": (c_int, []),
+    "nz_abi_sizeof": (c_int, [c_char_p]),
     "nz_has_cuda_kernels": (c_int, []),
     "nz_comm_init": (c_int, [c_int, c_int, c_int, c_char_p, c_int, POINTER(c_void_p)]),
     "nz_comm_init_loopback": (c_int, [c_int, c_int, c_int, c_char_p, c_int, POINTER(c_void_p)]),

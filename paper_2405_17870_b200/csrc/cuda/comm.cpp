@@ -336,6 +336,16 @@ extern "C" {
 const char* nz_last_error(void) { return nz::lastError(); }
 int nz_abi_version(void) { return NZ_ABI_VERSION; }
 
+int nz_abi_sizeof(const char* type_name) {
+  if (!type_name) return NZ_ERR_INVALID;
+  const std::string n = type_name;
+  if (n == "engine_config") return static_cast<int>(sizeof(nz_engine_config_t));
+  if (n == "failover_report") return static_cast<int>(sizeof(nz_failover_report_t));
+  if (n == "rail_status") return static_cast<int>(sizeof(nz_rail_status_t));
+  if (n == "fault_record") return static_cast<int>(sizeof(nz_fault_record_t));
+  return NZ_ERR_INVALID;
+}
+
 int nz_comm_init(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out) {
   return nz::commInit(rank, world, device, session, timeout_ms, false, out);
 }

@@ -22,7 +22,8 @@ def test_header_declares_the_abi():
     names = declared_functions()
     for must in ("nz_comm_init", "nz_buffer_alloc", "nz_rail_create", "nz_rail_allreduce", "nz_rail_poll_fault",
                  "nz_engine_create", "nz_engine_allreduce", "nz_engine_allreduce_host", "nz_engine_inject_failure",
-                 "nz_planner_run_trace", "nz_core_ring_volume", "nz_last_error"):
+                 "nz_planner_run_trace", "nz_core_ring_volume", "nz_last_error", "nz_comm_init_loopback",
+                 "nz_rail_inject_stall", "nz_rail_status", "nz_rail_revive", "nz_engine_failover_get"):
         assert must in names
 
 
@@ -65,3 +66,28 @@ def test_sm100a_cubin_present():
     assert "sm_100a" in out
     sass = subprocess.run([tool, "-sass", LIB], capture_output=True, text=True).stdout
     assert "LDGMC" in sass or "multimem" in sass.lower()  # NVLS ld_reduce made it to SASS
+
+
+def test_ctypes_struct_layouts_match_the_header():
+    """The Python mirror lays the ABI structs out exactly as the library does."""
+    import ctypes
+
+    from paper_2405_17870_b200 import _lib, lib
+
+    l = lib()
+    for name, cls in (("engine_config", _lib.EngineConfig), ("failover_report", _lib.FailoverReport),
+                      ("rail_status", _lib.RailStatus), ("fault_record", _lib.FaultRecord)):
+        assert l.nz_abi_sizeof(name.encode()) == ctypes.sizeof(cls), name
+    assert l.nz_abi_sizeof(b"nope") < 0
+
+
+def test_engine_config_defaults():
+    """Round-2 defaults: failure monitor on, Timer lag 16, SPEC heartbeats
+    (50 ms) and readmit hold (1 s), profiles measured at startup."""
+    from paper_2405_17870_b200 import default_engine_config
+
+    c = default_engine_config()
+    assert (c.num_rails, list(c.kinds)) == (3, [0, 1, 2])
+    assert c.monitor == 1 and c.timer_lag == 16 and c.heartbeat_us == 50000 and c.readmit_hold_us == 1e6
+    assert c.detect_us == 0 and c.sync_overhead_us < 0 and c.window == 100 and c.tau == 5.0
+    assert c.graph_safe == 0 and c.compute_pool == 0 and c.tune_budgets == 0
