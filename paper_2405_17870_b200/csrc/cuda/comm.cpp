@@ -256,6 +256,35 @@ std::vector<Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std:
   return out;
 }
 
+bool peekExchange(nz_comm* c, int channel, std::vector<char>* data) {
+  if (c->world == 1) return false;
+  Channel& ch = c->chan[channel];
+  if (c->loop) {
+    LoopGroup& g = *c->loop;
+    std::lock_guard<std::mutex> lk(g.m);
+    for (int p = 0; p < c->world; ++p) {
+      if (p == c->rank) continue;
+      auto it = g.box.find({channel, ch.seq, p});
+      if (it != g.box.end()) {
+        *data = it->second;
+        return true;
+      }
+    }
+    return false;
+  }
+  while (receiveOne(ch, 0)) {
+  }
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) continue;
+    auto it = ch.stash.find({ch.seq, p});
+    if (it != ch.stash.end()) {
+      *data = it->second.data;
+      return true;
+    }
+  }
+  return false;
+}
+
 namespace {
 
 int commInit(int rank, int world, int device, const char* session, int timeout_ms, bool loopback, nz_comm_t** out) {

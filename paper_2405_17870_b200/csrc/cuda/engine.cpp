@@ -133,6 +133,7 @@ void nz_engine::launchSegment(uint32_t seq, const nezha::Plan& plan, const nezha
   e.chunk = C;
   e.chunk_end = (o.seg_len + C - 1) / C;
   e.dtype = dtype;
+  e.ll = nz::railLLPath(r, o.seg_off, o.seg_len);
   e.plan = plan;
   {
     std::lock_guard<std::mutex> lk(mu);

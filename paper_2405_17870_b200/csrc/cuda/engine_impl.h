@@ -49,6 +49,7 @@ struct nz_engine {
     nz_buf* out = nullptr;
     uint64_t seg_off = 0, seg_len = 0, chunk = 0, chunk_end = 0;
     int dtype = NZ_F32;
+    bool ll = false;  // one-shot LL path (no end barrier: a timeout does not imply the others' data)
     nezha::Plan plan;
     cudaEvent_t end = nullptr;
   };
@@ -132,6 +133,7 @@ struct nz_engine {
   bool mon_stop = false;
   std::string mon_error;                      // surfaced at the next synchronize
   std::vector<nz_failover_report_t> reports;  // every failover, in order
+  std::deque<Entry> retired_ok;               // recent successes (a peer may ask about them)
   std::thread mon;
   uint64_t* rec_stamps_host = nullptr;  // [0] resume, [1] done of the current reroute
   uint64_t* rec_stamps_dev = nullptr;
@@ -206,9 +208,12 @@ struct nz_engine {
   void startMonitor();
   void stopMonitor();
   void monitorLoop();
-  // Handles the failed front entry: agreement on the orphan, P9 target,
-  // reroute on the target's twin, gate release, report.
-  void failover(Entry e, int64_t seen_ns);
+  // The agreement on an entry that failed on this rank (ok_here = false) or
+  // that a peer reported failed while it succeeded here (ok_here = true):
+  // orphan, P9 target, reroute on the target's twin, gate release, report.
+  void failover(Entry e, int64_t seen_ns, bool ok_here);
+  // Joins a peer's agreement on an entry this rank already retired.
+  void serviceRequests();
   // Applies agreed table events due before planning op `seq` (issuing thread).
   void applyTableEvents(uint32_t seq);
   // Waits until every entry issued so far retired or was rerouted.

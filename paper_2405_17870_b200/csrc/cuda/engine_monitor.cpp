@@ -36,6 +36,8 @@ struct AgreeMsg {
   uint64_t prog;    // chunks [0, prog) of the segment complete on this rank
   int64_t t_fail;   // host-clock ns of this rank's link death, 0 = none
   int64_t t_det;    // host-clock ns of this rank's device-side detection, 0 = none
+  int32_t ok;       // the entry succeeded on this rank (it joined a peer's agreement)
+  int32_t pad;
 };
 
 double nowUs() {
@@ -141,6 +143,12 @@ void nz_engine::monitorLoop() {
         front = inflight.front();
       }
     }
+    try {
+      serviceRequests();
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> lk(mu);
+      if (mon_error.empty()) mon_error = e.what();
+    }
     if (!front.end) {  // idle: re-anchor %globaltimer against the host clock
       try {
         calibrateClock();
@@ -176,8 +184,13 @@ void nz_engine::monitorLoop() {
           }
           health->heartbeat(specs[i].rail_id, now);
         }
+        // A two-shot launch left by its rank at the start barrier cannot
+        // complete anywhere (this rank never reaches the end barrier), so the
+        // abort keeps the ranks' outcomes equal; an LL launch is never
+        // aborted on a heartbeat (see kernels.cuh ll_body).
         for (int id : health->tick(now))
-          if (health->state(id).status == nezha::HealthStatus::Failed) aborted.push_back(id);
+          if (health->state(id).status == nezha::HealthStatus::Failed && !(id == specs[front.rail].rail_id && front.ll))
+            aborted.push_back(id);
       }
       for (int id : aborted) reinterpret_cast<volatile nz_rail_status_t*>(rails[index(id)]->status_host)->abort = 1;
       if (started) {
@@ -200,7 +213,7 @@ void nz_engine::monitorLoop() {
     const bool ok = static_cast<int32_t>(st->ok_tag - front.tag) >= 0;
     if (!ok) {
       try {
-        failover(front, seen);
+        failover(front, seen, false);
       } catch (const std::exception& e) {
         // The caller's stream must not stay gated: release it, report at sync.
         NZ_DRV(cuStreamWriteValue32)(reinterpret_cast<CUstream>(ctrl), nz::railGateAddr(rails[front.rail]), front.tag, 0);
@@ -212,6 +225,9 @@ void nz_engine::monitorLoop() {
     } else {
       std::lock_guard<std::mutex> lk(mu);
       health->heartbeat(specs[front.rail].rail_id, nowUs());
+      retired_ok.push_back(front);
+      retired_ok.back().end = nullptr;
+      if (retired_ok.size() > 4096) retired_ok.pop_front();
     }
     {
       std::lock_guard<std::mutex> lk(mu);
@@ -222,7 +238,32 @@ void nz_engine::monitorLoop() {
   }
 }
 
-void nz_engine::failover(Entry e, int64_t seen_ns) {
+void nz_engine::serviceRequests() {
+  std::vector<char> req;
+  while (nz::peekExchange(comm, nz::kChanMonitor, &req)) {
+    AgreeMsg m{};
+    if (req.size() != sizeof(m)) fail(NZ_ERR_SYSTEM, "monitor agreement: bad request");
+    std::memcpy(&m, req.data(), sizeof(m));
+    Entry hit;
+    bool found = false;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto it = retired_ok.rbegin(); it != retired_ok.rend(); ++it) {
+        if (it->op == m.op && specs[it->rail].rail_id == m.rail_id && it->tag == m.tag) {
+          hit = *it;
+          found = true;
+          break;
+        }
+      }
+    }
+    // Not retired here yet: this rank reaches the entry in issue order and
+    // joins then (as a failure of its own, or from the history).
+    if (!found) return;
+    failover(hit, realtimeNs(), true);
+  }
+}
+
+void nz_engine::failover(Entry e, int64_t seen_ns, bool ok_here) {
   nz_rail* fr = rails[e.rail];
   const int rail_id = specs[e.rail].rail_id;
   const volatile nz_rail_status_t* st = fr->status_host;
@@ -230,9 +271,14 @@ void nz_engine::failover(Entry e, int64_t seen_ns) {
   mine.op = e.op;
   mine.rail_id = rail_id;
   mine.tag = e.tag;
-  mine.prog = st->prog_tag == e.tag ? std::min<uint64_t>(static_cast<uint64_t>(st->prog_chunk), e.chunk_end) : 0;
-  mine.t_fail = st->fail_tag == e.tag && st->t_fail_ns ? static_cast<int64_t>(st->t_fail_ns) - clock_offset_ns : 0;
-  mine.t_det = st->det_tag == e.tag && st->t_det_ns ? static_cast<int64_t>(st->t_det_ns) - clock_offset_ns : 0;
+  mine.ok = ok_here ? 1 : 0;
+  if (ok_here) {
+    mine.prog = e.chunk_end;
+  } else {
+    mine.prog = st->prog_tag == e.tag ? std::min<uint64_t>(static_cast<uint64_t>(st->prog_chunk), e.chunk_end) : 0;
+    mine.t_fail = st->fail_tag == e.tag && st->t_fail_ns ? static_cast<int64_t>(st->t_fail_ns) - clock_offset_ns : 0;
+    mine.t_det = st->det_tag == e.tag && st->t_det_ns ? static_cast<int64_t>(st->t_det_ns) - clock_offset_ns : 0;
+  }
   {
     std::lock_guard<std::mutex> lk(mu);
     agreeing = true;  // planning waits: the table switch lands at an op index every rank agrees on
@@ -242,6 +288,7 @@ void nz_engine::failover(Entry e, int64_t seen_ns) {
   uint64_t k = mine.prog;
   uint32_t activation = mine.issued;
   int64_t t_fail = 0, t_det_first = 0;
+  int oks = 0;
   for (const auto& m : msgs) {
     AgreeMsg o{};
     if (m.data.size() != sizeof(o)) fail(NZ_ERR_SYSTEM, "monitor agreement: bad message");
@@ -251,10 +298,15 @@ void nz_engine::failover(Entry e, int64_t seen_ns) {
                               " rail " + std::to_string(rail_id) + " vs op " + std::to_string(o.op) + " rail " +
                               std::to_string(o.rail_id) + ")");
     k = std::min(k, o.prog);
+    oks += o.ok;
     if (static_cast<int32_t>(o.issued - activation) > 0) activation = o.issued;
     if (o.t_fail && (!t_fail || o.t_fail < t_fail)) t_fail = o.t_fail;
     if (o.t_det && (!t_det_first || o.t_det < t_det_first)) t_det_first = o.t_det;
   }
+  // Every rank takes the same decision from the same messages: the rail is
+  // failed by agreement from `activation` on, and its launches on this rank
+  // stop waiting from now on (abort), so launches already issued on it fail
+  // on every rank alike.
   std::vector<int> healthy;
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -267,6 +319,31 @@ void nz_engine::failover(Entry e, int64_t seen_ns) {
       if (!agreed_failed.count(s.rail_id)) healthy.push_back(s.rail_id);
   }
   cv.notify_all();
+  reinterpret_cast<volatile nz_rail_status_t*>(fr->status_host)->abort = 1;
+  nz_failover_report_t rep{};
+  rep.op_seq = e.op;
+  rep.failed_rail = rail_id;
+  rep.target_rail = -1;
+  rep.orphan_offset = e.seg_off + e.seg_len;
+  rep.stalled_here = mine.t_fail ? 1 : 0;
+  if (oks > 0) {
+    // Some rank passed the op's end barrier: every rank had arrived, i.e.
+    // every store of the op landed everywhere (two-shot, NVLS, CE). Nothing
+    // to reroute; the ranks that gave up early just release their callers.
+    // The LL path folds locally after its last wait, so there a rank that
+    // gave up still lacks its sum: that mix is reported, not hidden.
+    if (!ok_here) {
+      NZ_CU(NZ_DRV(cuStreamWriteValue32)(reinterpret_cast<CUstream>(ctrl), nz::railGateAddr(fr), e.tag, 0));
+      NZ_CUDA(cudaStreamSynchronize(ctrl));
+      if (e.ll)
+        fail(NZ_ERR_UNRECOVERABLE, "op " + std::to_string(e.op) + ": LL path on rail " + std::to_string(rail_id) +
+                                       " completed on some ranks only (a peer came back after the watchdog)");
+    }
+    rep.orphan_chunk = e.chunk_end;
+    std::lock_guard<std::mutex> lk(mu);
+    reports.push_back(rep);
+    return;
+  }
   const auto target = nezha::chooseHandoffTarget(e.plan, rail_id, healthy);
   if (!target) fail(NZ_ERR_UNRECOVERABLE, "no surviving rail to take over the orphaned segment");
   nz_rail* tw = twins[index(*target)];
@@ -297,14 +374,10 @@ void nz_engine::failover(Entry e, int64_t seen_ns) {
   NZ_CUDA(cudaStreamSynchronize(tw->stream));
   if (tag2 && static_cast<int32_t>(tw->status_host->ok_tag - tag2) < 0)
     fail(NZ_ERR_UNRECOVERABLE, "the reroute of op " + std::to_string(e.op) + " failed on rail " + std::to_string(*target));
-  nz_failover_report_t rep{};
-  rep.op_seq = e.op;
-  rep.failed_rail = rail_id;
   rep.target_rail = *target;
   rep.orphan_offset = orphan.offset;
   rep.orphan_length = orphan.length;
   rep.orphan_chunk = k;
-  rep.stalled_here = mine.t_fail ? 1 : 0;
   // All times on the shared host clock (each rank maps its %globaltimer).
   const double f = static_cast<double>(t_fail ? t_fail : (t_det_first ? t_det_first : seen_ns));
   const double resume = static_cast<double>(static_cast<int64_t>(stamps[0]) - clock_offset_ns);

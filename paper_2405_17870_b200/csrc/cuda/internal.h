@@ -223,6 +223,9 @@ struct LoopRail {
 // messages indexed by rank (own message included, fds only from peers).
 std::vector<Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std::vector<int>& fds,
                           int channel = kChanMain);
+// Non-blocking: true (and one peer's blob) when a peer already entered the
+// channel's next exchange, i.e. it waits for this rank to join it.
+bool peekExchange(nz_comm* c, int channel, std::vector<char>* data);
 nz_buf* allocSymmetric(nz_comm* c, size_t bytes);
 void freeSymmetric(nz_buf* b);
 int elemSizeOf(int dtype);
@@ -290,6 +293,8 @@ void railDestroy(nz_rail* r);
 // The rail's gate word (device memory, for cuStreamWaitValue32 /
 // cuStreamWriteValue32) and its reset after a failure (sticky, abort).
 CUdeviceptr railGateAddr(nz_rail* r);
+// Whether a call over this segment runs the one-shot LL path.
+bool railLLPath(nz_rail* r, uint64_t seg_off, uint64_t seg_len);
 void railRevive(nz_rail* r, cudaStream_t st);
 
 // rails_vr.cu: the virtual-rank (loopback) grids.

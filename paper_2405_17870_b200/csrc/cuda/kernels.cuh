@@ -611,7 +611,7 @@ struct LLArgs {
   uint64_t timeout_ns;
   FaultPost post;
   const uint32_t* seq;              // graph-safe rails: flag / parity from the device launch counter
-  const volatile uint32_t* abort;   // host-mapped monitor abort
+  const volatile uint32_t* abort;   // host-mapped; set only once the ranks agreed the rail failed
   RailCtl ctl;
 };
 
@@ -694,7 +694,13 @@ __device__ __forceinline__ void ll_body(const LLArgs& a) {
                    : "memory");
     }
   }
-  bool bail = false;  // a peer's words never arrived (watchdog / monitor abort)
+  // A peer's words never arrived (watchdog), or the ranks already agreed
+  // that the rail failed (abort). The monitor never aborts an LL wait on a
+  // heartbeat alone: a rank leaving early has pushed its own words, so a late
+  // peer could still complete the op while this rank's output stays unfolded.
+  // After an agreement some rank's launches on the rail exit at entry, so no
+  // rank can complete a later LL op and leaving is consistent.
+  bool bail = false;
   for (uint64_t w = tid; w < a.words && !bail; w += stride) {
     uint32_t v[N];
 #pragma unroll

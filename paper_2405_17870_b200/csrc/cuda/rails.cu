@@ -61,12 +61,13 @@ uint64_t watchdogNs() {
 
 // End-barrier budget: every rank passed the start barrier of the same op and
 // does the same work, so a peer missing for much longer than the op itself
-// takes has lost its link. max(floor, 2 x range / 100 GB/s),
-// floor NEZHA_DETECT_US (2000 us) or the rail's / engine's setting.
+// takes has lost its link. max(floor, 4 x range / 100 GB/s),
+// floor NEZHA_DETECT_US (5000 us) or the rail's / engine's setting: generous
+// against a slow-but-alive peer, still far below SPEC's 200 ms.
 uint64_t detectNs(const nz_rail* r, uint64_t range_bytes) {
-  static const double env_us = static_cast<double>(envLL("NEZHA_DETECT_US", 2000));
+  static const double env_us = static_cast<double>(envLL("NEZHA_DETECT_US", 5000));
   const double floor_us = r->detect_us > 0 ? r->detect_us : env_us;
-  const double scaled_us = 2.0 * static_cast<double>(range_bytes) / 100e9 * 1e6;
+  const double scaled_us = 4.0 * static_cast<double>(range_bytes) / 100e9 * 1e6;
   return static_cast<uint64_t>(std::max(floor_us, scaled_us) * 1000.0);
 }
 
@@ -616,6 +617,8 @@ int railComputeCtas(nz_rail* r, uint64_t seg_len) {
   if (r->kind == NZ_RAIL_SM) return smGrid(r, 0, seg_len);
   return gridFor(r, seg_len, r->comm->world, r->kind == NZ_RAIL_NVLS ? 4 : 2);
 }
+
+bool railLLPath(nz_rail* r, uint64_t seg_off, uint64_t seg_len) { return llPath(r, seg_off, seg_off + seg_len); }
 
 CUdeviceptr railGateAddr(nz_rail* r) { return reinterpret_cast<CUdeviceptr>(r->ctl_dev + kCtlGate); }
 
