@@ -509,6 +509,7 @@ void railWave(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, con
 
 // Orders a launch on `st` after the rail's previous launch on another stream.
 void orderOn(nz_rail* r, cudaStream_t st) {
+  if (st == r->last_stream) return;  // the common case: stream order already holds
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   NZ_CUDA(cudaStreamIsCapturing(st, &cap));
   if (cap != cudaStreamCaptureStatusNone) {
