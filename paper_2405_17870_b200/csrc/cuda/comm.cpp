@@ -256,7 +256,8 @@ std::vector<Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std:
   return out;
 }
 
-bool peekExchange(nz_comm* c, int channel, std::vector<char>* data) {
+bool peekExchange(nz_comm* c, int channel, std::vector<std::vector<char>>* blobs) {
+  blobs->clear();
   if (c->world == 1) return false;
   Channel& ch = c->chan[channel];
   if (c->loop) {
@@ -265,24 +266,18 @@ bool peekExchange(nz_comm* c, int channel, std::vector<char>* data) {
     for (int p = 0; p < c->world; ++p) {
       if (p == c->rank) continue;
       auto it = g.box.find({channel, ch.seq, p});
-      if (it != g.box.end()) {
-        *data = it->second;
-        return true;
-      }
+      if (it != g.box.end()) blobs->push_back(it->second);
     }
-    return false;
+    return !blobs->empty();
   }
   while (receiveOne(ch, 0)) {
   }
   for (int p = 0; p < c->world; ++p) {
     if (p == c->rank) continue;
     auto it = ch.stash.find({ch.seq, p});
-    if (it != ch.stash.end()) {
-      *data = it->second.data;
-      return true;
-    }
+    if (it != ch.stash.end()) blobs->push_back(it->second.data);
   }
-  return false;
+  return !blobs->empty();
 }
 
 namespace {

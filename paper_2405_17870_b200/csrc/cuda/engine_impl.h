@@ -208,10 +208,11 @@ struct nz_engine {
   void startMonitor();
   void stopMonitor();
   void monitorLoop();
-  // The agreement on an entry that failed on this rank (ok_here = false) or
-  // that a peer reported failed while it succeeded here (ok_here = true):
-  // orphan, P9 target, reroute on the target's twin, gate release, report.
-  void failover(Entry e, int64_t seen_ns, bool ok_here);
+  // One agreement (two rounds on the monitor channel): the ranks propose
+  // their failed front entry (`own`, or nullptr when joining a peer), settle
+  // the earliest proposed one — orphan, P9 target, reroute on the target's
+  // twin, gate release, report — and return whether it was `own`.
+  bool failover(const Entry* own, int64_t seen_ns);
   // Joins a peer's agreement on an entry this rank already retired.
   void serviceRequests();
   // Applies agreed table events due before planning op `seq` (issuing thread).

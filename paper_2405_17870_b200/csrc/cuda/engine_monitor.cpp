@@ -28,6 +28,19 @@ using nz::fail;
 
 namespace {
 
+// Round 1 of an agreement: the entry this rank wants agreed (its failed
+// front), or none (it joins a peer's request). The subject is the earliest
+// proposed entry in issue order (op, then rail order).
+struct Proposal {
+  uint32_t op;
+  int32_t rail_index;
+  int32_t rail_id;
+  uint32_t tag;
+  int32_t valid;
+  int32_t pad;
+};
+
+// Round 2: this rank's outcome of the subject.
 struct AgreeMsg {
   uint32_t op;
   int32_t rail_id;
@@ -213,7 +226,10 @@ void nz_engine::monitorLoop() {
     const bool ok = static_cast<int32_t>(st->ok_tag - front.tag) >= 0;
     if (!ok) {
       try {
-        failover(front, seen, false);
+        // Agreements run in issue order: an earlier entry a peer proposes is
+        // settled first, then this one is proposed again.
+        while (!failover(&front, seen)) {
+        }
       } catch (const std::exception& e) {
         // The caller's stream must not stay gated: release it, report at sync.
         NZ_DRV(cuStreamWriteValue32)(reinterpret_cast<CUstream>(ctrl), nz::railGateAddr(rails[front.rail]), front.tag, 0);
@@ -239,31 +255,72 @@ void nz_engine::monitorLoop() {
 }
 
 void nz_engine::serviceRequests() {
-  std::vector<char> req;
-  while (nz::peekExchange(comm, nz::kChanMonitor, &req)) {
-    AgreeMsg m{};
-    if (req.size() != sizeof(m)) fail(NZ_ERR_SYSTEM, "monitor agreement: bad request");
-    std::memcpy(&m, req.data(), sizeof(m));
-    Entry hit;
-    bool found = false;
-    {
+  std::vector<std::vector<char>> reqs;
+  while (nz::peekExchange(comm, nz::kChanMonitor, &reqs)) {
+    // Join only once this rank retired a proposed entry: then it can answer
+    // for it and for any earlier entry (all retired here, and every one that
+    // failed here was agreed before). Otherwise it reaches the entry in issue
+    // order and proposes or joins then.
+    bool past = false;
+    for (const auto& req : reqs) {
+      Proposal m{};
+      if (req.size() != sizeof(m)) fail(NZ_ERR_SYSTEM, "monitor agreement: bad request");
+      std::memcpy(&m, req.data(), sizeof(m));
+      if (!m.valid) continue;
       std::lock_guard<std::mutex> lk(mu);
-      for (auto it = retired_ok.rbegin(); it != retired_ok.rend(); ++it) {
-        if (it->op == m.op && specs[it->rail].rail_id == m.rail_id && it->tag == m.tag) {
-          hit = *it;
-          found = true;
-          break;
-        }
-      }
+      for (auto it = retired_ok.rbegin(); it != retired_ok.rend() && !past; ++it)
+        past = it->op == m.op && it->rail == m.rail_index && it->tag == m.tag;
     }
-    // Not retired here yet: this rank reaches the entry in issue order and
-    // joins then (as a failure of its own, or from the history).
-    if (!found) return;
-    failover(hit, realtimeNs(), true);
+    if (!past) return;
+    failover(nullptr, realtimeNs());
   }
 }
 
-void nz_engine::failover(Entry e, int64_t seen_ns, bool ok_here) {
+bool nz_engine::failover(const Entry* own, int64_t seen_ns) {
+  Proposal prop{};
+  if (own) {
+    prop.op = own->op;
+    prop.rail_index = own->rail;
+    prop.rail_id = specs[own->rail].rail_id;
+    prop.tag = own->tag;
+    prop.valid = 1;
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    agreeing = true;  // planning waits: the table switch lands at an op index every rank agrees on
+  }
+  const auto props = nz::exchange(comm, &prop, sizeof(prop), {}, nz::kChanMonitor);
+  Proposal subj{};
+  for (const auto& m : props) {
+    Proposal o{};
+    if (m.data.size() != sizeof(o)) fail(NZ_ERR_SYSTEM, "monitor agreement: bad proposal");
+    std::memcpy(&o, m.data.data(), sizeof(o));
+    if (!o.valid) continue;
+    if (!subj.valid || static_cast<int32_t>(o.op - subj.op) < 0 || (o.op == subj.op && o.rail_index < subj.rail_index))
+      subj = o;
+  }
+  if (!subj.valid) fail(NZ_ERR_SYSTEM, "monitor agreement: nobody proposed an entry");
+  const bool mine_is_subject = own && own->op == subj.op && own->rail == subj.rail_index && own->tag == subj.tag;
+  Entry e;
+  bool ok_here = false;
+  if (mine_is_subject) {
+    e = *own;
+  } else {
+    bool found = false;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto it = retired_ok.rbegin(); it != retired_ok.rend() && !found; ++it) {
+        if (it->op == subj.op && it->rail == subj.rail_index && it->tag == subj.tag) {
+          e = *it;
+          found = true;
+        }
+      }
+    }
+    if (!found)
+      fail(NZ_ERR_SYSTEM, "monitor agreement: op " + std::to_string(subj.op) + " rail " + std::to_string(subj.rail_id) +
+                              " is neither this rank's failure nor among its retired successes");
+    ok_here = true;
+  }
   nz_rail* fr = rails[e.rail];
   const int rail_id = specs[e.rail].rail_id;
   const volatile nz_rail_status_t* st = fr->status_host;
@@ -281,7 +338,6 @@ void nz_engine::failover(Entry e, int64_t seen_ns, bool ok_here) {
   }
   {
     std::lock_guard<std::mutex> lk(mu);
-    agreeing = true;  // planning waits: the table switch lands at an op index every rank agrees on
     mine.issued = issued;
   }
   const auto msgs = nz::exchange(comm, &mine, sizeof(mine), {}, nz::kChanMonitor);
@@ -342,7 +398,7 @@ void nz_engine::failover(Entry e, int64_t seen_ns, bool ok_here) {
     rep.orphan_chunk = e.chunk_end;
     std::lock_guard<std::mutex> lk(mu);
     reports.push_back(rep);
-    return;
+    return mine_is_subject;
   }
   const auto target = nezha::chooseHandoffTarget(e.plan, rail_id, healthy);
   if (!target) fail(NZ_ERR_UNRECOVERABLE, "no surviving rail to take over the orphaned segment");
@@ -390,6 +446,7 @@ void nz_engine::failover(Entry e, int64_t seen_ns, bool ok_here) {
   rep.resume_after_detect_us = (resume - static_cast<double>(seen_ns)) / 1000.0;
   std::lock_guard<std::mutex> lk(mu);
   reports.push_back(rep);
+  return mine_is_subject;
 }
 
 void nz_engine::readmit(int rail_id) {

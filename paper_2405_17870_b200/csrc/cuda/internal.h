@@ -223,9 +223,9 @@ struct LoopRail {
 // messages indexed by rank (own message included, fds only from peers).
 std::vector<Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std::vector<int>& fds,
                           int channel = kChanMain);
-// Non-blocking: true (and one peer's blob) when a peer already entered the
-// channel's next exchange, i.e. it waits for this rank to join it.
-bool peekExchange(nz_comm* c, int channel, std::vector<char>* data);
+// Non-blocking: true (and the blobs of the peers that did) when a peer
+// already entered the channel's next exchange, i.e. waits for this rank.
+bool peekExchange(nz_comm* c, int channel, std::vector<std::vector<char>>* blobs);
 nz_buf* allocSymmetric(nz_comm* c, size_t bytes);
 void freeSymmetric(nz_buf* b);
 int elemSizeOf(int dtype);
