@@ -273,16 +273,16 @@ def test_loopback_engine_unplanned_failover(fail_rail):
         assert fo["target_rail"] != fail_rail and fo["orphan_length"] > 0
         assert fo["stalled_here"] == (1 if rk["rank"] == world - 1 else 0), fo
         assert fo["resume_after_detect_us"] > 0 and fo["done_us"] > fo["resume_us"] > 0, fo
+        later = [r for r in rk["results"] if r["case"] == 0 and r["rep"] == 2] + \
+                [r for r in rk["results"] if r["case"] == 1]
+        for r in later:
+            assert all(s[0] != fail_rail for s in r["segs"]), r
     # Reroute within 1 ms of detection. With virtual ranks every rank's issuing
     # and monitor threads share this host's cores (2 x world spinning threads
     # on 8 cores), so one rank's monitor can be descheduled for a time slice:
     # the median rank must make it, every rank within 5 ms.
     ra = sorted(rk["results"][1]["failover"]["resume_after_detect_us"] for rk in res)
     assert ra[len(ra) // 2] < 1000 and ra[-1] < 5000, ra
-        later = [r for r in rk["results"] if r["case"] == 0 and r["rep"] == 2] + \
-                [r for r in rk["results"] if r["case"] == 1]
-        for r in later:
-            assert all(s[0] != fail_rail for s in r["segs"]), r
     # Identical reports on every rank (the agreement), timings aside.
     keys = ("op_seq", "failed_rail", "target_rail", "orphan_offset", "orphan_length", "orphan_chunk")
     reps = [tuple(rk["results"][1]["failover"][k] for k in keys) for rk in res]
