@@ -279,10 +279,21 @@ def main():
     from tests.workers import engine_worker, rail_worker
     import tests.test_gpu_loopback as T
 
-    for mod in (rail_worker, engine_worker):
-        mod.Rail = FakeRail if hasattr(mod, "Rail") else None
-        mod.SymmetricBuffer = FakeBuffer
-        mod.Engine = FakeEngine
+    saved = {(m, n): getattr(m, n) for m in (rail_worker, engine_worker) for n in ("Rail", "SymmetricBuffer", "Engine")
+             if hasattr(m, n)}
+    for (m, n) in saved:
+        setattr(m, n, {"Rail": FakeRail, "SymmetricBuffer": FakeBuffer, "Engine": FakeEngine}[n])
+    try:
+        _dry(rail_worker, engine_worker, T)
+    finally:
+        for (m, n), v in saved.items():  # the real objects again for anything running after this
+            setattr(m, n, v)
+        rail_worker.clear_cache()
+        engine_worker.clear_cache()
+    print("dry run ok")
+
+
+def _dry(rail_worker, engine_worker, T):
     # rail parity cases (the abort case recreates rails)
     for world in (2, 4):
         res = run_ranks(world, lambda c: rail_worker.run(c, [x for x in T.RAIL_CASES if x["nbytes"] <= (8 << 20)]))
@@ -308,7 +319,6 @@ def main():
             assert r["mismatch"] == 0, r
     fo = [r for r in res[0]["results"] if "failover" in r][0]["failover"]
     assert fo and fo["failed_rail"] == 1, fo
-    print("dry run ok")
 
 
 if __name__ == "__main__":
