@@ -458,8 +458,7 @@ void nz_engine::readmit(int rail_id) {
   }
   if (!monitored && bal->healthy(rail_id)) fail(NZ_ERR_INVALID, "readmit: rail is not failed");
   nz_rail* r = rails[idx];
-  nz::railRevive(r, nullptr);
-  if (idx < static_cast<int>(twins.size())) nz::railRevive(twins[idx], nullptr);
+  nz::railRevive(r, nullptr);  // its twin is the monitor's and never failed with it
   // the rail must keep beating for the hold period before it
   // carries data again. A beat is a probe allreduce on the rail that
   // succeeded on every rank.
