@@ -334,13 +334,34 @@ int gated(int grid, const ComputeGate* gate) {
   return gate && gate->max_ctas > 0 ? std::max(1, std::min(grid, gate->max_ctas)) : grid;
 }
 
-// Pieces of a CE shard pipelined through gather / fold / scatter: the gather
-// of piece i+1 (inbound NVLink) overlaps the fold of piece i and the scatter
-// of piece i-1 (outbound), so both link directions work at once.
-int cePieces(uint64_t shard) {
+// Pieces of a CE shard [s, e) pipelined through gather / fold / scatter:
+// the gather of piece i+1 (inbound NVLink) overlaps the fold of piece i and
+// the scatter of piece i-1 (outbound), so both link directions work at once.
+// RingChunked ("transmission of chunk k+1 overlaps reduction
+// of chunk k"): the pieces are the shard cut at the segment's chunk
+// boundaries (rounded to 16 bytes for the vector fold; pieces under 256 KiB
+// join their neighbour). Ring (one chunk): clamp(shard / 4 MiB, 1, 4) equal
+// pieces. NEZHA_CE_PIECES forces an equal-piece count (sweeps).
+std::vector<uint64_t> cePieces(uint64_t s, uint64_t e, const Geometry& g) {
+  std::vector<uint64_t> cut{s};
+  const uint64_t s16 = s & ~15ull;
   const long long env = envLL("NEZHA_CE_PIECES", 0);
-  if (env > 0) return static_cast<int>(std::min<long long>(env, 8));
-  return static_cast<int>(std::clamp<uint64_t>(shard / (uint64_t{4} << 20), 1, 4));
+  constexpr uint64_t kMinPiece = uint64_t{256} << 10;
+  if (env <= 0 && g.chunk < g.seg_len) {
+    for (uint64_t b = g.seg_off + ((s - g.seg_off) / g.chunk + 1) * g.chunk; b < e; b += g.chunk) {
+      const uint64_t c = b & ~15ull;
+      if (c > cut.back() && c - cut.back() >= kMinPiece && e - c >= kMinPiece) cut.push_back(c);
+    }
+  } else {
+    const uint64_t P = env > 0 ? static_cast<uint64_t>(std::min<long long>(env, 8))
+                               : std::clamp<uint64_t>((e - s) / (uint64_t{4} << 20), 1, 4);
+    for (uint64_t i = 1; i < P; ++i) {
+      const uint64_t c = std::max<uint64_t>(s, (s16 + (e - s16) * i / P) & ~15ull);
+      if (c > cut.back() && c < e) cut.push_back(c);
+    }
+  }
+  cut.push_back(e);
+  return cut;
 }
 
 // One launch sequence of a rail over [lo, hi) with order geometry g.
@@ -455,11 +476,8 @@ void railWave(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, con
       std::lock_guard<std::mutex> lk(g_retired_mu);
       ensureStaging(r, e - s16, st, &g_retired[r]);
     }
-    const int P = cePieces(len);
-    std::vector<uint64_t> cut(P + 1);
-    cut[0] = s;
-    cut[P] = e;
-    for (int i = 1; i < P; ++i) cut[i] = std::max<uint64_t>(s, (s16 + (e - s16) * i / P) & ~15ull);
+    const std::vector<uint64_t> cut = cePieces(s, e, g);
+    const int P = static_cast<int>(cut.size()) - 1;
     const int peers = N - 1;  // side[0 .. peers) gather, side[peers .. 2 peers) scatter
     NZ_CUDA(cudaEventRecord(r->fork, st));
     for (int j = 0; j < 2 * peers; ++j) NZ_CUDA(cudaStreamWaitEvent(r->side[j], r->fork, 0));
