@@ -81,6 +81,16 @@ std::vector<std::pair<std::uint64_t, std::uint64_t>> waveRanges(Bytes chunk_byte
 std::uint64_t completedBeforeStall(Bytes chunk_bytes, std::uint64_t cb, std::uint64_t ce, std::uint64_t stall,
                                    Bytes wave_bytes = kDefaultWaveBytes);
 
+// Cut points of the copy-engine rail's gather / reduce / scatter pipeline
+// over a rank's shard [s, e) of a segment with geometry g:
+// chunked geometry (chunk_bytes < seg_length, RingChunked) — the shard cut at
+// the chunk boundaries rounded down to 16 bytes, no piece under 256 KiB;
+// one chunk (Ring) or `equal_pieces` > 0 — that many (default
+// clamp(len / 4 MiB, 1, 4)) equal 16-byte-aligned pieces. Returns
+// {s, cut_1, ..., e}, strictly increasing.
+std::vector<std::uint64_t> pipelineCuts(std::uint64_t s, std::uint64_t e, const ChunkGeometry& g,
+                                        int equal_pieces = 0);
+
 // Pieces of the host-memory allreduce pipeline (nz_engine_allreduce_host,
 // DESIGN.md §4c): below 8 MiB one piece; else pieces of
 // clamp(roundup(S / 16, 64 KiB), 4 MiB, 64 MiB), the last one shorter.

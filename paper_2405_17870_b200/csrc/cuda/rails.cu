@@ -337,31 +337,12 @@ int gated(int grid, const ComputeGate* gate) {
 // Pieces of a CE shard [s, e) pipelined through gather / fold / scatter:
 // the gather of piece i+1 (inbound NVLink) overlaps the fold of piece i and
 // the scatter of piece i-1 (outbound), so both link directions work at once.
-// RingChunked ("transmission of chunk k+1 overlaps reduction
-// of chunk k"): the pieces are the shard cut at the segment's chunk
-// boundaries (rounded to 16 bytes for the vector fold; pieces under 256 KiB
-// join their neighbour). Ring (one chunk): clamp(shard / 4 MiB, 1, 4) equal
-// pieces. NEZHA_CE_PIECES forces an equal-piece count (sweeps).
+// Under RingChunked the pieces are the chunks (transmission
+// of chunk k+1 overlaps reduction of chunk k); nezha::pipelineCuts.
+// NEZHA_CE_PIECES forces an equal-piece count (sweeps).
 std::vector<uint64_t> cePieces(uint64_t s, uint64_t e, const Geometry& g) {
-  std::vector<uint64_t> cut{s};
-  const uint64_t s16 = s & ~15ull;
-  const long long env = envLL("NEZHA_CE_PIECES", 0);
-  constexpr uint64_t kMinPiece = uint64_t{256} << 10;
-  if (env <= 0 && g.chunk < g.seg_len) {
-    for (uint64_t b = g.seg_off + ((s - g.seg_off) / g.chunk + 1) * g.chunk; b < e; b += g.chunk) {
-      const uint64_t c = b & ~15ull;
-      if (c > cut.back() && c - cut.back() >= kMinPiece && e - c >= kMinPiece) cut.push_back(c);
-    }
-  } else {
-    const uint64_t P = env > 0 ? static_cast<uint64_t>(std::min<long long>(env, 8))
-                               : std::clamp<uint64_t>((e - s) / (uint64_t{4} << 20), 1, 4);
-    for (uint64_t i = 1; i < P; ++i) {
-      const uint64_t c = std::max<uint64_t>(s, (s16 + (e - s16) * i / P) & ~15ull);
-      if (c > cut.back() && c < e) cut.push_back(c);
-    }
-  }
-  cut.push_back(e);
-  return cut;
+  static const int forced = static_cast<int>(envLL("NEZHA_CE_PIECES", 0));
+  return nezha::pipelineCuts(s, e, nezha::ChunkGeometry{g.seg_off, g.seg_len, g.chunk}, forced);
 }
 
 // One launch sequence of a rail over [lo, hi) with order geometry g.

@@ -70,4 +70,27 @@ std::uint64_t completedBeforeStall(Bytes chunk_bytes, std::uint64_t cb, std::uin
   return ce;
 }
 
+std::vector<std::uint64_t> pipelineCuts(std::uint64_t s, std::uint64_t e, const ChunkGeometry& g, int equal_pieces) {
+  if (e < s) throw std::invalid_argument("pipelineCuts: e < s");
+  std::vector<std::uint64_t> cut{s};
+  constexpr std::uint64_t kMinPiece = std::uint64_t{256} << 10;
+  if (equal_pieces <= 0 && g.chunk_bytes > 0 && g.chunk_bytes < g.seg_length && s >= g.seg_offset) {
+    for (std::uint64_t b = g.seg_offset + ((s - g.seg_offset) / g.chunk_bytes + 1) * g.chunk_bytes; b < e;
+         b += g.chunk_bytes) {
+      const std::uint64_t c = b & ~std::uint64_t{15};
+      if (c > cut.back() && c - cut.back() >= kMinPiece && e - c >= kMinPiece) cut.push_back(c);
+    }
+  } else {
+    const std::uint64_t s16 = s & ~std::uint64_t{15};
+    const std::uint64_t P = equal_pieces > 0 ? static_cast<std::uint64_t>(std::min(equal_pieces, 8))
+                                             : std::clamp<std::uint64_t>((e - s) / (std::uint64_t{4} << 20), 1, 4);
+    for (std::uint64_t i = 1; i < P; ++i) {
+      const std::uint64_t c = std::max<std::uint64_t>(s, (s16 + (e - s16) * i / P) & ~std::uint64_t{15});
+      if (c > cut.back() && c < e) cut.push_back(c);
+    }
+  }
+  if (e > cut.back()) cut.push_back(e);
+  return cut;
+}
+
 }  // namespace nezha

@@ -41,6 +41,38 @@ TEST_CASE("host pipeline pieces (DESIGN.md 4c)") {
   CHECK_THROWS_AS(hostPipelinePieces(6, 4), std::invalid_argument);
 }
 
+TEST_CASE("waves and the completed prefix of an unplanned failure (DESIGN.md §3, §6b)") {
+  auto w = waveRanges(10ull << 20, 0, 16, 64ull << 20);  // 7 chunks per wave; the 2-chunk tail joins
+  CHECK(w.size() == 2);
+  CHECK(w[0] == std::make_pair<std::uint64_t, std::uint64_t>(0, 7));
+  CHECK(w[1] == std::make_pair<std::uint64_t, std::uint64_t>(7, 16));
+  CHECK(waveRanges(1ull << 20, 0, 1, 64ull << 20).size() == 1);
+  CHECK(waveRanges(1ull << 20, 3, 3, 64ull << 20).empty());
+  CHECK(completedBeforeStall(10ull << 20, 0, 16, 6, 64ull << 20) == 0);
+  CHECK(completedBeforeStall(10ull << 20, 0, 16, 7, 64ull << 20) == 7);
+  CHECK(completedBeforeStall(10ull << 20, 0, 16, 15, 64ull << 20) == 7);
+  CHECK(completedBeforeStall(10ull << 20, 0, 16, 16, 64ull << 20) == 16);  // never hit
+}
+
+TEST_CASE("copy-engine pipeline cuts (DESIGN.md §3)") {
+  // RingChunked: 64 MiB segment, 4 MiB chunks; a shard of 8 MiB starting mid-chunk.
+  const ChunkGeometry g{0, 64ull << 20, 4ull << 20};
+  auto c = pipelineCuts(6ull << 20, 14ull << 20, g);
+  CHECK(c == std::vector<std::uint64_t>{6ull << 20, 8ull << 20, 12ull << 20, 14ull << 20});
+  // Ring (one chunk): clamp(len / 4 MiB, 1, 4) equal pieces, 16-byte aligned.
+  const ChunkGeometry r{0, 64ull << 20, 64ull << 20};
+  auto d = pipelineCuts(0, 16ull << 20, r);
+  CHECK(d.size() == 5);
+  for (auto x : d) CHECK(x % 16 == 0);
+  CHECK(pipelineCuts(100, 100 + (1 << 20), r).size() == 2);  // one piece
+  // No piece under 256 KiB: a boundary 100 KiB before the end is skipped.
+  auto e = pipelineCuts(0, (4ull << 20) + (100 << 10), g);
+  CHECK(e == std::vector<std::uint64_t>{0, (4ull << 20) + (100 << 10)});
+  auto f = pipelineCuts(0, 16ull << 20, g, 3);  // forced equal pieces
+  CHECK(f.size() == 4);
+  CHECK(pipelineCuts(5, 5, g) == std::vector<std::uint64_t>{5});
+}
+
 TEST_CASE("chunk geometry (P10)") {
   CHECK(defaultChunkBytes(64ull << 20, 8, Algorithm::RingChunked) == (4ull << 20));
   CHECK(defaultChunkBytes(1 << 20, 8, Algorithm::RingChunked) == 65536);
