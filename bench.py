@@ -370,7 +370,7 @@ def run_loopback(args):
                       "bytes_per_rank": S, "ranks": V, "virtual_ranks": True, "same_config": True,
                       "l2": f"{V} x {S >> 20} MiB per buffer > 126 MB L2; no flush", "plan": plan,
                       "algbw_GBs": round(algbw, 2),
-                      "parity": "bit-exact vs the reference ring golden hash: tests/test_gpu_loopback.py::"
+                      "parity": "bit-exact vs the reference ring golden hash: tests/test_gpu_vranks.py::"
                                 "test_loopback_config1_hash (same engine call, oracle inputs)"},
            "roofline": roofline, "gpu_launches": res and shared.get("launches"), "clocks": clocks,
            "e2e": {"value": round(ring_volume(V, S) / te / 1e9, 3), "unit": "GB/s",

@@ -1,6 +1,6 @@
 """GPU: the multi-rail engine end to end (planner + rails + failure monitor)
 against the CPU oracle, one process per GPU, through the C ABI. The same
-checks with virtual ranks on one GPU are in test_gpu_loopback.py."""
+checks with virtual ranks on one GPU are in test_gpu_vranks.py."""
 import json
 import os
 

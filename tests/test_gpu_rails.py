@@ -2,7 +2,7 @@
 
 Single-GPU: the SM-rail and CE-reduce fold kernels are run for every virtual
 rank of an N-rank job with all ranks' buffers on cuda:0 (nz_emulate_fold);
-the full rail protocols with virtual ranks are in test_gpu_loopback.py.
+the full rail protocols with virtual ranks are in test_gpu_vranks.py.
 Multi-GPU (>= 2 GPUs in the box): real ranks, one process per GPU, through
 the C ABI (nz_comm_init / nz_buffer_alloc / nz_rail_allreduce), NVLS included.
 """

@@ -277,7 +277,7 @@ def run_ranks(world, fn):
 
 def main():
     from tests.workers import engine_worker, rail_worker
-    import tests.test_gpu_loopback as T
+    import tests.test_gpu_vranks as T
 
     saved = {(m, n): getattr(m, n) for m in (rail_worker, engine_worker) for n in ("Rail", "SymmetricBuffer", "Engine")
              if hasattr(m, n)}

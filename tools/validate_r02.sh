@@ -19,12 +19,12 @@ step() {  # step NAME SECONDS CMD...
 }
 nvidia-smi --query-gpu=index,name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/r02_gpus.csv 2>&1
 step smoke 600 "python -c 'import __graft_entry__ as g; g.smoke()'"
-step loopback 2400 "python -m pytest tests/test_gpu_loopback.py -m gpu -q -p no:cacheprovider --timeout 900 -rfE -x"
+step loopback 2400 "python -m pytest tests/test_gpu_vranks.py -m gpu -q -p no:cacheprovider --timeout 900 -rfE -x"
 step single 900 "python -m pytest tests/test_gpu_rails.py tests/test_gpu_engine.py -m gpu -q -p no:cacheprovider --timeout 600 -rfE"
 step bench1 900 "python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench1.json"
 step launches 900 "ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_launches.csv python tools/ncu_loopback.py 8 4"
 step ncu_fold 1500 "ncu --set full --clock-control none --import-source on -k regex:fold_kernel_vr -s 2 -c 1 -f -o gpurun_out/r02_ncu_fold_vr python tools/ncu_loopback.py 8 4"
-step memcheck 1500 "compute-sanitizer --tool memcheck --leak-check no --print-limit 20 python -m pytest tests/test_gpu_loopback.py -m gpu -q -p no:cacheprovider -k 'rails_bit_exact and 4'"
+step memcheck 1500 "compute-sanitizer --tool memcheck --leak-check no --print-limit 20 python -m pytest tests/test_gpu_vranks.py -m gpu -q -p no:cacheprovider -k 'rails_bit_exact and 4'"
 if [ "${1:-}" = "multi" ] && [ "$(nvidia-smi -L | wc -l)" -ge 2 ]; then
   step rails2 900 "python -m pytest tests/test_gpu_rails.py -m gpu -q -p no:cacheprovider --timeout 600 -rfE -k 'multi_gpu and 2'"
   step engine2 1500 "python -m pytest tests/test_gpu_engine.py -m gpu -q -p no:cacheprovider --timeout 900 -rfE"
