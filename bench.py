@@ -310,9 +310,20 @@ def run_loopback(args):
         # agrees on the orphan and reroutes it to the other rail.
         fo = None
         if not args.no_failover:
-            eng2 = Engine(comm, kinds=kinds, rails_toml=toml, algorithm=ALGO_RING_CHUNKED, window=1 << 30,
-                          sync_overhead_us=0.0)
-            b2i, b2o = SymmetricBuffer(comm, fo_bytes), SymmetricBuffer(comm, fo_bytes)
+            try:
+                fo = loop_failover(comm, g, stream)
+            except Exception as e:  # reported, never fatal to the headline line
+                fo = {"error": str(e)[:300]}
+        return {"t_step": t_step, "ktime": ktime, "te": te, "plan": plan, "fo": fo}
+
+    def loop_failover(comm, g, stream):
+        eng2 = Engine(comm, kinds=kinds, rails_toml=toml, algorithm=ALGO_RING_CHUNKED, window=1 << 30,
+                      sync_overhead_us=0.0)
+        b2i, b2o = SymmetricBuffer(comm, fo_bytes), SymmetricBuffer(comm, fo_bytes)
+        try:
+            mon = eng2.state()["monitor"]  # the same on every rank (agreed at engine creation)
+            if not mon["on"]:
+                return {"error": "failure monitor off: " + mon.get("off_reason", "")}
             xb = (torch.rand(fo_bytes // 2, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
             b2i.write(xb.data_ptr(), fo_bytes)
             torch.cuda.synchronize()
@@ -321,17 +332,17 @@ def run_loopback(args):
             segs = eng2.last_plans()[0]["segs"]
             victim = max(segs, key=lambda s_: s_[2])
             nch = -(-victim[2] // victim[3])
-            if r == V - 1:
+            if comm.rank == V - 1:
                 eng2.inject_failure(eng2.op_seq, victim[0], nch // 2)
             comm.barrier()
             eng2.allreduce(b2i, b2o, fo_bytes, BF16, stream)
             eng2.synchronize()
             fos = eng2.failovers()
-            fo = fos[-1] if fos else None
+            return fos[-1] if fos else None
+        finally:
             eng2.close()
             b2i.free()
             b2o.free()
-        return {"t_step": t_step, "ktime": ktime, "te": te, "plan": plan, "fo": fo}
 
     res = run_ranks(V, body, timeout=1800)
     t_step = max(r_["t_step"] for r_ in res)
@@ -383,7 +394,10 @@ def run_loopback(args):
         t_ce = kce["total_us"] / kce["launches"] * 1e-6
         out["kernels"]["ce"]["note"] = "copy-engine rail barrier grids (its DMA and reduce run on rank streams)"
         del t_ce
-    fos = [r_["fo"] for r_ in res if r_["fo"]]
+    errs = [r_["fo"]["error"] for r_ in res if r_["fo"] and "error" in r_["fo"]]
+    fos = [r_["fo"] for r_ in res if r_["fo"] and "error" not in r_["fo"]]
+    if errs:
+        out["failover_error"] = errs[0]
     if fos:
         out["failover"] = {"payload": "bf16 256 MiB, RingChunked, larger rail's link dies on the last rank at its "
                                       "middle chunk (unplanned)",
@@ -615,6 +629,10 @@ def run_multi(args):
     # Failover: config 4 shape (bf16 256 MiB, largest-alpha rail's link dies
     # on the last rank at its middle chunk, unplanned).
     if not args.no_failover and len(kinds) > 1:
+      try:
+        mon = eng.state()["monitor"]  # the same on every rank
+        if not mon["on"]:
+            raise RuntimeError("failure monitor off: " + mon.get("off_reason", ""))
         fs = 256 << 20
         eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
         eng.synchronize()
@@ -635,6 +653,8 @@ def run_multi(args):
                                "done_us": round(max_over_ranks(fo["done_us"]), 2), "payload": "bf16 256 MiB"}
             out["failover_ms"] = round(out["failover"]["done_us"] / 1e3, 4)
             eng.readmit(victim[0])
+      except Exception as e:  # reported, never fatal to the headline line
+        out["failover_error"] = str(e)[:300]
 
     # Config 3: mixed 8 KiB - 4 MiB stream through the state machine.
     if not args.no_sweep:
