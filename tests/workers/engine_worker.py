@@ -114,6 +114,9 @@ def run(comm, spec) -> dict:
                                  for r in range(world)])
         for rep in range(c.get("reps", 1)):
             failing = bool(c.get("fail")) and rep == c.get("fail_rep", 0)
+            if failing:  # every rank checks, so none is left waiting for the injecting one
+                mon = eng.state()["monitor"]
+                assert mon["on"], f"failure monitor off: {mon.get('off_reason')}"
             n_fo = len(eng.failovers())
             if failing and rank == c.get("fail_rank", world - 1):
                 eng.inject_failure(eng.op_seq, c["fail"][0], c["fail"][1])

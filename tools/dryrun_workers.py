@@ -247,7 +247,7 @@ class FakeEngine:
 
     def state(self):
         return {"sync_overhead_us": 0.0, "rails": [], "compute_pool": None,
-                "monitor": {"on": True, "failed": sorted(self.failed)}}
+                "monitor": {"on": True, "off_reason": "", "failed": sorted(self.failed)}}
 
     def close(self):
         pass
