@@ -10,6 +10,13 @@
 
 namespace nz {
 
+// One grid's arguments for all 8 virtual ranks travel as kernel parameters:
+// keep them inside the classic 4 KiB parameter space (no large-parameter
+// launch path needed).
+static_assert(sizeof(VPack<FoldArgs>) <= 4096, "fold pack exceeds 4 KiB of kernel parameters");
+static_assert(sizeof(VPack<LLArgs>) <= 4096, "LL pack exceeds 4 KiB of kernel parameters");
+static_assert(sizeof(VPack<BarrierKArgs>) <= 4096, "barrier pack exceeds 4 KiB of kernel parameters");
+
 namespace {
 
 template <typename DT, int N>
