@@ -121,11 +121,14 @@ bool llPath(nz_rail* r, uint64_t lo, uint64_t hi) {
   return r->comm->world > 1 && r->kind == NZ_RAIL_SM && r->ll && hi - lo <= r->ll_max && lo % 4 == 0;
 }
 
+// One thread per polled word, capped at the rail's CTA budget (default 64,
+// as its two-shot path): LL CTAs wait on peers' CTAs of the same index, so the
+// rail must stay inside the co-residency budget it shares with the other
+// rails' kernels (§3 "CTA budgets"), whichever path it takes.
 int llGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
   const uint64_t words = (hi - lo + 3) / 4;
-  const uint64_t threads = (words + 1) / 2 > words ? (words + 1) / 2 : words;
-  return static_cast<int>(
-      std::max<uint64_t>(1, std::min<uint64_t>((threads + kThreads - 1) / kThreads, r->comm->sm_count)));
+  const int budget = std::min(r->sm_budget > 0 ? r->sm_budget : 64, r->comm->sm_count);
+  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((words + kThreads - 1) / kThreads, budget)));
 }
 
 int copyGrid(nz_rail* r, uint64_t lo, uint64_t hi) {
