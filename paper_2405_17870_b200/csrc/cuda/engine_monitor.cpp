@@ -102,7 +102,10 @@ void nz_engine::startMonitor() {
     mon_off_reason = "CUDA stream memory operations unavailable";
     return;
   }
-  for (auto& s : specs) twins.push_back(nz::railCreate(comm, s.kind, s.rail_id, s.sm_budget, false, true));
+  // Twins run rarely (a reroute) but beside the main rails' kernels: a small
+  // CTA budget keeps every spinning kernel of the GPU co-resident (§3).
+  for (auto& s : specs)
+    twins.push_back(nz::railCreate(comm, s.kind, s.rail_id, s.kind == NZ_RAIL_CE ? s.sm_budget : 32, false, true));
   for (size_t i = 0; i < twins.size(); ++i) twins[i]->detect_us = cfg.detect_us;
   mon = std::thread([this] { monitorLoop(); });
 }
