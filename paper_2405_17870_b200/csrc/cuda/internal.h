@@ -167,7 +167,8 @@ struct nz_rail {
   // the control words, so a launch on a new stream first waits for the
   // previous stream's work ("one executor per rail").
   cudaStream_t last_stream = nullptr;
-  cudaEvent_t order_ev = nullptr;
+  cudaEvent_t order_ev = nullptr;  // recorded after every eager launch
+  bool order_valid = false;
   // Loopback: the group's combiner for this pad, and this rank's events.
   nz::LoopRail* lr = nullptr;
   cudaEvent_t lr_ready = nullptr;

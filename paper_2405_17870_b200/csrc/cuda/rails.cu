@@ -509,23 +509,20 @@ void railWave(nz_rail* r, nz_buf* in, nz_buf* out, uint64_t lo, uint64_t hi, con
   NZ_CUDA(cudaGetLastError());
 }
 
-// Orders a launch on `st` after the rail's previous launch on another stream.
-void orderOn(nz_rail* r, cudaStream_t st) {
-  if (st == r->last_stream) return;  // the common case: stream order already holds
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  NZ_CUDA(cudaStreamIsCapturing(st, &cap));
-  if (cap != cudaStreamCaptureStatusNone) {
-    r->last_stream = nullptr;  // the capture's own edges order it; nothing to record across
-    return;
-  }
-  if (r->last_stream && r->last_stream != st) {
-    cudaStreamCaptureStatus pc = cudaStreamCaptureStatusNone;
-    NZ_CUDA(cudaStreamIsCapturing(r->last_stream, &pc));
-    if (pc == cudaStreamCaptureStatusNone) {
-      NZ_CUDA(cudaEventRecord(r->order_ev, r->last_stream));
-      NZ_CUDA(cudaStreamWaitEvent(st, r->order_ev, 0));
-    }
-  }
+// A rail's launches share pads, LL slots and control words, so a launch on a
+// stream other than the one the rail's previous launch went to first waits
+// for that launch. The event is recorded after every eager launch, so the
+// wait never touches the previous stream itself (which the caller may have
+// destroyed since); captured launches are ordered by their graph instead.
+void orderBefore(nz_rail* r, cudaStream_t st, bool capturing) {
+  if (capturing || !r->order_valid || st == r->last_stream) return;
+  NZ_CUDA(cudaStreamWaitEvent(st, r->order_ev, 0));
+}
+
+void orderAfter(nz_rail* r, cudaStream_t st, bool capturing) {
+  if (capturing) return;
+  NZ_CUDA(cudaEventRecord(r->order_ev, st));
+  r->order_valid = true;
   r->last_stream = st;
 }
 
@@ -572,7 +569,10 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
   r->stall_chunk = -1;
   cudaStream_t st = op.st ? op.st : r->stream;
   NZ_CUDA(cudaSetDevice(r->comm->device));
-  orderOn(r, st);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  NZ_CUDA(cudaStreamIsCapturing(st, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  orderBefore(r, st, capturing);
   if (++r->tag == 0) r->tag = 1;
   const uint32_t tag = r->tag;
   const Geometry g{op.seg_off, op.seg_len, op.chunk_bytes};
@@ -583,7 +583,10 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
   ctl.host = r->status_dev;
   ctl.tag = tag;
   if (hi <= lo) {
-    if (!post.rec) return 0;
+    if (!post.rec) {
+      gateExit(op.gate, st);  // keeps the pool's ordering chain through an empty segment
+      return 0;
+    }
     // Nothing to reduce, but the trace-form failure is still posted.
     ctl.final_wave = op.status ? 1 : 0;
     ctl.prog_chunk = op.status ? stop : ~0ull;
@@ -591,6 +594,7 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
     launchBarrier(r, r->epoch + 1, true, post, ctl, st);
     r->epoch += 2;
     gateExit(op.gate, st);
+    orderAfter(r, st, capturing);
     return op.status ? tag : 0;
   }
   std::vector<std::pair<uint64_t, uint64_t>> waves;
@@ -610,6 +614,7 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
     railWave(r, op.in, op.out, wlo, whi, g, op.dtype, last ? post : FaultPost{}, ctl, st, op.gate);
   }
   gateExit(op.gate, st);
+  orderAfter(r, st, capturing);
   return op.status ? tag : 0;
 }
 
@@ -628,7 +633,7 @@ CUdeviceptr railGateAddr(nz_rail* r) { return reinterpret_cast<CUdeviceptr>(r->c
 void railRevive(nz_rail* r, cudaStream_t st) {
   NZ_CUDA(cudaSetDevice(r->comm->device));
   if (!st) st = r->stream;
-  orderOn(r, st);
+  orderBefore(r, st, false);
   NZ_CUDA(cudaMemsetAsync(r->ctl_dev + kCtlRetired, 0, 2 * sizeof(uint32_t), st));
   NZ_CUDA(cudaMemsetAsync(r->ctl_dev + kCtlSticky, 0, sizeof(uint32_t), st));
   NZ_CUDA(cudaStreamSynchronize(st));
@@ -803,7 +808,7 @@ int nz_rail_synchronize(nz_rail_t* r) {
     NZ_CUDA(cudaSetDevice(r->comm->device));
     for (auto s : r->side) NZ_CUDA(cudaStreamSynchronize(s));
     NZ_CUDA(cudaStreamSynchronize(r->stream));
-    if (r->last_stream && r->last_stream != r->stream) NZ_CUDA(cudaStreamSynchronize(r->last_stream));
+    if (r->order_valid) NZ_CUDA(cudaEventSynchronize(r->order_ev));
   });
 }
 void* nz_rail_stream(const nz_rail_t* r) { return r ? static_cast<void*>(r->stream) : nullptr; }
