@@ -140,19 +140,23 @@ nz_buf* allocSymmetric(nz_comm* c, size_t bytes) {
       }
     }
   } catch (...) {
-    freeSymmetric(b);
+    freeSymmetric(b, false);  // peers may have failed elsewhere: no rendezvous
     throw;
   }
   return b;
 }
 
-void freeSymmetric(nz_buf* b) {
+void freeSymmetric(nz_buf* b, bool collective) {
   if (!b) return;
   nz_comm* c = b->comm;
   cudaSetDevice(c->device);
-  if (c->loop) {
-    // A virtual rank's memory is its peers' too: free it only once every rank
-    // stopped using it (all ranks free in the same order).
+  if (collective && c->world > 1) {
+    // Peers read and write this memory over NVLink (or, for virtual ranks, in
+    // the same process): unmap it only once no kernel of any rank can still
+    // touch it — even after a failed op, whose late peers keep running until
+    // their own budgets expire. This rank's kernels first, then every peer's
+    // (all ranks free in the same order).
+    cudaDeviceSynchronize();
     try {
       exchange(c, nullptr, 0, {});
     } catch (...) {
@@ -190,13 +194,7 @@ int nz_buffer_alloc(nz_comm_t* comm, size_t bytes, nz_buf_t** out) {
 int nz_buffer_free(nz_buf_t* buf) {
   return guarded([&] {
     if (!buf) return;
-    // Collective: nobody unmaps while a peer may still touch the memory.
-    if (buf->comm->world > 1 && !buf->comm->loop) {
-      cudaSetDevice(buf->comm->device);
-      cudaDeviceSynchronize();
-      nz::exchange(buf->comm, nullptr, 0, {});
-    }
-    nz::freeSymmetric(buf);
+    nz::freeSymmetric(buf);  // collective: nobody unmaps while a peer may still touch the memory
   });
 }
 

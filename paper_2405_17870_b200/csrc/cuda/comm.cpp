@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -282,6 +284,25 @@ bool peekExchange(nz_comm* c, int channel, std::vector<std::vector<char>>* blobs
 
 namespace {
 
+// Multi-process communicators still open. A rank process that exits without
+// destroying its communicator (an exception on the host, a failed test) takes
+// its symmetric memory with it while a late peer's kernel may still read or
+// write that memory over NVLink — a fabric fault on the peer's GPU. At exit
+// the process therefore holds on for the device wait budget, after which
+// every peer kernel has given up on its own.
+std::atomic<int> g_open_shared{0};
+
+void holdAtExit() {
+  const int n = g_open_shared.load();
+  if (n <= 0) return;
+  const auto ms = static_cast<long long>(watchdogNs() / 1000000ull) + 1000;
+  fprintf(stderr,
+          "[nezha] exiting with %d open multi-process communicator(s): holding this rank's memory for %lld ms so "
+          "peers' kernels time out before it is unmapped\n",
+          n, ms);
+  std::this_thread::sleep_for(std::chrono::milliseconds(ms));
+}
+
 int commInit(int rank, int world, int device, const char* session, int timeout_ms, bool loopback, nz_comm_t** out) {
   return guarded([&] {
     if (!out || !session) fail(NZ_ERR_INVALID, "nz_comm_init: null argument");
@@ -334,6 +355,11 @@ int commInit(int rank, int world, int device, const char* session, int timeout_m
       NZ_CUDA(cudaMemset(c->ctrl->ptrs[rank], 0, c->ctrl->mapped));
       NZ_CUDA(cudaDeviceSynchronize());
       exchange(c, nullptr, 0, {});  // pads are zero everywhere before first use
+      if (!c->loop && world > 1) {
+        static std::once_flag once;
+        std::call_once(once, [] { std::atexit(holdAtExit); });
+        g_open_shared.fetch_add(1);
+      }
     } catch (...) {
       for (auto& ch : c->chan)
         if (ch.listen_fd >= 0) close(ch.listen_fd);
@@ -385,6 +411,7 @@ int nz_comm_destroy(nz_comm_t* comm) {
     if (!comm) return;
     cudaSetDevice(comm->device);
     if (comm->ctrl) nz::freeSymmetric(comm->ctrl);  // collective: ranks leave together
+    if (!comm->loop && comm->world > 1) nz::g_open_shared.fetch_sub(1);
     for (auto& ch : comm->chan) {
       for (auto& kv : ch.stash)
         for (int fd : kv.second.fds) close(fd);

@@ -228,7 +228,12 @@ std::vector<Msg> exchange(nz_comm* c, const void* data, size_t bytes, const std:
 // already entered the channel's next exchange, i.e. waits for this rank.
 bool peekExchange(nz_comm* c, int channel, std::vector<std::vector<char>>* blobs);
 nz_buf* allocSymmetric(nz_comm* c, size_t bytes);
-void freeSymmetric(nz_buf* b);
+// Device wait budget at the start of an op (NEZHA_WATCHDOG_MS, 20 s).
+uint64_t watchdogNs();
+
+// Collective unless `collective` is false (allocation error paths): waits for
+// every rank's kernels before unmapping.
+void freeSymmetric(nz_buf* b, bool collective = true);
 int elemSizeOf(int dtype);
 
 // rails.cu

@@ -51,6 +51,8 @@ long long envLL(const char* name, long long def) {
 // Device wait budget at the start of an op (ranks may legitimately arrive far
 // apart: the caller's stream decides when a launch starts). NEZHA_WATCHDOG_MS
 // overrides the 20 s default; past it a kernel gives up instead of hanging.
+}  // namespace
+
 uint64_t watchdogNs() {
   static const uint64_t ns = [] {
     const long long ms = envLL("NEZHA_WATCHDOG_MS", 20000);
@@ -58,6 +60,8 @@ uint64_t watchdogNs() {
   }();
   return ns;
 }
+
+namespace {
 
 // End-barrier budget: every rank passed the start barrier of the same op and
 // does the same work, so a peer missing for much longer than the op itself
