@@ -91,6 +91,11 @@ int nz_comm_init(int rank, int world, int device, const char* session, int timeo
  * no NVLS rail. Every other entry point is used exactly as with nz_comm_init. */
 int nz_comm_init_loopback(int rank, int world, int device, const char* session, int timeout_ms, nz_comm_t** out);
 int nz_comm_is_loopback(const nz_comm_t* comm);
+/* Loopback only: marks the job's virtual-rank group failed (a rank's host
+ * code raised), so every peer waiting in an exchange or a combined launch
+ * fails at once (NZ_ERR_TIMEOUT) instead of after `timeout_ms`. NZ_OK and no
+ * effect on a multi-process comm. */
+int nz_comm_abort(nz_comm_t* comm);
 int nz_comm_destroy(nz_comm_t* comm);
 int nz_comm_rank(const nz_comm_t* comm);
 int nz_comm_world(const nz_comm_t* comm);

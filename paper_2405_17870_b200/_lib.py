@@ -150,6 +150,7 @@ _SIGS = {
     "nz_comm_init": (c_int, [c_int, c_int, c_int, c_char_p, c_int, POINTER(c_void_p)]),
     "nz_comm_init_loopback": (c_int, [c_int, c_int, c_int, c_char_p, c_int, POINTER(c_void_p)]),
     "nz_comm_is_loopback": (c_int, [c_void_p]),
+    "nz_comm_abort": (c_int, [c_void_p]),
     "nz_comm_destroy": (c_int, [c_void_p]),
     "nz_comm_rank": (c_int, [c_void_p]),
     "nz_comm_world": (c_int, [c_void_p]),

@@ -163,6 +163,7 @@ std::vector<Msg> loopExchange(nz_comm* c, int channel, uint64_t seq, const void*
   const auto deadline = Clock::now() + std::chrono::milliseconds(c->timeout_ms);
   for (int p = 0; p < c->world; ++p) {
     while (g.box.find({channel, seq, p}) == g.box.end()) {
+      if (g.aborted) fail(NZ_ERR_TIMEOUT, "loopback group aborted: a virtual rank failed");
       if (g.cv.wait_until(lk, deadline) == std::cv_status::timeout && g.box.find({channel, seq, p}) == g.box.end()) {
         fail(NZ_ERR_TIMEOUT, "loopback rendezvous timeout waiting for virtual rank " + std::to_string(p));
       }
@@ -405,6 +406,21 @@ int nz_comm_init_loopback(int rank, int world, int device, const char* session, 
 }
 
 int nz_comm_is_loopback(const nz_comm_t* c) { return c ? (c->loop ? 1 : 0) : NZ_ERR_INVALID; }
+
+int nz_comm_abort(nz_comm_t* comm) {
+  return guarded([&] {
+    if (!comm) fail(NZ_ERR_INVALID, "null argument");
+    if (!comm->loop) return;
+    nz::LoopGroup& g = *comm->loop;
+    std::lock_guard<std::mutex> lk(g.m);
+    g.aborted = true;
+    g.cv.notify_all();
+    for (auto& kv : g.rails) {
+      std::lock_guard<std::mutex> rl(kv.second->m);
+      kv.second->cv.notify_all();
+    }
+  });
+}
 
 int nz_comm_destroy(nz_comm_t* comm) {
   return guarded([&] {

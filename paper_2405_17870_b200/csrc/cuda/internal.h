@@ -190,6 +190,7 @@ struct LoopGroup {
   int world = 0;
   int device = 0;
   uint32_t joined = 0;  // bitmask of ranks
+  std::atomic<bool> aborted{false};  // nz_comm_abort: a rank's host code failed
   std::mutex m;
   std::condition_variable cv;
   std::map<std::tuple<int, uint64_t, int>, std::vector<char>> box;  // (channel, seq, sender)

@@ -272,6 +272,7 @@ void combine(nz_rail* r, int kind, int dtype, const A& a, int grid, cudaStream_t
   } else {
     const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(c->timeout_ms);
     while (L.gen == gen) {
+      if (c->loop->aborted) fail(NZ_ERR_TIMEOUT, "loopback group aborted: a virtual rank failed");
       if (L.cv.wait_until(lk, deadline) == std::cv_status::timeout && L.gen == gen) {
         fail(NZ_ERR_TIMEOUT, "loopback launch: a virtual rank never reached rail " + std::to_string(r->rail_id));
       }

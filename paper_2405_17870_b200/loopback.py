@@ -41,6 +41,11 @@ def run_ranks(world: int, fn, device: int = 0, session: str | None = None, timeo
             results[rank] = fn(comm)
         except BaseException:  # noqa: BLE001 - reported below with the rank
             errors[rank] = traceback.format_exc()
+            if comm is not None:  # peers waiting on this rank fail now, not after timeout_ms
+                try:
+                    comm.abort()
+                except BaseException:  # noqa: BLE001
+                    pass
         finally:
             if comm is not None:
                 try:
@@ -52,8 +57,11 @@ def run_ranks(world: int, fn, device: int = 0, session: str | None = None, timeo
     threads = [threading.Thread(target=body, args=(r,), name=f"nz-vrank-{r}", daemon=True) for r in range(world)]
     for t in threads:
         t.start()
+    import time
+
+    deadline = time.monotonic() + timeout  # one deadline for the whole job
     for t in threads:
-        t.join(timeout)
+        t.join(max(0.0, deadline - time.monotonic()))
     hung = [r for r, t in enumerate(threads) if t.is_alive()]
     if hung or any(errors):
         msg = [f"virtual rank {r} did not finish within {timeout} s" for r in hung]

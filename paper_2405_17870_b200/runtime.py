@@ -79,6 +79,11 @@ class Comm:
         raw = out.raw
         return [raw[i * n:(i + 1) * n] for i in range(self.world)]
 
+    def abort(self) -> None:
+        """Loopback: fail every virtual rank still waiting on this group."""
+        if self.handle:
+            check(lib().nz_comm_abort(self.handle), "nz_comm_abort")
+
     def close(self) -> None:
         if self.handle:
             check(lib().nz_comm_destroy(self.handle), "nz_comm_destroy")

@@ -47,11 +47,13 @@ def test_core_known_answers_through_the_abi():
 
 
 def test_errors_map_to_codes_without_gpu():
-    from paper_2405_17870_b200 import Comm
+    from paper_2405_17870_b200 import Comm, lib
     from paper_2405_17870_b200._lib import NezhaError
 
     with pytest.raises(NezhaError):
         Comm(0, 9, 0, "too-many-ranks")  # world > 8 is a precondition violation
+    l = lib()
+    assert l.nz_comm_abort(None) == -1  # NZ_ERR_INVALID, no CUDA call made
 
 
 def test_sm100a_cubin_present():
