@@ -143,6 +143,7 @@ void nz_engine::monitorLoop() {
   uint64_t beat_key = ~0ull;  // (rail, tag) of the entry whose start was fed to the heartbeat clock
   for (;;) {
     Entry front;
+    bool recal = false;
     {
       std::unique_lock<std::mutex> lk(mu);
       if (mon_stop) return;
@@ -150,27 +151,30 @@ void nz_engine::monitorLoop() {
         const double now = nowUs();
         for (auto& s : specs)
           if (!agreed_failed.count(s.rail_id)) health->heartbeat(s.rail_id, now);
-        const bool recal = std::chrono::steady_clock::now() - last_clock > std::chrono::seconds(1);
-        if (!recal) {
-          cv.wait_for(lk, std::chrono::microseconds(200));
-          continue;
-        }
+        recal = std::chrono::steady_clock::now() - last_clock > std::chrono::seconds(1);
       } else {
         front = inflight.front();
       }
     }
+    // A peer's agreement request is answered even while this rank is idle
+    // (its entries all retired): the peer's failover waits on it.
     try {
       serviceRequests();
     } catch (const std::exception& e) {
       std::lock_guard<std::mutex> lk(mu);
       if (mon_error.empty()) mon_error = e.what();
     }
-    if (!front.end) {  // idle: re-anchor %globaltimer against the host clock
-      try {
-        calibrateClock();
-      } catch (const std::exception&) {
+    if (!front.end) {
+      if (recal) {  // idle: re-anchor %globaltimer against the host clock
+        try {
+          calibrateClock();
+        } catch (const std::exception&) {
+        }
+        last_clock = std::chrono::steady_clock::now();
+      } else {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait_for(lk, std::chrono::microseconds(200), [&] { return mon_stop || !inflight.empty(); });
       }
-      last_clock = std::chrono::steady_clock::now();
       continue;
     }
     const cudaError_t q = cudaEventQuery(front.end);
