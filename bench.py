@@ -454,7 +454,8 @@ def run_multi(args):
         eng1.allreduce(bin_, bout, S, 0, stream)
     e1.record(stream)
     e1.synchronize()
-    soak = max(1, min(4000, int(0.4 / max(1e-6, e0.elapsed_time(e1) / 3e3))))
+    # The soak is a collective: every rank takes the count from the slowest rank's estimate.
+    soak = max(1, min(4000, int(0.4 / max(1e-6, max_over_ranks(e0.elapsed_time(e1) / 3e3)))))
     comm.barrier()
     with ClockSampler(local) as clk:
         for _ in range(soak):  # same count on every rank (collective)
@@ -628,36 +629,60 @@ def run_multi(args):
 
     # Failover: config 4 shape (bf16 256 MiB, largest-alpha rail's link dies
     # on the last rank at its middle chunk, unplanned).
+    def agreed_error(err):
+        """Every rank's outcome of a section; the first error, or None."""
+        blobs = comm.allgather_bytes(json.dumps(err).encode()[:480].ljust(512))
+        errs = [json.loads(b_.decode().strip() or "null") for b_ in blobs]
+        return next((e_ for e_ in errs if e_), None)
+
+    eng_ok = True
     if not args.no_failover and len(kinds) > 1:
-      try:
-        mon = eng.state()["monitor"]  # the same on every rank
-        if not mon["on"]:
-            raise RuntimeError("failure monitor off: " + mon.get("off_reason", ""))
-        fs = 256 << 20
-        eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
-        eng.synchronize()
-        segs = eng.last_plans()[0]["segs"]
-        victim = max(segs, key=lambda s_: s_[2])
-        nch = -(-victim[2] // victim[3])
-        if rank == world - 1:
-            eng.inject_failure(eng.op_seq, victim[0], nch // 2)
-        comm.barrier()
-        eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
-        eng.synchronize()
-        fo = eng.last_failover()
-        if fo:
+        err, fo, victim = None, None, None
+        try:
+            mon = eng.state()["monitor"]  # the same on every rank
+            if not mon["on"]:
+                raise RuntimeError("failure monitor off: " + mon.get("off_reason", ""))
+            fs = 256 << 20
+            eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
+            eng.synchronize()
+            segs = eng.last_plans()[0]["segs"]
+            victim = max(segs, key=lambda s_: s_[2])
+            nch = -(-victim[2] // victim[3])
+            if rank == world - 1:
+                eng.inject_failure(eng.op_seq, victim[0], nch // 2)
+            comm.barrier()
+            eng.allreduce(bin_, bout, fs, DTYPES["bf16"], stream)
+            eng.synchronize()
+            fo = eng.last_failover()
+            if not fo:
+                raise RuntimeError("no failover recorded")
+        except Exception as e:  # reported, never fatal to the headline line
+            err = str(e)[:300]
+        # Agreed before any further collective: a rank that raised must not
+        # leave its peers inside a collective it skipped.
+        err = agreed_error(err)
+        if err:
+            out["failover_error"] = err
+            eng_ok = False  # the engine's collectives may be out of step: no more sections on it
+        else:
             out["failover"] = {"failed_rail": kinds[fo["failed_rail"]], "target_rail": kinds[fo["target_rail"]],
                                "orphan_bytes": fo["orphan_length"], "orphan_chunk": fo["orphan_chunk"],
                                "detect_us": round(max_over_ranks(fo["detect_us"]), 2),
                                "resume_after_detect_us": round(max_over_ranks(fo["resume_after_detect_us"]), 2),
                                "done_us": round(max_over_ranks(fo["done_us"]), 2), "payload": "bf16 256 MiB"}
             out["failover_ms"] = round(out["failover"]["done_us"] / 1e3, 4)
-            eng.readmit(victim[0])
-      except Exception as e:  # reported, never fatal to the headline line
-        out["failover_error"] = str(e)[:300]
+            try:
+                eng.readmit(victim[0])
+                err = None
+            except Exception as e:
+                err = str(e)[:300]
+            err = agreed_error(err)
+            if err:
+                out["readmit_error"] = err
+                eng_ok = False
 
     # Config 3: mixed 8 KiB - 4 MiB stream through the state machine.
-    if not args.no_sweep:
+    if not args.no_sweep and eng_ok:
         import random
 
         rnd = random.Random(7)
