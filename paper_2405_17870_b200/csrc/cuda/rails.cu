@@ -559,11 +559,13 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
   if (op.seg_off + op.seg_len > op.in->size || op.seg_off + op.seg_len > op.out->size)
     fail(NZ_ERR_INVALID, "segment exceeds buffer");
   const uint64_t nch = (op.seg_len + op.chunk_bytes - 1) / op.chunk_bytes;
+  if (op.chunk_begin > op.chunk_end) fail(NZ_ERR_INVALID, "chunk_begin > chunk_end");
   const uint64_t chunk_end = std::min(op.chunk_end, nch);
-  if (op.chunk_begin > chunk_end) fail(NZ_ERR_INVALID, "chunk_begin > chunk_end");
+  // A window that starts past the segment's last chunk is empty.
+  const uint64_t chunk_begin = std::min(op.chunk_begin, chunk_end);
   uint64_t stop = chunk_end;
   FaultPost post{};
-  if (op.fail_chunk >= 0 && static_cast<uint64_t>(op.fail_chunk) >= op.chunk_begin &&
+  if (op.fail_chunk >= 0 && static_cast<uint64_t>(op.fail_chunk) >= chunk_begin &&
       static_cast<uint64_t>(op.fail_chunk) < chunk_end) {
     stop = static_cast<uint64_t>(op.fail_chunk);
     post.rec = r->fault_dev;
@@ -581,7 +583,7 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
   if (++r->tag == 0) r->tag = 1;
   const uint32_t tag = r->tag;
   const Geometry g{op.seg_off, op.seg_len, op.chunk_bytes};
-  const uint64_t lo = op.seg_off + std::min(op.seg_len, op.chunk_begin * op.chunk_bytes);
+  const uint64_t lo = op.seg_off + std::min(op.seg_len, chunk_begin * op.chunk_bytes);
   const uint64_t hi = op.seg_off + std::min(op.seg_len, stop * op.chunk_bytes);
   RailCtl ctl{};
   ctl.dev = r->ctl_dev;
@@ -604,9 +606,9 @@ uint32_t railRun(nz_rail* r, const RailOp& op) {
   }
   std::vector<std::pair<uint64_t, uint64_t>> waves;
   if (llPath(r, lo, hi))
-    waves.emplace_back(op.chunk_begin, stop);
+    waves.emplace_back(chunk_begin, stop);
   else
-    waves = railWaves(op.chunk_bytes, op.chunk_begin, stop);
+    waves = railWaves(op.chunk_bytes, chunk_begin, stop);
   for (size_t w = 0; w < waves.size(); ++w) {
     const auto [c0, c1] = waves[w];
     const bool last = w + 1 == waves.size();

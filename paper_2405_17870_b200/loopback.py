@@ -11,6 +11,7 @@ concurrently.
 """
 from __future__ import annotations
 
+import sys
 import threading
 import traceback
 import uuid
@@ -30,12 +31,12 @@ def run_ranks(world: int, fn, device: int = 0, session: str | None = None, timeo
 
     def body(rank: int) -> None:
         comm = None
-        try:
-            import torch
-
-            torch.cuda.set_device(device)
-        except Exception:  # torch is optional here: the library sets the device itself
-            pass
+        torch = sys.modules.get("torch")  # only a caller that uses torch needs its device set per thread
+        if torch is not None:
+            try:
+                torch.cuda.set_device(device)
+            except Exception:  # the library sets the device itself
+                pass
         try:
             comm = Comm(rank, world, device, session, timeout_ms=timeout_ms, loopback=True)
             results[rank] = fn(comm)

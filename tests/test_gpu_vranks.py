@@ -26,8 +26,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+HOST_HARNESS = bool(os.environ.get("NEZHA_TEST_HOST_HARNESS_LIB"))  # tests/test_host_harness.py (CPU)
+
+
 @pytest.fixture(autouse=True)
 def _one_gpu():
+    if HOST_HARNESS:
+        return  # host logic against tests/fakecuda: no device, no torch
     if gpu_count() < 1:
         pytest.skip("no GPU")
     import torch
@@ -164,7 +169,7 @@ def test_loopback_unplanned_link_death_detected(world, kind):
                 assert r["stalled_here"], r
             elif r["nbytes"] > 65536:
                 assert r["detected_here"] and r["watchdog"] == 1, r
-                assert r["seconds"] < 5.0, r
+                assert HOST_HARNESS or r["seconds"] < 5.0, r  # timing is the device's, not the harness's
     big_res = [rr for rk in res for rr in rk["results"] if rr["case"] == 0]
     assert len({rr["progress"] for rr in big_res}) == 1  # every rank published the same completed waves
     assert big_res[0]["progress"] > 0
@@ -282,7 +287,7 @@ def test_loopback_engine_unplanned_failover(fail_rail):
     # on 8 cores), so one rank's monitor can be descheduled for a time slice:
     # the median rank must make it, every rank within 5 ms.
     ra = sorted(rk["results"][1]["failover"]["resume_after_detect_us"] for rk in res)
-    assert ra[len(ra) // 2] < 1000 and ra[-1] < 5000, ra
+    assert HOST_HARNESS or (ra[len(ra) // 2] < 1000 and ra[-1] < 5000), ra
     # Identical reports on every rank (the agreement), timings aside.
     keys = ("op_seq", "failed_rail", "target_rail", "orphan_offset", "orphan_length", "orphan_chunk")
     reps = [tuple(rk["results"][1]["failover"][k] for k in keys) for rk in res]
@@ -305,7 +310,7 @@ def test_loopback_failover_trials_acceptance5():
     fos = [r["failover"] for rk in res for r in rk["results"] if r.get("failover")]
     assert len(fos) >= 4 * world, fos
     ra = sorted(f["resume_after_detect_us"] for f in fos)
-    assert ra[len(ra) // 2] < 1000 and ra[-1] < 5000, ra  # see test_loopback_engine_unplanned_failover
+    assert HOST_HARNESS or (ra[len(ra) // 2] < 1000 and ra[-1] < 5000), ra  # see test_loopback_engine_unplanned_failover
 
 
 @pytest.mark.parametrize("mode", [1, 2])
@@ -340,6 +345,7 @@ def test_loopback_engine_oversized_split():
     assert len({(s[1] // (256 << 20)) for s in r["segs"]}) == 5
 
 
+@pytest.mark.skipif(HOST_HARNESS, reason="needs torch kernels on the device")
 def test_loopback_engine_under_foreign_compute_load():
     """The rails share SMs with the caller's kernels (VERDICT weak 10): every
     virtual rank keeps a matmul stream busy while its engine allreduces run;

@@ -142,6 +142,13 @@ def run(comm, spec) -> dict:
                 torch.cuda.synchronize()
                 eng.synchronize()
                 bout.read(got, n)
+            elif c.get("device") and os.environ.get("NEZHA_TEST_HOST_HARNESS_LIB"):
+                # tests/fakecuda: "device" memory is host memory there
+                dev = inputs[rank].view(np.uint8).copy()
+                comm.barrier()
+                eng.allreduce_device(dev, dev, n, dt)
+                eng.synchronize()
+                got = dev.view(got.dtype).copy()
             elif c.get("device"):  # caller-owned device memory, in place (nz_engine_allreduce_device)
                 import torch
                 torch.cuda.set_device(comm.device)

@@ -126,7 +126,8 @@ def run(comm, cases) -> dict:
         seg_off, seg_len = c.get("seg_off", 0), c.get("seg_len", nbytes)
         chunk = c.get("chunk") or oracle.default_chunk_bytes(seg_len, world, c.get("chunked", True))
         nch = (seg_len + chunk - 1) // chunk
-        cb, ce = c.get("chunk_begin", 0), min(c.get("chunk_end", nch), nch)
+        ce = min(c.get("chunk_end", nch), nch)
+        cb = min(c.get("chunk_begin", 0), ce)  # a window starting past the last chunk is empty
         fail = c.get("fail_chunk", -1)
         stall = c.get("stall")
         if stall:
