@@ -10,6 +10,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <ctime>
 #include <functional>
@@ -129,7 +130,22 @@ void post_fault(const FaultPost& p) {
   st(&p.rec->valid, 1u);
 }
 
-uint64_t end_budget(const BarrierArgs& b, const RailCtl& c) { return c.end_timeout_ns ? c.end_timeout_ns : b.timeout_ns; }
+// End-barrier budgets are sized for the device's speed (the op's own time
+// x 4 plus a floor): the host emulation of a wave is orders of magnitude
+// slower, so they are stretched here (FAKECUDA_END_DILATION, default 500).
+// Start-of-op budgets (the watchdog) are left alone.
+uint64_t dilation() {
+  static const uint64_t d = [] {
+    const char* e = getenv("FAKECUDA_END_DILATION");
+    const long long v = e ? atoll(e) : 500;
+    return static_cast<uint64_t>(v > 0 ? v : 1);
+  }();
+  return d;
+}
+
+uint64_t end_budget(const BarrierArgs& b, const RailCtl& c) {
+  return c.end_timeout_ns ? c.end_timeout_ns * dilation() : b.timeout_ns;
+}
 
 // ------------------------------------------------------------- arithmetic --
 enum class DT { F32, BF16, I32 };
