@@ -1,0 +1,120 @@
+"""CPU suite: the product's HOST logic end to end, without a GPU.
+
+tests/fakecuda links the product's own object files (the same ones as
+libnezha_b200.so) against a host stand-in for the CUDA runtime whose
+"kernels" are host emulations of the rail kernels' protocols (barrier epochs,
+LL flags, launch status, gates, injected stalls). Running the loopback GPU
+tests (tests/test_gpu_vranks.py) against it exercises, on CPU: the
+virtual-rank communicator and combined launches, the rails' waves, chunk
+windows and copy-engine pipelining, the engine's hot split / Timer / staged
+host path, the failure monitor's detection, two-round agreement, reroute and
+readmit — and checks every result against the oracle.
+
+This is a check of host logic only. It says nothing about the CUDA kernels
+(their parity is the GPU suite's job), and it is never the product: the
+harness library is loaded only by the subprocesses started here
+(NEZHA_TEST_HOST_HARNESS_LIB, accepted by _lib.py for this file name only).
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HARNESS = os.path.join(ROOT, "tests", "fakecuda", "build", "libnezha_b200_hostharness.so")
+
+# A cross-section of tests/test_gpu_vranks.py that runs in about a minute on
+# the emulation (the full file, ~7 min, is `python -m pytest
+# tests/test_gpu_vranks.py -m gpu` with the same environment).
+SELECTION = " or ".join([
+    "test_loopback_rails_bit_exact and 4",
+    "test_loopback_rails_randomized and 5",
+    "test_loopback_unplanned_link_death_detected and sm-4",
+    "test_loopback_unplanned_link_death_detected and ce-2",
+    "test_loopback_engine_multirail_parity and 4",
+    "test_loopback_engine_unplanned_failover and 1",
+    "test_loopback_engine_compute_pool_parity and 1",
+    "test_loopback_engine_calibrated",
+    "test_loopback_config1_hash",
+])
+
+
+@pytest.fixture(scope="module")
+def harness():
+    r = subprocess.run(["make", "-j8", "-C", os.path.join(ROOT, "tests", "fakecuda")], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.fail("harness build failed:\n" + r.stdout[-3000:] + r.stderr[-3000:])
+    return HARNESS
+
+
+def test_loopback_suite_host_logic(harness):
+    env = dict(os.environ)
+    env.update({"NEZHA_TEST_HOST_HARNESS_LIB": harness, "NEZHA_WATCHDOG_MS": "5000",
+                "NEZHA_DETECT_US": "2000000", "PYTHONPATH": ROOT})
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_vranks.py"), "-m", "gpu",
+                        "-q", "-p", "no:cacheprovider", "--timeout", "600", "-k", SELECTION, "-rfE"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    tail = r.stdout[-6000:] + r.stderr[-3000:]
+    assert r.returncode == 0, tail
+    assert " passed" in r.stdout and "skipped" not in r.stdout.split("passed")[0][-20:], tail
+
+
+def test_harness_is_not_the_product(harness):
+    """The harness build is accepted only under its own name, and the product
+    library never exports the stand-in's runtime."""
+    env = dict(os.environ)
+    env["NEZHA_TEST_HOST_HARNESS_LIB"] = os.path.join(ROOT, "paper_2405_17870_b200", "libnezha_b200.so")
+    r = subprocess.run([sys.executable, "-c", "import paper_2405_17870_b200 as p; p.lib()"], cwd=ROOT, env=env,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "must name the test harness build" in r.stderr
+    nm = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2405_17870_b200", "libnezha_b200.so")],
+                        capture_output=True, text=True).stdout
+    assert " fakecuda_launches" not in nm and " T cudaLaunchKernel" not in nm
+
+
+def _env(harness):
+    return {"NEZHA_TEST_HOST_HARNESS_LIB": harness, "NEZHA_WATCHDOG_MS": "5000", "NEZHA_DETECT_US": "2000000"}
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multiprocess_rails_host_logic(harness, world):
+    """One process per rank (nz_comm_init: abstract-socket bootstrap, VMM fds
+    over SCM_RIGHTS, peer mappings), the SM and CE rails' direct launches:
+    the multi-GPU path's host side, checked against the oracle."""
+    import json
+
+    from tests.mp_util import spawn
+    from tests.test_gpu_rails import MULTI
+
+    cases = [c for c in MULTI if c["kind"] != "nvls" and not c.get("graph")]  # no multicast / graphs here
+    res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(cases)], timeout=600,
+                extra_env=_env(harness))
+    for rank_res in res:
+        assert len(rank_res["results"]) == len(cases)
+        for r in rank_res["results"]:
+            assert r["watchdog"] == 0 and r["mismatch"] == 0 and r["outside_nonzero"] == 0, r
+            assert r["progress"] == r["stop"], r
+
+
+def test_multiprocess_engine_failover_host_logic(harness):
+    """The engine across processes: hot split, staged host path, an unplanned
+    link death agreed by the monitors over their own socket channel, the
+    orphan rerouted, readmit after the hold — results exact on every rank."""
+    import json
+
+    from tests.mp_util import spawn
+    from tests.test_gpu_vranks import KINDS3, TOML_LOOP
+
+    spec = {"rails": KINDS3, "rails_toml": TOML_LOOP, "sync_overhead_us": 0.0, "readmit_hold_us": 100000,
+            "cases": [{"dtype": "f32", "nbytes": 24 << 20, "reps": 2},
+                      {"dtype": "bf16", "nbytes": 64 << 20, "reps": 2, "fail": [2, 3], "fail_rep": 1},
+                      {"dtype": "f32", "nbytes": (1 << 20) + 4, "reps": 1, "host": True},
+                      {"dtype": "i32", "nbytes": 16 << 20, "reps": 1, "readmit": True}]}
+    res = spawn(2, os.path.join(ROOT, "tests", "workers", "engine_worker.py"), [json.dumps(spec)], timeout=600,
+                extra_env=_env(harness))
+    for rk in res:
+        for r in rk["results"]:
+            assert r["mismatch"] == 0, r
+        fos = [r["failover"] for r in rk["results"] if r.get("failover")]
+        assert len(fos) == 1 and fos[0]["failed_rail"] == 2 and fos[0]["orphan_length"] > 0, fos
