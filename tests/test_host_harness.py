@@ -118,3 +118,14 @@ def test_multiprocess_engine_failover_host_logic(harness):
             assert r["mismatch"] == 0, r
         fos = [r["failover"] for r in rk["results"] if r.get("failover")]
         assert len(fos) == 1 and fos[0]["failed_rail"] == 2 and fos[0]["orphan_length"] > 0, fos
+
+
+def test_smoke_host_logic(harness):
+    """The driver's smoke() minus its torch-only kernel check: the 4-virtual-
+    rank engine (hot split, unplanned failover) and the N = 1 engine."""
+    env = dict(os.environ)
+    env.update(_env(harness))
+    env["PYTHONPATH"] = ROOT
+    r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g._smoke_engine(); g._smoke_single(); "
+                        "print('smoke host logic ok')"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "smoke host logic ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
