@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define NZ_ABI_VERSION 2
+#define NZ_ABI_VERSION 3
 
 enum {
   NZ_OK = 0,
@@ -194,6 +194,9 @@ typedef struct {
   uint32_t det_tag;     /* entry whose cross-rank wait timed out / was aborted here */
   uint32_t abort;       /* host -> device: stop waiting on peers (rail declared Failed) */
   uint64_t t_det_ns;    /* %globaltimer of that detection */
+  uint32_t run_tag;     /* entry whose launch passed its start barrier (every rank arrived) */
+  uint32_t reserved;
+  uint64_t t_run_ns;    /* %globaltimer of that pass */
 } nz_rail_status_t;
 int nz_rail_status(const nz_rail_t* rail, nz_rail_status_t* out);
 /* Unplanned failure injection: THIS rank's link of the rail

@@ -137,6 +137,9 @@ class RailStatus(ctypes.Structure):
         ("det_tag", c_uint32),
         ("abort", c_uint32),
         ("t_det_ns", c_uint64),
+        ("run_tag", c_uint32),
+        ("reserved", c_uint32),
+        ("t_run_ns", c_uint64),
     ]
 
 

@@ -103,6 +103,9 @@ struct nz_engine {
   };
   std::vector<PlanRecord> last_plans;
   int64_t clock_offset_ns = 0;  // %globaltimer - CLOCK_REALTIME
+  // A launch waiting at its start barrier keeps beating this long (peers'
+  // hosts may be late); NEZHA_START_GRACE_US, default 1 s.
+  double start_grace_us = 1e6;
   struct RailStat {
     uint64_t ops = 0;
     double us = 0;

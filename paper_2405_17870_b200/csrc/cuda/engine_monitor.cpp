@@ -79,6 +79,7 @@ void nz_engine::calibrateClock() {
 void nz_engine::startMonitor() {
   monitored = cfg.monitor != 0 && comm->world > 1;
   if (!monitored) return;
+  if (const char* g = getenv("NEZHA_START_GRACE_US")) start_grace_us = std::max(0.0, atof(g));
   // The stream gates are CUDA stream memory operations: check once that the
   // driver takes them (a wait that is already satisfied, then a write) on
   // every rank; without them the engine runs unmonitored (round-1 behaviour:
@@ -184,6 +185,10 @@ void nz_engine::monitorLoop() {
       // aborted so its kernels leave their waits and the failure path runs.
       const volatile nz_rail_status_t* st = rails[front.rail]->status_host;
       const bool started = st->start_tag == front.tag;
+      // Running: this launch passed its start barrier (every rank arrived)
+      // after it started, so data is moving and a stop means a broken rail.
+      const uint64_t t_start = st->t_start_ns, t_run = st->t_run_ns;
+      const bool running = started && st->run_tag == front.tag && static_cast<int64_t>(t_run - t_start) >= 0;
       const double now = nowUs();
       std::vector<int> aborted;
       {
@@ -191,13 +196,22 @@ void nz_engine::monitorLoop() {
         for (size_t i = 0; i < specs.size(); ++i) {
           if (agreed_failed.count(specs[i].rail_id)) continue;
           if (static_cast<int>(i) == front.rail && started) {
-            // Its last sign of life is the start of the launch it is in:
-            // missed beats count from there, not from queueing time.
-            const uint64_t key = (static_cast<uint64_t>(front.rail) << 32) | front.tag;
+            // Its last sign of life is the start of the launch it is in, or
+            // the moment every rank was in: missed beats count from there,
+            // not from queueing time. A launch still waiting for peers at its
+            // start barrier is not the rail failing — a peer's host may just
+            // be late (stragglers) — so it keeps beating through the start
+            // grace and only then starts missing beats.
+            const int64_t t0 = static_cast<int64_t>(running ? t_run : t_start) - clock_offset_ns;
+            const double age_us = std::max(0.0, static_cast<double>(realtimeNs() - t0) / 1000.0);
+            if (!running && age_us < start_grace_us) {
+              health->heartbeat(specs[i].rail_id, now);
+              continue;
+            }
+            const uint64_t key = (static_cast<uint64_t>(front.rail) << 33) | (static_cast<uint64_t>(running) << 32) |
+                                 front.tag;
             if (key != beat_key) {
-              const double age_us =
-                  static_cast<double>(realtimeNs() - (static_cast<int64_t>(st->t_start_ns) - clock_offset_ns)) / 1000.0;
-              health->heartbeat(specs[i].rail_id, now - std::max(0.0, age_us));
+              health->heartbeat(specs[i].rail_id, now - (running ? age_us : age_us - start_grace_us));
               beat_key = key;
             }
             continue;

@@ -128,6 +128,16 @@ __device__ __forceinline__ void note_stall(const RailCtl& c) {
   }
 }
 
+// The launch passed its start barrier: every rank is in, data moves from
+// here on (the monitor's heartbeat clock runs from this point).
+__device__ __forceinline__ void note_run(const RailCtl& c) {
+  if (c.host && blockIdx.x == 0 && threadIdx.x == 0) {
+    volatile nz_rail_status_t* h = c.host;
+    h->t_run_ns = globaltimer();
+    h->run_tag = c.tag;
+  }
+}
+
 // Exit of every CTA (every thread calls it; `ok` is uniform over the CTA).
 // The last CTA of the launch on this rank publishes the outcome.
 __device__ __forceinline__ void rail_exit(const RailCtl& c, bool ok) {
@@ -417,6 +427,7 @@ __device__ __forceinline__ void fold_body(const FoldArgs& a) {
   const uint32_t ep = op_epoch(a.bar);
   if (a.use_barrier && !cta_barrier<N, false>(a.bar, ep, a.rank, a.bar.timeout_ns, &a.ctl))
     return rail_exit(a.ctl, false);
+  if (a.use_barrier) note_run(a.ctl);
   if (a.ctl.stall) {
     note_stall(a.ctl);
     return rail_exit(a.ctl, false);
@@ -486,6 +497,7 @@ __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ Nv
   if (!rail_enter(a.f.ctl)) return rail_exit(a.f.ctl, false);
   const uint32_t ep = op_epoch(a.f.bar);
   if (!cta_barrier<N, false>(a.f.bar, ep, a.f.rank, a.f.bar.timeout_ns, &a.f.ctl)) return rail_exit(a.f.ctl, false);
+  note_run(a.f.ctl);
   if (a.f.ctl.stall) {
     note_stall(a.f.ctl);
     return rail_exit(a.f.ctl, false);
@@ -701,6 +713,7 @@ __device__ __forceinline__ void barrier_body(const BarrierKArgs& k) {
   if (!rail_enter(k.ctl)) return rail_exit(k.ctl, false);
   const uint64_t budget = k.end ? end_budget(k.bar, k.ctl) : k.bar.timeout_ns;
   if (!cta_barrier<N, true>(k.bar, op_epoch(k.bar), k.rank, budget, &k.ctl)) return rail_exit(k.ctl, false);
+  if (!k.end) note_run(k.ctl);
   if (!k.end && k.ctl.stall) {
     note_stall(k.ctl);
     return rail_exit(k.ctl, false);

@@ -76,6 +76,13 @@ void note_stall(const RailCtl& c) {
   }
 }
 
+void note_run(const RailCtl& c) {
+  if (c.host) {
+    st(&c.host->t_run_ns, gtimer());
+    st(&c.host->run_tag, c.tag);
+  }
+}
+
 void rail_exit(const RailCtl& c, bool ok) {
   if (!c.dev) return;
   if (!ok) {
@@ -217,6 +224,7 @@ void fold_body(DT d, int N, int ndst, const FoldArgs& a) {
   if (!rail_enter(a.ctl)) return rail_exit(a.ctl, false);
   const uint32_t ep = op_epoch(a.bar);
   if (a.use_barrier && !cta_barrier(N, a.bar, ep, a.rank, a.bar.timeout_ns, &a.ctl)) return rail_exit(a.ctl, false);
+  if (a.use_barrier) note_run(a.ctl);
   if (a.ctl.stall) {
     note_stall(a.ctl);
     return rail_exit(a.ctl, false);
@@ -318,6 +326,7 @@ void barrier_body(int N, const BarrierKArgs& k) {
   if (!rail_enter(k.ctl)) return rail_exit(k.ctl, false);
   const uint64_t budget = k.end ? end_budget(k.bar, k.ctl) : k.bar.timeout_ns;
   if (!cta_barrier(N, k.bar, op_epoch(k.bar), k.rank, budget, &k.ctl)) return rail_exit(k.ctl, false);
+  if (!k.end) note_run(k.ctl);
   if (!k.end && k.ctl.stall) {
     note_stall(k.ctl);
     return rail_exit(k.ctl, false);

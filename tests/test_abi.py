@@ -43,7 +43,7 @@ def test_core_known_answers_through_the_abi():
     assert l.nz_core_ring_volume(16, 0) == 0
     assert l.nz_core_bucket_of(4096) == 12 and l.nz_core_bucket_of(8191) == 12 and l.nz_core_bucket_of(8192) == 13
     assert l.nz_core_default_chunk_bytes(64 << 20, 8, 1) == 4 << 20
-    assert l.nz_abi_version() == 2 and l.nz_has_cuda_kernels() == 1
+    assert l.nz_abi_version() == 3 and l.nz_has_cuda_kernels() == 1
 
 
 def test_errors_map_to_codes_without_gpu():

@@ -129,3 +129,21 @@ def test_smoke_host_logic(harness):
     r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g._smoke_engine(); g._smoke_single(); "
                         "print('smoke host logic ok')"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "smoke host logic ok" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("grace_us,spurious", [(1_000_000, False), (0, True)])
+def test_straggler_is_not_a_rail_failure(harness, grace_us, spurious):
+    """One process per rank; one rank's host issues its allreduce 0.6 s late,
+    so the other's launch waits at its start barrier for longer than three
+    missed heartbeats (150 ms). Within the start grace that wait is not a rail
+    failure: no failover, the rail stays in the table. With the grace off the
+    heartbeat detector fires on the straggler (the behaviour the grace
+    removes); the result is exact either way."""
+    from tests.mp_util import spawn
+
+    env = _env(harness)
+    env["NEZHA_START_GRACE_US"] = str(grace_us)
+    res = spawn(2, os.path.join(ROOT, "tests", "workers", "straggler_worker.py"), ["0.6"], timeout=300, extra_env=env)
+    for r in res:
+        assert r["monitor_on"] and r["mismatch"] == 0, r
+        assert (r["failovers"] > 0) == spurious, r
