@@ -390,3 +390,14 @@ def test_loopback_engine_under_foreign_compute_load():
                 oracle.reduce_range(inputs, oracle.F32, off, length, chunk, off, off + length, want)
                 a_, b_ = off // 4, (off + length) // 4
                 assert np.array_equal(got[a_:b_].view(np.uint32), want[a_:b_].view(np.uint32))
+
+
+@pytest.mark.skipif(HOST_HARNESS, reason="run by tests/test_host_harness.py with harness streams")
+def test_loopback_ops_on_two_caller_streams():
+    """Cold and hot ops on two torch streams in turn, never synchronised in
+    between: every rail launch stays ordered after the rail's previous one."""
+    from paper_2405_17870_b200 import run_ranks
+    from tests.workers import streams_worker
+
+    for rk in run_ranks(3, streams_worker.body, timeout=600):
+        assert rk["mismatch"] == 0 and rk["hot_ops"] > 0, rk

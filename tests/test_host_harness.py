@@ -147,3 +147,29 @@ def test_straggler_is_not_a_rail_failure(harness, grace_us, spurious):
     for r in res:
         assert r["monitor_on"] and r["mismatch"] == 0, r
         assert (r["failovers"] > 0) == spurious, r
+
+
+@pytest.mark.parametrize("mode", ["processes", "virtual"])
+def test_ops_on_two_caller_streams_stay_ordered(harness, mode):
+    """Cold and hot ops issued on two caller streams in turn, never
+    synchronised in between: each rail's launches stay ordered (orderBefore /
+    orderAfter) and every result is exact. (With the ordering removed this
+    run hangs or fails: the rails' pads and LL slots are shared.)"""
+    from tests.mp_util import spawn
+
+    env = _env(harness)
+    script = os.path.join(ROOT, "tests", "workers", "streams_worker.py")
+    if mode == "processes":
+        res = spawn(2, script, [], timeout=300, extra_env=env)
+    else:
+        full = dict(os.environ)
+        full.update(env)
+        full["PYTHONPATH"] = ROOT
+        r = subprocess.run([sys.executable, script, "3"], cwd=ROOT, env=full, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+        import json
+
+        res = json.loads(r.stdout.strip().splitlines()[-1])
+    for rk in res:
+        assert rk["mismatch"] == 0 and rk["hot_ops"] > 0 and rk["ops"] == 24, rk
