@@ -418,7 +418,11 @@ void nz_engine_config_default(nz_engine_config_t* c) {
   c->tune_budgets = 0;  // on once its hardware sweep is recorded in profiles/
   c->monitor = 1;
   c->detect_us = 0;
-  c->heartbeat_us = 50000;
+  c->heartbeat_us = 50000;  // SPEC.md:380-388; NEZHA_HEARTBEAT_US overrides the default
+  if (const char* h = getenv("NEZHA_HEARTBEAT_US")) {
+    const double v = atof(h);
+    if (v > 0) c->heartbeat_us = v;
+  }
   c->readmit_hold_us = 1e6;
 }
 

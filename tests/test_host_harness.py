@@ -173,3 +173,30 @@ def test_ops_on_two_caller_streams_stay_ordered(harness, mode):
         res = json.loads(r.stdout.strip().splitlines()[-1])
     for rk in res:
         assert rk["mismatch"] == 0 and rk["hot_ops"] > 0 and rk["ops"] == 24, rk
+
+
+def test_bench_loopback_line_host_logic(harness):
+    """bench.py's N = 1 path end to end (config 1, 8 virtual ranks, e2e,
+    failover section) with torch replaced by tests/fakecuda/torch_stub.py:
+    the JSON line carries every field of the contract. Numbers are the
+    emulation's and mean nothing; the code path is what is checked."""
+    import json
+
+    env = dict(os.environ)
+    env.update(_env(harness))
+    env.update({"PYTHONPATH": ROOT, "NEZHA_HEARTBEAT_US": "5000000", "NEZHA_WATCHDOG_MS": "20000"})
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "fakecuda", "run_bench.py"), "--steps", "2",
+                        "--warmup", "3", "--no-cpu"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "gpu_launches", "clocks", "e2e"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["steps"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["config"]["ranks"] == 8 and line["config"]["same_config"]
+    assert [s[2] for s in line["config"]["plan"]] == [32 << 20, 32 << 20]  # config 1's static 50/50
+    rf = line["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["achieved"] > 0 and 0 < rf["frac"] and "traffic" in rf
+    e2e = line["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] == e2e["d2h_bytes_per_step"] == 8 * (64 << 20)
+    assert "failover" in line and line["failover"]["failed_rail"] in ("sm", "ce"), line.get("failover_error")
