@@ -47,6 +47,9 @@ class Tensor:
     def view(self, dtype):
         return Tensor(self.a.view(dtype.np), dtype)
 
+    def __getitem__(self, k):
+        return Tensor(self.a[k], self.dtype)
+
     def cpu(self):
         return self
 

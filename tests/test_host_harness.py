@@ -200,3 +200,24 @@ def test_bench_loopback_line_host_logic(harness):
     e2e = line["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] == e2e["d2h_bytes_per_step"] == 8 * (64 << 20)
     assert "failover" in line and line["failover"]["failed_rail"] in ("sm", "ce"), line.get("failover_error")
+
+
+def test_bench_multi_rank_line_host_logic(harness):
+    """bench.py's N > 1 path (one process per rank, as torchrun runs it):
+    config-1 headline, e2e, 8 KiB latency, failover + readmit; NCCL and the
+    size sweep left out (no torch.distributed / time on the harness)."""
+    import json
+
+    from tests.mp_util import spawn
+
+    env = _env(harness)
+    env.update({"NEZHA_HEARTBEAT_US": "5000000", "NEZHA_WATCHDOG_MS": "20000"})
+    res = spawn(2, os.path.join(ROOT, "tests", "fakecuda", "run_bench.py"),
+                ["--gpus", "2", "--steps", "2", "--warmup", "3", "--no-nccl", "--no-sweep", "--latency-ops", "20",
+                 "--tune-ops", "2"], timeout=1200, extra_env=env)
+    line = res[0]
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0, line
+    assert line["roofline"]["bound"] == "nvlink" and line["e2e"]["h2d_bytes_per_step"] == 64 << 20
+    assert set(line["latency_8k"]) >= {"ops", "engine", "ce_alone", "sm_alone"}
+    assert "failover" in line and "readmit_error" not in line, (line.get("failover_error"), line.get("readmit_error"))
+    assert res[1] == {}  # only rank 0 prints the line
