@@ -33,7 +33,9 @@
 // the host sizes to be co-resident.
 #pragma once
 
+#ifndef NZ_SIMT_HOST
 #include <cuda_bf16.h>
+#endif
 #include <stdint.h>
 
 #include "kernel_args.h"
@@ -43,6 +45,11 @@ namespace nz {
 
 
 // ------------------------------------------------------------ primitives --
+// NZ_SIMT_HOST: the CPU test harness (tests/fakecuda/simt.h) supplies host
+// versions of these and runs this file's kernels on host fibers.
+#ifndef NZ_SIMT_HOST
+#define NZ_SHARED(T, name) __shared__ T name
+
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -73,6 +80,18 @@ __device__ __forceinline__ uint4 ld_v4(const void* p) {
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+
+// LL (K5): one 16-byte store of two {data, flag} words to a peer's slot; one
+// 8-byte poll of a {data, flag} word in this rank's slots.
+__device__ __forceinline__ void ll_push_pair(uint64_t* dst, uint32_t d0, uint32_t flag, uint32_t d1) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(flag), "r"(d1), "r"(flag)
+               : "memory");
+}
+
+__device__ __forceinline__ void ll_poll_word(const uint64_t* src, uint32_t* d, uint32_t* f) {
+  asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(*d), "=r"(*f) : "l"(src) : "memory");
+}
+#endif  // NZ_SIMT_HOST
 
 // ------------------------------------------------------ launch status ------
 __device__ __forceinline__ uint32_t seq_read(const uint32_t* seq) {
@@ -175,7 +194,7 @@ __device__ __forceinline__ void rail_exit(const RailCtl& c, bool ok) {
 template <int N, bool kPublish>
 __device__ __forceinline__ bool cta_barrier(const BarrierArgs& b, uint32_t epoch, int rank, uint64_t timeout_ns,
                                             const RailCtl* ctl) {
-  __shared__ int s_ok;
+  NZ_SHARED(int, s_ok);
   if (threadIdx.x == 0) s_ok = 1;
   if (kPublish) fence_acq_rel_sys();
   __syncthreads();
@@ -453,6 +472,8 @@ __global__ void __launch_bounds__(512, 2) fold_kernel_vr(const __grid_constant__
 template <typename DT>
 __device__ __forceinline__ uint4 mm_ld_reduce(const char* p);
 
+#ifndef NZ_SIMT_HOST
+
 #define NZ_MM_LDR(TY)                                                                            \
   asm volatile("multimem.ld_reduce.relaxed.sys.global.add." TY " {%0,%1,%2,%3}, [%4];"         \
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)                                    \
@@ -490,6 +511,7 @@ __device__ __forceinline__ void mm_st(char* p, uint4 v) {
                "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
                : "memory");
 }
+#endif  // NZ_SIMT_HOST (the harness's multicast emulation: tests/fakecuda/simt.h)
 
 template <typename DT, int N>
 __global__ void __launch_bounds__(512, 2) nvls_kernel(const __grid_constant__ NvlsArgs a) {
@@ -608,9 +630,7 @@ __device__ __forceinline__ void ll_body(const LLArgs& a) {
     const uint32_t d1 = x + 4 < a.hi ? ll_load_word(a.in, x + 4, a.hi) : 0u;
 #pragma unroll
     for (int r = 0; r < N; ++r) {
-      uint64_t* dst = a.peer[r] + my_slot + 2 * p;
-      asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dst), "r"(d0), "r"(flag), "r"(d1), "r"(flag)
-                   : "memory");
+      ll_push_pair(a.peer[r] + my_slot + 2 * p, d0, flag, d1);
     }
   }
   // A peer's words never arrived (watchdog), or the ranks already agreed
@@ -630,7 +650,7 @@ __device__ __forceinline__ void ll_body(const LLArgs& a) {
       int spins = 0;
       uint64_t t0 = 0;
       for (;;) {
-        asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(d), "=r"(f) : "l"(src) : "memory");
+        ll_poll_word(src, &d, &f);
         if (f == flag) break;
         if (++spins == 256) {
           spins = 0;

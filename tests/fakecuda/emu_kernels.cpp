@@ -1,5 +1,8 @@
-// TEST HARNESS ONLY (see fakecuda.cpp): host emulations of the rail kernels'
-// protocols, following csrc/cuda/kernels.cuh step by step — launch status
+// TEST HARNESS ONLY (see fakecuda.cpp): launch dispatch of the harness. By
+// default a launch runs the kernel source itself on fibers (simtKernel,
+// simt_kernels.cpp). With FAKECUDA_SIMT=0 it runs the host restatements
+// below: emulations of the rail kernels' protocols, following
+// csrc/cuda/kernels.cuh step by step — launch status
 // (rail_enter / rail_exit), per-CTA barriers with epochs and budgets, the
 // injected stall, the ring-order fold, the LL flag protocol, fault posts.
 // A launch's grid is emulated as ONE CTA per rank (barrier slot 0): the
@@ -401,15 +404,36 @@ std::map<std::string, uint64_t> g_counts;
 
 }  // namespace
 
+namespace nzsimt {
+uint64_t end_dilation() { return dilation(); }
+}  // namespace nzsimt
+
 namespace fakecuda {
+
+std::function<void()> simtKernel(const std::string& base, const std::vector<std::string>& targs, dim3 grid, dim3 block,
+                                 void** args);
+
+// FAKECUDA_SIMT=1 (the default): the kernels of csrc/cuda/kernels.cuh run
+// themselves, on host fibers (simt.h). 0: the protocol restatements above
+// (used by the sanitizer builds, which do not follow fiber stack switches).
+bool simtMode() {
+  static const bool on = [] {
+    const char* e = getenv("FAKECUDA_SIMT");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
 
 void countLaunch(const std::string& name) {
   std::lock_guard<std::mutex> lk(g_count_mu);
   ++g_counts[parse(name).base];
 }
 
-std::function<void()> emulatedKernel(const std::string& name, dim3, dim3, void** args) {
+std::function<void()> emulatedKernel(const std::string& name, dim3 grid, dim3 block, void** args) {
   const Parsed k = parse(name);
+  if (simtMode()) {
+    if (auto f = simtKernel(k.base, k.targs, grid, block, args)) return f;
+  }
   if (k.base == "fold_kernel" && k.targs.size() == 3) {
     const DT d = dtOf(k.targs[0]);
     const int N = std::stoi(k.targs[1]), nd = std::stoi(k.targs[2]);

@@ -6,15 +6,18 @@
 // run in the CPU test suite, where there is no GPU. Streams are worker
 // threads, device memory is host memory (VMM allocations are memfd mappings,
 // so several virtual addresses can alias one allocation as they do on the
-// device), and each kernel of csrc/cuda/kernels.cuh is replaced by a host
-// emulation of its PROTOCOL (emu_kernels.cpp): barrier epochs, LL flags,
-// launch status, sticky failure, gate release, injected stalls, timeouts.
+// device), and each kernel launch runs csrc/cuda/kernels.cuh ITSELF on host
+// fibers (simt.h / simt.cpp / simt_kernels.cpp: one fiber per CUDA thread,
+// per-CTA __syncthreads, yielding cross-rank polls). FAKECUDA_SIMT=0 selects
+// the older host restatements of the kernels' protocols (emu_kernels.cpp),
+// which the sanitizer builds use.
 //
 // What it checks: that the host code issues the right launches, on the
-// right streams, with the right geometry, waits and gates, and that its
-// control flow (agreement, reroute, readmit, pipelining) terminates with the
-// right results. What it does not check: the CUDA kernels themselves, memory
-// ordering on the GPU, timing. Parity claims rest on the GPU tests only.
+// right streams, with the right geometry, waits and gates, that its control
+// flow (agreement, reroute, readmit, pipelining) terminates with the right
+// results, and that the kernel source computes them bit-exactly. What it does
+// not check: the compiled SASS, memory ordering across GPUs, NVLink /
+// multicast, timing. Hardware parity claims rest on the GPU tests.
 //
 // Built into tests/fakecuda/build/libnezha_b200_hostharness.so together with
 // the product's own object files (linked -Bsymbolic so nothing else in the
@@ -197,7 +200,45 @@ thread_local std::vector<LaunchConfig> t_config;
 struct Alloc {
   int fd = -1;
   size_t size = 0;
+  struct McTable* mc = nullptr;  // a multicast object (FAKECUDA_MULTICAST=1)
 };
+
+// ---------------------------------------------------- NVSwitch multicast --
+// FAKECUDA_MULTICAST=1: a multicast object is a small shared table (memfd,
+// travels between rank processes like any VMM handle) in which every bound
+// rank records its process id and a descriptor of its memory. Mapping the
+// object reserves an INACCESSIBLE window: plain loads / stores there fault,
+// and the kernels' multimem accesses (simt.h) resolve an address of the
+// window to every member's memory at the same offset (/proc/<pid>/fd/<fd>),
+// reduce or store across them, and trap on a misaligned 16-byte access —
+// the round-1 NVLink incident's class of bug.
+constexpr uint64_t kMcMagic = 0x4e5a4d4354424c31ull;  // "NZMCTBL1"
+struct McTable {
+  uint64_t magic;
+  uint32_t ndev;
+  uint32_t nbound;
+  struct {
+    int32_t pid, fd;
+    uint64_t size;
+  } member[8];
+};
+
+struct McWindow {
+  char* va;
+  size_t size;
+  McTable* table;
+  std::vector<char*> bases;  // members' memory mapped here, once all are bound
+};
+std::mutex g_mc_mu;
+std::map<char*, McWindow> g_mc_windows;
+
+bool multicastOn() {
+  static const bool on = [] {
+    const char* e = getenv("FAKECUDA_MULTICAST");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
 
 constexpr size_t kGranularity = 2u << 20;
 
@@ -464,7 +505,9 @@ CUresult fDeviceGet(CUdevice* d, int ordinal) {
   return CUDA_SUCCESS;
 }
 CUresult fDeviceGetAttribute(int* v, CUdevice_attribute a, CUdevice) {
-  *v = a == CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT ? fakecuda::kSMs : 0;  // no multicast
+  *v = a == CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT ? fakecuda::kSMs
+       : a == CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED ? (multicastOn() ? 1 : 0)
+                                                       : 0;
   return CUDA_SUCCESS;
 }
 CUresult fGetErrorString(CUresult e, const char** s) {
@@ -477,8 +520,15 @@ CUresult fGranularity(size_t* g, const CUmemAllocationProp*, CUmemAllocationGran
   *g = kGranularity;
   return CUDA_SUCCESS;
 }
-CUresult fMcGranularity(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) {
-  return CUDA_ERROR_NOT_SUPPORTED;
+CUresult fMcGranularity(size_t* g, const CUmulticastObjectProp*, CUmulticastGranularity_flags) {
+  if (!multicastOn()) return CUDA_ERROR_NOT_SUPPORTED;
+  *g = kGranularity;
+  return CUDA_SUCCESS;
+}
+
+McTable* mapTable(int fd) {
+  void* p = mmap(nullptr, sizeof(McTable), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  return p == MAP_FAILED ? nullptr : static_cast<McTable*>(p);
 }
 CUresult fMemCreate(CUmemGenericAllocationHandle* h, size_t size, const CUmemAllocationProp*, unsigned long long) {
   const int fd = memfd_create("fakecuda", MFD_CLOEXEC);
@@ -497,12 +547,26 @@ CUresult fAddressReserve(CUdeviceptr* va, size_t size, size_t, CUdeviceptr, unsi
 }
 CUresult fMemMap(CUdeviceptr va, size_t size, size_t offset, CUmemGenericAllocationHandle h, unsigned long long) {
   auto* a = reinterpret_cast<Alloc*>(h);
+  if (a->mc) {  // the window stays PROT_NONE: only multimem accesses may touch it
+    std::lock_guard<std::mutex> lk(g_mc_mu);
+    g_mc_windows[reinterpret_cast<char*>(va)] = McWindow{reinterpret_cast<char*>(va), size, a->mc, {}};
+    return offset == 0 ? CUDA_SUCCESS : CUDA_ERROR_INVALID_VALUE;
+  }
   void* p = mmap(reinterpret_cast<void*>(va), size, PROT_READ | PROT_WRITE, MAP_SHARED | MAP_FIXED, a->fd,
                  static_cast<off_t>(offset));
   return p == MAP_FAILED ? CUDA_ERROR_INVALID_VALUE : CUDA_SUCCESS;
 }
 CUresult fSetAccess(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) { return CUDA_SUCCESS; }
 CUresult fMemUnmap(CUdeviceptr va, size_t size) {
+  {
+    std::lock_guard<std::mutex> lk(g_mc_mu);
+    auto it = g_mc_windows.find(reinterpret_cast<char*>(va));
+    if (it != g_mc_windows.end()) {
+      for (size_t i = 0; i < it->second.bases.size(); ++i) munmap(it->second.bases[i], it->second.table->member[i].size);
+      g_mc_windows.erase(it);
+      return CUDA_SUCCESS;
+    }
+  }
   // Back to a reserved, inaccessible range (as after cuMemUnmap).
   void* p = mmap(reinterpret_cast<void*>(va), size, PROT_NONE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_FIXED | MAP_NORESERVE,
                  -1, 0);
@@ -514,6 +578,7 @@ CUresult fAddressFree(CUdeviceptr va, size_t size) {
 }
 CUresult fMemRelease(CUmemGenericAllocationHandle h) {
   auto* a = reinterpret_cast<Alloc*>(h);
+  if (a->mc) munmap(a->mc, sizeof(McTable));
   close(a->fd);
   delete a;
   return CUDA_SUCCESS;
@@ -526,16 +591,52 @@ CUresult fImport(CUmemGenericAllocationHandle* h, void* os, CUmemAllocationHandl
   const int fd = dup(static_cast<int>(reinterpret_cast<intptr_t>(os)));
   struct stat stt {};
   fstat(fd, &stt);
-  *h = reinterpret_cast<CUmemGenericAllocationHandle>(new Alloc{fd, static_cast<size_t>(stt.st_size)});
+  auto* a = new Alloc{fd, static_cast<size_t>(stt.st_size)};
+  if (multicastOn() && a->size == sizeof(McTable)) {  // VMM allocations are 2 MiB multiples
+    McTable* t = mapTable(fd);
+    if (t && t->magic == kMcMagic) {
+      a->mc = t;
+    } else if (t) {
+      munmap(t, sizeof(McTable));
+    }
+  }
+  *h = reinterpret_cast<CUmemGenericAllocationHandle>(a);
   return CUDA_SUCCESS;
 }
-CUresult fMcCreate(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) { return CUDA_ERROR_NOT_SUPPORTED; }
-CUresult fMcAdd(CUmemGenericAllocationHandle, CUdevice) { return CUDA_ERROR_NOT_SUPPORTED; }
-CUresult fMcBind(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
-                 unsigned long long) {
-  return CUDA_ERROR_NOT_SUPPORTED;
+CUresult fMcCreate(CUmemGenericAllocationHandle* h, const CUmulticastObjectProp* prop) {
+  if (!multicastOn()) return CUDA_ERROR_NOT_SUPPORTED;
+  if (prop->numDevices < 1 || prop->numDevices > 8) return CUDA_ERROR_INVALID_VALUE;
+  const int fd = memfd_create("fakecuda-mc", MFD_CLOEXEC);
+  if (fd < 0 || ftruncate(fd, sizeof(McTable)) != 0) return CUDA_ERROR_OUT_OF_MEMORY;
+  McTable* t = mapTable(fd);
+  if (!t) return CUDA_ERROR_OUT_OF_MEMORY;
+  t->magic = kMcMagic;
+  t->ndev = prop->numDevices;
+  *h = reinterpret_cast<CUmemGenericAllocationHandle>(new Alloc{fd, sizeof(McTable), t});
+  return CUDA_SUCCESS;
 }
-CUresult fMcUnbind(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) { return CUDA_ERROR_NOT_SUPPORTED; }
+CUresult fMcAdd(CUmemGenericAllocationHandle h, CUdevice) {
+  return reinterpret_cast<Alloc*>(h)->mc ? CUDA_SUCCESS : CUDA_ERROR_INVALID_VALUE;
+}
+CUresult fMcBind(CUmemGenericAllocationHandle h, size_t mc_off, CUmemGenericAllocationHandle mem, size_t mem_off,
+                 size_t size, unsigned long long) {
+  McTable* t = reinterpret_cast<Alloc*>(h)->mc;
+  auto* m = reinterpret_cast<Alloc*>(mem);
+  if (!t || mc_off != 0 || mem_off != 0 || size > m->size) return CUDA_ERROR_INVALID_VALUE;
+  // Claim a member slot (ranks bind concurrently from their own processes).
+  for (uint32_t i = 0; i < t->ndev; ++i) {
+    int32_t expect = 0;
+    if (__atomic_compare_exchange_n(&t->member[i].pid, &expect, static_cast<int32_t>(getpid()), false,
+                                    __ATOMIC_ACQ_REL, __ATOMIC_ACQUIRE)) {
+      t->member[i].fd = dup(m->fd);  // kept open while the process lives: peers reopen it by /proc path
+      t->member[i].size = size;
+      __atomic_fetch_add(&t->nbound, 1u, __ATOMIC_RELEASE);
+      return CUDA_SUCCESS;
+    }
+  }
+  return CUDA_ERROR_INVALID_VALUE;
+}
+CUresult fMcUnbind(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) { return CUDA_SUCCESS; }
 CUresult fWaitValue32(CUstream s, CUdeviceptr addr, cuuint32_t value, unsigned int flags) {
   if ((flags & 0x3) != CU_STREAM_WAIT_VALUE_GEQ) return CUDA_ERROR_NOT_SUPPORTED;
   S(reinterpret_cast<cudaStream_t>(s))->push([addr, value] {
@@ -552,6 +653,37 @@ CUresult fWriteValue32(CUstream s, CUdeviceptr addr, cuuint32_t value, unsigned 
 }
 
 }  // namespace
+
+// The members' memory behind a multicast window address (simt.h's multimem
+// accesses): fills bases[] with each member's address of the same offset.
+extern "C" int fakecuda_mc_resolve(const void* addr, char** bases, int max) {
+  char* a = static_cast<char*>(const_cast<void*>(addr));
+  std::lock_guard<std::mutex> lk(g_mc_mu);
+  auto it = g_mc_windows.upper_bound(a);
+  if (it == g_mc_windows.begin()) return -1;
+  --it;
+  McWindow& w = it->second;
+  if (a >= w.va + w.size) return -1;
+  if (w.bases.empty()) {
+    const uint32_t n = __atomic_load_n(&w.table->nbound, __ATOMIC_ACQUIRE);
+    if (n != w.table->ndev) return -2;  // accessed before every rank bound (the product's exchange prevents it)
+    for (uint32_t i = 0; i < n; ++i) {
+      char path[64];
+      snprintf(path, sizeof(path), "/proc/%d/fd/%d", w.table->member[i].pid, w.table->member[i].fd);
+      const int fd = open(path, O_RDWR | O_CLOEXEC);
+      void* p = fd < 0 ? MAP_FAILED
+                       : mmap(nullptr, w.table->member[i].size, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+      if (fd >= 0) close(fd);
+      if (p == MAP_FAILED) return -3;
+      w.bases.push_back(static_cast<char*>(p));
+    }
+  }
+  const size_t off = static_cast<size_t>(a - w.va);
+  const int n = static_cast<int>(w.bases.size());
+  if (n > max) return -1;
+  for (int i = 0; i < n; ++i) bases[i] = w.bases[i] + off;
+  return n;
+}
 
 extern "C" cudaError_t cudaGetDriverEntryPoint(const char* symbol, void** fn, unsigned long long,
                                                cudaDriverEntryPointQueryResult* q) {

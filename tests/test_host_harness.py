@@ -1,17 +1,20 @@
 """CPU suite: the product's HOST logic end to end, without a GPU.
 
 tests/fakecuda links the product's own object files (the same ones as
-libnezha_b200.so) against a host stand-in for the CUDA runtime whose
-"kernels" are host emulations of the rail kernels' protocols (barrier epochs,
-LL flags, launch status, gates, injected stalls). Running the loopback GPU
+libnezha_b200.so) against a host stand-in for the CUDA runtime whose kernel
+launches run the product's CUDA kernel source itself on host fibers
+(tests/fakecuda/simt.h: one fiber per CUDA thread, per-CTA __syncthreads,
+cross-rank polls that yield; barrier epochs, LL flags, launch status, gates
+and injected stalls are the kernels' own code). Running the loopback GPU
 tests (tests/test_gpu_vranks.py) against it exercises, on CPU: the
 virtual-rank communicator and combined launches, the rails' waves, chunk
 windows and copy-engine pipelining, the engine's hot split / Timer / staged
 host path, the failure monitor's detection, two-round agreement, reroute and
 readmit — and checks every result against the oracle.
 
-This is a check of host logic only. It says nothing about the CUDA kernels
-(their parity is the GPU suite's job), and it is never the product: the
+It checks host logic and the kernel SOURCE (arithmetic, order, walking,
+protocols). It says nothing about the compiled SASS, cross-GPU memory
+ordering, NVLink or timing (the GPU suite's job), and it is never the product: the
 harness library is loaded only by the subprocesses started here
 (NEZHA_TEST_HOST_HARNESS_LIB, accepted by _lib.py for this file name only).
 """
@@ -73,23 +76,57 @@ def test_harness_is_not_the_product(harness):
     assert " fakecuda_launches" not in nm and " T cudaLaunchKernel" not in nm
 
 
+def test_multiprocess_engine_nvls_host_logic(harness):
+    """The engine across processes with the NVLS rail (emulated multicast):
+    cold plans on NVLS, the staged host and device paths, an unplanned NVLS
+    link death rerouted to a survivor, readmit — exact on every rank."""
+    import json
+
+    from tests.mp_util import spawn
+    from tests.test_gpu_engine import TOML3
+
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4, "readmit_hold_us": 100000,
+            "cases": [{"dtype": "f32", "nbytes": 24 << 20, "reps": 3},
+                      {"dtype": "bf16", "nbytes": (6 << 20) + 2, "reps": 1, "host": True},
+                      {"dtype": "i32", "nbytes": 12, "reps": 1},
+                      {"dtype": "bf16", "nbytes": 64 << 20, "reps": 2, "fail": [0, 3], "fail_rep": 1},
+                      {"dtype": "i32", "nbytes": 16 << 20, "reps": 1, "readmit": True},
+                      {"dtype": "f32", "nbytes": (8 << 20) + 4, "reps": 1, "device": True}]}
+    env = _env(harness)
+    env["FAKECUDA_MULTICAST"] = "1"
+    res = spawn(2, os.path.join(ROOT, "tests", "workers", "engine_worker.py"), [json.dumps(spec)], timeout=600,
+                extra_env=env)
+    for rk in res:
+        for r in rk["results"]:
+            assert r["mismatch"] == 0, r
+        fos = [r["failover"] for r in rk["results"] if r.get("failover")]
+        assert len(fos) == 1 and fos[0]["failed_rail"] == 0 and fos[0]["target_rail"] != 0, fos
+        assert fos[0]["orphan_length"] > 0, fos
+
+
 def _env(harness):
     return {"NEZHA_TEST_HOST_HARNESS_LIB": harness, "NEZHA_WATCHDOG_MS": "5000", "NEZHA_DETECT_US": "2000000"}
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_multiprocess_rails_host_logic(harness, world):
+@pytest.mark.parametrize("world,multicast", [(2, 0), (3, 0), (2, 1), (4, 1)])
+def test_multiprocess_rails_host_logic(harness, world, multicast):
     """One process per rank (nz_comm_init: abstract-socket bootstrap, VMM fds
-    over SCM_RIGHTS, peer mappings), the SM and CE rails' direct launches:
-    the multi-GPU path's host side, checked against the oracle."""
+    over SCM_RIGHTS, peer mappings), the rails' direct launches: the
+    multi-GPU path's host side and kernel source, checked against the oracle.
+    multicast=1 emulates the NVSwitch multicast object (FAKECUDA_MULTICAST:
+    a bound team table, an inaccessible window, multimem accesses resolved to
+    every member and trapping when misaligned), so the NVLS rail's kernel
+    (K1) runs too."""
     import json
 
     from tests.mp_util import spawn
     from tests.test_gpu_rails import MULTI
 
-    cases = [c for c in MULTI if c["kind"] != "nvls" and not c.get("graph")]  # no multicast / graphs here
+    cases = [c for c in MULTI if (multicast or c["kind"] != "nvls") and not c.get("graph")]  # no graphs here
+    env = _env(harness)
+    env["FAKECUDA_MULTICAST"] = str(multicast)
     res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(cases)], timeout=600,
-                extra_env=_env(harness))
+                extra_env=env)
     for rank_res in res:
         assert len(rank_res["results"]) == len(cases)
         for r in rank_res["results"]:
@@ -221,3 +258,26 @@ def test_bench_multi_rank_line_host_logic(harness):
     assert set(line["latency_8k"]) >= {"ops", "engine", "ce_alone", "sm_alone"}
     assert "failover" in line and "readmit_error" not in line, (line.get("failover_error"), line.get("readmit_error"))
     assert res[1] == {}  # only rank 0 prints the line
+
+
+@pytest.mark.parametrize("world,preempt", [(2, 0), (5, 0), (8, 0), (4, 20), (7, 20)])
+def test_kernel_source_on_host_fibers(harness, world, preempt):
+    """The rails' CUDA kernels themselves (csrc/cuda/kernels.cuh compiled for
+    the host SIMT stand-in, tests/fakecuda/simt.h: one fiber per CUDA thread,
+    per-CTA __syncthreads, yielding cross-rank polls) run the loopback rail
+    cases — SM two-shot fold with its barriers, LL one-shot, CE barriers and
+    reduce, ragged bf16 / i32 geometries, chunk windows, trace-form failures,
+    random geometries — bit-exact against the oracle. preempt > 0 fuzzes the
+    schedule: random yields at every data load / store and a shuffled fiber
+    order per pass."""
+    import json
+
+    env = dict(os.environ)
+    env.update(_env(harness))
+    env.update({"FAKECUDA_SIMT": "1", "FAKECUDA_SIMT_PREEMPT": str(preempt), "FAKECUDA_SIMT_SEED": str(world),
+                "PYTHONPATH": ROOT})
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "workers", "simt_rails.py"), str(world),
+                        str(300 + world)], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    out = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert out["grids"] > 0 and out["threads"] >= out["grids"] * 32, out  # the kernels ran, on fibers
