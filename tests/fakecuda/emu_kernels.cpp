@@ -410,8 +410,13 @@ uint64_t end_dilation() { return dilation(); }
 
 namespace fakecuda {
 
+#ifndef FAKECUDA_NO_SIMT
 std::function<void()> simtKernel(const std::string& base, const std::vector<std::string>& targs, dim3 grid, dim3 block,
                                  void** args);
+#else
+// Sanitizer builds (tools/harness_sanitize.sh): no fibers, protocol restatements only.
+std::function<void()> simtKernel(const std::string&, const std::vector<std::string>&, dim3, dim3, void**) { return {}; }
+#endif
 
 // FAKECUDA_SIMT=1 (the default): the kernels of csrc/cuda/kernels.cuh run
 // themselves, on host fibers (simt.h). 0: the protocol restatements above

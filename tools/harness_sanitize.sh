@@ -1,8 +1,10 @@
 #!/bin/bash
 # Host-logic harness (tests/fakecuda) under ThreadSanitizer or
 # AddressSanitizer: the product's host sources rebuilt with the sanitizer
-# (kernels as PTX only: the harness never runs them), linked against the
-# harness, then a loopback engine run with an unplanned failover and readmit.
+# (kernels as PTX only), linked against the harness with its protocol
+# restatements of the kernels (FAKECUDA_NO_SIMT: the sanitizers do not follow
+# the SIMT stand-in's fiber stack switches), then a loopback engine run with
+# an unplanned failover and readmit.
 #   bash tools/harness_sanitize.sh tsan|asan
 # TSan's expected reports: the failure monitor's volatile reads of the
 # host-mapped launch status (written by the "device"); anything else is a
@@ -26,7 +28,7 @@ done
 wait
 cd $ROOT/tests/fakecuda
 for f in fakecuda emu_kernels; do
-  /usr/bin/g++ -std=c++20 -O1 -g -fPIC $FLAG -I$ROOT/include -I$CU/include -I$ROOT/paper_2405_17870_b200/csrc/cuda -I. \
+  /usr/bin/g++ -std=c++20 -O1 -g -fPIC $FLAG -DFAKECUDA_NO_SIMT -I$ROOT/include -I$CU/include -I$ROOT/paper_2405_17870_b200/csrc/cuda -I. \
     -c $f.cpp -o $OUT/$f.o
 done
 /usr/bin/g++ -shared $FLAG -Wl,-Bsymbolic -o $OUT/libnezha_b200_hostharness.so $OUT/fakecuda.o $OUT/emu_kernels.o \
