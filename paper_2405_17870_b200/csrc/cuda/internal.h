@@ -121,10 +121,12 @@ struct nz_comm {
   nz_buf* ctrl = nullptr;  // barrier pads, one kPadBytes region per rail
   int next_pad = 0;
   std::vector<int> free_pads;  // returned by destroyed rails (same order on every rank)
-  // Rails alive on this rank: the loopback co-residency divisor is
-  // live_rails + (live_twins ? 1 : 0), since the engine's monitor runs one
-  // recovery (one twin grid) at a time.
+  // Rails alive on this rank, for the loopback co-residency budget
+  // (rails.cu combine): live_big = rails whose combined grids are large (SM:
+  // two-shot fold, LL); copy-engine rails only combine one-CTA barriers.
+  // The engine's monitor runs one recovery (one twin grid) at a time.
   int live_rails = 0;
+  int live_big = 0;
   int live_twins = 0;
 };
 

@@ -212,9 +212,26 @@ void dispatchBarrier(int world, const BarrierKArgs& k, cudaStream_t st) {
 // Loopback: the last virtual rank to reach this launch runs one grid for all
 // of them (blockIdx.y = rank) on the pad's group stream, ordered after every
 // rank's stream and before each rank's next work. The grid is capped so that
-// every rail of the comm (plus the one recovery twin that can be running)
-// can have its grid resident at once: the cross-rank waits inside are then
-// between co-resident CTAs, and no grid waits on another launch.
+// every cross-rank grid that can run at once is resident at once — the
+// cross-rank waits inside are then between co-resident CTAs, and no grid
+// waits on another launch:
+//   * copy-engine rails combine only their start / end barriers (N CTAs of
+//     32 threads): kLoopReserveSMs hold all of them;
+//   * the one recovery twin the monitor may be running gets kLoopTwinSMs;
+//   * the SM-kind rails (two-shot fold, LL) share the rest evenly.
+// Units are each kernel's own resident CTAs per SM (occupancy x SMs).
+constexpr int kLoopReserveSMs = 2;
+constexpr int kLoopTwinSMs = 8;
+
+int loopCap(const nz_rail* r, int kind, int dtype) {
+  const nz_comm* c = r->comm;
+  const int N = c->world;
+  const int occ = std::max(1, loopOccupancy(kind, N, dtype));
+  if (r->recovery) return std::max(1, occ * kLoopTwinSMs / N);
+  const int avail = std::max(1, c->sm_count - kLoopReserveSMs - (c->live_twins ? kLoopTwinSMs : 0));
+  return std::max(1, occ * avail / (N * std::max(1, c->live_big)));
+}
+
 template <typename A>
 void combine(nz_rail* r, int kind, int dtype, const A& a, int grid, cudaStream_t st) {
   nz_comm* c = r->comm;
@@ -242,9 +259,7 @@ void combine(nz_rail* r, int kind, int dtype, const A& a, int grid, cudaStream_t
     if (err.empty()) {
       try {
         for (int p = 0; p < N; ++p) NZ_CUDA(cudaStreamWaitEvent(L.stream, L.ready[p], 0));
-        const int occ = std::max(1, loopOccupancy(kind, N, dtype));
-        const int slots = std::max(1, c->live_rails + (c->live_twins ? 1 : 0));
-        const int cap_ctas = std::max(1, occ * c->sm_count / (N * slots));
+        const int cap_ctas = kind == kLoopBarrier ? 1 : loopCap(r, kind, dtype);
         std::pair<cudaEvent_t, cudaEvent_t>* tp = nullptr;
         if (L.timing) {
           if (L.tev_used == L.tev.size()) {
@@ -649,6 +664,17 @@ void railRevive(nz_rail* r, cudaStream_t st) {
   r->stall_chunk = -1;
 }
 
+// The comm's live-rail counts (loopback co-residency budget, loopCap).
+static void countLive(const nz_rail* r, int d) {
+  nz_comm* c = r->comm;
+  if (r->recovery) {
+    c->live_twins = std::max(0, c->live_twins + d);
+    return;
+  }
+  c->live_rails = std::max(0, c->live_rails + d);
+  if (r->kind != NZ_RAIL_CE) c->live_big = std::max(0, c->live_big + d);
+}
+
 nz_rail* railCreate(nz_comm* comm, int kind, int rail_id, int sm_budget, bool graph_safe, bool recovery) {
   if (kind < NZ_RAIL_NVLS || kind > NZ_RAIL_SM) fail(NZ_ERR_INVALID, "unknown rail kind");
   if (kind == NZ_RAIL_NVLS && comm->world > 1 && !comm->multicast) {
@@ -731,11 +757,11 @@ nz_rail* railCreate(nz_comm* comm, int kind, int rail_id, int sm_budget, bool gr
       r->lr = slot.get();
     }
   } catch (...) {
-    (recovery ? comm->live_twins : comm->live_rails)++;  // railDestroy returns the pad and the count
+    countLive(r, +1);  // railDestroy returns the pad and the counts
     railDestroy(r);
     throw;
   }
-  (recovery ? comm->live_twins : comm->live_rails)++;
+  countLive(r, +1);
   return r;
 }
 
@@ -773,8 +799,7 @@ void railDestroy(nz_rail* r) {
   if (r->status_host) cudaFreeHost(r->status_host);
   if (r->ctl_dev) cudaFree(r->ctl_dev);
   comm->free_pads.push_back(r->pad);
-  int& live = r->recovery ? comm->live_twins : comm->live_rails;
-  live = std::max(0, live - 1);
+  countLive(r, -1);
   delete r;
 }
 

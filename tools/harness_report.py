@@ -70,6 +70,32 @@ def rails_multiprocess(world: int, multicast: int) -> dict:
     return rec
 
 
+def engine_multiprocess(world: int) -> dict:
+    """Config-4 shape on the emulated NVSwitch box: 256 MiB bf16 through the
+    engine (NVLS + CE + SM), one rank's NVLS link dies mid-op (unplanned),
+    the ranks agree and reroute, then readmit (int32, exact on every rail)."""
+    from tests.mp_util import spawn
+    from tests.test_gpu_engine import TOML3
+
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000,
+            "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 2, "fail": [0, 3], "fail_rep": 1},
+                      {"dtype": "i32", "nbytes": 64 << 20, "reps": 1, "readmit": True},
+                      {"dtype": "f32", "nbytes": 8192, "reps": 2}]}
+    env = dict(ENV)
+    env["FAKECUDA_MULTICAST"] = "1"
+    t0 = time.time()
+    res = spawn(world, os.path.join(ROOT, "tests", "workers", "engine_worker.py"), [json.dumps(spec)], timeout=1800,
+                extra_env=env)
+    bad = sum(r["mismatch"] != 0 for rk in res for r in rk["results"])
+    fos = [{k: f[k] for k in ("failed_rail", "target_rail", "orphan_offset", "orphan_length", "orphan_chunk")}
+           for rk in res[:1] for r in rk["results"] if (f := r.get("failover"))]
+    rec = {"cmd": f"tests/workers/engine_worker.py x {world} processes (config-4 shape)",
+           "env": {"FAKECUDA_MULTICAST": 1}, "rc": 0, "seconds": round(time.time() - t0, 1),
+           "result": {"world": world, "ops": sum(len(rk["results"]) for rk in res), "bad": bad, "failovers_rank0": fos}}
+    print(json.dumps(rec), flush=True)
+    return rec
+
+
 def main() -> None:
     subprocess.run(["make", "-j8", "-C", os.path.join(ROOT, "tests", "fakecuda")], check=True, capture_output=True)
     head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], cwd=ROOT, capture_output=True, text=True).stdout.strip()
@@ -83,6 +109,7 @@ def main() -> None:
         runs.append(run([os.path.join(ROOT, "tests", "workers", "simt_fold.py"), str(seed)]))
     for w, mc in ((2, 0), (2, 1), (3, 1), (4, 1), (8, 1)):
         runs.append(rails_multiprocess(w, mc))
+    runs.append(engine_multiprocess(8))
     ok = all(r["rc"] == 0 and not r["result"].get("bad") for r in runs)
     out = {"what": "rail kernels of csrc/cuda/kernels.cuh run from source on host fibers (tests/fakecuda/simt.h), "
                    "checked against the CPU oracle; NOT a hardware record",
