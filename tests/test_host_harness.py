@@ -120,7 +120,10 @@ def test_multiprocess_rails_host_logic(harness, world, multicast):
     from tests.mp_util import spawn
     from tests.test_gpu_rails import MULTI
 
-    cases = [c for c in MULTI if (multicast or c["kind"] != "nvls") and not c.get("graph")]  # no graphs here
+    # No CUDA graph capture here: the graph cases run their graph-safe rails
+    # eagerly (epochs / LL flags from the device launch counter).
+    cases = [dict({k: v for k, v in c.items() if k != "graph"}, graph_safe=True) if c.get("graph") else c
+             for c in MULTI if multicast or c["kind"] != "nvls"]
     env = _env(harness)
     env["FAKECUDA_MULTICAST"] = str(multicast)
     res = spawn(world, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(cases)], timeout=600,
@@ -129,7 +132,7 @@ def test_multiprocess_rails_host_logic(harness, world, multicast):
         assert len(rank_res["results"]) == len(cases)
         for r in rank_res["results"]:
             assert r["watchdog"] == 0 and r["mismatch"] == 0 and r["outside_nonzero"] == 0, r
-            assert r["progress"] == r["stop"], r
+            assert r["progress"] == r["stop"] and r.get("graph_mismatch", 0) == 0, r
 
 
 def test_multiprocess_engine_failover_host_logic(harness):

@@ -106,9 +106,10 @@ def run(comm, cases) -> dict:
     results = []
     for ci, c in enumerate(cases):
         kind = c["kind"]
-        key = (kind, c.get("sm_budget", 0), bool(c.get("graph")))
+        gsafe = bool(c.get("graph") or c.get("graph_safe"))
+        key = (kind, c.get("sm_budget", 0), gsafe)
         if key not in rails:
-            rails[key] = Rail(comm, RAIL_KINDS[kind], len(rails), c.get("sm_budget", 0), graph_safe=bool(c.get("graph")))
+            rails[key] = Rail(comm, RAIL_KINDS[kind], len(rails), c.get("sm_budget", 0), graph_safe=gsafe)
         rail = rails[key]
         dt = DTYPES[c["dtype"]]
         es = 2 if dt == oracle.BF16 else 4
@@ -210,6 +211,22 @@ def run(comm, cases) -> dict:
                     rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce)
                     rail.synchronize()
                 torch.cuda.synchronize()
+                got = np.zeros(nbytes // es, dtype=oracle.NP_DTYPE[dt])
+                bout.read(got, nbytes)
+                bad += compare(kind, dt, got, want, inputs, lo, hi, es)["mismatch"]
+            res["graph_mismatch"] = bad
+            res["watchdog"] = max(res["watchdog"], rail.watchdog())
+        if c.get("graph_safe") and check:
+            # Graph-safe rail run eagerly (no capture: the host harness): the
+            # barrier epochs and LL flags / parities come from the device
+            # launch counter; three more ops, each equal to the oracle.
+            want = _want(ci, dt, nbytes, world, seg_off, seg_len, chunk, lo, hi)
+            bad = 0
+            for _ in range(3):
+                bout.zero()
+                comm.barrier()
+                rail.allreduce(bin_, bout, seg_off, seg_len, chunk, dt, op_seq=ci, chunk_begin=cb, chunk_end=ce)
+                rail.synchronize()
                 got = np.zeros(nbytes // es, dtype=oracle.NP_DTYPE[dt])
                 bout.read(got, nbytes)
                 bad += compare(kind, dt, got, want, inputs, lo, hi, es)["mismatch"]
