@@ -300,3 +300,29 @@ def test_fold_kernel_awkward_geometries_on_host_fibers(harness, seed):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     out = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
     assert out["cases"] >= 60 and out["bad"] == [], out
+
+
+def test_multiprocess_link_death_and_watchdog_host_logic(harness):
+    """One rank's link dies mid-op on each rail, NVLS included (emulated
+    multicast), the other rank not told: every rank's launch fails, the
+    completed waves are exact, and after revive the op is exact; then a peer
+    that never arrives at all: the waiting kernel leaves at the watchdog."""
+    import json
+
+    from tests.mp_util import spawn
+
+    env = _env(harness)
+    env["FAKECUDA_MULTICAST"] = "1"
+    cases = [{"kind": k, "dtype": "f32", "nbytes": 160 << 20, "stall": [1, 3], "detect_us": 2000}
+             for k in ("sm", "nvls", "ce")]
+    res = spawn(2, os.path.join(ROOT, "tests", "workers", "rail_worker.py"), [json.dumps(cases)], timeout=600,
+                extra_env=env)
+    for rank_res in res:
+        for r in rank_res["results"]:
+            assert r["failed"] and r["mismatch"] == 0 and r["after_revive_mismatch"] == 0, r
+            assert r["stalled_here"] == (rank_res["rank"] == 1) and r["detected_here"] == (rank_res["rank"] == 0), r
+    for kind in ("sm", "nvls"):
+        res = spawn(2, os.path.join(ROOT, "tests", "workers", "watchdog_worker.py"), [kind], timeout=120,
+                    extra_env=dict(env, NEZHA_WATCHDOG_MS="300"))
+        r0 = [r for r in res if r["rank"] == 0][0]
+        assert r0["watchdog"] == 1 and r0["seconds"] < 30, r0
