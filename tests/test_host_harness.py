@@ -54,7 +54,7 @@ def test_loopback_suite_host_logic(harness):
     env.update({"NEZHA_TEST_HOST_HARNESS_LIB": harness, "NEZHA_WATCHDOG_MS": "5000",
                 "NEZHA_DETECT_US": "2000000", "PYTHONPATH": ROOT})
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_vranks.py"), "-m", "gpu",
-                        "-q", "-p", "no:cacheprovider", "--timeout", "600", "-k", SELECTION, "-rfE"],
+                        "-q", "-p", "no:cacheprovider", "-n", "3", "--timeout", "600", "-k", SELECTION, "-rfE"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
     tail = r.stdout[-6000:] + r.stderr[-3000:]
     assert r.returncode == 0, tail
