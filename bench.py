@@ -416,6 +416,52 @@ def run_loopback(args):
 
 
 # ------------------------------------------------------ N > 1: real GPUs ----
+def multirail_ab(comm, bin_, bout, dt, cap, max_over_ranks):
+    from paper_2405_17870_b200 import Rail
+    from paper_2405_17870_b200._lib import RAIL_KINDS
+
+    world = comm.world
+    base = "nvls" if comm.multicast else "sm"
+    others = [k for k in ("sm", "ce") if k != base]
+    rails = {k: Rail(comm, RAIL_KINDS[k], 30 + i) for i, k in enumerate([base] + others)}
+    rows = []
+    try:
+        for S_ in [s_ for s_ in (64 << 20, 256 << 20, GiB) if s_ <= cap]:
+            iters = 20 if S_ <= (64 << 20) else (10 if S_ <= (256 << 20) else 5)
+            row = {"bytes": S_}
+            for other in [None] + others:
+                for f in ((0.0,) if other is None else (0.1, 0.2, 0.3)):
+                    split = (int(S_ * (1 - f)) >> 21) << 21  # 2 MiB multiples
+                    parts = [(rails[base], 0, split)] + ([(rails[other], split, S_ - split)] if other else [])
+
+                    def op():
+                        for r_, off, ln in parts:
+                            chunk = max(65536, ((ln // (2 * world)) + 3) & ~3)  # P10
+                            r_.allreduce(bin_, bout, off, ln, chunk, dt)
+
+                    for _ in range(2):
+                        op()
+                    for r_, _, _ in parts:
+                        r_.synchronize()
+                    comm.barrier()
+                    t0 = time.perf_counter()
+                    for _ in range(iters):
+                        op()
+                    for r_, _, _ in parts:
+                        r_.synchronize()
+                    t = max_over_ranks((time.perf_counter() - t0) / iters)
+                    key = base if other is None else f"{base}+{other}@{f:.1f}"
+                    row[key] = round(ring_volume(world, S_) / t / 1e9, 2)
+            rows.append(row)
+    except Exception as e:  # reported, never fatal to the headline line
+        rows.append({"error": str(e)[:300]})
+    finally:
+        for r_ in rails.values():
+            r_.close()
+    return {"unit": "busbw GB/s", "base": base, "rows": rows,
+            "note": "fixed shares f on the second rail, no planner; wall clock over K concurrent ops"}
+
+
 def run_multi(args):
     import torch
 
@@ -626,6 +672,13 @@ def run_multi(args):
         t8 = torch.empty(2048, dtype=torch.float32, device="cuda")
         lat["nccl"] = p50_host(lambda: pg.all_reduce(t8), n_lat)
     out["latency_8k"] = lat
+
+    # Multi-rail worth on one NVSwitch: the base rail (NVLS, or
+    # SM without multicast) alone against the base plus a FIXED share f of
+    # the payload on a second rail, the two rails' launches concurrent on
+    # their own streams; wall clock over K ops, max over ranks.
+    if not args.no_sweep:
+        out["multirail_ab"] = multirail_ab(comm, bin_, bout, dt, cap, max_over_ranks)
 
     # Failover: config 4 shape (bf16 256 MiB, largest-alpha rail's link dies
     # on the last rank at its middle chunk, unplanned).
