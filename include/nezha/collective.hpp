@@ -68,10 +68,12 @@ inline int ringBlockOf(std::uint64_t elem, std::uint64_t chunk_elems, int world)
 std::vector<Segment> splitOversized(Bytes payload);
 
 // Waves of one rail call over chunks [cb, ce): consecutive
-// groups of ceil(wave_bytes / chunk_bytes) chunks, a last group shorter than
-// half a group joined to the one before; one launch sequence per wave, whose
-// success publishes its end chunk (the failure monitor's progress unit).
+// groups of max(ceil(wave_bytes / chunk_bytes), ceil((ce - cb) / kMaxWaves))
+// chunks, a last group shorter than half a group joined to the one before;
+// one launch sequence per wave, whose success publishes its end chunk (the
+// failure monitor's progress unit).
 inline constexpr Bytes kDefaultWaveBytes = Bytes{64} << 20;
+inline constexpr std::uint64_t kMaxWaves = 4;
 std::vector<std::pair<std::uint64_t, std::uint64_t>> waveRanges(Bytes chunk_bytes, std::uint64_t cb, std::uint64_t ce,
                                                                  Bytes wave_bytes = kDefaultWaveBytes);
 // Chunks complete on every rank when one rank's link dies at chunk `stall`

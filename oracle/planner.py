@@ -534,13 +534,16 @@ def truth(sc, op, rail_id, n, multi):
     return us
 
 
+MAX_WAVES = 4  # nezha::kMaxWaves
+
+
 def wave_ranges(C, cb, ce, wave_bytes):
     """Waves of a rail call over chunks [cb, ce): groups of
-    ceil(wave_bytes / C) chunks; a last group shorter than half a group joins
-    the one before."""
+    max(ceil(wave_bytes / C), ceil((ce - cb) / MAX_WAVES)) chunks; a last group
+    shorter than half a group joins the one before."""
     if ce <= cb or C == 0:
         return []
-    per = max(1, -(-max(wave_bytes, 1) // C))
+    per = max(1, -(-max(wave_bytes, 1) // C), -(-(ce - cb) // MAX_WAVES))
     w = [[c0, min(ce, c0 + per)] for c0 in range(cb, ce, per)]
     if len(w) > 1 and (w[-1][1] - w[-1][0]) * 2 < per:
         w[-2][1] = w[-1][1]

@@ -54,7 +54,10 @@ std::vector<std::pair<std::uint64_t, std::uint64_t>> waveRanges(Bytes chunk_byte
                                                                  Bytes wave_bytes) {
   std::vector<std::pair<std::uint64_t, std::uint64_t>> w;
   if (ce <= cb || chunk_bytes == 0) return w;
-  const std::uint64_t per = std::max<std::uint64_t>(1, (std::max<Bytes>(wave_bytes, 1) + chunk_bytes - 1) / chunk_bytes);
+  // At least wave_bytes per wave, and at most kMaxWaves waves per call: each
+  // wave pays a launch and two cross-rank barriers.
+  const std::uint64_t per = std::max<std::uint64_t>(
+      {1, (std::max<Bytes>(wave_bytes, 1) + chunk_bytes - 1) / chunk_bytes, (ce - cb + kMaxWaves - 1) / kMaxWaves});
   for (std::uint64_t c0 = cb; c0 < ce; c0 += per) w.emplace_back(c0, std::min(ce, c0 + per));
   if (w.size() > 1 && (w.back().second - w.back().first) * 2 < per) {
     w[w.size() - 2].second = w.back().second;

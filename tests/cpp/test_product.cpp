@@ -52,6 +52,11 @@ TEST_CASE("waves and the completed prefix of an unplanned failure (DESIGN.md §3
   CHECK(completedBeforeStall(10ull << 20, 0, 16, 7, 64ull << 20) == 7);
   CHECK(completedBeforeStall(10ull << 20, 0, 16, 15, 64ull << 20) == 7);
   CHECK(completedBeforeStall(10ull << 20, 0, 16, 16, 64ull << 20) == 16);  // never hit
+  // At most kMaxWaves waves: 1 GiB in 16 MiB chunks is 4 waves of 256 MiB, not 16 of 64 MiB.
+  auto big = waveRanges(16ull << 20, 0, 64, 64ull << 20);
+  CHECK(big.size() == 4);
+  CHECK(big[1] == std::make_pair<std::uint64_t, std::uint64_t>(16, 32));
+  CHECK(completedBeforeStall(16ull << 20, 0, 64, 40, 64ull << 20) == 32);
 }
 
 TEST_CASE("copy-engine pipeline cuts (DESIGN.md §3)") {
