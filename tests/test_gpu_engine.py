@@ -14,6 +14,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WORKER = os.path.join(ROOT, "tests", "workers", "engine_worker.py")
 
 # Rails with a fixed profile so the hot split is exercised deterministically.
+# The failover tests also pin sync_overhead_us = 0 and turn P12 demotion off:
+# the plan must be the hot split over all three rails (whatever the measured
+# concurrent times say), so that the rail killed always carries a segment.
+PINNED_HOT = {"sync_overhead_us": 0.0, "demote_after": 0}
 TOML3 = """
 [[rail]]
 protocol = "nvls"
@@ -141,7 +145,7 @@ def test_engine_failover_reroute(fail_rail):
     world = 4 if gpu_count() >= 4 else 2
     if gpu_count() < 2:
         pytest.skip("needs 2 GPUs")
-    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000,
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000, **PINNED_HOT,
             "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 3, "fail": [fail_rail, 3], "fail_rep": 1},
                       {"dtype": "i32", "nbytes": 64 << 20, "reps": 2},
                       {"dtype": "i32", "nbytes": 96 << 20, "reps": 1, "readmit": True}]}
@@ -174,7 +178,7 @@ def test_engine_failover_trials_acceptance5():
     for _ in range(16):
         cases.append({"dtype": "i32", "nbytes": 256 << 20, "reps": 1, "fail": [rng.randrange(3), rng.randrange(6)],
                       "fail_rank": rng.randrange(world), "readmit": True})
-    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000,
+    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000, **PINNED_HOT,
                        "cases": cases}, timeout=600)
     fos = [r["failover"] for rk in res for r in rk["results"] if r.get("failover")]
     assert len(fos) >= 8, fos
@@ -190,7 +194,7 @@ def test_engine_failover_int32_every_rail_exact():
     cases = []
     for rail in (0, 1, 2):
         cases.append({"dtype": "i32", "nbytes": 256 << 20, "reps": 1, "fail": [rail, 2], "readmit": True})
-    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000, "cases": cases},
+    res = _run(world, {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000, **PINNED_HOT, "cases": cases},
                timeout=420)
     for rk in res:
         assert len([r for r in rk["results"] if r.get("failover")]) == 3

@@ -96,6 +96,40 @@ def engine_multiprocess(world: int) -> dict:
     return rec
 
 
+def engine_failover_each_rail(world: int) -> dict:
+    """tests/test_gpu_engine.py::test_engine_failover_reroute's spec on the
+    emulated NVSwitch box: a hot split over NVLS + CE + SM (pinned), one
+    rank's link of rail 0, 1, then 2 dies mid-op, reroute, readmit."""
+    from tests.mp_util import spawn
+    from tests.test_gpu_engine import PINNED_HOT, TOML3
+
+    env = dict(ENV)
+    env["FAKECUDA_MULTICAST"] = "1"
+    t0 = time.time()
+    out = []
+    bad = 0
+    for fr in (0, 1, 2):
+        spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "readmit_hold_us": 100000, **PINNED_HOT,
+                "cases": [{"dtype": "bf16", "nbytes": 256 << 20, "reps": 3, "fail": [fr, 3], "fail_rep": 1},
+                          {"dtype": "i32", "nbytes": 64 << 20, "reps": 2},
+                          {"dtype": "i32", "nbytes": 96 << 20, "reps": 1, "readmit": True}]}
+        res = spawn(world, os.path.join(ROOT, "tests", "workers", "engine_worker.py"), [json.dumps(spec)], timeout=1800,
+                    extra_env=env)
+        bad += sum(r["mismatch"] != 0 for rk in res for r in rk["results"])
+        fos = [[r["failover"] for r in rk["results"] if r.get("failover")] for rk in res]
+        ok = all(len(f) == 1 and f[0]["failed_rail"] == fr and f[0]["target_rail"] != fr and f[0]["orphan_length"] > 0
+                 for f in fos)
+        bad += not ok
+        f0 = fos[0][0] if fos[0] else {}
+        out.append({k: f0.get(k) for k in ("failed_rail", "target_rail", "orphan_offset", "orphan_length",
+                                           "orphan_chunk")})
+    rec = {"cmd": f"tests/workers/engine_worker.py x {world} processes (failover of each rail, hot split)",
+           "env": {"FAKECUDA_MULTICAST": 1}, "rc": 0, "seconds": round(time.time() - t0, 1),
+           "result": {"world": world, "bad": bad, "failovers_rank0": out}}
+    print(json.dumps(rec), flush=True)
+    return rec
+
+
 def main() -> None:
     subprocess.run(["make", "-j8", "-C", os.path.join(ROOT, "tests", "fakecuda")], check=True, capture_output=True)
     head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], cwd=ROOT, capture_output=True, text=True).stdout.strip()
@@ -110,6 +144,7 @@ def main() -> None:
     for w, mc in ((2, 0), (2, 1), (3, 1), (4, 1), (8, 1)):
         runs.append(rails_multiprocess(w, mc))
     runs.append(engine_multiprocess(8))
+    runs.append(engine_failover_each_rail(4))
     ok = all(r["rc"] == 0 and not r["result"].get("bad") for r in runs)
     out = {"what": "rail kernels of csrc/cuda/kernels.cuh run from source on host fibers (tests/fakecuda/simt.h), "
                    "checked against the CPU oracle; NOT a hardware record",
