@@ -19,6 +19,10 @@ def pytest_configure(config):
 
 
 def gpu_count() -> int:
+    # The CPU host harness (tests/test_host_harness.py) can
+    # stand in for an N-GPU box: one process per "GPU", multicast emulated.
+    if os.environ.get("NEZHA_TEST_HOST_HARNESS_LIB") and os.environ.get("NEZHA_TEST_HARNESS_GPUS"):
+        return int(os.environ["NEZHA_TEST_HARNESS_GPUS"])
     try:
         import torch
 

@@ -12,11 +12,16 @@ from tests.mp_util import spawn
 pytestmark = [pytest.mark.gpu]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WORKER = os.path.join(ROOT, "tests", "workers", "engine_worker.py")
+# tests/test_host_harness.py runs this file on the CPU harness (processes as
+# GPUs, emulated multicast): no torch device, no CUDA graph capture there.
+HOST_HARNESS = bool(os.environ.get("NEZHA_TEST_HOST_HARNESS_LIB"))
+needs_torch_device = pytest.mark.skipif(HOST_HARNESS, reason="torch device / CUDA graphs")
 
 # Rails with a fixed profile so the hot split is exercised deterministically.
-# The failover tests also pin sync_overhead_us = 0 and turn P12 demotion off:
-# the plan must be the hot split over all three rails (whatever the measured
-# concurrent times say), so that the rail killed always carries a segment.
+# The failover and ComputePool tests also pin sync_overhead_us = 0 and turn
+# P12 demotion off: the plan must be the hot split over all three rails
+# (whatever the measured concurrent times say), so that the rail killed
+# always carries a segment and concurrent rails are always arbitrated.
 PINNED_HOT = {"sync_overhead_us": 0.0, "demote_after": 0}
 TOML3 = """
 [[rail]]
@@ -79,7 +84,8 @@ def test_engine_multirail_parity(world):
     # Startup budget tuning picked a candidate grid, the same on every rank.
     budgets = [[(x["kind"], x["sm_budget"]) for x in rk["state"]["rails"]] for rk in res]
     assert all(b == budgets[0] for b in budgets)
-    cands = {"nvls": {16, 32, 64}, "sm": {32, 64, 128}, "ce": {0}}
+    sms = 16 if HOST_HARNESS else 1 << 30  # the harness reports 16 SMs; budgets are capped by the SM count
+    cands = {"nvls": {min(c, sms) for c in (16, 32, 64)}, "sm": {min(c, sms) for c in (32, 64, 128)}, "ce": {0}}
     assert all(v in cands[k] for k, v in budgets[0]), budgets[0]
 
 
@@ -93,7 +99,7 @@ def test_engine_compute_pool_parity(mode):
     from oracle.compute_pool import plan_grants
 
     tokens = 100
-    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4, "compute_pool": mode,
+    spec = {"rails": ["nvls", "ce", "sm"], "rails_toml": TOML3, "window": 4, "compute_pool": mode, **PINNED_HOT,
             "pool_tokens": tokens,
             "cases": [{"dtype": "f32", "nbytes": 64 << 20, "reps": 6},
                       {"dtype": "bf16", "nbytes": 24 << 20, "reps": 2},
@@ -111,6 +117,7 @@ def test_engine_compute_pool_parity(mode):
     assert arbitrated > 0
 
 
+@needs_torch_device
 @pytest.mark.multigpu
 def test_engine_graph_capture():
     """graph_safe engine (device op counters in the rails): allreduces captured
@@ -154,7 +161,7 @@ def test_engine_failover_reroute(fail_rail):
         fo = [r for r in rk["results"] if "failover" in r][0]["failover"]
         assert fo is not None and fo["failed_rail"] == fail_rail
         assert fo["target_rail"] != fail_rail and fo["orphan_length"] > 0
-        assert fo["done_us"] > 0 and 0 < fo["resume_after_detect_us"] < 1000, fo
+        assert fo["done_us"] > 0 and 0 < fo["resume_after_detect_us"] < (1e12 if HOST_HARNESS else 1000), fo
         assert fo["stalled_here"] == (1 if rk["rank"] == world - 1 else 0), fo
         # After the failure the rail carries nothing until it is readmitted.
         later = [r for r in rk["results"] if r["case"] == 0 and r["rep"] == 2] + \
@@ -182,7 +189,7 @@ def test_engine_failover_trials_acceptance5():
                        "cases": cases}, timeout=600)
     fos = [r["failover"] for rk in res for r in rk["results"] if r.get("failover")]
     assert len(fos) >= 8, fos
-    assert all(f["resume_after_detect_us"] < 1000 for f in fos), fos
+    assert HOST_HARNESS or all(f["resume_after_detect_us"] < 1000 for f in fos), fos  # device timing only
 
 
 @pytest.mark.multigpu
@@ -200,6 +207,7 @@ def test_engine_failover_int32_every_rail_exact():
         assert len([r for r in rk["results"] if r.get("failover")]) == 3
 
 
+@needs_torch_device
 @pytest.mark.multigpu
 def test_ddp_comm_hook_matches_nccl():
     """The engine as a PyTorch DDP comm hook (paper_2405_17870_b200/ddp.py)."""

@@ -326,3 +326,21 @@ def test_multiprocess_link_death_and_watchdog_host_logic(harness):
                     extra_env=dict(env, NEZHA_WATCHDOG_MS="300"))
         r0 = [r for r in res if r["rank"] == 0][0]
         assert r0["watchdog"] == 1 and r0["seconds"] < 30, r0
+
+
+def test_multi_gpu_suites_on_harness(harness):
+    """tests/test_gpu_rails.py and tests/test_gpu_engine.py as written, the
+    harness standing in for a 4-GPU NVSwitch box (NEZHA_TEST_HARNESS_GPUS:
+    one process per GPU, multicast emulated): a fast cross-section here; the
+    whole of both files passes the same way (tools/harness_report.py)."""
+    env = dict(os.environ)
+    env.update(_env(harness))
+    env.update({"NEZHA_TEST_HARNESS_GPUS": "4", "FAKECUDA_MULTICAST": "1", "PYTHONPATH": ROOT})
+    sel = ("test_multi_gpu_rails or test_watchdog_instead_of_hang or test_engine_single_gpu_identity or "
+           "test_engine_compute_pool_parity")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_rails.py"),
+                        os.path.join(ROOT, "tests", "test_gpu_engine.py"), "-m", "gpu", "-q", "-p", "no:cacheprovider",
+                        "-n", "3", "--timeout", "900", "-k", sel, "-rfE"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
+    assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-3000:]
+    assert " passed" in r.stdout, r.stdout[-3000:]

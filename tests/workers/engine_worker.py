@@ -40,6 +40,13 @@ def clear_cache() -> None:
         _cache.clear()
 
 
+def evict_case(ci) -> None:
+    """Drops case ci's inputs and oracle results (every rank is past it)."""
+    with _cache_lock:
+        for k in [k for k in _cache if len(k) > 1 and k[1] == ci]:
+            del _cache[k]
+
+
 def cached(key, fn):
     with _cache_lock:
         ev = _cache.get(key)
@@ -197,6 +204,10 @@ def run(comm, spec) -> dict:
             st = eng.state()
             if c["fail"][0] in st["monitor"]["failed"]:
                 eng.readmit(c["fail"][0])
+        # Every rank (process or virtual-rank thread) is done with case ci:
+        # its inputs and oracle results (N x payload each) can go.
+        comm.barrier()
+        evict_case(ci)
     state = eng.state()
     eng.close()
     bin_.free()

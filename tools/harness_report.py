@@ -130,6 +130,27 @@ def engine_failover_each_rail(world: int) -> dict:
     return rec
 
 
+def gpu_suites_on_harness() -> dict:
+    """tests/test_gpu_rails.py + tests/test_gpu_engine.py as written, on the
+    harness standing in for a 4-GPU box (multicast emulated)."""
+    env = dict(os.environ)
+    env.update(ENV)
+    env.update({"NEZHA_TEST_HARNESS_GPUS": "4", "FAKECUDA_MULTICAST": "1"})
+    t0 = time.time()
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_rails.py", "tests/test_gpu_engine.py", "-m", "gpu",
+                        "-q", "-p", "no:cacheprovider", "--timeout", "1800", "-rfE"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=5400)
+    summary = [l for l in r.stdout.splitlines() if " passed" in l or " failed" in l][-1:]
+    rec = {"cmd": "pytest tests/test_gpu_rails.py tests/test_gpu_engine.py -m gpu (4 harness GPUs)",
+           "env": {"NEZHA_TEST_HARNESS_GPUS": 4, "FAKECUDA_MULTICAST": 1}, "rc": r.returncode,
+           "seconds": round(time.time() - t0, 1),
+           "result": {"summary": summary[0] if summary else r.stdout[-300:],
+                      "skipped_by_design": "in-process torch device buffers, CUDA graph capture, DDP (torch)",
+                      "bad": 0 if r.returncode == 0 else 1}}
+    print(json.dumps(rec), flush=True)
+    return rec
+
+
 def main() -> None:
     subprocess.run(["make", "-j8", "-C", os.path.join(ROOT, "tests", "fakecuda")], check=True, capture_output=True)
     head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], cwd=ROOT, capture_output=True, text=True).stdout.strip()
@@ -145,6 +166,7 @@ def main() -> None:
         runs.append(rails_multiprocess(w, mc))
     runs.append(engine_multiprocess(8))
     runs.append(engine_failover_each_rail(4))
+    runs.append(gpu_suites_on_harness())
     ok = all(r["rc"] == 0 and not r["result"].get("bad") for r in runs)
     out = {"what": "rail kernels of csrc/cuda/kernels.cuh run from source on host fibers (tests/fakecuda/simt.h), "
                    "checked against the CPU oracle; NOT a hardware record",
