@@ -57,6 +57,8 @@ namespace {
 constexpr size_t kStack = 32 * 1024;
 
 struct Cta {
+  bool admitted = false;  // resident on the (modelled) device
+  int live = 0;           // fibers not finished
   int expected = 0;     // fibers still running (exited ones leave the barrier)
   int arrived = 0;
   uint64_t gen = 0;
@@ -183,6 +185,36 @@ void* shared_slot(const void* key, size_t bytes) {
   return v.data();
 }
 
+// Residency model (FAKECUDA_SIMT_RESIDENT_THREADS, default 16 SMs x 2 CTAs
+// x 512 threads, matching the harness's reported SM count and occupancy; 0 =
+// unlimited): a CTA runs only once it is resident, CTAs become resident in
+// launch (linear block) order as earlier CTAs of any grid in the process
+// retire, and a grid's CTAs never all start at once unless they fit. A
+// cross-rank wait between CTAs that cannot be co-resident then behaves as on
+// the device: it waits for a CTA that never starts, until its watchdog.
+static int64_t residentCapacity() {
+  static const int64_t v = [] {
+    const char* e = getenv("FAKECUDA_SIMT_RESIDENT_THREADS");
+    return e ? static_cast<int64_t>(atoll(e)) : int64_t{16} * 2 * 512;
+  }();
+  return v;
+}
+static std::atomic<int64_t> g_resident{0};  // threads of resident CTAs, process-wide
+
+static bool acquireResidency(int64_t threads) {
+  const int64_t cap = residentCapacity();
+  if (cap <= 0) return true;
+  int64_t cur = g_resident.load();
+  while (cur + threads <= cap) {
+    if (g_resident.compare_exchange_weak(cur, cur + threads)) return true;
+  }
+  return false;
+}
+
+static void releaseResidency(int64_t threads) {
+  if (residentCapacity() > 0) g_resident.fetch_sub(threads);
+}
+
 // Runs `body` once per thread of the grid, to completion.
 void run_grid(dim3 grid, dim3 block, const std::function<void()>& body) {
   Grid g;
@@ -206,6 +238,7 @@ void run_grid(dim3 grid, dim3 block, const std::function<void()>& body) {
       for (unsigned bx = 0; bx < grid.x; ++bx) {
         Cta* cta = &g.ctas[(static_cast<size_t>(bz) * grid.y + by) * grid.x + bx];
         cta->expected = static_cast<int>(nthr);
+        cta->live = static_cast<int>(nthr);
         for (unsigned tz = 0; tz < block.z; ++tz)
           for (unsigned ty = 0; ty < block.y; ++ty)
             for (unsigned tx = 0; tx < block.x; ++tx, ++i) {
@@ -231,14 +264,23 @@ void run_grid(dim3 grid, dim3 block, const std::function<void()>& body) {
   int idle_passes = 0;
   std::vector<uint32_t> order(n);
   for (size_t k = 0; k < n; ++k) order[k] = static_cast<uint32_t>(k);
+  if (residentCapacity() > 0 && static_cast<int64_t>(nthr) > residentCapacity()) {
+    fprintf(stderr, "simt: a CTA of %zu threads exceeds the modelled device\n", nthr);
+    abort();
+  }
+  size_t next_cta = 0;
   while (live > 0) {
+    while (next_cta < nctas && acquireResidency(static_cast<int64_t>(nthr))) {
+      g.ctas[next_cta++].admitted = true;
+      g.events++;
+    }
     const uint64_t ev0 = g.events;
     if (preempt_pm()) {
       for (size_t k = n; k > 1; --k) std::swap(order[k - 1], order[rnd() % k]);
     }
     for (uint32_t idx : order) {
       Fiber& f = g.fibers[idx];
-      if (f.done) continue;
+      if (f.done || !f.cta->admitted) continue;
       f.spun = false;
       g.running = &f;
       g_cur = &f.cur;
@@ -246,6 +288,7 @@ void run_grid(dim3 grid, dim3 block, const std::function<void()>& body) {
       if (f.done) {
         --live;
         g.events++;
+        if (--f.cta->live == 0) releaseResidency(static_cast<int64_t>(nthr));  // the CTA retired
       }
     }
     if (g.events != ev0) {
