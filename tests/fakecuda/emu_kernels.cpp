@@ -10,6 +10,7 @@
 // loopback *_vr grids run one host thread per virtual rank.
 #include <cuda_runtime_api.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -427,6 +428,12 @@ bool simtMode() {
     return !e || atoi(e) != 0;
   }();
   return on;
+}
+
+int occupancyOf(const std::string& name, int block_threads) {
+  if (name.find("ll_kernel") != std::string::npos) return 1;
+  if (block_threads >= 512) return 2;
+  return std::max(1, std::min(32, 1024 / std::max(1, block_threads)));
 }
 
 void countLaunch(const std::string& name) {

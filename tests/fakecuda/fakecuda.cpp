@@ -333,8 +333,16 @@ cudaError_t cudaMemGetInfo(size_t* fr, size_t* tot) {
   *tot = size_t(180) << 30;
   return cudaSuccess;
 }
-cudaError_t cudaOccupancyMaxActiveBlocksPerMultiprocessorWithFlags(int* n, const void*, int, size_t, unsigned int) {
-  *n = 2;
+cudaError_t cudaOccupancyMaxActiveBlocksPerMultiprocessorWithFlags(int* n, const void* func, int block, size_t,
+                                                                   unsigned int) {
+  std::string name;
+  {
+    Registry& r = registry();
+    std::lock_guard<std::mutex> lk(r.m);
+    auto it = r.names.find(func);
+    if (it != r.names.end()) name = it->second;
+  }
+  *n = fakecuda::occupancyOf(name, block);
   return cudaSuccess;
 }
 

@@ -19,4 +19,10 @@ std::function<void()> emulatedKernel(const std::string& name, dim3 grid, dim3 bl
 
 void countLaunch(const std::string& name);
 
+// Resident CTAs per SM of a kernel (the harness's cudaOccupancy* answer, and
+// the SIMT residency model's per-CTA cost): the B200 figures of the rail
+// kernels — LL 1 (76-96 registers x 512 threads), the other 512-thread
+// kernels 2 (<= 64 registers), small CTAs up to 32 per SM.
+int occupancyOf(const std::string& name, int block_threads);
+
 }  // namespace fakecuda

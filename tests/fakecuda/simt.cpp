@@ -8,6 +8,7 @@
 
 #include <sys/mman.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -185,21 +186,23 @@ void* shared_slot(const void* key, size_t bytes) {
   return v.data();
 }
 
-// Residency model (FAKECUDA_SIMT_RESIDENT_THREADS, default 16 SMs x 2 CTAs
-// x 512 threads, matching the harness's reported SM count and occupancy; 0 =
-// unlimited): a CTA runs only once it is resident, CTAs become resident in
-// launch (linear block) order as earlier CTAs of any grid in the process
-// retire, and a grid's CTAs never all start at once unless they fit. A
-// cross-rank wait between CTAs that cannot be co-resident then behaves as on
-// the device: it waits for a CTA that never starts, until its watchdog.
+// Residency model (FAKECUDA_SIMT_RESIDENT_SMS, default 16 — the SM count
+// the harness reports; 0 = unlimited): a CTA runs only once it is resident,
+// CTAs become resident in launch (linear block) order as earlier CTAs of any
+// grid in the process retire, and a CTA of a kernel with occupancy k costs
+// 1/k of an SM (fakecuda::occupancyOf, the same figures the harness's
+// cudaOccupancy* returns). A cross-rank wait between CTAs that cannot be
+// co-resident then behaves as on the device: it waits for a CTA that never
+// starts, until its watchdog.
+constexpr int64_t kUnitsPerSM = 64;
 static int64_t residentCapacity() {
   static const int64_t v = [] {
-    const char* e = getenv("FAKECUDA_SIMT_RESIDENT_THREADS");
-    return e ? static_cast<int64_t>(atoll(e)) : int64_t{16} * 2 * 512;
+    const char* e = getenv("FAKECUDA_SIMT_RESIDENT_SMS");
+    return (e ? static_cast<int64_t>(atoll(e)) : int64_t{16}) * kUnitsPerSM;
   }();
   return v;
 }
-static std::atomic<int64_t> g_resident{0};  // threads of resident CTAs, process-wide
+static std::atomic<int64_t> g_resident{0};  // SM units held by resident CTAs, process-wide
 
 static bool acquireResidency(int64_t threads) {
   const int64_t cap = residentCapacity();
@@ -216,7 +219,7 @@ static void releaseResidency(int64_t threads) {
 }
 
 // Runs `body` once per thread of the grid, to completion.
-void run_grid(dim3 grid, dim3 block, const std::function<void()>& body) {
+void run_grid(dim3 grid, dim3 block, const std::function<void()>& body, int occupancy) {
   Grid g;
   const size_t nctas = static_cast<size_t>(grid.x) * grid.y * grid.z;
   const size_t nthr = static_cast<size_t>(block.x) * block.y * block.z;
@@ -264,13 +267,14 @@ void run_grid(dim3 grid, dim3 block, const std::function<void()>& body) {
   int idle_passes = 0;
   std::vector<uint32_t> order(n);
   for (size_t k = 0; k < n; ++k) order[k] = static_cast<uint32_t>(k);
-  if (residentCapacity() > 0 && static_cast<int64_t>(nthr) > residentCapacity()) {
-    fprintf(stderr, "simt: a CTA of %zu threads exceeds the modelled device\n", nthr);
+  const int64_t cost = kUnitsPerSM / std::max(1, std::min<int>(occupancy, kUnitsPerSM));
+  if (residentCapacity() > 0 && cost > residentCapacity()) {
+    fprintf(stderr, "simt: a CTA exceeds the modelled device\n");
     abort();
   }
   size_t next_cta = 0;
   while (live > 0) {
-    while (next_cta < nctas && acquireResidency(static_cast<int64_t>(nthr))) {
+    while (next_cta < nctas && acquireResidency(cost)) {
       g.ctas[next_cta++].admitted = true;
       g.events++;
     }
@@ -288,7 +292,7 @@ void run_grid(dim3 grid, dim3 block, const std::function<void()>& body) {
       if (f.done) {
         --live;
         g.events++;
-        if (--f.cta->live == 0) releaseResidency(static_cast<int64_t>(nthr));  // the CTA retired
+        if (--f.cta->live == 0) releaseResidency(cost);  // the CTA retired
       }
     }
     if (g.events != ev0) {

@@ -9,9 +9,12 @@
 #include "kernels.cuh"
 
 namespace nzsimt {
-void run_grid(dim3 grid, dim3 block, const std::function<void()>& body);
+void run_grid(dim3 grid, dim3 block, const std::function<void()>& body, int occupancy);
 uint64_t end_dilation();
 }  // namespace nzsimt
+namespace fakecuda {
+int occupancyOf(const std::string& name, int block_threads);
+}
 
 using namespace nz;
 
@@ -35,10 +38,11 @@ void dilate(VPack<A>& p) {
 // The launch's arguments are copied (and their end budgets stretched) once;
 // every fiber of the grid then runs the kernel on that copy.
 template <typename A, typename F>
-std::function<void()> launch(dim3 grid, dim3 block, void** args, F kernel) {
+std::function<void()> launch(const std::string& base, dim3 grid, dim3 block, void** args, F kernel) {
   auto a = std::make_shared<A>(*static_cast<const A*>(args[0]));
   dilate(*a);
-  return [=] { nzsimt::run_grid(grid, block, [&] { kernel(*a); }); };
+  const int occ = fakecuda::occupancyOf(base, static_cast<int>(block.x * block.y * block.z));
+  return [=] { nzsimt::run_grid(grid, block, [&] { kernel(*a); }, occ); };
 }
 
 template <typename DT>
@@ -46,16 +50,16 @@ std::function<void()> byN(const std::string& base, int N, int nd, dim3 grid, dim
 #define NZ_N(n)                                                                                          \
   if (N == n) {                                                                                          \
     if (base == "fold_kernel") {                                                                         \
-      if (nd == 1) return launch<FoldArgs>(grid, block, args, [](const FoldArgs& a) { fold_kernel<DT, n, 1>(a); }); \
-      if (nd == n) return launch<FoldArgs>(grid, block, args, [](const FoldArgs& a) { fold_kernel<DT, n, n>(a); }); \
+      if (nd == 1) return launch<FoldArgs>(base, grid, block, args, [](const FoldArgs& a) { fold_kernel<DT, n, 1>(a); }); \
+      if (nd == n) return launch<FoldArgs>(base, grid, block, args, [](const FoldArgs& a) { fold_kernel<DT, n, n>(a); }); \
     }                                                                                                    \
     if (base == "fold_kernel_vr" && nd == n)                                                             \
-      return launch<VPack<FoldArgs>>(grid, block, args, [](const VPack<FoldArgs>& p) { fold_kernel_vr<DT, n, n>(p); });                                                                                                \
+      return launch<VPack<FoldArgs>>(base, grid, block, args, [](const VPack<FoldArgs>& p) { fold_kernel_vr<DT, n, n>(p); });                                                                                                \
     if constexpr (n >= 2) {                                                                              \
-      if (base == "nvls_kernel") return launch<NvlsArgs>(grid, block, args, [](const NvlsArgs& a) { nvls_kernel<DT, n>(a); }); \
-      if (base == "ll_kernel") return launch<LLArgs>(grid, block, args, [](const LLArgs& a) { ll_kernel<DT, n>(a); }); \
+      if (base == "nvls_kernel") return launch<NvlsArgs>(base, grid, block, args, [](const NvlsArgs& a) { nvls_kernel<DT, n>(a); }); \
+      if (base == "ll_kernel") return launch<LLArgs>(base, grid, block, args, [](const LLArgs& a) { ll_kernel<DT, n>(a); }); \
       if (base == "ll_kernel_vr")                                                                        \
-        return launch<VPack<LLArgs>>(grid, block, args, [](const VPack<LLArgs>& p) { ll_kernel_vr<DT, n>(p); }); \
+        return launch<VPack<LLArgs>>(base, grid, block, args, [](const VPack<LLArgs>& p) { ll_kernel_vr<DT, n>(p); }); \
     }                                                                                                    \
   }
   NZ_N(1) NZ_N(2) NZ_N(3) NZ_N(4) NZ_N(5) NZ_N(6) NZ_N(7) NZ_N(8)
@@ -66,9 +70,9 @@ std::function<void()> byN(const std::string& base, int N, int nd, dim3 grid, dim
 template <int n>
 std::function<void()> barrierN(const std::string& base, dim3 grid, dim3 block, void** args) {
   if (base == "barrier_kernel")
-    return launch<BarrierKArgs>(grid, block, args, [](const BarrierKArgs& k) { barrier_kernel<n>(k); });
+    return launch<BarrierKArgs>(base, grid, block, args, [](const BarrierKArgs& k) { barrier_kernel<n>(k); });
   if (base == "barrier_kernel_vr")
-    return launch<VPack<BarrierKArgs>>(grid, block, args, [](const VPack<BarrierKArgs>& p) { barrier_kernel_vr<n>(p); });
+    return launch<VPack<BarrierKArgs>>(base, grid, block, args, [](const VPack<BarrierKArgs>& p) { barrier_kernel_vr<n>(p); });
   return {};
 }
 
@@ -95,7 +99,10 @@ std::function<void()> simtKernel(const std::string& base, const std::vector<std:
                                                  *static_cast<const uint64_t*>(args[3]),
                                                  *static_cast<const FaultPost*>(args[4]),
                                                  *static_cast<const RailCtl*>(args[5])});
-    return [=] { nzsimt::run_grid(grid, block, [&] { copy_kernel(a->src, a->dst, a->lo, a->hi, a->post, a->ctl); }); };
+    const int occ = fakecuda::occupancyOf(base, static_cast<int>(block.x * block.y * block.z));
+    return [=] {
+      nzsimt::run_grid(grid, block, [&] { copy_kernel(a->src, a->dst, a->lo, a->hi, a->post, a->ctl); }, occ);
+    };
   }
   if ((base == "barrier_kernel" || base == "barrier_kernel_vr") && targs.size() == 1) {
     switch (std::stoi(targs[0])) {
